@@ -1,0 +1,580 @@
+// C-ABI implementation (include/spttn_b200.h): device CSF construction,
+// plan creation (nest-shape -> kernel, device allocation, work
+// decomposition) and execution. Mirrors the reference executor's contract
+// (proj/src/executor.cpp:112-200 for validation and errors, :492-520 for
+// execute) with CUDA status codes mapped to the reference exception types.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../../include/spttn_b200.h"
+#include "internal.cuh"
+
+using spttn_dev::Status;
+
+struct spttn_csf {
+  spttn_dev::DevCsf d;
+};
+
+struct spttn_plan {
+  int kind = 0;
+  int flags = 0;
+  int64_t R = 0, S = 0, T = 0;
+  spttn_csf* csf = nullptr;
+  int nf = 0;
+  double* fac[8] = {nullptr};
+  int64_t fac_size[8] = {0};
+  bool own_fac = true;
+  double* out = nullptr;
+  int64_t out_count = 0;
+  int vec = 0;
+  spttn_dev::Decomp dec;
+  spttn_dev::GenericState gen;
+  spg_program* prog = nullptr;  // host copy (GENERIC)
+  const double** d_dense = nullptr;
+  int64_t launches = 0;
+  int64_t last_madds = -1;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return SPTTN_OK;
+  } catch (const Status& s) {
+    g_err = s.what();
+    return s.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return SPTTN_ENOMEM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return SPTTN_EINVAL;
+  }
+}
+
+void fail(int code, const std::string& msg) { throw Status(code, msg); }
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+void dev_malloc(void** p, size_t bytes) {
+  const cudaError_t e = cudaMalloc(p, bytes ? bytes : 1);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    fail(SPTTN_ENOMEM, "device allocation of " + std::to_string(bytes) + " bytes failed");
+  }
+  if (e != cudaSuccess) fail(SPTTN_ECUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+}
+
+// int64 -> int32 narrowing with range / monotonicity checks.
+__global__ void k_narrow(const int64_t* src, int32_t* dst, int64_t n, int64_t limit,
+                         int monotone, int* err) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t v = src[i];
+  if (v < 0 || v >= limit) atomicOr(err, 1);
+  if (monotone && i + 1 < n && src[i + 1] < v) atomicOr(err, 2);
+  dst[i] = static_cast<int32_t>(v);
+}
+
+// Packed leaf keys for sparse-output lookups (executor.cpp:342-366); the CSF
+// is lexicographic, so the keys come out sorted with leaf_pos = identity.
+__global__ void k_leaf_keys(spttn_dev::CsfView t, const spg_program* P, int64_t* keys,
+                            int64_t* pos) {
+  const int64_t leaf = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int d = t.order;
+  if (leaf >= t.nlev[d - 1]) return;
+  int64_t node = leaf, key = 0;
+  for (int l = d - 1; l >= 0; --l) {
+    key += static_cast<int64_t>(t.idx[l][node]) * P->mode_key_stride[l];
+    if (l > 0) {
+      int64_t lo = 0, hi = t.nlev[l - 1];
+      while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (t.ptr[l - 1][mid] <= node) lo = mid; else hi = mid;
+      }
+      node = lo;
+    }
+  }
+  keys[leaf] = key;
+  pos[leaf] = leaf;
+}
+
+int64_t env_int(const char* name, int64_t dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::atoll(v) : dflt;
+}
+
+int sm_count() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+void copy_factors(spttn_plan* p, const double* const* src, bool on_device, cudaStream_t s) {
+  for (int f = 0; f < p->nf; ++f) {
+    if (on_device) {
+      p->fac[f] = const_cast<double*>(src[f]);
+    } else {
+      if (!p->fac[f]) dev_malloc(reinterpret_cast<void**>(&p->fac[f]), p->fac_size[f] * sizeof(double));
+      if (p->fac_size[f] > 0)
+        SPTTN_CUDA(cudaMemcpyAsync(p->fac[f], src[f], p->fac_size[f] * sizeof(double),
+                                   cudaMemcpyHostToDevice, s));
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* spttn_last_error(void) { return g_err.c_str(); }
+
+#define SPTTN_STR2(x) #x
+#define SPTTN_STR(x) SPTTN_STR2(x)
+const char* spttn_build_info(void) {
+  return "spttn_b200 sm_100a nvcc " SPTTN_STR(__CUDACC_VER_MAJOR__) "." SPTTN_STR(__CUDACC_VER_MINOR__);
+}
+
+int spttn_device_info(int64_t* out, int n) {
+  return guarded([&] {
+    int dev = 0;
+    SPTTN_CUDA(cudaGetDevice(&dev));
+    cudaDeviceProp pr{};
+    SPTTN_CUDA(cudaGetDeviceProperties(&pr, dev));
+    const int64_t v[4] = {pr.multiProcessorCount, pr.major * 10 + pr.minor, pr.l2CacheSize,
+                          static_cast<int64_t>(pr.sharedMemPerBlockOptin)};
+    for (int i = 0; i < n && i < 4; ++i) out[i] = v[i];
+  });
+}
+
+int spttn_csf_create(const spttn_csf_host* h, void* stream, spttn_csf** out) {
+  return guarded([&] {
+    if (!h || !out) fail(SPTTN_EINVAL, "spttn_csf_create: null argument");
+    *out = nullptr;
+    const int d = h->order;
+    if (d < 1 || d > spttn_dev::kMaxOrder) fail(SPTTN_EINVAL, "CSF order must be 1..8");
+    auto c = std::make_unique<spttn_csf>();
+    auto& D = c->d;
+    D.order = d;
+    SPTTN_CUDA(cudaGetDevice(&D.device));
+    cudaStream_t s = as_stream(stream);
+    int64_t maxn = 1;
+    for (int l = 0; l < d; ++l) {
+      D.dims[l] = h->dims[l];
+      D.level_size[l] = h->level_size[l];
+      if (h->dims[l] < 1 || h->dims[l] > INT32_MAX)
+        fail(SPTTN_EINVAL, "CSF mode size must be in [1, 2^31)");
+      if (h->level_size[l] < 0 || h->level_size[l] >= INT32_MAX)
+        fail(SPTTN_EINVAL, "CSF level size exceeds the int32 device layout");
+      if (l > 0 && h->level_size[l] < h->level_size[l - 1])
+        fail(SPTTN_EINVAL, "CSF level sizes must be non-decreasing");
+      maxn = std::max(maxn, h->level_size[l] + 1);
+    }
+    for (int l = 0; l + 1 < d; ++l) {
+      const int64_t n = h->level_size[l];
+      if (h->ptr[l][0] != 0 || h->ptr[l][n] != h->level_size[l + 1])
+        fail(SPTTN_EINVAL, "CSF ptr[" + std::to_string(l) + "] does not close its child range");
+    }
+    int64_t* stage = nullptr;
+    int* err = nullptr;
+    dev_malloc(reinterpret_cast<void**>(&stage), maxn * sizeof(int64_t));
+    dev_malloc(reinterpret_cast<void**>(&err), sizeof(int));
+    SPTTN_CUDA(cudaMemsetAsync(err, 0, sizeof(int), s));
+    auto narrow = [&](const int64_t* src, int32_t** dst, int64_t n, int64_t limit, int mono) {
+      dev_malloc(reinterpret_cast<void**>(dst), std::max<int64_t>(1, n) * sizeof(int32_t));
+      D.bytes += n * sizeof(int32_t);
+      if (n == 0) return;
+      SPTTN_CUDA(cudaMemcpyAsync(stage, src, n * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+      k_narrow<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(stage, *dst, n, limit, mono,
+                                                                       err);
+      SPTTN_CUDA(cudaGetLastError());
+    };
+    try {
+      for (int l = 0; l < d; ++l) {
+        narrow(h->idx[l], &D.idx[l], h->level_size[l], h->dims[l], 0);
+        if (l + 1 < d)
+          narrow(h->ptr[l], &D.ptr[l], h->level_size[l] + 1, h->level_size[l + 1] + 1, 1);
+      }
+      const int64_t nnz = h->level_size[d - 1];
+      dev_malloc(reinterpret_cast<void**>(&D.vals), std::max<int64_t>(1, nnz) * sizeof(double));
+      D.bytes += nnz * sizeof(double);
+      if (nnz > 0)
+        SPTTN_CUDA(cudaMemcpyAsync(D.vals, h->values, nnz * sizeof(double),
+                                   cudaMemcpyHostToDevice, s));
+      int herr = 0;
+      SPTTN_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, s));
+      SPTTN_CUDA(cudaStreamSynchronize(s));
+      if (herr & 1) fail(SPTTN_EINVAL, "CSF coordinate or child pointer out of range");
+      if (herr & 2) fail(SPTTN_EINVAL, "CSF child pointers are not monotone");
+    } catch (...) {
+      cudaFree(stage);
+      cudaFree(err);
+      for (int l = 0; l < d; ++l) {
+        cudaFree(D.idx[l]);
+        cudaFree(D.ptr[l]);
+      }
+      cudaFree(D.vals);
+      throw;
+    }
+    cudaFree(stage);
+    cudaFree(err);
+    *out = c.release();
+  });
+}
+
+int spttn_csf_destroy(spttn_csf* c) {
+  return guarded([&] {
+    if (!c) return;
+    for (int l = 0; l < c->d.order; ++l) {
+      cudaFree(c->d.idx[l]);
+      cudaFree(c->d.ptr[l]);
+    }
+    cudaFree(c->d.vals);
+    delete c;
+  });
+}
+
+int64_t spttn_csf_level_size(const spttn_csf* c, int l) {
+  return (c && l >= 0 && l < c->d.order) ? c->d.level_size[l] : -1;
+}
+
+int64_t spttn_csf_device_bytes(const spttn_csf* c) { return c ? c->d.bytes : -1; }
+
+int spttn_plan_destroy(spttn_plan* p) {
+  return guarded([&] {
+    if (!p) return;
+    if (p->own_fac)
+      for (int f = 0; f < p->nf; ++f) cudaFree(p->fac[f]);
+    cudaFree(p->out);
+    cudaFree(p->d_dense);
+    spttn_dev::free_decomp(p->dec);
+    spttn_dev::generic_free(p->gen);
+    delete p->prog;
+    delete p;
+  });
+}
+
+int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
+                      spttn_plan** out) {
+  spttn_plan* raw = nullptr;
+  const int rc = guarded([&] {
+    if (!desc || !csf || !out) fail(SPTTN_EINVAL, "spttn_plan_create: null argument");
+    *out = nullptr;
+    cudaStream_t s = as_stream(stream);
+    auto p = new spttn_plan;
+    raw = p;
+    const auto& D = csf->d;
+    p->kind = desc->kind;
+    p->flags = desc->flags;
+    p->R = desc->rank[0];
+    p->S = desc->rank[1];
+    p->T = desc->rank[2];
+    p->csf = csf;
+    p->nf = desc->num_factors;
+    if (p->nf < 0 || p->nf > 8) fail(SPTTN_EINVAL, "num_factors must be 0..8");
+    for (int f = 0; f < p->nf; ++f) p->fac_size[f] = desc->factor_size[f];
+    const bool on_dev = (desc->flags & SPTTN_FLAG_FACTORS_ON_DEVICE) != 0;
+    p->own_fac = !on_dev;
+    const int64_t nnz = D.level_size[D.order - 1];
+
+    auto need = [&](int order, int nf, std::initializer_list<int64_t> sizes) {
+      if (D.order != order)
+        fail(SPTTN_EINVAL, "sparse tensor order mismatch for this nest");
+      if (p->nf != nf) fail(SPTTN_EINVAL, "wrong number of dense inputs for this nest");
+      int f = 0;
+      for (int64_t sz : sizes) {
+        if (p->fac_size[f] != sz) fail(SPTTN_EINVAL, "dense tensor shape mismatch");
+        ++f;
+      }
+    };
+    const int64_t R = p->R, S = p->S, T = p->T;
+    int64_t tile = 0;
+    switch (p->kind) {
+      case SPTTN_NEST_MTTKRP3:
+        need(3, 2, {D.dims[1] * R, D.dims[2] * R});
+        if (R < 1 || R > 128) fail(SPTTN_EUNSUPPORTED, "MTTKRP kernel supports 1 <= R <= 128");
+        tile = R;
+        break;
+      case SPTTN_NEST_MTTKRP4:
+        need(4, 3, {D.dims[1] * R, D.dims[2] * R, D.dims[3] * R});
+        if (R < 1 || R > 128) fail(SPTTN_EUNSUPPORTED, "MTTKRP kernel supports 1 <= R <= 128");
+        tile = R;
+        break;
+      case SPTTN_NEST_TTTP3:
+        need(3, 3, {D.dims[0] * R, D.dims[1] * R, D.dims[2] * R});
+        if (R < 1 || R > 128) fail(SPTTN_EUNSUPPORTED, "TTTP kernel supports 1 <= R <= 128");
+        break;
+      case SPTTN_NEST_TTMC3:
+        need(3, 2, {D.dims[1] * R, D.dims[2] * S});
+        if (R < 1 || R > 16 || S < 1 || S > 16)
+          fail(SPTTN_EUNSUPPORTED, "TTMc-3 DMMA kernel supports R, S <= 16");
+        tile = R * S;
+        break;
+      case SPTTN_NEST_TTMC4:
+        need(4, 3, {D.dims[1] * R, D.dims[2] * S, D.dims[3] * T});
+        if (R < 1 || R > 8 || S < 1 || S > 8 || T < 1 || T > 8)
+          fail(SPTTN_EUNSUPPORTED, "TTMc-4 DMMA kernel supports R, S, T <= 8");
+        tile = R * S * T;
+        break;
+      case SPTTN_NEST_GENERIC: {
+        if (!desc->program || desc->program_bytes != static_cast<int64_t>(sizeof(spg_program)))
+          fail(SPTTN_EINVAL, "GENERIC plan needs a spg_program");
+        p->prog = new spg_program;
+        std::memcpy(p->prog, desc->program, sizeof(spg_program));
+        if (p->prog->magic != SPG_MAGIC) fail(SPTTN_EINVAL, "bad program magic");
+        if (p->prog->csf_order != D.order) fail(SPTTN_EINVAL, "sparse tensor order mismatch");
+        for (int f = 0; f < p->nf; ++f)
+          if (p->fac_size[f] != p->prog->dense_size[f + 1])
+            fail(SPTTN_EINVAL, "dense tensor shape mismatch");
+        int64_t bytes = 0;
+        for (int b = 0; b < p->prog->num_buffers; ++b) bytes += p->prog->buffer_size[b] * 8;
+        if (bytes > desc->buffer_limit_bytes)
+          fail(SPTTN_ENOMEM, "intermediate buffers exceed the buffer byte limit");
+        break;
+      }
+      default:
+        fail(SPTTN_EINVAL, "unknown nest kind " + std::to_string(p->kind));
+    }
+
+    copy_factors(p, desc->factors, on_dev, s);
+    bool facs_aligned32 = true, facs_aligned16 = true;
+    for (int f = 0; f < p->nf; ++f) {
+      facs_aligned32 &= aligned(p->fac[f], 32);
+      facs_aligned16 &= aligned(p->fac[f], 16);
+    }
+
+    if (p->kind == SPTTN_NEST_GENERIC) {
+      p->out_count = p->prog->out_size;
+      dev_malloc(reinterpret_cast<void**>(&p->out), std::max<int64_t>(1, p->out_count) * 8);
+      const double* hp[16] = {nullptr};
+      for (int f = 0; f < p->nf; ++f) hp[f + 1] = p->fac[f];
+      dev_malloc(reinterpret_cast<void**>(&p->d_dense), sizeof(hp));
+      SPTTN_CUDA(cudaMemcpyAsync(p->d_dense, hp, sizeof(hp), cudaMemcpyHostToDevice, s));
+      spttn_dev::generic_prepare(*p->prog, D, p->gen, s);
+      if (p->prog->need_leaf_lookup && nnz > 0) {
+        dev_malloc(reinterpret_cast<void**>(&p->gen.leaf_keys), nnz * sizeof(int64_t));
+        dev_malloc(reinterpret_cast<void**>(&p->gen.leaf_pos), nnz * sizeof(int64_t));
+        p->gen.n_leaf_keys = nnz;
+        k_leaf_keys<<<static_cast<unsigned>((nnz + 255) / 256), 256, 0, s>>>(
+            D.view(), p->gen.d_prog, p->gen.leaf_keys, p->gen.leaf_pos);
+        SPTTN_CUDA(cudaGetLastError());
+      }
+      p->launches = 4;
+    } else {
+      const bool sparse_out = p->kind == SPTTN_NEST_TTTP3;
+      p->out_count = sparse_out ? nnz : D.dims[0] * tile;
+      dev_malloc(reinterpret_cast<void**>(&p->out), std::max<int64_t>(1, p->out_count) * 8);
+      const int sms = sm_count();
+      if (p->kind == SPTTN_NEST_TTMC3 || p->kind == SPTTN_NEST_TTMC4) {
+        const bool vu = (R % 2 == 0) && facs_aligned16;
+        const bool vv = p->kind == SPTTN_NEST_TTMC3 ? (S % 2 == 0 && facs_aligned16)
+                                                    : (S == 8 && facs_aligned32);
+        p->vec = (vu ? 1 : 0) | (vv ? 2 : 0);
+        const int seg_len = static_cast<int>(
+            env_int("SPTTN_SEG_LEN", p->kind == SPTTN_NEST_TTMC3 ? 16 : 8));
+        const int64_t units = D.level_size[1];
+        const int64_t warps = static_cast<int64_t>(sms) * 32 * 2;
+        int64_t chunk = env_int("SPTTN_CHUNK", 0);
+        if (chunk <= 0) chunk = std::clamp<int64_t>((units + warps - 1) / warps, 8, 1024);
+        spttn_dev::build_segments(D, 1, seg_len, chunk, p->dec, tile, s);
+      } else {
+        const int G = spttn_dev::group_lanes_for(static_cast<int>(R));
+        p->vec = (R % 4 == 0) && facs_aligned32 ? 1 : 0;
+        const int64_t groups = static_cast<int64_t>(sms) * (2048 / G) * 2;
+        int64_t chunk = env_int("SPTTN_CHUNK", 0);
+        if (chunk <= 0) chunk = std::clamp<int64_t>((nnz + groups - 1) / groups, 16, 4096);
+        spttn_dev::build_leaf_items(D, chunk, p->dec, sparse_out ? 0 : tile, s);
+      }
+      p->launches = 1 + (p->dec.n_split > 0) + (p->dec.n_absent > 0);
+    }
+    SPTTN_CUDA(cudaStreamSynchronize(s));
+    *out = p;
+    raw = nullptr;
+  });
+  if (rc != SPTTN_OK && raw) {
+    std::string keep = g_err;
+    spttn_plan_destroy(raw);
+    g_err = keep;
+  }
+  return rc;
+}
+
+int spttn_plan_set_factors(spttn_plan* p, const double* const* factors, int32_t on_device,
+                           void* stream) {
+  return guarded([&] {
+    if (!p) fail(SPTTN_EINVAL, "null plan");
+    if (on_device && p->own_fac) fail(SPTTN_EINVAL, "plan owns its factor copies; pass host arrays");
+    if (!on_device && !p->own_fac) fail(SPTTN_EINVAL, "plan uses device factors; pass device arrays");
+    copy_factors(p, factors, on_device != 0, as_stream(stream));
+    if (p->kind == SPTTN_NEST_GENERIC && on_device) {
+      const double* hp[16] = {nullptr};
+      for (int f = 0; f < p->nf; ++f) hp[f + 1] = p->fac[f];
+      SPTTN_CUDA(cudaMemcpyAsync(p->d_dense, hp, sizeof(hp), cudaMemcpyHostToDevice,
+                                 as_stream(stream)));
+    }
+  });
+}
+
+int spttn_execute(spttn_plan* p, void* stream) {
+  return guarded([&] {
+    if (!p) fail(SPTTN_EINVAL, "null plan");
+    cudaStream_t s = as_stream(stream);
+    const auto& D = p->csf->d;
+    if (p->kind == SPTTN_NEST_GENERIC) {
+      spttn_dev::generic_execute(*p->prog, D, p->d_dense, p->out, p->gen, s);
+      return;
+    }
+    spttn_dev::RootOutArgs a{};
+    a.t = D.view();
+    a.R = static_cast<int>(p->R);
+    a.S = static_cast<int>(p->S);
+    a.T = static_cast<int>(p->T);
+    a.vec = p->vec;
+    a.item_pos = p->dec.item_pos;
+    a.n_items = p->dec.n_items;
+    a.chunk = p->dec.chunk;
+    a.out = p->out;
+    a.part = p->dec.part;
+    a.flags = (p->flags & SPTTN_FLAG_RESIDUAL) ? 1 : 0;
+    a.seg_begin = p->dec.seg_begin;
+    a.seg_node = p->dec.seg_node;
+    a.slice_seg = p->dec.slice_seg;
+    a.n_seg = p->dec.n_seg;
+    switch (p->kind) {
+      case SPTTN_NEST_MTTKRP3:
+        a.f[1] = p->fac[0];
+        a.f[2] = p->fac[1];
+        spttn_dev::launch_mttkrp3(a, s);
+        break;
+      case SPTTN_NEST_MTTKRP4:
+        a.f[1] = p->fac[0];
+        a.f[2] = p->fac[1];
+        a.f[3] = p->fac[2];
+        spttn_dev::launch_mttkrp4(a, s);
+        break;
+      case SPTTN_NEST_TTTP3:
+        a.f[0] = p->fac[0];
+        a.f[1] = p->fac[1];
+        a.f[2] = p->fac[2];
+        spttn_dev::launch_tttp3(a, s);
+        break;
+      case SPTTN_NEST_TTMC3:
+        a.f[1] = p->fac[0];
+        a.f[2] = p->fac[1];
+        spttn_dev::launch_ttmc3(a, s);
+        break;
+      case SPTTN_NEST_TTMC4:
+        a.f[1] = p->fac[0];
+        a.f[2] = p->fac[1];
+        a.f[3] = p->fac[2];
+        spttn_dev::launch_ttmc4(a, s);
+        break;
+    }
+    if (p->kind != SPTTN_NEST_TTTP3) spttn_dev::launch_fixup(p->dec, a.t, p->out, s);
+  });
+}
+
+int64_t spttn_output_count(const spttn_plan* p) { return p ? p->out_count : -1; }
+const double* spttn_output_device(const spttn_plan* p) { return p ? p->out : nullptr; }
+
+int spttn_read_output(spttn_plan* p, double* host_out, int64_t count, void* stream) {
+  return guarded([&] {
+    if (!p || (!host_out && count)) fail(SPTTN_EINVAL, "null argument");
+    if (count != p->out_count) fail(SPTTN_EINVAL, "output count mismatch");
+    cudaStream_t s = as_stream(stream);
+    if (count)
+      SPTTN_CUDA(cudaMemcpyAsync(host_out, p->out, count * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (p->kind == SPTTN_NEST_GENERIC) {
+      int64_t madds = 0;
+      SPTTN_CUDA(cudaMemcpyAsync(&madds, p->gen.counters, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      SPTTN_CUDA(cudaStreamSynchronize(s));
+      p->last_madds = madds;
+    }
+    SPTTN_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int spttn_plan_info(const spttn_plan* p, int64_t* out, int n) {
+  return guarded([&] {
+    if (!p) fail(SPTTN_EINVAL, "null plan");
+    const int64_t v[8] = {p->launches,   p->dec.n_items, p->dec.n_split, p->dec.n_absent,
+                          p->dec.n_items * 2 * p->dec.tile * 8,
+                          p->kind,        p->dec.n_seg,   p->kind == SPTTN_NEST_GENERIC ? p->last_madds : -1};
+    for (int i = 0; i < n && i < 8; ++i) out[i] = v[i];
+  });
+}
+
+int spttn_generic_resets(const spttn_plan* p, int64_t* out, int n) {
+  return guarded([&] {
+    if (!p || p->kind != SPTTN_NEST_GENERIC) fail(SPTTN_EINVAL, "not a GENERIC plan");
+    const int nb = p->prog->num_buffers;
+    std::vector<int64_t> h(nb + 3);
+    SPTTN_CUDA(cudaMemcpy(h.data(), p->gen.counters, (nb + 3) * sizeof(int64_t),
+                          cudaMemcpyDeviceToHost));
+    for (int b = 0; b < n && b < nb; ++b) out[b] = h[1 + b];
+    if (h[2 + nb]) fail(SPTTN_ENOMEM, "observer log overflowed");
+  });
+}
+
+int64_t spttn_generic_log_bytes(const spttn_plan* p) {
+  if (!p || p->kind != SPTTN_NEST_GENERIC || !p->prog->observe) return 0;
+  int64_t cur = 0;
+  if (cudaMemcpy(&cur, p->gen.counters + 1 + p->prog->num_buffers, sizeof(int64_t),
+                 cudaMemcpyDeviceToHost) != cudaSuccess)
+    return -1;
+  return cur;
+}
+
+int spttn_generic_read_log(spttn_plan* p, void* host_out, int64_t bytes, void* stream) {
+  return guarded([&] {
+    if (!p || p->kind != SPTTN_NEST_GENERIC) fail(SPTTN_EINVAL, "not a GENERIC plan");
+    if (bytes > p->gen.log_bytes) fail(SPTTN_EINVAL, "log read beyond capacity");
+    if (bytes > 0)
+      SPTTN_CUDA(cudaMemcpyAsync(host_out, p->gen.log, bytes, cudaMemcpyDeviceToHost,
+                                 as_stream(stream)));
+    SPTTN_CUDA(cudaStreamSynchronize(as_stream(stream)));
+  });
+}
+
+int spttn_unfactorized(const spttn_unfact_desc* desc, spttn_csf* csf, double* host_out,
+                       int64_t out_count, void* stream) {
+  std::vector<double*> tmp;
+  double* dout = nullptr;
+  const int rc = guarded([&] {
+    if (!desc || !csf) fail(SPTTN_EINVAL, "null argument");
+    cudaStream_t s = as_stream(stream);
+    if (desc->num_factors < 0 || desc->num_factors > 8) fail(SPTTN_EINVAL, "bad factor count");
+    const double* dptr[8] = {nullptr};
+    for (int f = 0; f < desc->num_factors; ++f) {
+      int64_t n = 1;
+      for (int k = 0; k < desc->factor_order[f]; ++k) n *= desc->dims[desc->factor_ids[f][k]];
+      double* d = nullptr;
+      dev_malloc(reinterpret_cast<void**>(&d), n * sizeof(double));
+      tmp.push_back(d);
+      SPTTN_CUDA(cudaMemcpyAsync(d, desc->factors[f], n * sizeof(double), cudaMemcpyHostToDevice, s));
+      dptr[f] = d;
+    }
+    dev_malloc(reinterpret_cast<void**>(&dout), std::max<int64_t>(1, out_count) * sizeof(double));
+    spttn_dev::unfactorized_run(desc, csf->d, dptr, dout, out_count, s);
+    if (out_count)
+      SPTTN_CUDA(cudaMemcpyAsync(host_out, dout, out_count * sizeof(double), cudaMemcpyDeviceToHost, s));
+    SPTTN_CUDA(cudaStreamSynchronize(s));
+  });
+  for (double* d : tmp) cudaFree(d);
+  cudaFree(dout);
+  return rc;
+}
+
+}  // extern "C"

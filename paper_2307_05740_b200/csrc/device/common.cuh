@@ -1,0 +1,109 @@
+// Shared device helpers for the sm_100a SpTTN kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+namespace spttn_dev {
+
+// Status exception used inside the C-ABI implementation; converted to a
+// status code + message at the extern "C" boundary (capi.cu).
+struct Status : std::runtime_error {
+  int code;
+  Status(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define SPTTN_CUDA(call)                                                                 \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      throw ::spttn_dev::Status(4, std::string(#call ": ") + cudaGetErrorString(e_));    \
+  } while (0)
+
+constexpr int kWarp = 32;
+
+__device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+__device__ __forceinline__ double4 ld256(const double* p) {
+  double4 v;
+  asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+               : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ double2 ld128(const double* p) {
+  double2 v;
+  asm volatile("ld.global.nc.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ int ldg_i32(const int32_t* p) { return __ldg(p); }
+__device__ __forceinline__ double ldg_f64(const double* p) { return __ldg(p); }
+
+// fp64 tensor-core MMA (SASS: DMMA.8x8x4). Fragment layout, lane L:
+//   A (8x4, row-major):  a = A[L/4][L%4]
+//   B (4x8, col-major):  b = B[L%4][L/4]
+//   C/D (8x8):           d0 = D[L/4][2(L%4)], d1 = D[L/4][2(L%4)+1]
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// Row slice of 4 consecutive doubles starting at column c of a row of
+// length R; columns >= R read as zero. VEC requires R % 4 == 0 and a
+// 32-byte aligned base (checked on the host).
+template <bool VEC>
+__device__ __forceinline__ double4 row4(const double* row, int c, int R) {
+  if (VEC) {
+    if (c < R) return ld256(row + c);
+    return make_double4(0, 0, 0, 0);
+  } else {
+    double4 v;
+    v.x = c + 0 < R ? __ldg(row + c + 0) : 0.0;
+    v.y = c + 1 < R ? __ldg(row + c + 1) : 0.0;
+    v.z = c + 2 < R ? __ldg(row + c + 2) : 0.0;
+    v.w = c + 3 < R ? __ldg(row + c + 3) : 0.0;
+    return v;
+  }
+}
+
+template <bool VEC>
+__device__ __forceinline__ double2 row2(const double* row, int c, int R) {
+  if (VEC) {
+    if (c < R) return ld128(row + c);
+    return make_double2(0, 0);
+  } else {
+    double2 v;
+    v.x = c + 0 < R ? __ldg(row + c + 0) : 0.0;
+    v.y = c + 1 < R ? __ldg(row + c + 1) : 0.0;
+    return v;
+  }
+}
+
+__device__ __forceinline__ void fma4(double4& acc, double s, const double4& v) {
+  acc.x = fma(s, v.x, acc.x);
+  acc.y = fma(s, v.y, acc.y);
+  acc.z = fma(s, v.z, acc.z);
+  acc.w = fma(s, v.w, acc.w);
+}
+
+__device__ __forceinline__ void fma4v(double4& acc, const double4& a, const double4& b) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.y = fma(a.y, b.y, acc.y);
+  acc.z = fma(a.z, b.z, acc.z);
+  acc.w = fma(a.w, b.w, acc.w);
+}
+
+__device__ __forceinline__ void store4(double* row, int c, int R, const double4& v) {
+  if (c + 0 < R) row[c + 0] = v.x;
+  if (c + 1 < R) row[c + 1] = v.y;
+  if (c + 2 < R) row[c + 2] = v.z;
+  if (c + 3 < R) row[c + 3] = v.w;
+}
+
+}  // namespace spttn_dev

@@ -1,0 +1,265 @@
+// Plan-time work decomposition (built once per plan on the device) and the
+// deterministic fix-up epilogue for root slices split across work items.
+#include <cub/cub.cuh>
+
+#include "internal.cuh"
+
+namespace spttn_dev {
+
+namespace {
+
+// Largest node n in [0, count) with ptr[n] <= key (ptr ascending).
+__device__ __forceinline__ int32_t parent_of(const int32_t* ptr, int32_t count, int32_t key) {
+  int32_t lo = 0, hi = count;  // invariant: ptr[lo] <= key, answer in [lo, hi)
+  while (hi - lo > 1) {
+    const int32_t mid = (lo + hi) >> 1;
+    if (ptr[mid] <= key) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void k_leaf_items(CsfView t, int64_t chunk, int64_t n_items, int32_t* item_pos) {
+  const int64_t it = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (it >= n_items) return;
+  const int d = t.order;
+  int32_t pos = static_cast<int32_t>(it * chunk);
+  item_pos[it * d + d - 1] = pos;
+  for (int l = d - 2; l >= 0; --l) {
+    pos = parent_of(t.ptr[l], t.nlev[l], pos);
+    item_pos[it * d + l] = pos;
+  }
+}
+
+// Root slices whose leaves span more than one item.
+__global__ void k_leaf_splits(CsfView t, int64_t chunk, int32_t* node, int32_t* first,
+                              int32_t* last, int32_t* count, unsigned char* present) {
+  const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= t.nlev[0]) return;
+  int32_t a = s, b = s + 1;
+  for (int l = 0; l + 1 < t.order; ++l) {
+    a = t.ptr[l][a];
+    b = t.ptr[l][b];
+  }
+  const int64_t f = a / chunk, g = (static_cast<int64_t>(b) - 1) / chunk;
+  if (f != g) {
+    const int32_t slot = atomicAdd(count, 1);
+    node[slot] = s;
+    first[slot] = static_cast<int32_t>(f);
+    last[slot] = static_cast<int32_t>(g);
+  }
+  present[t.idx[0][s]] = 1;
+}
+
+__global__ void k_absent(const unsigned char* present, int64_t dim0, int32_t* rows,
+                         int32_t* count) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= dim0) return;
+  if (!present[i]) rows[atomicAdd(count, 1)] = static_cast<int32_t>(i);
+}
+
+// Segment counts per unit node: ceil(children / seg_len).
+__global__ void k_seg_count(CsfView t, int unit_level, int seg_len, int32_t* cnt) {
+  const int32_t f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= t.nlev[unit_level]) return;
+  const int32_t n = t.ptr[unit_level][f + 1] - t.ptr[unit_level][f];
+  cnt[f] = (n + seg_len - 1) / seg_len;
+}
+
+__global__ void k_seg_fill(CsfView t, int unit_level, int seg_len, const int32_t* off,
+                           int32_t* seg_begin, int32_t* seg_node) {
+  const int32_t f = blockIdx.x * blockDim.x + threadIdx.x;
+  const int32_t nf = t.nlev[unit_level];
+  if (f >= nf) return;
+  const int32_t b = t.ptr[unit_level][f], e = t.ptr[unit_level][f + 1];
+  const int32_t coord = t.idx[unit_level][f];
+  int32_t o = off[f];
+  for (int32_t x = b; x < e; x += seg_len, ++o) {
+    seg_begin[o] = x;
+    seg_node[o] = coord;
+  }
+  if (f == nf - 1) seg_begin[o] = e;
+}
+
+// slice_seg[s] = first segment of root slice s (unit_level == 1).
+__global__ void k_slice_seg(CsfView t, const int32_t* off, int32_t* slice_seg) {
+  const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s > t.nlev[0]) return;
+  slice_seg[s] = off[t.ptr[0][s]];
+}
+
+__global__ void k_seg_items(const int32_t* slice_seg, int32_t n0, int64_t chunk, int64_t n_items,
+                            int32_t* item_pos) {
+  const int64_t w = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (w >= n_items) return;
+  item_pos[w] = parent_of(slice_seg, n0, static_cast<int32_t>(w * chunk));
+}
+
+__global__ void k_seg_splits(CsfView t, const int32_t* slice_seg, int64_t chunk, int32_t* node,
+                             int32_t* first, int32_t* last, int32_t* count,
+                             unsigned char* present) {
+  const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= t.nlev[0]) return;
+  const int64_t f = slice_seg[s] / chunk, g = (static_cast<int64_t>(slice_seg[s + 1]) - 1) / chunk;
+  if (f != g) {
+    const int32_t slot = atomicAdd(count, 1);
+    node[slot] = s;
+    first[slot] = static_cast<int32_t>(f);
+    last[slot] = static_cast<int32_t>(g);
+  }
+  present[t.idx[0][s]] = 1;
+}
+
+// One block per split slice: TAIL of its first item + HEADs of the later
+// items, summed in item order (deterministic).
+__global__ void k_fixup(const int32_t* node, const int32_t* first, const int32_t* last,
+                        const int32_t* idx0, const double* part, int64_t tile, double* out) {
+  const int32_t sidx = blockIdx.x;
+  const int32_t f = first[sidx], g = last[sidx];
+  const int64_t row = idx0[node[sidx]];
+  for (int64_t e = threadIdx.x; e < tile; e += blockDim.x) {
+    double sum = part[(static_cast<int64_t>(f) * 2 + 1) * tile + e];
+    for (int32_t it = f + 1; it <= g; ++it) sum += part[(static_cast<int64_t>(it) * 2) * tile + e];
+    out[row * tile + e] = sum;
+  }
+}
+
+__global__ void k_zero_rows(const int32_t* rows, int64_t n, int64_t tile, double* out) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= n * tile) return;
+  out[static_cast<int64_t>(rows[e / tile]) * tile + e % tile] = 0.0;
+}
+
+unsigned blocks_for(int64_t n, int b) { return static_cast<unsigned>((n + b - 1) / b); }
+
+void find_splits_and_absent(const DevCsf& csf, Decomp& d, bool segments, cudaStream_t s) {
+  const CsfView t = csf.view();
+  const int32_t n0 = static_cast<int32_t>(csf.level_size[0]);
+  int32_t* counts = nullptr;
+  unsigned char* present = nullptr;
+  SPTTN_CUDA(cudaMallocAsync(&counts, 2 * sizeof(int32_t), s));
+  SPTTN_CUDA(cudaMemsetAsync(counts, 0, 2 * sizeof(int32_t), s));
+  SPTTN_CUDA(cudaMallocAsync(&present, csf.dims[0], s));
+  SPTTN_CUDA(cudaMemsetAsync(present, 0, csf.dims[0], s));
+  const int64_t nsplit_cap = n0 > 0 ? n0 : 1;
+  SPTTN_CUDA(cudaMalloc(&d.split_node, nsplit_cap * sizeof(int32_t)));
+  SPTTN_CUDA(cudaMalloc(&d.split_first, nsplit_cap * sizeof(int32_t)));
+  SPTTN_CUDA(cudaMalloc(&d.split_last, nsplit_cap * sizeof(int32_t)));
+  SPTTN_CUDA(cudaMalloc(&d.absent_rows, csf.dims[0] * sizeof(int32_t)));
+  if (n0 > 0) {
+    if (segments)
+      k_seg_splits<<<blocks_for(n0, 256), 256, 0, s>>>(t, d.slice_seg, d.chunk, d.split_node,
+                                                       d.split_first, d.split_last, counts,
+                                                       present);
+    else
+      k_leaf_splits<<<blocks_for(n0, 256), 256, 0, s>>>(t, d.chunk, d.split_node, d.split_first,
+                                                        d.split_last, counts, present);
+    SPTTN_CUDA(cudaGetLastError());
+  }
+  k_absent<<<blocks_for(csf.dims[0], 256), 256, 0, s>>>(present, csf.dims[0], d.absent_rows,
+                                                          counts + 1);
+  SPTTN_CUDA(cudaGetLastError());
+  int32_t h[2] = {0, 0};
+  SPTTN_CUDA(cudaMemcpyAsync(h, counts, sizeof(h), cudaMemcpyDeviceToHost, s));
+  SPTTN_CUDA(cudaStreamSynchronize(s));
+  d.n_split = h[0];
+  d.n_absent = h[1];
+  SPTTN_CUDA(cudaFreeAsync(counts, s));
+  SPTTN_CUDA(cudaFreeAsync(present, s));
+}
+
+}  // namespace
+
+void build_leaf_items(const DevCsf& csf, int64_t chunk, Decomp& d, int64_t tile, cudaStream_t s) {
+  const int64_t nnz = csf.level_size[csf.order - 1];
+  d.chunk = chunk;
+  d.tile = tile;
+  d.n_items = (nnz + chunk - 1) / chunk;
+  const CsfView t = csf.view();
+  SPTTN_CUDA(cudaMalloc(&d.item_pos, std::max<int64_t>(1, d.n_items * csf.order) * sizeof(int32_t)));
+  if (d.n_items > 0) {
+    k_leaf_items<<<blocks_for(d.n_items, 256), 256, 0, s>>>(t, chunk, d.n_items, d.item_pos);
+    SPTTN_CUDA(cudaGetLastError());
+  }
+  if (tile > 0) {  // dense root-indexed output
+    SPTTN_CUDA(cudaMalloc(&d.part, std::max<int64_t>(1, d.n_items * 2 * tile) * sizeof(double)));
+    find_splits_and_absent(csf, d, false, s);
+  }
+}
+
+void build_segments(const DevCsf& csf, int unit_level, int seg_len, int64_t chunk, Decomp& d,
+                    int64_t tile, cudaStream_t s) {
+  const CsfView t = csf.view();
+  const int32_t nf = static_cast<int32_t>(csf.level_size[unit_level]);
+  const int32_t n0 = static_cast<int32_t>(csf.level_size[0]);
+  d.seg_len = seg_len;
+  d.chunk = chunk;
+  d.tile = tile;
+  int32_t* off = nullptr;
+  SPTTN_CUDA(cudaMallocAsync(&off, (static_cast<int64_t>(nf) + 1) * sizeof(int32_t), s));
+  SPTTN_CUDA(cudaMemsetAsync(off, 0, (static_cast<int64_t>(nf) + 1) * sizeof(int32_t), s));
+  if (nf > 0) {
+    k_seg_count<<<blocks_for(nf, 256), 256, 0, s>>>(t, unit_level, seg_len, off);
+    SPTTN_CUDA(cudaGetLastError());
+  }
+  size_t temp_bytes = 0;
+  SPTTN_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp_bytes, off, off, nf + 1, s));
+  void* temp = nullptr;
+  SPTTN_CUDA(cudaMallocAsync(&temp, temp_bytes, s));
+  SPTTN_CUDA(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, off, off, nf + 1, s));
+  SPTTN_CUDA(cudaFreeAsync(temp, s));
+  int32_t nseg = 0;
+  SPTTN_CUDA(cudaMemcpyAsync(&nseg, off + nf, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  SPTTN_CUDA(cudaStreamSynchronize(s));
+  d.n_seg = nseg;
+  SPTTN_CUDA(cudaMalloc(&d.seg_begin, (static_cast<int64_t>(nseg) + 1) * sizeof(int32_t)));
+  SPTTN_CUDA(cudaMalloc(&d.seg_node, std::max<int64_t>(1, nseg) * sizeof(int32_t)));
+  SPTTN_CUDA(cudaMalloc(&d.slice_seg, (static_cast<int64_t>(n0) + 1) * sizeof(int32_t)));
+  SPTTN_CUDA(cudaMemsetAsync(d.seg_begin, 0, sizeof(int32_t), s));
+  if (nf > 0) {
+    k_seg_fill<<<blocks_for(nf, 256), 256, 0, s>>>(t, unit_level, seg_len, off, d.seg_begin,
+                                                   d.seg_node);
+    SPTTN_CUDA(cudaGetLastError());
+  }
+  // unit_level is 1 for both TTMc kernels: slices own contiguous unit nodes.
+  k_slice_seg<<<blocks_for(static_cast<int64_t>(n0) + 1, 256), 256, 0, s>>>(t, off, d.slice_seg);
+  SPTTN_CUDA(cudaGetLastError());
+  SPTTN_CUDA(cudaFreeAsync(off, s));
+  d.n_items = (nseg + chunk - 1) / chunk;
+  SPTTN_CUDA(cudaMalloc(&d.item_pos, std::max<int64_t>(1, d.n_items) * sizeof(int32_t)));
+  if (d.n_items > 0) {
+    k_seg_items<<<blocks_for(d.n_items, 256), 256, 0, s>>>(d.slice_seg, n0, chunk, d.n_items,
+                                                          d.item_pos);
+    SPTTN_CUDA(cudaGetLastError());
+  }
+  SPTTN_CUDA(cudaMalloc(&d.part, std::max<int64_t>(1, d.n_items * 2 * tile) * sizeof(double)));
+  find_splits_and_absent(csf, d, true, s);
+}
+
+void launch_fixup(const Decomp& d, const CsfView& t, double* out, cudaStream_t s) {
+  if (d.n_split > 0) {
+    const int threads = d.tile >= 256 ? 256 : (d.tile >= 64 ? 64 : 32);
+    k_fixup<<<static_cast<unsigned>(d.n_split), threads, 0, s>>>(
+        d.split_node, d.split_first, d.split_last, t.idx[0], d.part, d.tile, out);
+    SPTTN_CUDA(cudaGetLastError());
+  }
+  if (d.n_absent > 0) {
+    k_zero_rows<<<blocks_for(d.n_absent * d.tile, 256), 256, 0, s>>>(d.absent_rows, d.n_absent,
+                                                                     d.tile, out);
+    SPTTN_CUDA(cudaGetLastError());
+  }
+}
+
+void free_decomp(Decomp& d) {
+  cudaFree(d.item_pos);
+  cudaFree(d.part);
+  cudaFree(d.split_node);
+  cudaFree(d.split_first);
+  cudaFree(d.split_last);
+  cudaFree(d.absent_rows);
+  cudaFree(d.seg_begin);
+  cudaFree(d.seg_node);
+  cudaFree(d.slice_seg);
+  d = Decomp{};
+}
+
+}  // namespace spttn_dev

@@ -1,0 +1,429 @@
+// GENERIC device forest interpreter and the device execute_unfactorized.
+//
+// The interpreter runs any admissible fused loop forest (every order the
+// reference planner can emit, including sparse-output nests that iterate
+// modes densely) on the GPU. It walks the serialized program exactly like the
+// reference's exec_node / exec_leaf / exec_hook (proj/src/executor.cpp:
+// 389-490): same loop order, same reset points, same hook arithmetic, so the
+// floating-point results are bit-identical to the reference and the
+// multiply-add / reset counters are counted, not estimated. It is the
+// coverage path (one device thread per plan; the pinned nests have dedicated
+// kernels), used for non-pinned orders and small ranks.
+//
+// The unfactorized oracle (executor.cpp:522-626) runs one thread per output
+// entry (dense output) or per leaf (sparse output); each thread accumulates
+// its entry's contributions in the reference's order, so it is deterministic
+// and bit-identical as well.
+#include "../../../include/spttn_b200.h"
+#include "internal.cuh"
+
+namespace spttn_dev {
+
+namespace {
+
+struct Interp {
+  const spg_program* P;
+  CsfView t;
+  const double* const* dense;
+  double* out;
+  double* bufs;
+  const int64_t* boff;
+  int64_t* counters;
+  unsigned char* log;
+  int64_t log_cap;
+  const int64_t* leaf_keys;
+  const int64_t* leaf_pos;
+  int64_t nkeys;
+  int64_t ival[SPG_MAX_IDX];
+  int64_t pos[SPG_MAX_LEVELS];
+  int64_t madds;
+
+  __device__ int64_t offset(const spg_access& a) const {
+    int64_t off = 0;
+    for (int k = 0; k < a.naddr; ++k) off += ival[a.ids[k]] * a.strides[k];
+    return off;
+  }
+  __device__ double* base(const spg_access& a) const {
+    switch (a.kind) {
+      case SPG_OP_DENSE: return const_cast<double*>(dense[a.slot]);
+      case SPG_OP_BUFFER: return bufs + boff[a.slot];
+      case SPG_OP_OUT_DENSE: return out;
+      default: return nullptr;
+    }
+  }
+  __device__ double read(const spg_access& a) const {
+    if (a.kind == SPG_OP_SPARSE) return t.vals[pos[t.order - 1]];
+    if (a.kind == SPG_OP_OUT_SPARSE) return 0.0;
+    return base(a)[offset(a)];
+  }
+
+  __device__ void leaf(int term) {
+    const double v = read(P->lhs[term]) * read(P->rhs[term]);
+    madds += 2;
+    const spg_access& o = P->out[term];
+    if (o.kind == SPG_OP_OUT_SPARSE) {
+      if (P->need_leaf_lookup) {
+        int64_t key = 0;
+        for (int l = 0; l < t.order; ++l) key += ival[P->sparse_mode_ids[l]] * P->mode_key_stride[l];
+        int64_t lo = 0, hi = nkeys;
+        while (lo < hi) {
+          const int64_t mid = (lo + hi) >> 1;
+          if (leaf_keys[mid] < key) lo = mid + 1; else hi = mid;
+        }
+        // off-pattern coordinates only produce exact zeros (executor.cpp:400)
+        if (lo < nkeys && leaf_keys[lo] == key) out[leaf_pos[lo]] += v;
+      } else {
+        out[pos[t.order - 1]] += v;
+      }
+      return;
+    }
+    base(o)[offset(o)] += v;
+  }
+
+  __device__ void hook(const spg_hook& h) {
+    const int term = h.term;
+    for (int k = 0; k < h.nspan; ++k) ival[h.span[k]] = 0;
+    const spg_access& lhs = P->lhs[term];
+    const spg_access& rhs = P->rhs[term];
+    const spg_access& o = P->out[term];
+    double* y = base(o) + offset(o);
+    if (h.kind == SPG_HOOK_VEC) {
+      const spg_access& vec = h.vec_is_lhs ? lhs : rhs;
+      const spg_access& sca = h.vec_is_lhs ? rhs : lhs;
+      const double alpha = read(sca);
+      const double* x = base(vec) + offset(vec);
+      // scaled_vector_accumulate (micro_kernels.hpp:11-14)
+      for (int64_t i = 0; i < h.len; ++i) y[i * h.out_inc] += alpha * x[i * h.vec_inc];
+      madds += 2 * h.len;
+      return;
+    }
+    const spg_access& xa = h.x_is_lhs ? lhs : rhs;
+    const spg_access& ya = h.x_is_lhs ? rhs : lhs;
+    const double* x = base(xa) + offset(xa);
+    const double* yv = base(ya) + offset(ya);
+    // rank1_update (micro_kernels.hpp:17-23)
+    for (int64_t i = 0; i < h.m; ++i) {
+      const double xi = x[i * h.x_inc];
+      for (int64_t j = 0; j < h.n; ++j) y[i * h.out_row + j * h.out_col] += xi * yv[j * h.y_inc];
+    }
+    madds += 2 * h.m * h.n;
+  }
+
+  __device__ void resets(const spg_node& nd) {
+    for (int r = 0; r < nd.reset_count; ++r) {
+      const int b = P->resets[nd.reset_begin + r];
+      double* buf = bufs + boff[b];
+      const int64_t n = P->buffer_size[b];
+      for (int64_t i = 0; i < n; ++i) buf[i] = 0.0;
+      counters[1 + b] += 1;
+      if (P->observe) {
+        int64_t* cursor = &counters[1 + P->num_buffers];
+        const int64_t need = 16 + 8 * n;
+        if (*cursor + need > log_cap) {
+          counters[2 + P->num_buffers] = 1;  // overflow
+        } else {
+          int64_t* hdr = reinterpret_cast<int64_t*>(log + *cursor);
+          hdr[0] = b;
+          hdr[1] = n;
+          double* dst = reinterpret_cast<double*>(hdr + 2);
+          for (int64_t i = 0; i < n; ++i) dst[i] = buf[i];
+          *cursor += need;
+        }
+      }
+    }
+  }
+};
+
+struct Frame {
+  int node;
+  int child;
+  int64_t it, end;
+};
+
+__device__ void set_iter(Interp& I, const spg_node& nd, int64_t it) {
+  if (nd.kind == SPG_SPARSE) {
+    I.pos[nd.csf_level] = it;
+    I.ival[nd.index] = I.t.idx[nd.csf_level][it];
+  } else {
+    I.ival[nd.index] = it;
+  }
+}
+
+__global__ void k_generic(Interp I) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  const spg_program* P = I.P;
+  for (int k = 0; k < SPG_MAX_IDX; ++k) I.ival[k] = 0;
+  for (int k = 0; k < SPG_MAX_LEVELS; ++k) I.pos[k] = 0;
+  I.madds = 0;
+  Frame st[SPG_MAX_IDX + 2];
+  int sp = 0;
+  for (int ri = 0; ri < P->num_roots; ++ri) {
+    // enter(root) then run the frame stack
+    int pending = P->roots[ri];
+    for (;;) {
+      if (pending >= 0) {
+        const spg_node& nd = P->nodes[pending];
+        I.resets(nd);
+        if (nd.kind == SPG_LEAF) {
+          I.leaf(nd.term);
+        } else if (nd.hook >= 0) {
+          I.hook(P->hooks[nd.hook]);
+        } else {
+          int64_t lo = 0, hi = 0;
+          if (nd.kind == SPG_SPARSE) {
+            if (nd.csf_level == 0) {
+              hi = I.t.nlev[0];
+            } else {
+              lo = I.t.ptr[nd.csf_level - 1][I.pos[nd.csf_level - 1]];
+              hi = I.t.ptr[nd.csf_level - 1][I.pos[nd.csf_level - 1] + 1];
+            }
+          } else {
+            hi = P->dims[nd.index];
+          }
+          if (lo < hi) {
+            st[sp++] = Frame{pending, 0, lo, hi};
+            set_iter(I, nd, lo);
+          }
+        }
+        pending = -1;
+      }
+      if (sp == 0) break;
+      Frame& f = st[sp - 1];
+      const spg_node& fn = P->nodes[f.node];
+      if (f.child < fn.child_count) {
+        pending = P->children[fn.child_begin + f.child];
+        ++f.child;
+        continue;
+      }
+      ++f.it;
+      if (f.it < f.end) {
+        f.child = 0;
+        set_iter(I, fn, f.it);
+      } else {
+        --sp;
+      }
+    }
+  }
+  I.counters[0] = I.madds;
+}
+
+// ---- unfactorized ---------------------------------------------------------
+
+struct Unf {
+  spttn_unfact_desc d;
+  CsfView t;
+  const double* dense[8];
+  double* out;
+  int64_t out_count;
+};
+
+__device__ double unf_body(const Unf& u, const int64_t* ival, int64_t leaf) {
+  double v = u.t.vals[leaf];
+  for (int f = 0; f < u.d.num_factors; ++f) {
+    int64_t off = 0;
+    for (int k = 0; k < u.d.factor_order[f]; ++k) {
+      const int id = u.d.factor_ids[f][k];
+      off = off * u.d.dims[id] + ival[id];
+    }
+    v *= u.dense[f][off];
+  }
+  return v;
+}
+
+// Dense output: one thread per output entry; walks the CSF in order and the
+// non-output free indices in first-appearance order.
+__global__ void k_unf_dense(Unf u) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= u.out_count) return;
+  int64_t ival[32];
+  for (int k = 0; k < 32; ++k) ival[k] = 0;
+  bool fixed[32];
+  for (int k = 0; k < 32; ++k) fixed[k] = false;
+  int64_t rest = e;
+  for (int q = u.d.out_order - 1; q >= 0; --q) {
+    const int id = u.d.out_ids[q];
+    ival[id] = rest % u.d.dims[id];
+    rest /= u.d.dims[id];
+    fixed[id] = true;
+  }
+  // non-output free indices, in first-appearance order
+  int loop_ids[32];
+  int nloop = 0;
+  int64_t loop_total = 1;
+  for (int q = 0; q < u.d.num_free; ++q) {
+    const int id = u.d.free_ids[q];
+    if (!fixed[id]) {
+      loop_ids[nloop++] = id;
+      loop_total *= u.d.dims[id];
+    }
+  }
+  const int d = u.t.order;
+  // root restriction when the output carries the level-0 mode
+  int64_t r_lo = 0, r_hi = u.t.nlev[0];
+  int root_id = -1;
+  for (int id = 0; id < u.d.num_indices; ++id)
+    if (u.d.csf_level[id] == 0) root_id = id;
+  if (root_id >= 0 && fixed[root_id]) {
+    int64_t lo = 0, hi = u.t.nlev[0];
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (u.t.idx[0][mid] < ival[root_id]) lo = mid + 1; else hi = mid;
+    }
+    if (lo < u.t.nlev[0] && u.t.idx[0][lo] == ival[root_id]) {
+      r_lo = lo;
+      r_hi = lo + 1;
+    } else {
+      u.out[e] = 0.0;
+      return;
+    }
+  }
+  int lvl_id[8];
+  for (int id = 0; id < u.d.num_indices; ++id)
+    if (u.d.csf_level[id] >= 0) lvl_id[u.d.csf_level[id]] = id;
+  double sum = 0.0;
+  int64_t pos[8], hi[8];
+  int lvl = 0;
+  pos[0] = r_lo;
+  hi[0] = r_hi;
+  while (true) {
+    if (pos[lvl] >= hi[lvl]) {
+      if (lvl == 0) break;
+      --lvl;
+      ++pos[lvl];
+      continue;
+    }
+    const int id = lvl_id[lvl];
+    const int64_t coord = u.t.idx[lvl][pos[lvl]];
+    if (fixed[id] && coord != ival[id]) {
+      ++pos[lvl];
+      continue;
+    }
+    ival[id] = coord;
+    if (lvl + 1 < d) {
+      pos[lvl + 1] = u.t.ptr[lvl][pos[lvl]];
+      hi[lvl + 1] = u.t.ptr[lvl][pos[lvl] + 1];
+      ++lvl;
+      continue;
+    }
+    for (int64_t f = 0; f < loop_total; ++f) {
+      int64_t r = f;
+      for (int q = nloop - 1; q >= 0; --q) {
+        ival[loop_ids[q]] = r % u.d.dims[loop_ids[q]];
+        r /= u.d.dims[loop_ids[q]];
+      }
+      sum += unf_body(u, ival, pos[lvl]);
+    }
+    ++pos[lvl];
+  }
+  u.out[e] = sum;
+}
+
+// Sparse output: one thread per leaf.
+__global__ void k_unf_sparse(Unf u, const int32_t* leaf_parent /* unused */) {
+  const int64_t leaf = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int d = u.t.order;
+  if (leaf >= u.t.nlev[d - 1]) return;
+  int64_t ival[32];
+  for (int k = 0; k < 32; ++k) ival[k] = 0;
+  int lvl_id[8];
+  for (int id = 0; id < u.d.num_indices; ++id)
+    if (u.d.csf_level[id] >= 0) lvl_id[u.d.csf_level[id]] = id;
+  // coordinates of the leaf: parent search level by level
+  int64_t node = leaf;
+  for (int l = d - 1; l >= 0; --l) {
+    ival[lvl_id[l]] = u.t.idx[l][node];
+    if (l > 0) {
+      int64_t lo = 0, hi = u.t.nlev[l - 1];
+      while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (u.t.ptr[l - 1][mid] <= node) lo = mid; else hi = mid;
+      }
+      node = lo;
+    }
+  }
+  int64_t total = 1;
+  for (int q = 0; q < u.d.num_free; ++q) total *= u.d.dims[u.d.free_ids[q]];
+  double sum = 0.0;
+  for (int64_t f = 0; f < total; ++f) {
+    int64_t r = f;
+    for (int q = u.d.num_free - 1; q >= 0; --q) {
+      const int id = u.d.free_ids[q];
+      ival[id] = r % u.d.dims[id];
+      r /= u.d.dims[id];
+    }
+    sum += unf_body(u, ival, leaf);
+  }
+  u.out[leaf] = sum;
+}
+
+}  // namespace
+
+void generic_prepare(const spg_program& prog, const DevCsf& csf, GenericState& g,
+                     cudaStream_t s) {
+  SPTTN_CUDA(cudaMalloc(&g.d_prog, sizeof(spg_program)));
+  SPTTN_CUDA(cudaMemcpyAsync(g.d_prog, &prog, sizeof(spg_program), cudaMemcpyHostToDevice, s));
+  std::vector<int64_t> off(prog.num_buffers + 1, 0);
+  for (int b = 0; b < prog.num_buffers; ++b) off[b + 1] = off[b] + prog.buffer_size[b];
+  g.total_buffer_elems = off[prog.num_buffers];
+  SPTTN_CUDA(cudaMalloc(&g.buffers, std::max<int64_t>(1, g.total_buffer_elems) * sizeof(double)));
+  SPTTN_CUDA(cudaMalloc(&g.buffer_off, (prog.num_buffers + 1) * sizeof(int64_t)));
+  SPTTN_CUDA(cudaMemcpyAsync(g.buffer_off, off.data(), off.size() * sizeof(int64_t),
+                             cudaMemcpyHostToDevice, s));
+  SPTTN_CUDA(cudaMalloc(&g.counters, (prog.num_buffers + 4) * sizeof(int64_t)));
+  g.log_bytes = prog.observe ? prog.observe_log_bytes : 0;
+  if (g.log_bytes > 0) SPTTN_CUDA(cudaMalloc(&g.log, g.log_bytes));
+  SPTTN_CUDA(cudaStreamSynchronize(s));
+}
+
+void generic_execute(const spg_program& prog, const DevCsf& csf, const double* const* dense,
+                     double* out, GenericState& g, cudaStream_t s) {
+  SPTTN_CUDA(cudaMemsetAsync(g.counters, 0, (prog.num_buffers + 4) * sizeof(int64_t), s));
+  SPTTN_CUDA(cudaMemsetAsync(g.buffers, 0,
+                             std::max<int64_t>(1, g.total_buffer_elems) * sizeof(double), s));
+  SPTTN_CUDA(cudaMemsetAsync(out, 0, std::max<int64_t>(1, prog.out_size) * sizeof(double), s));
+  Interp I{};
+  I.P = g.d_prog;
+  I.t = csf.view();
+  I.dense = dense;
+  I.out = out;
+  I.bufs = g.buffers;
+  I.boff = g.buffer_off;
+  I.counters = g.counters;
+  I.log = g.log;
+  I.log_cap = g.log_bytes;
+  I.leaf_keys = g.leaf_keys;
+  I.leaf_pos = g.leaf_pos;
+  I.nkeys = g.n_leaf_keys;
+  k_generic<<<1, 1, 0, s>>>(I);
+  SPTTN_CUDA(cudaGetLastError());
+}
+
+void generic_free(GenericState& g) {
+  cudaFree(g.d_prog);
+  cudaFree(g.buffers);
+  cudaFree(g.buffer_off);
+  cudaFree(g.counters);
+  cudaFree(g.log);
+  cudaFree(g.leaf_keys);
+  cudaFree(g.leaf_pos);
+  g = GenericState{};
+}
+
+void unfactorized_run(const void* desc, const DevCsf& csf, const double* const* dense,
+                      double* out, int64_t out_count, cudaStream_t s) {
+  Unf u{};
+  u.d = *static_cast<const spttn_unfact_desc*>(desc);
+  u.t = csf.view();
+  for (int f = 0; f < u.d.num_factors; ++f) u.dense[f] = dense[f];
+  u.out = out;
+  u.out_count = out_count;
+  if (out_count == 0) return;
+  const unsigned blocks = static_cast<unsigned>((out_count + 127) / 128);
+  if (u.d.out_sparse)
+    k_unf_sparse<<<blocks, 128, 0, s>>>(u, nullptr);
+  else
+    k_unf_dense<<<blocks, 128, 0, s>>>(u);
+  SPTTN_CUDA(cudaGetLastError());
+}
+
+}  // namespace spttn_dev

@@ -1,0 +1,138 @@
+// Internal device-side structures shared by the kernels and the C-ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+#include "common.cuh"
+#include "program.h"
+
+namespace spttn_dev {
+
+constexpr int kMaxOrder = 8;
+
+// Device CSF: SoA int32 coordinates / child pointers per level, fp64 leaf
+// values (cudaMalloc: 256-B aligned, so LDG.256-friendly).
+struct CsfView {
+  int order;
+  int32_t nlev[kMaxOrder];
+  const int32_t* idx[kMaxOrder];
+  const int32_t* ptr[kMaxOrder];
+  const double* vals;
+};
+
+struct DevCsf {
+  int order = 0;
+  int device = 0;
+  int64_t dims[kMaxOrder] = {0};
+  int64_t level_size[kMaxOrder] = {0};
+  int32_t* idx[kMaxOrder] = {nullptr};
+  int32_t* ptr[kMaxOrder] = {nullptr};
+  double* vals = nullptr;
+  int64_t bytes = 0;
+
+  CsfView view() const {
+    CsfView v{};
+    v.order = order;
+    for (int l = 0; l < order; ++l) {
+      v.nlev[l] = static_cast<int32_t>(level_size[l]);
+      v.idx[l] = idx[l];
+      v.ptr[l] = ptr[l];
+    }
+    v.vals = vals;
+    return v;
+  }
+};
+
+// Work decomposition shared by the root-output kernels.
+//  * group kernels (MTTKRP-3/4, TTTP-3): items are fixed leaf ranges of
+//    `chunk` leaves, item_pos[t*order + l] = node at level l holding the
+//    item's first leaf.
+//  * DMMA kernels (TTMc-3/4): items are fixed ranges of `chunk` segments
+//    (a segment = a fiber piece of <= seg_len children), item_pos[t] = root
+//    slice holding the item's first segment.
+//  Root slices spread over several items are combined by the fix-up kernel
+//  from per-item HEAD (slot 0) / TAIL (slot 1) partial tiles in item order.
+struct Decomp {
+  int64_t n_items = 0;
+  int64_t chunk = 0;
+  int32_t* item_pos = nullptr;
+  double* part = nullptr;  // [n_items][2][tile]
+  int64_t tile = 0;
+  int64_t n_split = 0;
+  int32_t* split_node = nullptr;   // root node ids
+  int32_t* split_first = nullptr;  // first item touching it
+  int32_t* split_last = nullptr;   // last item touching it
+  int64_t n_absent = 0;
+  int32_t* absent_rows = nullptr;  // root coordinates absent from the CSF
+  // DMMA kernels
+  int64_t n_seg = 0;
+  int32_t seg_len = 0;
+  int32_t* seg_begin = nullptr;    // [n_seg+1] child-node (or leaf) offsets
+  int32_t* seg_node = nullptr;     // [n_seg]  coordinate of the segment's fiber
+  int32_t* slice_seg = nullptr;    // [n0+1]   segment offset of each slice
+};
+
+// ---- kernel launchers (nest_*.cu) --------------------------------------
+struct RootOutArgs {
+  CsfView t;
+  const double* f[4];   // factors by CSF level 1..order-1 (f[0] unused) or by role
+  int R, S, T;
+  int vec;              // vector loads allowed
+  const int32_t* item_pos;
+  int64_t n_items;
+  int64_t chunk;
+  double* out;
+  double* part;
+  int flags;
+  // DMMA kernels
+  const int32_t* seg_begin;
+  const int32_t* seg_node;
+  const int32_t* slice_seg;
+  int64_t n_seg;
+};
+
+void launch_mttkrp3(const RootOutArgs& a, cudaStream_t s);
+void launch_mttkrp4(const RootOutArgs& a, cudaStream_t s);
+void launch_tttp3(const RootOutArgs& a, cudaStream_t s);
+void launch_ttmc3(const RootOutArgs& a, cudaStream_t s);
+void launch_ttmc4(const RootOutArgs& a, cudaStream_t s);
+
+// group geometry used by the leaf-range kernels: lanes per group for a
+// padded row width (4 doubles per lane).
+int group_lanes_for(int R);
+
+// ---- plan-time helpers (decomp.cu) ----------------------------------------
+void build_leaf_items(const DevCsf& csf, int64_t chunk, Decomp& d, int64_t tile, cudaStream_t s);
+void build_segments(const DevCsf& csf, int unit_level, int seg_len, int64_t chunk, Decomp& d,
+                    int64_t tile, cudaStream_t s);
+void launch_fixup(const Decomp& d, const CsfView& t, double* out, cudaStream_t s);
+void free_decomp(Decomp& d);
+
+// ---- generic interpreter (generic.cu) -------------------------------------
+struct GenericState {
+  spg_program* d_prog = nullptr;
+  double* buffers = nullptr;       // all buffers back to back
+  int64_t* buffer_off = nullptr;   // device offsets
+  int64_t* counters = nullptr;     // [0] madds, [1..] resets per buffer, [..] log cursor, error
+  unsigned char* log = nullptr;
+  int64_t log_bytes = 0;
+  int64_t* leaf_keys = nullptr;    // sorted packed coordinates (sparse-out lookup)
+  int64_t* leaf_pos = nullptr;
+  int64_t n_leaf_keys = 0;
+  int64_t total_buffer_elems = 0;
+};
+
+void generic_prepare(const spg_program& prog, const DevCsf& csf, GenericState& g,
+                     cudaStream_t s);
+void generic_execute(const spg_program& prog, const DevCsf& csf, const double* const* dense,
+                     double* out, GenericState& g, cudaStream_t s);
+void generic_free(GenericState& g);
+
+struct UnfactArgs;
+void unfactorized_run(const void* desc, const DevCsf& csf, const double* const* dense,
+                      double* out, int64_t out_count, cudaStream_t s);
+
+}  // namespace spttn_dev

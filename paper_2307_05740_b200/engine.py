@@ -1,0 +1,195 @@
+"""Python bindings of the device engine (C-ABI in include/spttn_b200.h).
+
+The C++ shim (csrc/shim/executor_b200.cpp) is the reference-facing drop-in
+(`spttn::prepare` / `spttn::execute`). This module exposes the same engine to
+Python for the parity tests and bench.py:
+
+    csf_dev = DeviceCsf(csf)                       # H2D + device layout
+    plan = Plan(NEST_TTMC3, csf_dev, [U, V], ranks=(R, S))
+    plan.execute(stream)                           # async on `stream`
+    y = plan.read_output()                         # D2H + sync
+
+Errors raise the Python analogue of the reference's exception types
+(ValueError ~ std::invalid_argument, UnsupportedOrderError,
+ResourceError); CUDA failures raise RuntimeError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _native as N
+from .tensor import Csf
+
+NEST_MTTKRP3 = 1
+NEST_TTMC3 = 2
+NEST_TTTP3 = 3
+NEST_MTTKRP4 = 4
+NEST_TTMC4 = 5
+NEST_GENERIC = 100
+
+FLAG_RESIDUAL = 1
+FLAG_FACTORS_ON_DEVICE = 2
+
+
+class UnsupportedOrderError(RuntimeError):
+    pass
+
+
+class ResourceError(RuntimeError):
+    pass
+
+
+def _check(rc: int) -> None:
+    if rc == 0:
+        return
+    msg = N.engine().spttn_last_error().decode()
+    if rc == 1:
+        raise ValueError(msg)
+    if rc == 2:
+        raise UnsupportedOrderError(msg)
+    if rc == 3:
+        raise ResourceError(msg)
+    raise RuntimeError(f"spttn_b200 CUDA failure: {msg}")
+
+
+def _stream_ptr(stream) -> C.c_void_p:
+    if stream is None:
+        return C.c_void_p(0)
+    if isinstance(stream, int):
+        return C.c_void_p(stream)
+    return C.c_void_p(int(stream.cuda_stream))
+
+
+def device_info() -> dict:
+    out = (C.c_int64 * 4)()
+    _check(N.engine().spttn_device_info(out, 4))
+    return {"sm_count": out[0], "cc": out[1], "l2_bytes": out[2], "smem_optin": out[3]}
+
+
+class DeviceCsf:
+    """spttn_csf_create: copies a host Csf and builds the int32 device layout."""
+
+    def __init__(self, csf: Csf, stream=None):
+        lib = N.engine()
+        self.csf = csf
+        d = csf.order
+        self._dims = (C.c_int64 * d)(*csf.dims)
+        self._sizes = (C.c_int64 * d)(*csf.level_sizes())
+        self._keep = [np.ascontiguousarray(a, np.int64) for a in csf.idx + csf.ptr]
+        idx_p = (N.c_i64_p * d)(*[a.ctypes.data_as(N.c_i64_p) for a in self._keep[:d]])
+        ptr_p = (N.c_i64_p * max(1, d - 1))(*[a.ctypes.data_as(N.c_i64_p) for a in self._keep[d:]])
+        vals = np.ascontiguousarray(csf.values, np.float64)
+        host = N.CsfHost(d, self._dims, self._sizes, idx_p, ptr_p, vals.ctypes.data_as(N.c_dbl_p))
+        h = C.c_void_p()
+        _check(lib.spttn_csf_create(C.byref(host), _stream_ptr(stream), C.byref(h)))
+        self.handle = h
+        self._keep = None
+
+    def device_bytes(self) -> int:
+        return int(N.engine().spttn_csf_device_bytes(self.handle))
+
+    def close(self):
+        if getattr(self, "handle", None):
+            N.engine().spttn_csf_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Plan:
+    """spttn_plan_create: one fused nest bound to a device CSF and factors.
+
+    factors: numpy fp64 arrays (copied) or, with on_device=True, integer
+    device pointers (e.g. torch tensor .data_ptr()) that outlive the plan.
+    """
+
+    def __init__(self, kind: int, csf: DeviceCsf, factors, ranks=(0, 0, 0), flags: int = 0,
+                 stream=None, on_device: bool = False, factor_sizes=None, program=None,
+                 buffer_limit_bytes: int = 1 << 30):
+        lib = N.engine()
+        self.csf = csf
+        desc = N.PlanDesc()
+        desc.kind = kind
+        desc.flags = flags | (FLAG_FACTORS_ON_DEVICE if on_device else 0)
+        for i, r in enumerate(list(ranks)[:3]):
+            desc.rank[i] = int(r)
+        desc.num_factors = len(factors)
+        self._factors = []
+        for f, a in enumerate(factors):
+            if on_device:
+                desc.factors[f] = C.cast(C.c_void_p(int(a)), N.c_dbl_p)
+                desc.factor_size[f] = int(factor_sizes[f])
+            else:
+                arr = np.ascontiguousarray(a, np.float64).ravel()
+                self._factors.append(arr)
+                desc.factors[f] = arr.ctypes.data_as(N.c_dbl_p)
+                desc.factor_size[f] = arr.shape[0]
+        desc.buffer_limit_bytes = buffer_limit_bytes
+        self._program = program
+        if program is not None:
+            desc.program = C.cast(C.byref(program), C.c_void_p)
+            desc.program_bytes = C.sizeof(program)
+        h = C.c_void_p()
+        _check(lib.spttn_plan_create(C.byref(desc), csf.handle, _stream_ptr(stream), C.byref(h)))
+        self.handle = h
+        self._factors = None
+        self.kind = kind
+
+    @property
+    def output_count(self) -> int:
+        return int(N.engine().spttn_output_count(self.handle))
+
+    @property
+    def output_ptr(self) -> int:
+        return int(N.engine().spttn_output_device(self.handle) or 0)
+
+    def info(self) -> dict:
+        out = (C.c_int64 * 8)()
+        _check(N.engine().spttn_plan_info(self.handle, out, 8))
+        keys = ["launches", "items", "split_slices", "absent_rows", "scratch_bytes", "kind",
+                "segments", "device_madds"]
+        return dict(zip(keys, list(out)))
+
+    def set_factors(self, factors, stream=None, on_device=False):
+        arrs = []
+        ptrs = (N.c_dbl_p * 8)()
+        for f, a in enumerate(factors):
+            if on_device:
+                ptrs[f] = C.cast(C.c_void_p(int(a)), N.c_dbl_p)
+            else:
+                arr = np.ascontiguousarray(a, np.float64).ravel()
+                arrs.append(arr)
+                ptrs[f] = arr.ctypes.data_as(N.c_dbl_p)
+        _check(N.engine().spttn_plan_set_factors(self.handle, ptrs, int(on_device),
+                                                 _stream_ptr(stream)))
+        if not on_device:  # host copies are async: keep them alive until the stream drains
+            import torch
+            (torch.cuda.synchronize() if stream is None else stream.synchronize())
+
+    def execute(self, stream=None) -> None:
+        _check(N.engine().spttn_execute(self.handle, _stream_ptr(stream)))
+
+    def read_output(self, stream=None, out: np.ndarray | None = None) -> np.ndarray:
+        n = self.output_count
+        if out is None:
+            out = np.empty(n, dtype=np.float64)
+        _check(N.engine().spttn_read_output(self.handle, out.ctypes.data_as(N.c_dbl_p), n,
+                                            _stream_ptr(stream)))
+        return out
+
+    def close(self):
+        if getattr(self, "handle", None):
+            N.engine().spttn_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
