@@ -22,10 +22,12 @@ HOSTFLAGS := -std=c++20 -O2 -fPIC -I$(REF)/include -Iinclude -I$(PKG)/csrc/devic
 
 DEV_OBJS  := $(patsubst $(PKG)/csrc/device/%.cu,build/device/%.o,$(DEV_SRC))
 
-all: device datagen oracle host
+all: device datagen probe oracle host
 device: $(LIB)/libspttn_b200.so
+probe: $(LIB)/libspttn_probe.so
 datagen: $(LIB)/libspttn_datagen.so
-ifneq ($(wildcard $(REF)/src/loop_nest.cpp),)
+HAVE_HOST := $(and $(wildcard $(REF)/src/loop_nest.cpp),$(wildcard $(PKG)/csrc/shim/executor_b200.cpp))
+ifneq ($(HAVE_HOST),)
 host: $(LIB)/libspttn_b200_host.so build/tests/test_executor_b200 build/tests/acceptance_b200
 else
 host:
@@ -39,6 +41,10 @@ build/device/%.o: $(PKG)/csrc/device/%.cu $(DEV_HDR)
 $(LIB)/libspttn_b200.so: $(DEV_OBJS)
 	@mkdir -p $(LIB)
 	$(NVCC) $(ARCH) -shared $^ -o $@
+
+$(LIB)/libspttn_probe.so: $(PKG)/csrc/probe/fp64_peak.cu
+	@mkdir -p $(LIB)
+	$(NVCC) $(NVFLAGS) -shared $< -o $@
 
 $(LIB)/libspttn_datagen.so: $(PKG)/csrc/host/datagen.cpp
 	@mkdir -p $(LIB)
@@ -77,4 +83,4 @@ clean:
 	rm -rf build $(LIB)
 	$(MAKE) -C oracle clean
 
-.PHONY: all device datagen host oracle clean
+.PHONY: all device datagen probe host oracle clean

@@ -1,0 +1,397 @@
+"""SpTTN fused-nest benchmark on B200 (BASELINE.json metric: nnz/s + roofline).
+
+A "step" is one execution of the pinned fused nest over the whole synthetic
+tensor of a BASELINE.json config. The headline line (value / ms_per_step /
+roofline / e2e / cpu_baseline) is configs[1], Order-3 TTMc (Zipf 1.1,
+1e7 nnz, R=S=16); the other four configs are measured the same way and
+reported under "configs" (skip with --configs ttmc3).
+
+  value        nnz/s of the whole job, inputs resident in HBM, device-timed
+               with CUDA events on the launch stream, L2 flushed (256 MB
+               write) between timed steps, max over ranks.
+  e2e          same metric through the C-ABI with HOST (pinned) buffers:
+               CSF + factor H2D, device layout + plan build, kernels, D2H.
+  roofline     dominant kernel (the fused nest kernel) against the north-star
+               roof max(bytes_alg/HBM, flops_alg/FP64): "bound" names the
+               larger term; fp64 peaks are measured here (DMMA / DFMA probe)
+               because MEASURED_PEAKS.json has none.
+  cpu_baseline the reference executor (oracle/_ref, compiled from
+               /root/reference) on the same pinned nest, 1 host core, on a
+               bounded root-slice sample of the same tensor.
+
+--impl reference runs the reference's CPU implementation of the path on all
+host threads (one plan per thread over nnz-balanced root-slice partitions)
+on a bounded sample, printing the same JSON keys.
+
+Multi-GPU (torchrun): each rank owns an independent tensor of the config's
+size (seed + rank): no data-path collective, "scaling": "weak".
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+HEADLINE = "ttmc3"
+ORDER = ["mttkrp3", "ttmc3", "tttp3", "mttkrp4", "ttmc4"]
+L2_FLUSH_BYTES = 256 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--configs", default="all", help="comma list or 'all'")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="target CPU time of a bounded reference sample")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return json.loads(p.read_text()), "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.f = None
+
+    def __enter__(self):
+        try:
+            self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.f.flush()
+        rows = []
+        for line in Path(self.f.name).read_text().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def fp64_peaks():
+    lib = C.CDLL(str(ROOT / "paper_2307_05740_b200" / "lib" / "libspttn_probe.so"))
+    lib.spttn_probe_fp64_tflops.restype = C.c_double
+    lib.spttn_probe_fp64_tflops.argtypes = [C.c_int, C.c_int]
+    return {"dmma_tflops": lib.spttn_probe_fp64_tflops(0, 3),
+            "dfma_tflops": lib.spttn_probe_fp64_tflops(1, 3)}
+
+
+def pinned_copy(a: np.ndarray):
+    import torch
+    t = torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype, pin_memory=True)
+    t.numpy()[...] = a
+    return t
+
+
+def device_time_config(P, w, steps, warmup, stream, flush, ev):
+    """Device-timed steps of one workload. Returns per-stage mean ms and plan."""
+    import torch
+    c = w.cfg
+    dev = P.DeviceCsf(w.csf, stream=stream)
+    tfac = [torch.from_numpy(np.ascontiguousarray(f)).to("cuda") for f in w.factors]
+    plan = P.Plan(c.kind, dev, [t.data_ptr() for t in tfac], ranks=c.ranks,
+                  flags=P.FLAG_RESIDUAL if c.residual else 0, stream=stream, on_device=True,
+                  factor_sizes=[t.numel() for t in tfac])
+    for _ in range(warmup):
+        plan.execute(stream)
+    torch.cuda.synchronize()
+    main, epi = [], []
+    with torch.cuda.stream(stream):
+        for _ in range(steps):
+            flush.zero_()  # evict L2 (256 MB write) between timed steps
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0.record(stream)
+            plan.execute_stage(0, stream)
+            e1.record(stream)
+            plan.execute_stage(1, stream)
+            e2.record(stream)
+            ev.append((e0, e1, e2))
+            main.append((e0, e1))
+            epi.append((e1, e2))
+    torch.cuda.synchronize()
+    m = [a.elapsed_time(b) for a, b in main]
+    e = [a.elapsed_time(b) for a, b in epi]
+    return {"main_ms": statistics.mean(m), "epi_ms": statistics.mean(e),
+            "main_ms_min": min(m), "step_ms": statistics.mean(m) + statistics.mean(e)}, plan, dev, tfac
+
+
+def e2e_config(P, w, steps, stream):
+    """Through the C-ABI from pinned host buffers: H2D CSF + factors, device
+    layout + plan build, fused nest, D2H of the output — every step."""
+    import torch
+    from paper_2307_05740_b200.tensor import Csf
+    c = w.cfg
+    pin_idx = [pinned_copy(a) for a in w.csf.idx]
+    pin_ptr = [pinned_copy(a) for a in w.csf.ptr]
+    pin_val = pinned_copy(w.csf.values)
+    pin_fac = [pinned_copy(np.ascontiguousarray(f)) for f in w.factors]
+    host = Csf(w.csf.dims, [t.numpy() for t in pin_idx], [t.numpy() for t in pin_ptr],
+               pin_val.numpy())
+    out = pinned_copy(np.zeros(w.out_count))
+    h2d = sum(t.numel() * 8 for t in pin_idx + pin_ptr) + pin_val.numel() * 8 + \
+        sum(t.numel() * 8 for t in pin_fac)
+    d2h = w.out_count * 8
+    times = []
+    for it in range(steps + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        dev = P.DeviceCsf(host, stream=stream)
+        plan = P.Plan(c.kind, dev, [t.numpy() for t in pin_fac], ranks=c.ranks,
+                      flags=P.FLAG_RESIDUAL if c.residual else 0, stream=stream)
+        plan.execute(stream)
+        plan.read_output(stream, out=out.numpy())
+        t1 = time.perf_counter()
+        plan.close()
+        dev.close()
+        if it > 0:
+            times.append(t1 - t0)
+    return {"seconds": statistics.mean(times), "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h)}
+
+
+def ref_args(w):
+    c = w.cfg
+    dims = dict(zip(c.mode_names, w.dims))
+    rank_names = {1: ["r"], 2: ["r", "s"], 3: ["r"], 4: ["r"], 5: ["r", "s", "t"]}[c.kind]
+    for n, r in zip(rank_names, c.ranks):
+        dims[n] = r
+    return c.kernel, dims, c.path, c.order_text
+
+
+CPU_NS_PER_NNZ = {1: 600, 2: 800, 3: 5000, 4: 1500, 5: 1200}  # survey-measured scale
+
+
+def cpu_sample(w, seconds, threads):
+    """Every k-th root slice, k chosen so the reference needs ~`seconds`."""
+    est = w.csf.nnz * CPU_NS_PER_NNZ[w.cfg.kind] * 1e-9 / max(1, threads)
+    stride = max(1, int(np.ceil(est / seconds)))
+    sub = w.csf if stride == 1 else w.csf.root_sample(stride)
+    return sub, stride
+
+
+def cpu_reference(w, seconds, threads, repeats=1):
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_bindings as OB  # the reference build (test infrastructure)
+    from paper_2307_05740_b200.configs import Workload
+    sub, stride = cpu_sample(w, seconds, threads)
+    ws = Workload(w.cfg, sub, w.factors, w.dims, sub.nnz)
+    kernel, dims, path, order = ref_args(w)
+    if w.cfg.residual:  # reference flow for rho: S on unit values
+        sub = sub.with_values(np.ones_like(sub.values))
+    if threads == 1:
+        _, st = OB.ref_execute(kernel, dims, path, order, sub, w.factors, ws.out_count,
+                               repeats=repeats)
+        secs = st["seconds"]
+    else:
+        _, secs = OB.ref_execute_threads(kernel, dims, path, order, sub, w.factors, ws.out_count,
+                                         threads, repeats=repeats)
+    return {"value": sub.nnz / secs, "unit": "nnz/s", "cores": threads, "kind": "reference",
+            "sample": f"every {stride}th root slice of the same tensor: {sub.nnz} nnz "
+                      f"({sub.level_sizes()[0]} slices), best of {repeats}, spttn_ref::execute "
+                      f"on the pinned nest {path}", "seconds": secs}
+
+
+def run_reference_impl(args, rank, world):
+    """--impl reference: the reference CPU executor on all host threads."""
+    from paper_2307_05740_b200.configs import make_workload
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    w = make_workload(HEADLINE)
+    vals = []
+    res = None
+    for step in range(args.warmup + args.steps):
+        res = cpu_reference(w, args.cpu_seconds / max(1, args.steps + args.warmup) * threads,
+                            threads)
+        if step >= args.warmup:
+            vals.append(res["value"])
+    v = statistics.median(vals)
+    line = {"impl": "reference", "metric": "SpTTN nnz/s (TTMc-3 Zipf 1e7, fused nest)",
+            "value": v, "unit": "nnz/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": res["seconds"] * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": "ttmc3 (BASELINE configs[1])"},
+            "cpu_baseline": {"value": v, "unit": "nnz/s", "cores": threads, "kind": "reference",
+                             "sample": res["sample"]},
+            "e2e": {"value": v, "unit": "nnz/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference_impl(args, rank, world)
+        return
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2307_05740_b200 as P
+    from paper_2307_05740_b200.configs import (algorithmic_bytes, algorithmic_flops, gather_bytes,
+                                               make_workload)
+    keys = ORDER if args.configs == "all" else args.configs.split(",")
+    if HEADLINE not in keys:
+        keys = [HEADLINE] + keys
+    peaks, peak_src = measured_peaks()
+    fp64 = fp64_peaks()
+    stream = torch.cuda.Stream()
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+    results = {}
+    head_clocks = None
+    for key in keys:
+        w = make_workload(key, seed_offset=rank)
+        ev = []
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        with Clocks(local) as clk:
+            t0 = time.perf_counter()
+            st, plan, dev, tfac = device_time_config(P, w, args.steps, args.warmup, stream,
+                                                     flush, ev)
+            region = time.perf_counter() - t0
+        torch.cuda.synchronize()
+        step_ms = st["step_ms"]
+        if world > 1:
+            t = torch.tensor([step_ms], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            step_ms = float(t.item())
+        info = plan.info()
+        nnz = w.csf.nnz
+        bytes_alg = algorithmic_bytes(w)
+        flops_alg = algorithmic_flops(w)
+        main_s = st["main_ms"] * 1e-3
+        hbm = peaks["hbm_gbs"]
+        fp_peak = fp64["dmma_tflops"] if w.cfg.kind in (P.NEST_TTMC3, P.NEST_TTMC4) else \
+            fp64["dfma_tflops"]
+        t_hbm = bytes_alg / (hbm * 1e9)
+        t_fp = flops_alg / (fp_peak * 1e12)
+        bound = "tensor" if t_fp >= t_hbm else "hbm"
+        if bound == "hbm":
+            roof = {"bound": "hbm", "achieved": bytes_alg / main_s / 1e9, "peak": hbm,
+                    "unit": "GB/s"}
+        else:
+            roof = {"bound": "tensor", "achieved": flops_alg / main_s / 1e12, "peak": fp_peak,
+                    "unit": "TFLOP/s"}
+        roof["frac"] = roof["achieved"] / roof["peak"]
+        roof["traffic"] = None
+        roof["peak_source"] = (f"{peak_src} MEASURED_PEAKS.json hbm_gbs" if bound == "hbm" else
+                               "fp64 " + ("DMMA" if fp_peak == fp64["dmma_tflops"] else "DFMA") +
+                               " probe measured by bench.py (MEASURED_PEAKS.json has no fp64)")
+        roof["t_roof_us"] = max(t_hbm, t_fp) * 1e6
+        roof["north_star_frac"] = max(t_hbm, t_fp) / main_s
+        roof["hbm_frac"] = (bytes_alg / main_s / 1e9) / hbm
+        roof["fp64_frac"] = (flops_alg / main_s / 1e12) / fp_peak
+        roof["bytes_alg"] = bytes_alg
+        roof["flops_alg"] = flops_alg
+        roof["gather_bytes"] = gather_bytes(w)
+        r = {"nnz": nnz, "level_sizes": w.csf.level_sizes(),
+             "value": nnz * world / (step_ms * 1e-3), "ms_per_step": step_ms,
+             "kernel_ms": st["main_ms"], "kernel_ms_min": st["main_ms_min"],
+             "epilogue_ms": st["epi_ms"], "launches_per_step": info["launches"],
+             "items": info["items"], "split_slices": info["split_slices"],
+             "region_s": region, "roofline": roof}
+        plan.close()
+        dev.close()
+        del tfac
+        if key == HEADLINE or args.e2e_steps > 0:
+            e = e2e_config(P, w, max(1, args.e2e_steps), stream)
+            secs = e["seconds"]
+            if world > 1:
+                t = torch.tensor([secs], device="cuda", dtype=torch.float64)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                secs = float(t.item())
+            r["e2e"] = {"value": nnz * world / secs, "unit": "nnz/s",
+                        "h2d_bytes_per_step": e["h2d_bytes_per_step"],
+                        "d2h_bytes_per_step": e["d2h_bytes_per_step"], "ms_per_step": secs * 1e3}
+        if rank == 0 and world == 1 and not args.no_cpu:
+            r["cpu_baseline"] = cpu_reference(w, args.cpu_seconds, 1)
+        if key == HEADLINE:
+            head_clocks = clk.summary()
+        else:
+            r["clocks"] = clk.summary()
+        results[key] = r
+        print(f"[bench] {key}: {r['value']:.3e} nnz/s kernel {st['main_ms']:.3f} ms "
+              f"roof {roof['frac']:.3f} ({bound})", file=sys.stderr, flush=True)
+
+    h = results[HEADLINE]
+    line = {
+        "metric": "SpTTN nnz/s (MTTKRP, TTMc, TTTP) + % of HBM/fp64 roofline on 1 B200",
+        "value": h["value"], "unit": "nnz/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": h["ms_per_step"], "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "ttmc3: BASELINE configs[1] Order-3 TTMc 20000^3, 1e7 nnz "
+                               "Zipf(1.1), U,V 20000x16 N(0,1), pinned nest ((T*V)*U)",
+                   "l2": "256 MB L2 flush write between timed steps",
+                   "parallelism": f"weak x{world} (independent tensor per rank)"},
+        "roofline": h["roofline"], "gpu_launches": h["launches_per_step"] * args.steps,
+        "clocks": head_clocks, "e2e": h.get("e2e"), "cpu_baseline": h.get("cpu_baseline"),
+        "fp64_peaks": fp64,
+        "configs": {k: v for k, v in results.items()},
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

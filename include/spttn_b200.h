@@ -107,6 +107,10 @@ int spttn_plan_set_factors(spttn_plan* plan, const double* const* factors, int32
 
 /* Runs the fused nest; output stays in device memory. */
 int spttn_execute(spttn_plan* plan, void* stream);
+/* One stage of spttn_execute, for per-kernel timing: stage 0 = the fused
+ * nest kernel, stage 1 = the epilogue (split-slice fix-up, absent-row
+ * zeroing); spttn_execute == stage 0 then stage 1. */
+int spttn_execute_stage(spttn_plan* plan, int stage, void* stream);
 
 int64_t spttn_output_count(const spttn_plan* plan);
 const double* spttn_output_device(const spttn_plan* plan);

@@ -66,7 +66,7 @@ class UnfactDesc(C.Structure):
 ENGINE_SYMBOLS = [
     "spttn_last_error", "spttn_csf_create", "spttn_csf_destroy", "spttn_csf_level_size",
     "spttn_csf_device_bytes", "spttn_plan_create", "spttn_plan_destroy",
-    "spttn_plan_set_factors", "spttn_execute", "spttn_output_count", "spttn_output_device",
+    "spttn_plan_set_factors", "spttn_execute", "spttn_execute_stage", "spttn_output_count", "spttn_output_device",
     "spttn_read_output", "spttn_plan_info", "spttn_generic_resets", "spttn_generic_log_bytes",
     "spttn_generic_read_log", "spttn_unfactorized", "spttn_device_info", "spttn_build_info",
 ]
@@ -101,6 +101,7 @@ def engine() -> C.CDLL:
         lib.spttn_plan_destroy.argtypes = [P]
         lib.spttn_plan_set_factors.argtypes = [P, C.POINTER(c_dbl_p), c_i32, P]
         lib.spttn_execute.argtypes = [P, P]
+        lib.spttn_execute_stage.argtypes = [P, C.c_int, P]
         lib.spttn_output_count.argtypes = [P]
         lib.spttn_output_count.restype = c_i64
         lib.spttn_output_device.argtypes = [P]

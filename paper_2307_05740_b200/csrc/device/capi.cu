@@ -427,13 +427,16 @@ int spttn_plan_set_factors(spttn_plan* p, const double* const* factors, int32_t 
   });
 }
 
-int spttn_execute(spttn_plan* p, void* stream) {
+int spttn_execute(spttn_plan* p, void* stream) { return spttn_execute_stage(p, -1, stream); }
+
+int spttn_execute_stage(spttn_plan* p, int stage, void* stream) {
   return guarded([&] {
     if (!p) fail(SPTTN_EINVAL, "null plan");
+    if (stage < -1 || stage > 1) fail(SPTTN_EINVAL, "stage must be -1, 0 or 1");
     cudaStream_t s = as_stream(stream);
     const auto& D = p->csf->d;
     if (p->kind == SPTTN_NEST_GENERIC) {
-      spttn_dev::generic_execute(*p->prog, D, p->d_dense, p->out, p->gen, s);
+      if (stage != 1) spttn_dev::generic_execute(*p->prog, D, p->d_dense, p->out, p->gen, s);
       return;
     }
     spttn_dev::RootOutArgs a{};
@@ -452,7 +455,7 @@ int spttn_execute(spttn_plan* p, void* stream) {
     a.seg_node = p->dec.seg_node;
     a.slice_seg = p->dec.slice_seg;
     a.n_seg = p->dec.n_seg;
-    switch (p->kind) {
+    if (stage != 1) switch (p->kind) {
       case SPTTN_NEST_MTTKRP3:
         a.f[1] = p->fac[0];
         a.f[2] = p->fac[1];
@@ -482,7 +485,7 @@ int spttn_execute(spttn_plan* p, void* stream) {
         spttn_dev::launch_ttmc4(a, s);
         break;
     }
-    if (p->kind != SPTTN_NEST_TTTP3) spttn_dev::launch_fixup(p->dec, a.t, p->out, s);
+    if (stage != 0 && p->kind != SPTTN_NEST_TTTP3) spttn_dev::launch_fixup(p->dec, a.t, p->out, s);
   });
 }
 

@@ -175,6 +175,10 @@ class Plan:
     def execute(self, stream=None) -> None:
         _check(N.engine().spttn_execute(self.handle, _stream_ptr(stream)))
 
+    def execute_stage(self, stage: int, stream=None) -> None:
+        """0 = fused nest kernel, 1 = epilogue (fix-up / absent rows)."""
+        _check(N.engine().spttn_execute_stage(self.handle, stage, _stream_ptr(stream)))
+
     def read_output(self, stream=None, out: np.ndarray | None = None) -> np.ndarray:
         n = self.output_count
         if out is None:

@@ -127,12 +127,11 @@ def oracle_nest(kind: int, csf, factors, ranks, residual=False) -> np.ndarray:
 def oracle_abs_nest(kind, csf, factors, ranks, residual=False) -> np.ndarray:
     """Per-entry normaliser: sum of |contributions| (nest on |T|, |factors|);
     for the residual, |t| is added."""
-    s = oracle_nest(kind, csf.abs(), [np.abs(f) for f in factors], ranks, residual=False)
-    if kind == 3:
-        if residual:
-            return s + np.abs(csf.values)
-        return s
-    return s
+    absf = [np.abs(f) for f in factors]
+    if kind == 3 and residual:
+        unit = csf.with_values(np.ones_like(csf.values))
+        return oracle_nest(kind, unit, absf, ranks, residual=False) + np.abs(csf.values)
+    return oracle_nest(kind, csf.abs(), absf, ranks, residual=False)
 
 
 # ---- reference bridge (prepare/execute of any order) ------------------------

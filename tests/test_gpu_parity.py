@@ -1,0 +1,223 @@
+"""GPU parity suite: the sm_100a kernels (through the C-ABI) against the oracle.
+
+Bar (BASELINE.json north star): sparsity / index structure bit-exact, fp64
+values within 1e-10 x sum|contributions| per output entry; exact zeros stay
+exact; repeated execution is bit-identical (proj/tests/test_executor.cpp:
+203-220).
+"""
+import json
+import os
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import oracle_bindings as OB
+from parity import assert_parity, oracle_with_norm
+
+pytestmark = pytest.mark.gpu
+
+GOLD = Path(__file__).resolve().parent / "golden"
+MANIFEST = json.loads((GOLD / "manifest.json").read_text())
+CASES = [m for m in MANIFEST if "kernel" in m]
+
+
+@pytest.fixture(scope="module")
+def E():
+    import torch
+    assert torch.cuda.is_available(), "GPU suite needs a CUDA device"
+    import paper_2307_05740_b200 as P
+    return P
+
+
+def load_case(m):
+    from paper_2307_05740_b200.tensor import Csf
+    z = np.load(GOLD / f"{m['name']}.npz")
+    d = len(m["sparse_dims"])
+    csf = Csf(list(m["sparse_dims"]), [z[f"idx{l}"] for l in range(d)],
+              [z[f"ptr{l}"] for l in range(d - 1)], z["values"])
+    nf = len([k for k in z.files if k.startswith("factor")])
+    return csf, [z[f"factor{f}"] for f in range(nf)], z
+
+
+def run(E, kind, csf, factors, ranks, flags=0):
+    dev = E.DeviceCsf(csf)
+    plan = E.Plan(kind, dev, factors, ranks=ranks, flags=flags)
+    plan.execute()
+    out = plan.read_output()
+    return out, plan, dev
+
+
+@pytest.mark.parametrize("m", CASES, ids=[m["name"] for m in CASES])
+def test_golden_reference_outputs(E, m):
+    csf, factors, z = load_case(m)
+    out, plan, _ = run(E, m["kind"], csf, factors, m["ranks"])
+    _, norm = oracle_with_norm(m["kind"], csf, factors, m["ranks"])
+    assert_parity(out, z["fused"], norm, m["name"])
+    # second run on the same plan: bit-identical
+    plan.execute()
+    assert np.array_equal(plan.read_output(), out)
+
+
+@pytest.mark.parametrize("m", [m for m in CASES if m["sparse_out"]],
+                         ids=[m["name"] for m in CASES if m["sparse_out"]])
+def test_golden_completion_residual(E, m):
+    csf, factors, z = load_case(m)
+    out, _, _ = run(E, m["kind"], csf, factors, m["ranks"], flags=E.FLAG_RESIDUAL)
+    _, norm = oracle_with_norm(m["kind"], csf, factors, m["ranks"], residual=True)
+    assert_parity(out, z["residual"], norm, m["name"] + " residual")
+
+
+@pytest.mark.parametrize("chunk", ["1", "2", "3", "7", "64"])
+@pytest.mark.parametrize("name", ["mttkrp3_r32", "ttmc3_r16", "tttp3_r64", "mttkrp4_r32",
+                                  "ttmc4_r8"])
+def test_partition_independence(E, name, chunk, monkeypatch):
+    """Tiny work items force split fibers, split slices and many HEAD/TAIL
+    partials; results must stay within tolerance and be deterministic."""
+    m = [c for c in CASES if c["name"] == name][0]
+    csf, factors, z = load_case(m)
+    monkeypatch.setenv("SPTTN_CHUNK", chunk)
+    monkeypatch.setenv("SPTTN_SEG_LEN", "1" if chunk in ("1", "2") else "3")
+    out, plan, _ = run(E, m["kind"], csf, factors, m["ranks"])
+    _, norm = oracle_with_norm(m["kind"], csf, factors, m["ranks"])
+    assert_parity(out, z["fused"], norm, f"{name} chunk={chunk}")
+    if m["kind"] != 3 and chunk == "1":
+        assert plan.info()["split_slices"] > 0
+
+
+@pytest.mark.parametrize("key", ["mttkrp3", "ttmc3", "tttp3", "mttkrp4", "ttmc4"])
+def test_baseline_shaped_reduced_scale(E, key):
+    from paper_2307_05740_b200.configs import make_workload
+    w = make_workload(key, scale=1e-3)
+    c = w.cfg
+    flags = E.FLAG_RESIDUAL if c.residual else 0
+    out, _, _ = run(E, c.kind, w.csf, w.factors, c.ranks, flags)
+    want, norm = oracle_with_norm(c.kind, w.csf, w.factors, c.ranks, residual=c.residual)
+    assert_parity(out, want, norm, key)
+
+
+def _skewed_csf(order, dims, nnz_in_one_fiber, extra, seed):
+    """One giant fiber (all under root 0 / fiber 0) plus scattered extras."""
+    from paper_2307_05740_b200.tensor import Csf
+    rng = np.random.default_rng(seed)
+    big = np.zeros((nnz_in_one_fiber, order), np.int64)
+    big[:, order - 1] = np.arange(nnz_in_one_fiber) % dims[order - 1]
+    if order == 4:
+        big[:, 2] = np.arange(nnz_in_one_fiber) // dims[3] % dims[2]
+    rest = rng.integers(0, dims, size=(extra, order))
+    coords = np.concatenate([big, rest])
+    vals = rng.uniform(-1, 1, coords.shape[0])
+    return Csf.from_coo(list(dims), coords, vals)
+
+
+@pytest.mark.parametrize("kind,ranks,order", [(1, (32, 0, 0), 3), (2, (16, 16, 0), 3),
+                                              (3, (64, 0, 0), 3), (4, (32, 0, 0), 4),
+                                              (5, (8, 8, 8), 4)])
+def test_extreme_skew_long_fiber(E, kind, ranks, order):
+    """A single fiber with ~20k leaves (MTTKRP-4's largest fiber holds 2e5;
+    SURVEY.md §0.8) must be split across work items deterministically."""
+    dims = (50, 40, 300, 70) if order == 4 else (50, 40, 20000)
+    csf = _skewed_csf(order, dims[:order], 20000, 3000, 5)
+    rng = np.random.default_rng(1)
+    R, S, T = ranks
+    if kind in (1, 4):
+        fs = [rng.standard_normal((dims[l], R)) for l in range(1, order)]
+    elif kind == 2:
+        fs = [rng.standard_normal((dims[1], R)), rng.standard_normal((dims[2], S))]
+    elif kind == 3:
+        fs = [rng.standard_normal((dims[l], R)) for l in range(3)]
+    else:
+        fs = [rng.standard_normal((dims[1], R)), rng.standard_normal((dims[2], S)),
+              rng.standard_normal((dims[3], T))]
+    out, plan, _ = run(E, kind, csf, fs, ranks)
+    want, norm = oracle_with_norm(kind, csf, fs, ranks)
+    assert_parity(out, want, norm, f"skew kind={kind}")
+    plan.execute()
+    assert np.array_equal(plan.read_output(), out)
+
+
+@pytest.mark.parametrize("kind,ranks,order", [(1, (32, 0, 0), 3), (2, (16, 16, 0), 3),
+                                              (3, (64, 0, 0), 3), (4, (32, 0, 0), 4),
+                                              (5, (8, 8, 8), 4)])
+def test_empty_and_single_entry(E, kind, ranks, order):
+    from paper_2307_05740_b200.tensor import Csf
+    dims = [5, 4, 6, 3][:order]
+    R, S, T = ranks
+    rng = np.random.default_rng(0)
+    rows = {1: [1, 2], 4: [1, 2, 3], 2: [1, 2], 3: [0, 1, 2], 5: [1, 2, 3]}[kind]
+    cols = {1: [R, R], 4: [R, R, R], 2: [R, S], 3: [R, R, R], 5: [R, S, T]}[kind]
+    fs = [rng.standard_normal((dims[r], c)) for r, c in zip(rows, cols)]
+    empty = Csf.from_coo(dims, np.zeros((0, order), np.int64), np.zeros(0))
+    out, _, _ = run(E, kind, empty, fs, ranks)
+    assert np.all(out == 0.0)
+    one = Csf.from_coo(dims, np.array([[d - 1 for d in dims]]), np.array([0.75]))
+    out, _, _ = run(E, kind, one, fs, ranks)
+    want, norm = oracle_with_norm(kind, one, fs, ranks)
+    assert_parity(out, want, norm, "single entry")
+
+
+@pytest.mark.parametrize("m", [CASES[1], CASES[3], CASES[7], CASES[9]],
+                         ids=[CASES[i]["name"] for i in (1, 3, 7, 9)])
+def test_zero_factor_gives_exact_zero(E, m):
+    """proj/tests/test_executor.cpp:122-132."""
+    csf, factors, _ = load_case(m)
+    factors = [np.zeros_like(factors[0])] + factors[1:]
+    out, _, _ = run(E, m["kind"], csf, factors, m["ranks"])
+    assert np.all(out == 0.0)
+
+
+def test_errors_map_to_reference_exception_types(E):
+    """Shape errors -> invalid_argument, unsupported rank -> unsupported_order_error,
+    malformed CSF -> invalid_argument (executor.cpp:112-140, :176-178)."""
+    m = [c for c in CASES if c["name"] == "ttmc3_r16"][0]
+    csf, factors, _ = load_case(m)
+    dev = E.DeviceCsf(csf)
+    with pytest.raises(ValueError):
+        E.Plan(E.NEST_TTMC3, dev, [factors[0][:, :8], factors[1]], ranks=(16, 16))
+    with pytest.raises(ValueError):
+        E.Plan(E.NEST_MTTKRP4, dev, factors, ranks=(16, 0))
+    big = [np.zeros((csf.dims[1], 17)), np.zeros((csf.dims[2], 16))]
+    with pytest.raises(E.UnsupportedOrderError):
+        E.Plan(E.NEST_TTMC3, dev, big, ranks=(17, 16))
+    bad = csf.with_values(csf.values)
+    bad.idx = [a.copy() for a in csf.idx]
+    bad.idx[2][0] = csf.dims[2] + 5
+    with pytest.raises(ValueError):
+        E.DeviceCsf(bad)
+
+
+def test_device_factors_and_set_factors(E):
+    """Factors resident on the device (FACTORS_ON_DEVICE) and refreshed
+    between executions (ALS-style), against the oracle each time."""
+    import torch
+    m = [c for c in CASES if c["name"] == "mttkrp3_r32"][0]
+    csf, factors, _ = load_case(m)
+    dev = E.DeviceCsf(csf)
+    tf = [torch.from_numpy(np.ascontiguousarray(f)).cuda() for f in factors]
+    plan = E.Plan(E.NEST_MTTKRP3, dev, [t.data_ptr() for t in tf], ranks=(32,),
+                  on_device=True, factor_sizes=[t.numel() for t in tf])
+    plan.execute()
+    out = plan.read_output()
+    want, norm = oracle_with_norm(1, csf, factors, (32, 0, 0))
+    assert_parity(out, want, norm, "device factors")
+    tf[0].mul_(-2.0)
+    plan.execute()
+    out2 = plan.read_output()
+    want2, norm2 = oracle_with_norm(1, csf, [factors[0] * -2.0, factors[1]], (32, 0, 0))
+    assert_parity(out2, want2, norm2, "updated device factors")
+    hplan = E.Plan(E.NEST_MTTKRP3, dev, factors, ranks=(32,))
+    hplan.set_factors([factors[0] * -2.0, factors[1]])
+    hplan.execute()
+    assert_parity(hplan.read_output(), want2, norm2, "set_factors")
+
+
+def test_unit_values_tttp_equals_residual_flow(E):
+    """rho = T - S(unit values): the residual flag equals the oracle flow the
+    survey prescribes."""
+    m = [c for c in CASES if c["name"] == "tttp3_r64"][0]
+    csf, factors, z = load_case(m)
+    unit = csf.with_values(np.ones_like(csf.values))
+    s_unit, _, _ = run(E, 3, unit, factors, m["ranks"])
+    rho, _, _ = run(E, 3, csf, factors, m["ranks"], flags=E.FLAG_RESIDUAL)
+    _, norm = oracle_with_norm(3, csf, factors, m["ranks"], residual=True)
+    assert_parity(rho, csf.values - s_unit, norm, "residual vs T - S(1)")
