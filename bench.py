@@ -351,7 +351,7 @@ def main():
         plan.close()
         dev.close()
         del tfac
-        if key == HEADLINE or args.e2e_steps > 0:
+        if args.e2e_steps > 0:
             e = e2e_config(P, w, max(1, args.e2e_steps), stream)
             secs = e["seconds"]
             if world > 1:

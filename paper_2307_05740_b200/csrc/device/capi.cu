@@ -33,6 +33,7 @@ struct spttn_plan {
   double* out = nullptr;
   int64_t out_count = 0;
   int vec = 0;
+  int mode = 0;  // kernel variant (TTMc-3)
   spttn_dev::Decomp dec;
   spttn_dev::GenericState gen;
   spg_program* prog = nullptr;  // host copy (GENERIC)
@@ -382,8 +383,16 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
         const bool vv = p->kind == SPTTN_NEST_TTMC3 ? (S % 2 == 0 && facs_aligned16)
                                                     : (S == 8 && facs_aligned32);
         p->vec = (vu ? 1 : 0) | (vv ? 2 : 0);
-        const int seg_len = static_cast<int>(
-            env_int("SPTTN_SEG_LEN", p->kind == SPTTN_NEST_TTMC3 ? 16 : 8));
+        // TTMc-3 stages a group's <= 4 segments of leaves in one warp-wide
+        // register block: seg_len <= 8.
+        int seg_len = static_cast<int>(
+            env_int("SPTTN_SEG_LEN", p->kind == SPTTN_NEST_TTMC3 ? 4 : 8));
+        if (p->kind == SPTTN_NEST_TTMC3) {
+          // 3 = pipelined direct-load kernel (default); 0-2 = earlier variants
+          p->mode = static_cast<int>(env_int("SPTTN_TTMC3_MODE", 3));
+          seg_len = std::clamp(seg_len, 1, p->mode == 0 ? 8 : 4);
+        }
+        seg_len = std::max(seg_len, 1);
         const int64_t units = D.level_size[1];
         const int64_t warps = static_cast<int64_t>(sms) * 32 * 2;
         int64_t chunk = env_int("SPTTN_CHUNK", 0);
@@ -450,7 +459,7 @@ int spttn_execute_stage(spttn_plan* p, int stage, void* stream) {
     a.chunk = p->dec.chunk;
     a.out = p->out;
     a.part = p->dec.part;
-    a.flags = (p->flags & SPTTN_FLAG_RESIDUAL) ? 1 : 0;
+    a.flags = ((p->flags & SPTTN_FLAG_RESIDUAL) ? 1 : 0) | (p->mode << 8);
     a.seg_begin = p->dec.seg_begin;
     a.seg_node = p->dec.seg_node;
     a.slice_seg = p->dec.slice_seg;

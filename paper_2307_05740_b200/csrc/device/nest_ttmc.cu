@@ -35,7 +35,7 @@ __device__ __forceinline__ int warp_max4(int v) {
 }
 
 template <bool VECU, bool VECV>
-__global__ void __launch_bounds__(kBlock) k_ttmc3(RootOutArgs a) {
+__global__ void __launch_bounds__(kBlock, 3) k_ttmc3(RootOutArgs a) {
   const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
   if (w >= a.n_items) return;  // warp-uniform
   const int lane = threadIdx.x & 31;
@@ -50,10 +50,148 @@ __global__ void __launch_bounds__(kBlock) k_ttmc3(RootOutArgs a) {
   const int32_t* __restrict__ seg_begin = a.seg_begin;
   const int32_t* __restrict__ seg_node = a.seg_node;
 
-  int64_t c = w * a.chunk;
-  const int64_t cend = min64(c + a.chunk, a.n_seg);
+  int32_t c = static_cast<int32_t>(w * a.chunk);
+  const int32_t cend = static_cast<int32_t>(min64(c + a.chunk, a.n_seg));
+  const int32_t n_seg = static_cast<int32_t>(a.n_seg);
   int32_t sl = a.item_pos[w];
-  int64_t sl_end = a.slice_seg[sl + 1];
+  int32_t sl_end = a.slice_seg[sl + 1];
+  bool head = a.slice_seg[sl] < c;
+  int32_t row = t.idx[0][sl];
+  bool pending = false;
+  double acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.0;
+
+  auto flush = [&](int slot) {
+    double* dst = slot < 0 ? a.out + static_cast<int64_t>(row) * R * S
+                           : a.part + (w * 2 + slot) * static_cast<int64_t>(R) * S;
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = 2 * h + mt;
+          const int s = 2 * (2 * q + e) + nt;
+          if (r < R && s < S) dst[r * S + s] = acc[(mt * 2 + nt) * 2 + e];
+        }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = 0.0;
+  };
+
+  const int32_t nnz = t.nlev[2];
+  // Software pipeline: the leaf block (<= 32 leaves) of the next group is
+  // loaded while the current group's V rows are in flight.
+  int32_t pf_base = -1, pf_k = 0;
+  double pf_t = 0.0;
+  while (c < cend) {
+    // segment metadata for a window of 32 segments, one per lane
+    const int32_t wb = c;
+    const int32_t wend = min(wb + 32, cend);
+    const int32_t sb = wb + lane <= n_seg ? __ldg(seg_begin + wb + lane) : nnz;
+    const int32_t sb32 = __ldg(seg_begin + min(wb + 32, n_seg));
+    const int32_t sn = wb + lane < n_seg ? __ldg(seg_node + wb + lane) : 0;
+    while (c < wend) {
+      const int32_t lim = min(wend, sl_end);
+      const int nvalid = min(4, lim - c);
+      const int r0 = c - wb;
+      const int rq = r0 + q;
+      const bool valid = q < nvalid;
+      const int32_t L0 = __shfl_sync(0xffffffffu, sb, r0);
+      const int32_t L1a = __shfl_sync(0xffffffffu, sb, min(r0 + nvalid, 31));
+      const int32_t L1 = r0 + nvalid < 32 ? L1a : sb32;
+      int32_t lb = __shfl_sync(0xffffffffu, sb, min(rq, 31));
+      const int32_t lea = __shfl_sync(0xffffffffu, sb, min(rq + 1, 31));
+      int32_t le = rq + 1 < 32 ? lea : sb32;
+      int32_t j = __shfl_sync(0xffffffffu, sn, min(rq, 31));
+      if (!valid) lb = le = j = 0;
+      // this group's leaves [L0, L1) (at most 4 * seg_len <= 32), lane-parallel
+      int32_t kreg;
+      double treg;
+      if (pf_base == L0) {
+        kreg = pf_k;
+        treg = pf_t;
+      } else {
+        kreg = L0 + lane < L1 ? __ldg(kidx + L0 + lane) : 0;
+        treg = L0 + lane < L1 ? __ldg(vals + L0 + lane) : 0.0;
+      }
+      pf_base = L1;
+      pf_k = L1 + lane < nnz ? __ldg(kidx + L1 + lane) : 0;
+      pf_t = L1 + lane < nnz ? __ldg(vals + L1 + lane) : 0.0;
+      const double2 u = valid ? row2<VECU>(U + static_cast<int64_t>(j) * R, 2 * h, R)
+                              : make_double2(0, 0);
+      const int n = le - lb;
+      const int nmax = warp_max4(n);
+      const int base = lb - L0;
+      double x0 = 0.0, x1 = 0.0;
+      for (int it = 0; it < nmax; it += 4) {
+        int32_t kk[4];
+        double tt[4];
+        double2 vr[4];
+#pragma unroll
+        for (int u4 = 0; u4 < 4; ++u4) {
+          const int src = (base + it + u4) & 31;
+          kk[u4] = __shfl_sync(0xffffffffu, kreg, src);
+          tt[u4] = __shfl_sync(0xffffffffu, treg, src);
+        }
+#pragma unroll
+        for (int u4 = 0; u4 < 4; ++u4)
+          vr[u4] = it + u4 < n ? row2<VECV>(V + static_cast<int64_t>(kk[u4]) * S, 2 * h, S)
+                               : make_double2(0, 0);
+#pragma unroll
+        for (int u4 = 0; u4 < 4; ++u4) {
+          const double tv = it + u4 < n ? tt[u4] : 0.0;
+          x0 = fma(tv, vr[u4].x, x0);  // X[s] += t * V[k,s]
+          x1 = fma(tv, vr[u4].y, x1);
+        }
+      }
+      // rank-1 updates of 4 segments: D[mt][nt] += A[mt] (8x4) * B[nt] (4x8)
+      dmma_8x8x4(acc[0], acc[1], u.x, x0);
+      dmma_8x8x4(acc[2], acc[3], u.x, x1);
+      dmma_8x8x4(acc[4], acc[5], u.y, x0);
+      dmma_8x8x4(acc[6], acc[7], u.y, x1);
+      pending = true;
+      c += nvalid;
+      if (c == sl_end) {
+        flush(head ? 0 : -1);
+        pending = false;
+        head = false;
+        if (c < cend) {
+          ++sl;
+          sl_end = a.slice_seg[sl + 1];
+          row = t.idx[0][sl];
+        }
+      }
+    }
+  }
+  if (pending) flush(head ? 0 : 1);
+}
+
+// Direct-load variant: seg_len <= 4, fully unrolled leaf loop (no
+// data-dependent trip counts), each lane loads its slot's leaf indices /
+// values itself (4 distinct addresses per instruction, broadcast within the
+// 8 lanes of a slot); NG groups of 4 segments are in flight per step.
+template <bool VECU, bool VECV, int NG>
+__global__ void __launch_bounds__(kBlock, NG == 1 ? 4 : 3) k_ttmc3d(RootOutArgs a) {
+  const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
+  if (w >= a.n_items) return;  // warp-uniform
+  const int lane = threadIdx.x & 31;
+  const int q = lane & 3;
+  const int h = lane >> 2;
+  const int R = a.R, S = a.S;
+  const CsfView& t = a.t;
+  const double* __restrict__ U = a.f[1];
+  const double* __restrict__ V = a.f[2];
+  const int32_t* __restrict__ kidx = t.idx[2];
+  const double* __restrict__ vals = t.vals;
+  const int32_t* __restrict__ seg_begin = a.seg_begin;
+  const int32_t* __restrict__ seg_node = a.seg_node;
+  const int32_t n_seg = static_cast<int32_t>(a.n_seg);
+
+  int32_t c = static_cast<int32_t>(w * a.chunk);
+  const int32_t cend = static_cast<int32_t>(min64(c + a.chunk, a.n_seg));
+  int32_t sl = a.item_pos[w];
+  int32_t sl_end = a.slice_seg[sl + 1];
   bool head = a.slice_seg[sl] < c;
   int32_t row = t.idx[0][sl];
   bool pending = false;
@@ -79,55 +217,191 @@ __global__ void __launch_bounds__(kBlock) k_ttmc3(RootOutArgs a) {
   };
 
   while (c < cend) {
-    const int64_t lim = min(cend, sl_end);
-    const int64_t my = c + q;
-    const bool valid = my < lim;
-    int32_t lb = 0, le = 0, j = 0;
-    if (valid) {
-      lb = __ldg(seg_begin + my);
-      le = __ldg(seg_begin + my + 1);
-      j = __ldg(seg_node + my);
-    }
-    const double2 u = valid ? row2<VECU>(U + static_cast<int64_t>(j) * R, 2 * h, R)
-                            : make_double2(0, 0);
-    const int n = le - lb;
-    const int nmax = warp_max4(n);
-    double x0 = 0.0, x1 = 0.0;
-    int it = 0;
-    for (; it + 2 <= nmax; it += 2) {
-      int32_t k0 = 0, k1 = 0;
-      double v0 = 0, v1 = 0;
-      if (it < n) {
-        k0 = __ldg(kidx + lb + it);
-        v0 = __ldg(vals + lb + it);
+    const int32_t wb = c;
+    const int32_t wend = min(wb + 32, cend);
+    const int32_t sb = wb + lane <= n_seg ? __ldg(seg_begin + wb + lane) : 0;
+    const int32_t sb32 = __ldg(seg_begin + min(wb + 32, n_seg));
+    const int32_t sn = wb + lane < n_seg ? __ldg(seg_node + wb + lane) : 0;
+    while (c < wend) {
+      const int32_t lim = min(wend, sl_end);
+      int32_t lb[NG], n[NG], nv[NG];
+      double2 u[NG];
+      int32_t cg = c;
+#pragma unroll
+      for (int g = 0; g < NG; ++g) {
+        nv[g] = max(0, min(4, lim - cg));
+        const int rq = cg - wb + q;
+        const bool valid = q < nv[g];
+        const int32_t b = __shfl_sync(0xffffffffu, sb, min(rq, 31));
+        const int32_t ea = __shfl_sync(0xffffffffu, sb, min(rq + 1, 31));
+        const int32_t jj = __shfl_sync(0xffffffffu, sn, min(rq, 31));
+        const int32_t e = rq + 1 < 32 ? ea : sb32;
+        lb[g] = valid ? b : 0;
+        n[g] = valid ? e - b : 0;
+        u[g] = valid ? row2<VECU>(U + static_cast<int64_t>(jj) * R, 2 * h, R)
+                     : make_double2(0, 0);
+        cg += nv[g];
       }
-      if (it + 1 < n) {
-        k1 = __ldg(kidx + lb + it + 1);
-        v1 = __ldg(vals + lb + it + 1);
-      }
-      const double2 r0 = it < n ? row2<VECV>(V + static_cast<int64_t>(k0) * S, 2 * h, S)
+      int32_t kk[NG][4];
+      double tt[NG][4];
+#pragma unroll
+      for (int g = 0; g < NG; ++g)
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          kk[g][it] = it < n[g] ? __ldg(kidx + lb[g] + it) : 0;
+          tt[g][it] = it < n[g] ? __ldg(vals + lb[g] + it) : 0.0;
+        }
+      double2 vr[NG][4];
+#pragma unroll
+      for (int g = 0; g < NG; ++g)
+#pragma unroll
+        for (int it = 0; it < 4; ++it)
+          vr[g][it] = it < n[g] ? row2<VECV>(V + static_cast<int64_t>(kk[g][it]) * S, 2 * h, S)
                                 : make_double2(0, 0);
-      const double2 r1 = it + 1 < n ? row2<VECV>(V + static_cast<int64_t>(k1) * S, 2 * h, S)
-                                    : make_double2(0, 0);
-      x0 = fma(v0, r0.x, x0);
-      x1 = fma(v0, r0.y, x1);
-      x0 = fma(v1, r1.x, x0);
-      x1 = fma(v1, r1.y, x1);
+#pragma unroll
+      for (int g = 0; g < NG; ++g) {
+        double x0 = 0.0, x1 = 0.0;
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          x0 = fma(tt[g][it], vr[g][it].x, x0);  // X[s] += t * V[k,s]
+          x1 = fma(tt[g][it], vr[g][it].y, x1);
+        }
+        dmma_8x8x4(acc[0], acc[1], u[g].x, x0);
+        dmma_8x8x4(acc[2], acc[3], u[g].x, x1);
+        dmma_8x8x4(acc[4], acc[5], u[g].y, x0);
+        dmma_8x8x4(acc[6], acc[7], u[g].y, x1);
+      }
+      pending = true;
+      c = cg;
+      if (c == sl_end) {
+        flush(head ? 0 : -1);
+        pending = false;
+        head = false;
+        if (c < cend) {
+          ++sl;
+          sl_end = a.slice_seg[sl + 1];
+          row = t.idx[0][sl];
+        }
+      }
     }
-    if (it < nmax && it < n) {
-      const int32_t k0 = __ldg(kidx + lb + it);
-      const double v0 = __ldg(vals + lb + it);
-      const double2 r0 = row2<VECV>(V + static_cast<int64_t>(k0) * S, 2 * h, S);
-      x0 = fma(v0, r0.x, x0);
-      x1 = fma(v0, r0.y, x1);
+  }
+  if (pending) flush(head ? 0 : 1);
+}
+
+// Pipelined direct-load variant (seg_len <= 4). Groups are speculated to be
+// the next 4 segments: segment metadata is loaded two groups ahead and leaf
+// coordinates one group ahead, so the only round trip on a group's critical
+// path is its V-row gather (issued together with its values and U rows).
+// A group shortened by a slice / item end falls back to direct loads.
+struct SegMeta {
+  int32_t lb, n, j;
+};
+
+__device__ __forceinline__ SegMeta load_meta(const RootOutArgs& a, int32_t base, int q,
+                                             int32_t n_seg) {
+  SegMeta m{0, 0, 0};
+  const int32_t seg = base + q;
+  if (seg < n_seg) {
+    m.lb = __ldg(a.seg_begin + seg);
+    m.n = __ldg(a.seg_begin + seg + 1) - m.lb;
+    m.j = __ldg(a.seg_node + seg);
+  }
+  return m;
+}
+
+template <bool VECU, bool VECV>
+__global__ void __launch_bounds__(kBlock, 3) k_ttmc3p(RootOutArgs a) {
+  const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
+  if (w >= a.n_items) return;  // warp-uniform
+  const int lane = threadIdx.x & 31;
+  const int q = lane & 3;
+  const int h = lane >> 2;
+  const int R = a.R, S = a.S;
+  const CsfView& t = a.t;
+  const double* __restrict__ U = a.f[1];
+  const double* __restrict__ V = a.f[2];
+  const int32_t* __restrict__ kidx = t.idx[2];
+  const double* __restrict__ vals = t.vals;
+  const int32_t n_seg = static_cast<int32_t>(a.n_seg);
+
+  int32_t c = static_cast<int32_t>(w * a.chunk);
+  const int32_t cend = static_cast<int32_t>(min64(c + a.chunk, a.n_seg));
+  int32_t sl = a.item_pos[w];
+  int32_t sl_end = a.slice_seg[sl + 1];
+  bool head = a.slice_seg[sl] < c;
+  int32_t row = t.idx[0][sl];
+  bool pending = false;
+  double acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.0;
+
+  auto flush = [&](int slot) {
+    double* dst = slot < 0 ? a.out + static_cast<int64_t>(row) * R * S
+                           : a.part + (w * 2 + slot) * static_cast<int64_t>(R) * S;
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = 2 * h + mt;
+          const int s = 2 * (2 * q + e) + nt;
+          if (r < R && s < S) dst[r * S + s] = acc[(mt * 2 + nt) * 2 + e];
+        }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = 0.0;
+  };
+  auto load_k = [&](const SegMeta& m, int32_t* k) {
+#pragma unroll
+    for (int it = 0; it < 4; ++it) k[it] = it < m.n ? __ldg(kidx + m.lb + it) : 0;
+  };
+
+  SegMeta mc = load_meta(a, c, q, n_seg);
+  SegMeta mn = load_meta(a, c + 4, q, n_seg);
+  int32_t kc[4];
+  load_k(mc, kc);
+  while (c < cend) {
+    const int32_t lim = min(cend, sl_end);
+    const int nv = min(4, lim - c);
+    const bool valid = q < nv;
+    const int n = valid ? mc.n : 0;
+    double tt[4];
+    double2 vr[4];
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      tt[it] = it < n ? __ldg(vals + mc.lb + it) : 0.0;
+      vr[it] = it < n ? row2<VECV>(V + static_cast<int64_t>(kc[it]) * S, 2 * h, S)
+                      : make_double2(0, 0);
     }
-    // rank-1 updates of 4 segments: D[mt][nt] += A[mt] (8x4) * B[nt] (4x8)
+    const double2 u = valid ? row2<VECU>(U + static_cast<int64_t>(mc.j) * R, 2 * h, R)
+                            : make_double2(0, 0);
+    // speculative prefetch: next group = the next 4 segments
+    const SegMeta mnn = load_meta(a, c + 8, q, n_seg);
+    int32_t kn[4];
+    load_k(mn, kn);
+    double x0 = 0.0, x1 = 0.0;
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      x0 = fma(tt[it], vr[it].x, x0);  // X[s] += t * V[k,s]
+      x1 = fma(tt[it], vr[it].y, x1);
+    }
     dmma_8x8x4(acc[0], acc[1], u.x, x0);
     dmma_8x8x4(acc[2], acc[3], u.x, x1);
     dmma_8x8x4(acc[4], acc[5], u.y, x0);
     dmma_8x8x4(acc[6], acc[7], u.y, x1);
     pending = true;
-    c = min(c + 4, lim);
+    const int32_t cn = c + nv;
+    if (nv == 4) {
+      mc = mn;
+      mn = mnn;
+#pragma unroll
+      for (int it = 0; it < 4; ++it) kc[it] = kn[it];
+    } else {  // group cut by a slice / item end: restart the pipeline
+      mc = load_meta(a, cn, q, n_seg);
+      mn = load_meta(a, cn + 4, q, n_seg);
+      load_k(mc, kc);
+    }
+    c = cn;
     if (c == sl_end) {
       flush(head ? 0 : -1);
       pending = false;
@@ -267,6 +541,38 @@ void launch_ttmc3(const RootOutArgs& a, cudaStream_t s) {
   const int64_t blocks = (a.n_items * 32 + kBlock - 1) / kBlock;
   if (blocks == 0) return;
   const bool vu = a.vec & 1, vv = a.vec & 2;
+  const int mode = a.flags >> 8;  // kernel variant chosen at plan time
+  if (mode == 3) {
+    if (vu && vv)
+      k_ttmc3p<true, true><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
+    else if (vu)
+      k_ttmc3p<true, false><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
+    else if (vv)
+      k_ttmc3p<false, true><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
+    else
+      k_ttmc3p<false, false><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
+    SPTTN_CUDA(cudaGetLastError());
+    return;
+  }
+  if (mode == 1 || mode == 2) {
+#define SPTTN_TTMC3D(NG)                                                                  \
+  if (vu && vv)                                                                           \
+    k_ttmc3d<true, true, NG><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);         \
+  else if (vu)                                                                            \
+    k_ttmc3d<true, false, NG><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);        \
+  else if (vv)                                                                            \
+    k_ttmc3d<false, true, NG><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);        \
+  else                                                                                    \
+    k_ttmc3d<false, false, NG><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
+    if (mode == 1) {
+      SPTTN_TTMC3D(1)
+    } else {
+      SPTTN_TTMC3D(2)
+    }
+#undef SPTTN_TTMC3D
+    SPTTN_CUDA(cudaGetLastError());
+    return;
+  }
   if (vu && vv)
     k_ttmc3<true, true><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
   else if (vu)
