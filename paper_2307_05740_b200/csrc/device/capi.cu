@@ -33,7 +33,10 @@ struct spttn_plan {
   double* out = nullptr;
   int64_t out_count = 0;
   int vec = 0;
-  int mode = 0;  // kernel variant (TTMc-3)
+  int mode = 0;  // kernel variant (TTMc-3, TTTP-3)
+  int batch = 4;  // TTTP leaves per group step
+  int32_t* leaf_i = nullptr;  // TTTP leaf kernel: per-leaf root / level-1 coordinates
+  int32_t* leaf_j = nullptr;
   spttn_dev::Decomp dec;
   spttn_dev::GenericState gen;
   spg_program* prog = nullptr;  // host copy (GENERIC)
@@ -260,6 +263,8 @@ int spttn_plan_destroy(spttn_plan* p) {
       for (int f = 0; f < p->nf; ++f) cudaFree(p->fac[f]);
     cudaFree(p->out);
     cudaFree(p->d_dense);
+    cudaFree(p->leaf_i);
+    cudaFree(p->leaf_j);
     spttn_dev::free_decomp(p->dec);
     spttn_dev::generic_free(p->gen);
     delete p->prog;
@@ -404,7 +409,15 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
         const int64_t groups = static_cast<int64_t>(sms) * (2048 / G) * 2;
         int64_t chunk = env_int("SPTTN_CHUNK", 0);
         if (chunk <= 0) chunk = std::clamp<int64_t>((nnz + groups - 1) / groups, 16, 4096);
-        spttn_dev::build_leaf_items(D, chunk, p->dec, sparse_out ? 0 : tile, s);
+        if (sparse_out) {
+          // 1 = leaf-parallel kernel over expanded (i, j) coordinates (default)
+          p->mode = static_cast<int>(env_int("SPTTN_TTTP_MODE", 1));
+          p->batch = static_cast<int>(env_int("SPTTN_TTTP_BATCH", 4));
+        }
+        if (sparse_out && p->mode == 1)
+          spttn_dev::build_leaf_coords(D, &p->leaf_i, &p->leaf_j, s);
+        else
+          spttn_dev::build_leaf_items(D, chunk, p->dec, sparse_out ? 0 : tile, s);
       }
       p->launches = 1 + (p->dec.n_split > 0) + (p->dec.n_absent > 0);
     }
@@ -480,7 +493,10 @@ int spttn_execute_stage(spttn_plan* p, int stage, void* stream) {
         a.f[0] = p->fac[0];
         a.f[1] = p->fac[1];
         a.f[2] = p->fac[2];
-        spttn_dev::launch_tttp3(a, s);
+        if (p->mode == 1)
+          spttn_dev::launch_tttp3_leaf(a, p->leaf_i, p->leaf_j, p->batch, s);
+        else
+          spttn_dev::launch_tttp3(a, s);
         break;
       case SPTTN_NEST_TTMC3:
         a.f[1] = p->fac[0];

@@ -110,16 +110,40 @@ __global__ void k_seg_splits(CsfView t, const int32_t* slice_seg, int64_t chunk,
 }
 
 // One block per split slice: TAIL of its first item + HEADs of the later
-// items, summed in item order (deterministic).
-__global__ void k_fixup(const int32_t* node, const int32_t* first, const int32_t* last,
-                        const int32_t* idx0, const double* part, int64_t tile, double* out) {
+// items. Columns of the tile map to threads; when the tile is narrower than
+// the block, several "item lanes" per column sum strided item subsets that
+// are then combined by a fixed shared-memory tree: the summation order is a
+// function of (items, block shape) only, so results are deterministic.
+constexpr int kFixThreads = 1024;
+
+__global__ void __launch_bounds__(kFixThreads) k_fixup(const int32_t* node, const int32_t* first,
+                                                       const int32_t* last, const int32_t* idx0,
+                                                       const double* part, int64_t tile,
+                                                       double* out) {
+  __shared__ double red[kFixThreads];
   const int32_t sidx = blockIdx.x;
   const int32_t f = first[sidx], g = last[sidx];
   const int64_t row = idx0[node[sidx]];
-  for (int64_t e = threadIdx.x; e < tile; e += blockDim.x) {
-    double sum = part[(static_cast<int64_t>(f) * 2 + 1) * tile + e];
-    for (int32_t it = f + 1; it <= g; ++it) sum += part[(static_cast<int64_t>(it) * 2) * tile + e];
-    out[row * tile + e] = sum;
+  const int cols = tile < kFixThreads ? static_cast<int>(tile) : kFixThreads;
+  const int lanes = kFixThreads / cols;  // item lanes per column (power of two not required)
+  const int col = threadIdx.x % cols;
+  const int il = threadIdx.x / cols;
+  for (int64_t e0 = 0; e0 < tile; e0 += cols) {
+    const int64_t e = e0 + col;
+    double sum = 0.0;
+    if (il < lanes && e < tile) {
+      if (il == 0) sum = part[(static_cast<int64_t>(f) * 2 + 1) * tile + e];
+      for (int32_t it = f + 1 + il; it <= g; it += lanes)
+        sum += part[(static_cast<int64_t>(it) * 2) * tile + e];
+    }
+    red[threadIdx.x] = sum;
+    __syncthreads();
+    if (il == 0 && e < tile) {
+      double tot = red[col];
+      for (int k = 1; k < lanes; ++k) tot += red[k * cols + col];
+      out[row * tile + e] = tot;
+    }
+    __syncthreads();
   }
 }
 
@@ -235,10 +259,49 @@ void build_segments(const DevCsf& csf, int unit_level, int seg_len, int64_t chun
   find_splits_and_absent(csf, d, true, s);
 }
 
+namespace {
+
+// parent coordinate broadcast one level down: child c of node n gets idx[n]
+__global__ void k_expand_level(const int32_t* ptr, const int32_t* coord, int32_t n,
+                               int32_t* child_coord) {
+  const int32_t node = blockIdx.x * blockDim.x + threadIdx.x;
+  if (node >= n) return;
+  const int32_t v = coord[node];
+  for (int32_t c = ptr[node]; c < ptr[node + 1]; ++c) child_coord[c] = v;
+}
+
+__global__ void k_gather_level(const int32_t* ptr, const int32_t* parent_val, int32_t n,
+                               int32_t* child_val) {
+  const int32_t node = blockIdx.x * blockDim.x + threadIdx.x;
+  if (node >= n) return;
+  const int32_t v = parent_val[node];
+  for (int32_t c = ptr[node]; c < ptr[node + 1]; ++c) child_val[c] = v;
+}
+
+}  // namespace
+
+void build_leaf_coords(const DevCsf& csf, int32_t** leaf_i, int32_t** leaf_j, cudaStream_t s) {
+  const int64_t n0 = csf.level_size[0], n1 = csf.level_size[1], nnz = csf.level_size[2];
+  int32_t* fib_i = nullptr;
+  SPTTN_CUDA(cudaMalloc(leaf_i, std::max<int64_t>(1, nnz) * sizeof(int32_t)));
+  SPTTN_CUDA(cudaMalloc(leaf_j, std::max<int64_t>(1, nnz) * sizeof(int32_t)));
+  SPTTN_CUDA(cudaMallocAsync(&fib_i, std::max<int64_t>(1, n1) * sizeof(int32_t), s));
+  if (n0 > 0)
+    k_expand_level<<<blocks_for(n0, 256), 256, 0, s>>>(csf.ptr[0], csf.idx[0],
+                                                       static_cast<int32_t>(n0), fib_i);
+  if (n1 > 0) {
+    k_expand_level<<<blocks_for(n1, 256), 256, 0, s>>>(csf.ptr[1], csf.idx[1],
+                                                       static_cast<int32_t>(n1), *leaf_j);
+    k_gather_level<<<blocks_for(n1, 256), 256, 0, s>>>(csf.ptr[1], fib_i,
+                                                       static_cast<int32_t>(n1), *leaf_i);
+  }
+  SPTTN_CUDA(cudaGetLastError());
+  SPTTN_CUDA(cudaFreeAsync(fib_i, s));
+}
+
 void launch_fixup(const Decomp& d, const CsfView& t, double* out, cudaStream_t s) {
   if (d.n_split > 0) {
-    const int threads = d.tile >= 256 ? 256 : (d.tile >= 64 ? 64 : 32);
-    k_fixup<<<static_cast<unsigned>(d.n_split), threads, 0, s>>>(
+    k_fixup<<<static_cast<unsigned>(d.n_split), kFixThreads, 0, s>>>(
         d.split_node, d.split_first, d.split_last, t.idx[0], d.part, d.tile, out);
     SPTTN_CUDA(cudaGetLastError());
   }

@@ -99,6 +99,10 @@ void launch_mttkrp4(const RootOutArgs& a, cudaStream_t s);
 void launch_tttp3(const RootOutArgs& a, cudaStream_t s);
 void launch_ttmc3(const RootOutArgs& a, cudaStream_t s);
 void launch_ttmc4(const RootOutArgs& a, cudaStream_t s);
+void launch_tttp3_leaf(const RootOutArgs& a, const int32_t* leaf_i, const int32_t* leaf_j,
+                       int batch, cudaStream_t s);
+// Per-leaf root / level-1 coordinates of an order-3 CSF (TTTP leaf kernel).
+void build_leaf_coords(const DevCsf& csf, int32_t** leaf_i, int32_t** leaf_j, cudaStream_t s);
 
 // group geometry used by the leaf-range kernels: lanes per group for a
 // padded row width (4 doubles per lane).

@@ -49,14 +49,16 @@ def main():
         with torch.cuda.stream(s):
             for _ in range(10):
                 flush.zero_()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
                 e0.record(s)
                 plan.execute_stage(0, s)
                 e1.record(s)
                 plan.execute_stage(1, s)
-                ts.append((e0, e1))
+                e2.record(s)
+                ts.append((e0, e1, e2))
         torch.cuda.synchronize()
-        ms = [a.elapsed_time(b) for a, b in ts]
+        ms = [a.elapsed_time(b) for a, b, _ in ts]
+        epi = statistics.median(b.elapsed_time(c) for _, b, c in ts)
         out = plan.read_output(s)
         if ref is None:
             ref = out
@@ -64,7 +66,7 @@ def main():
         else:
             err = float(np.max(np.abs(out - ref)) / max(1e-300, np.max(np.abs(ref))))
         info = plan.info()
-        print(f"{key} [{v}] kernel {statistics.median(ms)*1e3:8.1f} us (min {min(ms)*1e3:.1f})"
+        print(f"{key} [{v}] kernel {statistics.median(ms)*1e3:8.1f} us (min {min(ms)*1e3:.1f}) epi {epi*1e3:6.1f} us"
               f"  {flops/statistics.median(ms)/1e9:6.2f} TF/s  items {info['items']} "
               f"segs {info['segments']} split {info['split_slices']}  relerr {err:.2e}",
               flush=True)
