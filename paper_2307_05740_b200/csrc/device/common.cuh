@@ -41,6 +41,22 @@ __device__ __forceinline__ double2 ld128(const double* p) {
   return v;
 }
 
+// Ampere-style asynchronous global->shared copies (SASS LDGSTS): the CSF
+// streams of a work window are staged into shared memory one window ahead.
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 __device__ __forceinline__ int ldg_i32(const int32_t* p) { return __ldg(p); }
 __device__ __forceinline__ double ldg_f64(const double* p) { return __ldg(p); }
 

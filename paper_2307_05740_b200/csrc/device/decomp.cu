@@ -57,6 +57,15 @@ __global__ void k_absent(const unsigned char* present, int64_t dim0, int32_t* ro
   if (!present[i]) rows[atomicAdd(count, 1)] = static_cast<int32_t>(i);
 }
 
+// Parent coordinate broadcast one level down: child c of node n gets idx[n].
+__global__ void k_child_coord(const int32_t* ptr, const int32_t* coord, int32_t n,
+                              int32_t* child_coord) {
+  const int32_t node = blockIdx.x * blockDim.x + threadIdx.x;
+  if (node >= n) return;
+  const int32_t v = coord[node];
+  for (int32_t c = ptr[node]; c < ptr[node + 1]; ++c) child_coord[c] = v;
+}
+
 // Segment counts per unit node: ceil(children / seg_len).
 __global__ void k_seg_count(CsfView t, int unit_level, int seg_len, int32_t* cnt) {
   const int32_t f = blockIdx.x * blockDim.x + threadIdx.x;
@@ -66,25 +75,31 @@ __global__ void k_seg_count(CsfView t, int unit_level, int seg_len, int32_t* cnt
 }
 
 __global__ void k_seg_fill(CsfView t, int unit_level, int seg_len, const int32_t* off,
-                           int32_t* seg_begin, int32_t* seg_node) {
+                           const int32_t* unit_parent, int32_t* seg_begin, int32_t* seg_node,
+                           int32_t* seg_node1) {
   const int32_t f = blockIdx.x * blockDim.x + threadIdx.x;
   const int32_t nf = t.nlev[unit_level];
   if (f >= nf) return;
   const int32_t b = t.ptr[unit_level][f], e = t.ptr[unit_level][f + 1];
   const int32_t coord = t.idx[unit_level][f];
+  const int32_t pc = unit_parent ? unit_parent[f] : 0;
   int32_t o = off[f];
   for (int32_t x = b; x < e; x += seg_len, ++o) {
     seg_begin[o] = x;
     seg_node[o] = coord;
+    if (seg_node1) seg_node1[o] = pc;
   }
   if (f == nf - 1) seg_begin[o] = e;
 }
 
-// slice_seg[s] = first segment of root slice s (unit_level == 1).
-__global__ void k_slice_seg(CsfView t, const int32_t* off, int32_t* slice_seg) {
+// slice_seg[s] = first segment of root slice s: its first unit node is found
+// by following the child pointers from level 0 down to unit_level.
+__global__ void k_slice_seg(CsfView t, int unit_level, const int32_t* off, int32_t* slice_seg) {
   const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s > t.nlev[0]) return;
-  slice_seg[s] = off[t.ptr[0][s]];
+  int32_t node = s;
+  for (int l = 0; l < unit_level; ++l) node = t.ptr[l][node];
+  slice_seg[s] = off[node];
 }
 
 __global__ void k_seg_items(const int32_t* slice_seg, int32_t n0, int64_t chunk, int64_t n_items,
@@ -107,44 +122,6 @@ __global__ void k_seg_splits(CsfView t, const int32_t* slice_seg, int64_t chunk,
     last[slot] = static_cast<int32_t>(g);
   }
   present[t.idx[0][s]] = 1;
-}
-
-// One block per split slice: TAIL of its first item + HEADs of the later
-// items. Columns of the tile map to threads; when the tile is narrower than
-// the block, several "item lanes" per column sum strided item subsets that
-// are then combined by a fixed shared-memory tree: the summation order is a
-// function of (items, block shape) only, so results are deterministic.
-constexpr int kFixThreads = 1024;
-
-__global__ void __launch_bounds__(kFixThreads) k_fixup(const int32_t* node, const int32_t* first,
-                                                       const int32_t* last, const int32_t* idx0,
-                                                       const double* part, int64_t tile,
-                                                       double* out) {
-  __shared__ double red[kFixThreads];
-  const int32_t sidx = blockIdx.x;
-  const int32_t f = first[sidx], g = last[sidx];
-  const int64_t row = idx0[node[sidx]];
-  const int cols = tile < kFixThreads ? static_cast<int>(tile) : kFixThreads;
-  const int lanes = kFixThreads / cols;  // item lanes per column (power of two not required)
-  const int col = threadIdx.x % cols;
-  const int il = threadIdx.x / cols;
-  for (int64_t e0 = 0; e0 < tile; e0 += cols) {
-    const int64_t e = e0 + col;
-    double sum = 0.0;
-    if (il < lanes && e < tile) {
-      if (il == 0) sum = part[(static_cast<int64_t>(f) * 2 + 1) * tile + e];
-      for (int32_t it = f + 1 + il; it <= g; it += lanes)
-        sum += part[(static_cast<int64_t>(it) * 2) * tile + e];
-    }
-    red[threadIdx.x] = sum;
-    __syncthreads();
-    if (il == 0 && e < tile) {
-      double tot = red[col];
-      for (int k = 1; k < lanes; ++k) tot += red[k * cols + col];
-      out[row * tile + e] = tot;
-    }
-    __syncthreads();
-  }
 }
 
 __global__ void k_zero_rows(const int32_t* rows, int64_t n, int64_t tile, double* out) {
@@ -187,6 +164,7 @@ void find_splits_and_absent(const DevCsf& csf, Decomp& d, bool segments, cudaStr
   SPTTN_CUDA(cudaStreamSynchronize(s));
   d.n_split = h[0];
   d.n_absent = h[1];
+  build_fixup_chunks(d, s);
   SPTTN_CUDA(cudaFreeAsync(counts, s));
   SPTTN_CUDA(cudaFreeAsync(present, s));
 }
@@ -239,13 +217,22 @@ void build_segments(const DevCsf& csf, int unit_level, int seg_len, int64_t chun
   SPTTN_CUDA(cudaMalloc(&d.seg_node, std::max<int64_t>(1, nseg) * sizeof(int32_t)));
   SPTTN_CUDA(cudaMalloc(&d.slice_seg, (static_cast<int64_t>(n0) + 1) * sizeof(int32_t)));
   SPTTN_CUDA(cudaMemsetAsync(d.seg_begin, 0, sizeof(int32_t), s));
+  int32_t* unit_parent = nullptr;  // level-1 coordinate of each unit node (unit_level 2)
+  if (unit_level == 2) {
+    SPTTN_CUDA(cudaMalloc(&d.seg_node1, std::max<int64_t>(1, nseg) * sizeof(int32_t)));
+    SPTTN_CUDA(cudaMallocAsync(&unit_parent, std::max<int32_t>(1, nf) * sizeof(int32_t), s));
+    const int32_t n1 = static_cast<int32_t>(csf.level_size[1]);
+    if (n1 > 0)
+      k_child_coord<<<blocks_for(n1, 256), 256, 0, s>>>(t.ptr[1], t.idx[1], n1, unit_parent);
+  }
   if (nf > 0) {
-    k_seg_fill<<<blocks_for(nf, 256), 256, 0, s>>>(t, unit_level, seg_len, off, d.seg_begin,
-                                                   d.seg_node);
+    k_seg_fill<<<blocks_for(nf, 256), 256, 0, s>>>(t, unit_level, seg_len, off, unit_parent,
+                                                   d.seg_begin, d.seg_node, d.seg_node1);
     SPTTN_CUDA(cudaGetLastError());
   }
-  // unit_level is 1 for both TTMc kernels: slices own contiguous unit nodes.
-  k_slice_seg<<<blocks_for(static_cast<int64_t>(n0) + 1, 256), 256, 0, s>>>(t, off, d.slice_seg);
+  if (unit_parent) SPTTN_CUDA(cudaFreeAsync(unit_parent, s));
+  k_slice_seg<<<blocks_for(static_cast<int64_t>(n0) + 1, 256), 256, 0, s>>>(t, unit_level, off,
+                                                                          d.slice_seg);
   SPTTN_CUDA(cudaGetLastError());
   SPTTN_CUDA(cudaFreeAsync(off, s));
   d.n_items = (nseg + chunk - 1) / chunk;
@@ -259,27 +246,6 @@ void build_segments(const DevCsf& csf, int unit_level, int seg_len, int64_t chun
   find_splits_and_absent(csf, d, true, s);
 }
 
-namespace {
-
-// parent coordinate broadcast one level down: child c of node n gets idx[n]
-__global__ void k_expand_level(const int32_t* ptr, const int32_t* coord, int32_t n,
-                               int32_t* child_coord) {
-  const int32_t node = blockIdx.x * blockDim.x + threadIdx.x;
-  if (node >= n) return;
-  const int32_t v = coord[node];
-  for (int32_t c = ptr[node]; c < ptr[node + 1]; ++c) child_coord[c] = v;
-}
-
-__global__ void k_gather_level(const int32_t* ptr, const int32_t* parent_val, int32_t n,
-                               int32_t* child_val) {
-  const int32_t node = blockIdx.x * blockDim.x + threadIdx.x;
-  if (node >= n) return;
-  const int32_t v = parent_val[node];
-  for (int32_t c = ptr[node]; c < ptr[node + 1]; ++c) child_val[c] = v;
-}
-
-}  // namespace
-
 void build_leaf_coords(const DevCsf& csf, int32_t** leaf_i, int32_t** leaf_j, cudaStream_t s) {
   const int64_t n0 = csf.level_size[0], n1 = csf.level_size[1], nnz = csf.level_size[2];
   int32_t* fib_i = nullptr;
@@ -287,22 +253,91 @@ void build_leaf_coords(const DevCsf& csf, int32_t** leaf_i, int32_t** leaf_j, cu
   SPTTN_CUDA(cudaMalloc(leaf_j, std::max<int64_t>(1, nnz) * sizeof(int32_t)));
   SPTTN_CUDA(cudaMallocAsync(&fib_i, std::max<int64_t>(1, n1) * sizeof(int32_t), s));
   if (n0 > 0)
-    k_expand_level<<<blocks_for(n0, 256), 256, 0, s>>>(csf.ptr[0], csf.idx[0],
-                                                       static_cast<int32_t>(n0), fib_i);
+    k_child_coord<<<blocks_for(n0, 256), 256, 0, s>>>(csf.ptr[0], csf.idx[0],
+                                                      static_cast<int32_t>(n0), fib_i);
   if (n1 > 0) {
-    k_expand_level<<<blocks_for(n1, 256), 256, 0, s>>>(csf.ptr[1], csf.idx[1],
-                                                       static_cast<int32_t>(n1), *leaf_j);
-    k_gather_level<<<blocks_for(n1, 256), 256, 0, s>>>(csf.ptr[1], fib_i,
-                                                       static_cast<int32_t>(n1), *leaf_i);
+    k_child_coord<<<blocks_for(n1, 256), 256, 0, s>>>(csf.ptr[1], csf.idx[1],
+                                                      static_cast<int32_t>(n1), *leaf_j);
+    k_child_coord<<<blocks_for(n1, 256), 256, 0, s>>>(csf.ptr[1], fib_i,
+                                                      static_cast<int32_t>(n1), *leaf_i);
   }
   SPTTN_CUDA(cudaGetLastError());
   SPTTN_CUDA(cudaFreeAsync(fib_i, s));
 }
 
+namespace {
+
+// Two-level fix-up for slices spread over many items. Level 1: one block per
+// chunk of <= kFixChunk consecutive items of one split slice sums their
+// partial tiles (TAIL of the slice's first item, HEAD of the others) in item
+// order; level 2: one block per split slice sums its chunk tiles in chunk
+// order. Both orders are fixed by the plan, so results are deterministic.
+__global__ void k_fix1(const int32_t* chunk_split, const int32_t* chunk_lo,
+                       const int32_t* chunk_hi, const int32_t* split_first, const double* part,
+                       int64_t tile, double* part2) {
+  const int32_t c = blockIdx.x;
+  const int32_t first = split_first[chunk_split[c]];
+  const int32_t lo = chunk_lo[c], hi = chunk_hi[c];
+  for (int64_t e = threadIdx.x; e < tile; e += blockDim.x) {
+    double sum = 0.0;
+    for (int32_t it = lo; it <= hi; ++it)
+      sum += part[(static_cast<int64_t>(it) * 2 + (it == first ? 1 : 0)) * tile + e];
+    part2[static_cast<int64_t>(c) * tile + e] = sum;
+  }
+}
+
+__global__ void k_fix2(const int32_t* split_node, const int32_t* split_chunk, const int32_t* idx0,
+                       const double* part2, int64_t tile, double* out) {
+  const int32_t sidx = blockIdx.x;
+  const int32_t c0 = split_chunk[sidx], c1 = split_chunk[sidx + 1];
+  const int64_t row = idx0[split_node[sidx]];
+  for (int64_t e = threadIdx.x; e < tile; e += blockDim.x) {
+    double sum = part2[static_cast<int64_t>(c0) * tile + e];
+    for (int32_t c = c0 + 1; c < c1; ++c) sum += part2[static_cast<int64_t>(c) * tile + e];
+    out[row * tile + e] = sum;
+  }
+}
+
+}  // namespace
+
+void build_fixup_chunks(Decomp& d, cudaStream_t s) {
+  if (d.n_split == 0) return;
+  std::vector<int32_t> first(d.n_split), last(d.n_split);
+  SPTTN_CUDA(cudaMemcpyAsync(first.data(), d.split_first, d.n_split * sizeof(int32_t),
+                             cudaMemcpyDeviceToHost, s));
+  SPTTN_CUDA(cudaMemcpyAsync(last.data(), d.split_last, d.n_split * sizeof(int32_t),
+                             cudaMemcpyDeviceToHost, s));
+  SPTTN_CUDA(cudaStreamSynchronize(s));
+  std::vector<int32_t> cs, clo, chi, sc(d.n_split + 1, 0);
+  for (int64_t k = 0; k < d.n_split; ++k) {
+    sc[k] = static_cast<int32_t>(cs.size());
+    for (int32_t lo = first[k]; lo <= last[k]; lo += kFixChunk) {
+      cs.push_back(static_cast<int32_t>(k));
+      clo.push_back(lo);
+      chi.push_back(std::min(last[k], lo + kFixChunk - 1));
+    }
+  }
+  sc[d.n_split] = static_cast<int32_t>(cs.size());
+  d.n_chunk = static_cast<int64_t>(cs.size());
+  auto up = [&](int32_t** dst, const std::vector<int32_t>& v) {
+    SPTTN_CUDA(cudaMalloc(dst, std::max<size_t>(1, v.size()) * sizeof(int32_t)));
+    SPTTN_CUDA(cudaMemcpyAsync(*dst, v.data(), v.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  };
+  up(&d.chunk_split, cs);
+  up(&d.chunk_lo, clo);
+  up(&d.chunk_hi, chi);
+  up(&d.split_chunk, sc);
+  SPTTN_CUDA(cudaMalloc(&d.part2, std::max<int64_t>(1, d.n_chunk * d.tile) * sizeof(double)));
+  SPTTN_CUDA(cudaStreamSynchronize(s));
+}
+
 void launch_fixup(const Decomp& d, const CsfView& t, double* out, cudaStream_t s) {
   if (d.n_split > 0) {
-    k_fixup<<<static_cast<unsigned>(d.n_split), kFixThreads, 0, s>>>(
-        d.split_node, d.split_first, d.split_last, t.idx[0], d.part, d.tile, out);
+    const int threads = d.tile >= 256 ? 256 : (d.tile >= 128 ? 128 : (d.tile >= 64 ? 64 : 32));
+    k_fix1<<<static_cast<unsigned>(d.n_chunk), threads, 0, s>>>(
+        d.chunk_split, d.chunk_lo, d.chunk_hi, d.split_first, d.part, d.tile, d.part2);
+    k_fix2<<<static_cast<unsigned>(d.n_split), threads, 0, s>>>(d.split_node, d.split_chunk,
+                                                                 t.idx[0], d.part2, d.tile, out);
     SPTTN_CUDA(cudaGetLastError());
   }
   if (d.n_absent > 0) {
@@ -321,6 +356,12 @@ void free_decomp(Decomp& d) {
   cudaFree(d.absent_rows);
   cudaFree(d.seg_begin);
   cudaFree(d.seg_node);
+  cudaFree(d.seg_node1);
+  cudaFree(d.chunk_split);
+  cudaFree(d.chunk_lo);
+  cudaFree(d.chunk_hi);
+  cudaFree(d.split_chunk);
+  cudaFree(d.part2);
   cudaFree(d.slice_seg);
   d = Decomp{};
 }

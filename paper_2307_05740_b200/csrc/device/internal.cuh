@@ -72,6 +72,14 @@ struct Decomp {
   int32_t seg_len = 0;
   int32_t* seg_begin = nullptr;    // [n_seg+1] child-node (or leaf) offsets
   int32_t* seg_node = nullptr;     // [n_seg]  coordinate of the segment's fiber
+  int32_t* seg_node1 = nullptr;    // [n_seg]  level-1 coordinate (unit level 2 only)
+  // two-level fix-up: chunks of <= kFixChunk items per split slice
+  int64_t n_chunk = 0;
+  int32_t* chunk_split = nullptr;
+  int32_t* chunk_lo = nullptr;
+  int32_t* chunk_hi = nullptr;
+  int32_t* split_chunk = nullptr;  // [n_split+1] first chunk of each split slice
+  double* part2 = nullptr;         // [n_chunk][tile]
   int32_t* slice_seg = nullptr;    // [n0+1]   segment offset of each slice
 };
 
@@ -99,6 +107,9 @@ void launch_mttkrp4(const RootOutArgs& a, cudaStream_t s);
 void launch_tttp3(const RootOutArgs& a, cudaStream_t s);
 void launch_ttmc3(const RootOutArgs& a, cudaStream_t s);
 void launch_ttmc4(const RootOutArgs& a, cudaStream_t s);
+// Segment-form MTTKRP (R <= 32): order 3 units = level-1 fibers, order 4 =
+// level-2 fibers (seg_node1 carries the level-1 coordinate).
+void launch_mttkrp_seg(const RootOutArgs& a, const int32_t* seg_node1, int order, cudaStream_t s);
 void launch_tttp3_leaf(const RootOutArgs& a, const int32_t* leaf_i, const int32_t* leaf_j,
                        int batch, cudaStream_t s);
 // Per-leaf root / level-1 coordinates of an order-3 CSF (TTTP leaf kernel).
@@ -112,6 +123,8 @@ int group_lanes_for(int R);
 void build_leaf_items(const DevCsf& csf, int64_t chunk, Decomp& d, int64_t tile, cudaStream_t s);
 void build_segments(const DevCsf& csf, int unit_level, int seg_len, int64_t chunk, Decomp& d,
                     int64_t tile, cudaStream_t s);
+constexpr int kFixChunk = 32;
+void build_fixup_chunks(Decomp& d, cudaStream_t s);
 void launch_fixup(const Decomp& d, const CsfView& t, double* out, cudaStream_t s);
 void free_decomp(Decomp& d);
 

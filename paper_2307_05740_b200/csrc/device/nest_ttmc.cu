@@ -416,6 +416,158 @@ __global__ void __launch_bounds__(kBlock, 3) k_ttmc3p(RootOutArgs a) {
   if (pending) flush(head ? 0 : 1);
 }
 
+// Stream-staged variant (default). The warp's CSF stream — segment metadata
+// and the leaves' coordinates / values — is copied into a per-warp shared
+// memory ring with cp.async (LDGSTS) one 32-segment window ahead (metadata
+// two windows ahead, since a window's leaf range comes from its metadata),
+// so HBM latency never sits on the critical path; the only round trip left
+// per 4-segment step is the factor-row gather (L1/L2 resident rows).
+constexpr int kWin = 32;
+constexpr int kWinLeaves = kWin * 4;  // seg_len <= 4
+
+struct Stage3 {
+  int32_t sb[3][kWin + 1];
+  int32_t sn[3][kWin];
+  int32_t kk[2][kWinLeaves];
+  double tv[2][kWinLeaves];
+};
+
+template <bool VECU, bool VECV>
+__global__ void __launch_bounds__(kBlock, 3) k_ttmc3s(RootOutArgs a) {
+  __shared__ Stage3 stage[kBlock / 32];
+  const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
+  if (w >= a.n_items) return;  // warp-uniform
+  Stage3& S = stage[threadIdx.x / 32];
+  const int lane = threadIdx.x & 31;
+  const int q = lane & 3;
+  const int h = lane >> 2;
+  const int R = a.R, S_ = a.S;
+  const CsfView& t = a.t;
+  const double* __restrict__ U = a.f[1];
+  const double* __restrict__ V = a.f[2];
+  const int32_t* __restrict__ kidx = t.idx[2];
+  const double* __restrict__ vals = t.vals;
+  const int32_t* __restrict__ seg_begin = a.seg_begin;
+  const int32_t* __restrict__ seg_node = a.seg_node;
+  const int32_t* __restrict__ slice_seg = a.slice_seg;
+
+  const int32_t cbeg = static_cast<int32_t>(w * a.chunk);
+  const int32_t cend = static_cast<int32_t>(min64(cbeg + a.chunk, a.n_seg));
+  int32_t sl = a.item_pos[w];
+  int32_t sl_end = slice_seg[sl + 1];
+  bool head = slice_seg[sl] < cbeg;
+  int32_t row = t.idx[0][sl];
+  // one-slice lookahead so slice switches do not wait on global loads
+  int32_t nx_end = sl + 2 <= t.nlev[0] ? __ldg(slice_seg + sl + 2) : 0;
+  int32_t nx_row = sl + 1 < t.nlev[0] ? __ldg(t.idx[0] + sl + 1) : 0;
+  bool pending = false;
+  double acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.0;
+
+  auto flush = [&](int slot) {
+    double* dst = slot < 0 ? a.out + static_cast<int64_t>(row) * R * S_
+                           : a.part + (w * 2 + slot) * static_cast<int64_t>(R) * S_;
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = 2 * h + mt;
+          const int s = 2 * (2 * q + e) + nt;
+          if (r < R && s < S_) dst[r * S_ + s] = acc[(mt * 2 + nt) * 2 + e];
+        }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = 0.0;
+  };
+  auto issue_meta = [&](int buf, int32_t ws) {
+    const int32_t nsw = min(ws + kWin, cend) - ws;
+    if (lane <= nsw) cp_async4(&S.sb[buf][lane], seg_begin + ws + lane);
+    if (lane == 0 && nsw == kWin) cp_async4(&S.sb[buf][kWin], seg_begin + ws + kWin);
+    if (lane < nsw) cp_async4(&S.sn[buf][lane], seg_node + ws + lane);
+  };
+  auto issue_leaves = [&](int lbuf, int mbuf, int32_t ws) {
+    const int32_t nsw = min(ws + kWin, cend) - ws;
+    const int32_t L0 = S.sb[mbuf][0];
+    const int32_t nl = S.sb[mbuf][nsw] - L0;
+    for (int32_t i = lane; i < nl; i += 32) {
+      cp_async4(&S.kk[lbuf][i], kidx + L0 + i);
+      cp_async8(&S.tv[lbuf][i], vals + L0 + i);
+    }
+  };
+
+  const int32_t nwin = (cend - cbeg + kWin - 1) / kWin;
+  issue_meta(0, cbeg);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncwarp();
+  issue_leaves(0, 0, cbeg);
+  if (nwin > 1) issue_meta(1, cbeg + kWin);
+  cp_async_commit();
+  int32_t cs = cbeg;
+  for (int32_t win = 0; win < nwin; ++win) {
+    cp_async_wait<0>();
+    __syncwarp();
+    const int mb = win % 3, lbf = win & 1;
+    const int32_t ws = cbeg + win * kWin;
+    if (win + 1 < nwin) issue_leaves((win + 1) & 1, (win + 1) % 3, ws + kWin);
+    if (win + 2 < nwin) issue_meta((win + 2) % 3, ws + 2 * kWin);
+    cp_async_commit();
+    const int32_t we = min(ws + kWin, cend);
+    const int32_t L0 = S.sb[mb][0];
+    while (cs < we) {
+      const int32_t lim = min(we, sl_end);
+      const int nv = min(4, lim - cs);
+      const int r = cs - ws + q;
+      const bool valid = q < nv;
+      int32_t lb = 0, n = 0, j = 0;
+      if (valid) {
+        lb = S.sb[mb][r] - L0;
+        n = S.sb[mb][r + 1] - S.sb[mb][r];
+        j = S.sn[mb][r];
+      }
+      double2 vr[4];
+      double tt[4];
+#pragma unroll
+      for (int it = 0; it < 4; ++it) {
+        const int32_t k = it < n ? S.kk[lbf][lb + it] : 0;
+        tt[it] = it < n ? S.tv[lbf][lb + it] : 0.0;
+        vr[it] = it < n ? row2<VECV>(V + static_cast<int64_t>(k) * S_, 2 * h, S_)
+                        : make_double2(0, 0);
+      }
+      const double2 u = valid ? row2<VECU>(U + static_cast<int64_t>(j) * R, 2 * h, R)
+                              : make_double2(0, 0);
+      double x0 = 0.0, x1 = 0.0;
+#pragma unroll
+      for (int it = 0; it < 4; ++it) {
+        x0 = fma(tt[it], vr[it].x, x0);  // X[s] += t * V[k,s]
+        x1 = fma(tt[it], vr[it].y, x1);
+      }
+      dmma_8x8x4(acc[0], acc[1], u.x, x0);
+      dmma_8x8x4(acc[2], acc[3], u.x, x1);
+      dmma_8x8x4(acc[4], acc[5], u.y, x0);
+      dmma_8x8x4(acc[6], acc[7], u.y, x1);
+      pending = true;
+      cs += nv;
+      if (cs == sl_end) {
+        flush(head ? 0 : -1);
+        pending = false;
+        head = false;
+        if (cs < cend) {
+          ++sl;
+          sl_end = nx_end;
+          row = nx_row;
+          nx_end = sl + 2 <= t.nlev[0] ? __ldg(slice_seg + sl + 2) : 0;
+          nx_row = sl + 1 < t.nlev[0] ? __ldg(t.idx[0] + sl + 1) : 0;
+        }
+      }
+    }
+    __syncwarp();
+  }
+  if (pending) flush(head ? 0 : 1);
+}
+
 template <bool VECV>
 __global__ void __launch_bounds__(kBlock) k_ttmc4(RootOutArgs a) {
   const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
@@ -542,6 +694,18 @@ void launch_ttmc3(const RootOutArgs& a, cudaStream_t s) {
   if (blocks == 0) return;
   const bool vu = a.vec & 1, vv = a.vec & 2;
   const int mode = a.flags >> 8;  // kernel variant chosen at plan time
+  if (mode == 4) {
+    if (vu && vv)
+      k_ttmc3s<true, true><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
+    else if (vu)
+      k_ttmc3s<true, false><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
+    else if (vv)
+      k_ttmc3s<false, true><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
+    else
+      k_ttmc3s<false, false><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
+    SPTTN_CUDA(cudaGetLastError());
+    return;
+  }
   if (mode == 3) {
     if (vu && vv)
       k_ttmc3p<true, true><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
