@@ -211,22 +211,10 @@ def ref_args(w):
     return c.kernel, dims, c.path, c.order_text
 
 
-CPU_NS_PER_NNZ = {1: 600, 2: 800, 3: 5000, 4: 1500, 5: 1200}  # survey-measured scale
-
-
-def cpu_sample(w, seconds, threads):
-    """Every k-th root slice, k chosen so the reference needs ~`seconds`."""
-    est = w.csf.nnz * CPU_NS_PER_NNZ[w.cfg.kind] * 1e-9 / max(1, threads)
-    stride = max(1, int(np.ceil(est / seconds)))
-    sub = w.csf if stride == 1 else w.csf.root_sample(stride)
-    return sub, stride
-
-
-def cpu_reference(w, seconds, threads, repeats=1):
+def _ref_run(w, sub, threads, repeats=1):
     sys.path.insert(0, str(ROOT / "tests"))
     import oracle_bindings as OB  # the reference build (test infrastructure)
     from paper_2307_05740_b200.configs import Workload
-    sub, stride = cpu_sample(w, seconds, threads)
     ws = Workload(w.cfg, sub, w.factors, w.dims, sub.nnz)
     kernel, dims, path, order = ref_args(w)
     if w.cfg.residual:  # reference flow for rho: S on unit values (SURVEY.md §0.6)
@@ -234,10 +222,37 @@ def cpu_reference(w, seconds, threads, repeats=1):
     if threads == 1:
         _, st = OB.ref_execute(kernel, dims, path, order, sub, w.factors, ws.out_count,
                                repeats=repeats)
-        secs = st["seconds"]
-    else:
-        _, secs = OB.ref_execute_threads(kernel, dims, path, order, sub, w.factors, ws.out_count,
-                                         threads, repeats=repeats)
+        return st["seconds"]
+    _, secs = OB.ref_execute_threads(kernel, dims, path, order, sub, w.factors, ws.out_count,
+                                     threads, repeats=repeats)
+    return secs
+
+
+def cpu_sample(w, seconds, threads):
+    """Every k-th root slice of the tensor, k calibrated on a ~1/64 probe so
+    the reference executor needs about `seconds`."""
+    n0 = w.csf.level_sizes()[0]
+    # two probes (1/64 and 1/16 of the root slices) fit t = fixed + per_nnz * nnz;
+    # the fixed part (the reference allocates and zeroes the whole dense
+    # output every execute) does not shrink with the sample.
+    pts = []
+    for frac in (64, 16):
+        st = max(1, n0 // frac)
+        probe = w.csf if st == 1 else w.csf.root_sample(st)
+        pts.append((probe.nnz, _ref_run(w, probe, threads)))
+    (n1, t1), (n2, t2) = pts
+    per = max((t2 - t1) / max(1, n2 - n1), 1e-12)
+    fixed = max(0.0, t1 - per * n1)
+    budget = max(seconds - fixed, 0.25 * seconds)
+    stride = max(1, int(np.ceil(per * w.csf.nnz / budget)))
+    sub = w.csf if stride == 1 else w.csf.root_sample(stride)
+    return sub, stride
+
+
+def cpu_reference(w, seconds, threads, repeats=1, sample=None):
+    sub, stride = sample if sample is not None else cpu_sample(w, seconds, threads)
+    path = ref_args(w)[2]
+    secs = _ref_run(w, sub, threads, repeats)
     return {"value": sub.nnz / secs, "unit": "nnz/s", "cores": threads, "kind": "reference",
             "sample": f"every {stride}th root slice of the same tensor: {sub.nnz} nnz "
                       f"({sub.level_sizes()[0]} slices), best of {repeats}, spttn_ref::execute "
@@ -251,11 +266,12 @@ def run_reference_impl(args, rank, world):
         return
     threads = os.cpu_count() or 1
     w = make_workload(HEADLINE)
+    # one bounded sample, sized so all warmup + timed steps take ~cpu_seconds
+    sample = cpu_sample(w, args.cpu_seconds / max(1, args.steps + args.warmup), threads)
     vals = []
     res = None
     for step in range(args.warmup + args.steps):
-        res = cpu_reference(w, args.cpu_seconds / max(1, args.steps + args.warmup) * threads,
-                            threads)
+        res = cpu_reference(w, 0, threads, sample=sample)
         if step >= args.warmup:
             vals.append(res["value"])
     v = statistics.median(vals)

@@ -393,8 +393,9 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
         int seg_len = static_cast<int>(
             env_int("SPTTN_SEG_LEN", p->kind == SPTTN_NEST_TTMC3 ? 4 : 8));
         if (p->kind == SPTTN_NEST_TTMC3) {
-          // 3 = pipelined direct-load kernel (default); 0-2 = earlier variants
-          p->mode = static_cast<int>(env_int("SPTTN_TTMC3_MODE", 3));
+          // 4 = stream-staged kernel (default); 3 = pipelined direct loads;
+          // 0-2 = earlier variants kept for A/B measurements (tools/sweep.py)
+          p->mode = static_cast<int>(env_int("SPTTN_TTMC3_MODE", 4));
           seg_len = std::clamp(seg_len, 1, p->mode == 0 ? 8 : 4);
         }
         seg_len = std::max(seg_len, 1);
