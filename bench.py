@@ -184,13 +184,15 @@ def e2e_config(P, w, steps, stream):
     h2d = sum(t.numel() * 8 for t in pin_idx + pin_ptr) + pin_val.numel() * 8 + \
         sum(t.numel() * 8 for t in pin_fac)
     d2h = w.out_count * 8
-    times = []
+    times, parts = [], []
     for it in range(steps + 1):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         dev = P.DeviceCsf(host, stream=stream)
+        ta = time.perf_counter()
         plan = P.Plan(c.kind, dev, [t.numpy() for t in pin_fac], ranks=c.ranks,
                       flags=P.FLAG_RESIDUAL if c.residual else 0, stream=stream)
+        tb = time.perf_counter()
         plan.execute(stream)
         plan.read_output(stream, out=out.numpy())
         t1 = time.perf_counter()
@@ -198,8 +200,12 @@ def e2e_config(P, w, steps, stream):
         dev.close()
         if it > 0:
             times.append(t1 - t0)
+            parts.append((ta - t0, tb - ta, t1 - tb))
+    brk = [statistics.mean(p[i] for p in parts) * 1e3 for i in range(3)]
     return {"seconds": statistics.mean(times), "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(d2h)}
+            "d2h_bytes_per_step": int(d2h),
+            "breakdown_ms": {"csf_h2d_layout": brk[0], "plan_h2d_decomp": brk[1],
+                             "execute_d2h": brk[2]}}
 
 
 def ref_args(w):
@@ -237,7 +243,7 @@ def cpu_sample(w, seconds, threads):
     # output every execute) does not shrink with the sample.
     pts = []
     for frac in (64, 16):
-        st = max(1, n0 // frac)
+        st = max(1, min(frac, n0 // 4))  # every st-th slice ~ 1/st of the tensor
         probe = w.csf if st == 1 else w.csf.root_sample(st)
         pts.append((probe.nnz, _ref_run(w, probe, threads)))
     (n1, t1), (n2, t2) = pts
@@ -376,7 +382,8 @@ def main():
                 secs = float(t.item())
             r["e2e"] = {"value": nnz * world / secs, "unit": "nnz/s",
                         "h2d_bytes_per_step": e["h2d_bytes_per_step"],
-                        "d2h_bytes_per_step": e["d2h_bytes_per_step"], "ms_per_step": secs * 1e3}
+                        "d2h_bytes_per_step": e["d2h_bytes_per_step"], "ms_per_step": secs * 1e3,
+                        "breakdown_ms": e["breakdown_ms"]}
         if rank == 0 and world == 1 and not args.no_cpu:
             r["cpu_baseline"] = cpu_reference(w, args.cpu_seconds, 1)
         if key == HEADLINE:
