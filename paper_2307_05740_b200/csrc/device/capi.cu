@@ -388,6 +388,8 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
         const bool vv = p->kind == SPTTN_NEST_TTMC3 ? (S % 2 == 0 && facs_aligned16)
                                                     : (S == 8 && facs_aligned32);
         p->vec = (vu ? 1 : 0) | (vv ? 2 : 0);
+        if (p->kind == SPTTN_NEST_TTMC3)  // 256-bit row gathers (wide kernel)
+          p->vec |= ((R % 4 == 0) && facs_aligned32 ? 4 : 0) | ((S % 4 == 0) && facs_aligned32 ? 8 : 0);
         // TTMc-3 stages a group's <= 4 segments of leaves in one warp-wide
         // register block: seg_len <= 8.
         int seg_len = static_cast<int>(

@@ -568,6 +568,166 @@ __global__ void __launch_bounds__(kBlock, 3) k_ttmc3s(RootOutArgs a) {
   if (pending) flush(head ? 0 : 1);
 }
 
+// Wide-gather variant (default): 8 segments per warp step as two DMMA
+// K-chunks. Lane L = (q = L%4, c4 = (L/4)%4, ch = L/16) handles segment
+// ch*4+q and the 4 rank columns [4*c4, 4*c4+4) of its factor rows, so every
+// gather is one 256-bit load (4 lanes per 128-byte row, 8 rows per
+// instruction) — measured 123 B/clk/SM from L1 against 84 B/clk/SM for
+// 16-byte lanes (tools/gather_probe.cu). One xor-16 exchange of two doubles
+// then turns the per-lane column quads into the DMMA fragments of both
+// K-chunks, with rows / columns interleaved as r|s = 4(h%4) + 2(h/4) + t.
+template <bool VECU, bool VECV>
+__global__ void __launch_bounds__(kBlock, 3) k_ttmc3w(RootOutArgs a) {
+  __shared__ Stage3 stage[kBlock / 32];
+  const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
+  if (w >= a.n_items) return;  // warp-uniform
+  Stage3& S = stage[threadIdx.x / 32];
+  const int lane = threadIdx.x & 31;
+  const int q = lane & 3;
+  const int c4 = (lane >> 2) & 3;
+  const int ch = lane >> 4;
+  const int slot = ch * 4 + q;
+  const int h = lane >> 2;
+  const int R = a.R, S_ = a.S;
+  const CsfView& t = a.t;
+  const double* __restrict__ U = a.f[1];
+  const double* __restrict__ V = a.f[2];
+  const int32_t* __restrict__ kidx = t.idx[2];
+  const double* __restrict__ vals = t.vals;
+  const int32_t* __restrict__ seg_begin = a.seg_begin;
+  const int32_t* __restrict__ seg_node = a.seg_node;
+  const int32_t* __restrict__ slice_seg = a.slice_seg;
+
+  const int32_t cbeg = static_cast<int32_t>(w * a.chunk);
+  const int32_t cend = static_cast<int32_t>(min64(cbeg + a.chunk, a.n_seg));
+  int32_t sl = a.item_pos[w];
+  int32_t sl_end = slice_seg[sl + 1];
+  bool head = slice_seg[sl] < cbeg;
+  int32_t row = t.idx[0][sl];
+  int32_t nx_end = sl + 2 <= t.nlev[0] ? __ldg(slice_seg + sl + 2) : 0;
+  int32_t nx_row = sl + 1 < t.nlev[0] ? __ldg(t.idx[0] + sl + 1) : 0;
+  bool pending = false;
+  double acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.0;
+
+  auto flush = [&](int dslot) {
+    double* dst = dslot < 0 ? a.out + static_cast<int64_t>(row) * R * S_
+                            : a.part + (w * 2 + dslot) * static_cast<int64_t>(R) * S_;
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = 4 * (h & 3) + 2 * (h >> 2) + mt;
+          const int n = 2 * q + e;
+          const int s = 4 * (n & 3) + 2 * (n >> 2) + nt;
+          if (r < R && s < S_) dst[r * S_ + s] = acc[(mt * 2 + nt) * 2 + e];
+        }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = 0.0;
+  };
+  auto issue_meta = [&](int buf, int32_t ws) {
+    const int32_t nsw = min(ws + kWin, cend) - ws;
+    if (lane <= nsw) cp_async4(&S.sb[buf][lane], seg_begin + ws + lane);
+    if (lane == 0 && nsw == kWin) cp_async4(&S.sb[buf][kWin], seg_begin + ws + kWin);
+    if (lane < nsw) cp_async4(&S.sn[buf][lane], seg_node + ws + lane);
+  };
+  auto issue_leaves = [&](int lbuf, int mbuf, int32_t ws) {
+    const int32_t nsw = min(ws + kWin, cend) - ws;
+    const int32_t L0 = S.sb[mbuf][0];
+    const int32_t nl = S.sb[mbuf][nsw] - L0;
+    for (int32_t i = lane; i < nl; i += 32) {
+      cp_async4(&S.kk[lbuf][i], kidx + L0 + i);
+      cp_async8(&S.tv[lbuf][i], vals + L0 + i);
+    }
+  };
+
+  const int32_t nwin = (cend - cbeg + kWin - 1) / kWin;
+  issue_meta(0, cbeg);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncwarp();
+  issue_leaves(0, 0, cbeg);
+  if (nwin > 1) issue_meta(1, cbeg + kWin);
+  cp_async_commit();
+  int32_t cs = cbeg;
+  for (int32_t win = 0; win < nwin; ++win) {
+    cp_async_wait<0>();
+    __syncwarp();
+    const int mb = win % 3, lbf = win & 1;
+    const int32_t ws = cbeg + win * kWin;
+    if (win + 1 < nwin) issue_leaves((win + 1) & 1, (win + 1) % 3, ws + kWin);
+    if (win + 2 < nwin) issue_meta((win + 2) % 3, ws + 2 * kWin);
+    cp_async_commit();
+    const int32_t we = min(ws + kWin, cend);
+    const int32_t L0 = S.sb[mb][0];
+    while (cs < we) {
+      const int32_t lim = min(we, sl_end);
+      const int nv = min(8, lim - cs);
+      const int r = cs - ws + slot;
+      const bool valid = slot < nv;
+      int32_t lb = 0, n = 0, j = 0;
+      if (valid) {
+        lb = S.sb[mb][r] - L0;
+        n = S.sb[mb][r + 1] - S.sb[mb][r];
+        j = S.sn[mb][r];
+      }
+      double4 vr[4];
+      double tt[4];
+#pragma unroll
+      for (int it = 0; it < 4; ++it) {
+        const int32_t k = it < n ? S.kk[lbf][lb + it] : 0;
+        tt[it] = it < n ? S.tv[lbf][lb + it] : 0.0;
+        vr[it] = it < n ? row4<VECV>(V + static_cast<int64_t>(k) * S_, 4 * c4, S_)
+                        : make_double4(0, 0, 0, 0);
+      }
+      const double4 ur = valid ? row4<VECU>(U + static_cast<int64_t>(j) * R, 4 * c4, R)
+                               : make_double4(0, 0, 0, 0);
+      double4 x = make_double4(0, 0, 0, 0);
+#pragma unroll
+      for (int it = 0; it < 4; ++it) fma4(x, tt[it], vr[it]);  // X[s] += t * V[k,s]
+      // column quads -> fragments of both K-chunks (one xor-16 exchange)
+      const double sx0 = ch == 0 ? x.z : x.x, sx1 = ch == 0 ? x.w : x.y;
+      const double su0 = ch == 0 ? ur.z : ur.x, su1 = ch == 0 ? ur.w : ur.y;
+      const double rx0 = __shfl_xor_sync(0xffffffffu, sx0, 16);
+      const double rx1 = __shfl_xor_sync(0xffffffffu, sx1, 16);
+      const double ru0 = __shfl_xor_sync(0xffffffffu, su0, 16);
+      const double ru1 = __shfl_xor_sync(0xffffffffu, su1, 16);
+      const double bA0 = ch == 0 ? x.x : rx0, bA1 = ch == 0 ? x.y : rx1;
+      const double bB0 = ch == 0 ? rx0 : x.z, bB1 = ch == 0 ? rx1 : x.w;
+      const double aA0 = ch == 0 ? ur.x : ru0, aA1 = ch == 0 ? ur.y : ru1;
+      const double aB0 = ch == 0 ? ru0 : ur.z, aB1 = ch == 0 ? ru1 : ur.w;
+      // rank-1 updates of 8 segments: two K-chunks into the same 16x16 tile
+      dmma_8x8x4(acc[0], acc[1], aA0, bA0);
+      dmma_8x8x4(acc[2], acc[3], aA0, bA1);
+      dmma_8x8x4(acc[4], acc[5], aA1, bA0);
+      dmma_8x8x4(acc[6], acc[7], aA1, bA1);
+      dmma_8x8x4(acc[0], acc[1], aB0, bB0);
+      dmma_8x8x4(acc[2], acc[3], aB0, bB1);
+      dmma_8x8x4(acc[4], acc[5], aB1, bB0);
+      dmma_8x8x4(acc[6], acc[7], aB1, bB1);
+      pending = true;
+      cs += nv;
+      if (cs == sl_end) {
+        flush(head ? 0 : -1);
+        pending = false;
+        head = false;
+        if (cs < cend) {
+          ++sl;
+          sl_end = nx_end;
+          row = nx_row;
+          nx_end = sl + 2 <= t.nlev[0] ? __ldg(slice_seg + sl + 2) : 0;
+          nx_row = sl + 1 < t.nlev[0] ? __ldg(t.idx[0] + sl + 1) : 0;
+        }
+      }
+    }
+    __syncwarp();
+  }
+  if (pending) flush(head ? 0 : 1);
+}
+
 template <bool VECV>
 __global__ void __launch_bounds__(kBlock) k_ttmc4(RootOutArgs a) {
   const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
@@ -694,6 +854,20 @@ void launch_ttmc3(const RootOutArgs& a, cudaStream_t s) {
   if (blocks == 0) return;
   const bool vu = a.vec & 1, vv = a.vec & 2;
   const int mode = a.flags >> 8;  // kernel variant chosen at plan time
+  if (mode == 5) {
+    // wide gathers need 32-byte aligned rows: R, S multiples of 4 (a.vec bits 4/8)
+    const bool wu = a.vec & 4, wv = a.vec & 8;
+    if (wu && wv)
+      k_ttmc3w<true, true><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
+    else if (wu)
+      k_ttmc3w<true, false><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
+    else if (wv)
+      k_ttmc3w<false, true><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
+    else
+      k_ttmc3w<false, false><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
+    SPTTN_CUDA(cudaGetLastError());
+    return;
+  }
   if (mode == 4) {
     if (vu && vv)
       k_ttmc3s<true, true><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
