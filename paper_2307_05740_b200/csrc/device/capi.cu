@@ -405,7 +405,17 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
         const int64_t warps = static_cast<int64_t>(sms) * 32 * 2;
         int64_t chunk = env_int("SPTTN_CHUNK", 0);
         if (chunk <= 0) chunk = std::clamp<int64_t>((units + warps - 1) / warps, 8, 1024);
-        spttn_dev::build_segments(D, 1, seg_len, chunk, p->dec, tile, s);
+        if (p->kind == SPTTN_NEST_TTMC3 && (p->mode == 6 || p->mode == 7)) {
+          // packed length-sorted groups of 8 segments (pack.cu)
+          spttn_dev::build_segments(D, 1, seg_len, chunk, p->dec, tile, s, false);
+          spttn_dev::build_packed(D, 2, p->dec, s);
+          int64_t gchunk = env_int("SPTTN_GCHUNK", 0);
+          if (gchunk <= 0)
+            gchunk = std::clamp<int64_t>((p->dec.n_groups + warps - 1) / warps, 4, 512);
+          spttn_dev::finish_unit_items(D, p->dec, p->dec.slice_grp, p->dec.n_groups, gchunk, tile, s);
+        } else {
+          spttn_dev::build_segments(D, 1, seg_len, chunk, p->dec, tile, s);
+        }
       } else if (!sparse_out && R <= 32 && env_int("SPTTN_MTTKRP_MODE", 1) == 1) {
         // segment-form MTTKRP (default for R <= 32)
         p->mode = 1;
@@ -491,6 +501,13 @@ int spttn_execute_stage(spttn_plan* p, int stage, void* stream) {
     a.seg_node = p->dec.seg_node;
     a.slice_seg = p->dec.slice_seg;
     a.n_seg = p->dec.n_seg;
+    a.grp_hdr = p->dec.grp_hdr;
+    a.grp_node = p->dec.grp_node;
+    a.grp_node1 = p->dec.grp_node1;
+    a.pk = p->dec.pk;
+    a.pv = p->dec.pv;
+    a.slice_grp = p->dec.slice_grp;
+    a.n_groups = p->dec.n_groups;
     if (stage != 1) switch (p->kind) {
       case SPTTN_NEST_MTTKRP3:
         a.f[1] = p->fac[0];

@@ -35,6 +35,20 @@ __device__ __forceinline__ double4 ld256(const double* p) {
   return v;
 }
 
+// Predicated 256-bit load without a branch: the load is issued (or not) in
+// straight-line code, so several gathers stay in flight together; inactive
+// lanes / iterations read as zero.
+__device__ __forceinline__ double4 ld256_if(const double* p, bool pred) {
+  double4 v;
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.b32 q, %5, 0;\n"
+      " mov.b64 %0, 0;\n mov.b64 %1, 0;\n mov.b64 %2, 0;\n mov.b64 %3, 0;\n"
+      " @q ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];\n}\n"
+      : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+      : "l"(p), "r"(static_cast<int>(pred)));
+  return v;
+}
+
 __device__ __forceinline__ double2 ld128(const double* p) {
   double2 v;
   asm volatile("ld.global.nc.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));

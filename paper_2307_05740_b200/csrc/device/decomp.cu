@@ -132,7 +132,11 @@ __global__ void k_zero_rows(const int32_t* rows, int64_t n, int64_t tile, double
 
 unsigned blocks_for(int64_t n, int b) { return static_cast<unsigned>((n + b - 1) / b); }
 
-void find_splits_and_absent(const DevCsf& csf, Decomp& d, bool segments, cudaStream_t s) {
+// slice_units: first work unit (segment / packed group) of every root slice,
+// or nullptr when items are leaf ranges.
+void find_splits_and_absent(const DevCsf& csf, Decomp& d, const int32_t* slice_units,
+                            cudaStream_t s) {
+  const bool segments = slice_units != nullptr;
   const CsfView t = csf.view();
   const int32_t n0 = static_cast<int32_t>(csf.level_size[0]);
   int32_t* counts = nullptr;
@@ -148,7 +152,7 @@ void find_splits_and_absent(const DevCsf& csf, Decomp& d, bool segments, cudaStr
   SPTTN_CUDA(cudaMalloc(&d.absent_rows, csf.dims[0] * sizeof(int32_t)));
   if (n0 > 0) {
     if (segments)
-      k_seg_splits<<<blocks_for(n0, 256), 256, 0, s>>>(t, d.slice_seg, d.chunk, d.split_node,
+      k_seg_splits<<<blocks_for(n0, 256), 256, 0, s>>>(t, slice_units, d.chunk, d.split_node,
                                                        d.split_first, d.split_last, counts,
                                                        present);
     else
@@ -184,12 +188,12 @@ void build_leaf_items(const DevCsf& csf, int64_t chunk, Decomp& d, int64_t tile,
   }
   if (tile > 0) {  // dense root-indexed output
     SPTTN_CUDA(cudaMalloc(&d.part, std::max<int64_t>(1, d.n_items * 2 * tile) * sizeof(double)));
-    find_splits_and_absent(csf, d, false, s);
+    find_splits_and_absent(csf, d, nullptr, s);
   }
 }
 
 void build_segments(const DevCsf& csf, int unit_level, int seg_len, int64_t chunk, Decomp& d,
-                    int64_t tile, cudaStream_t s) {
+                    int64_t tile, cudaStream_t s, bool make_items) {
   const CsfView t = csf.view();
   const int32_t nf = static_cast<int32_t>(csf.level_size[unit_level]);
   const int32_t n0 = static_cast<int32_t>(csf.level_size[0]);
@@ -235,15 +239,23 @@ void build_segments(const DevCsf& csf, int unit_level, int seg_len, int64_t chun
                                                                           d.slice_seg);
   SPTTN_CUDA(cudaGetLastError());
   SPTTN_CUDA(cudaFreeAsync(off, s));
-  d.n_items = (nseg + chunk - 1) / chunk;
+  if (make_items) finish_unit_items(csf, d, d.slice_seg, d.n_seg, chunk, tile, s);
+}
+
+void finish_unit_items(const DevCsf& csf, Decomp& d, const int32_t* slice_units, int64_t n_units,
+                       int64_t chunk, int64_t tile, cudaStream_t s) {
+  const int32_t n0 = static_cast<int32_t>(csf.level_size[0]);
+  d.chunk = chunk;
+  d.tile = tile;
+  d.n_items = (n_units + chunk - 1) / chunk;
   SPTTN_CUDA(cudaMalloc(&d.item_pos, std::max<int64_t>(1, d.n_items) * sizeof(int32_t)));
   if (d.n_items > 0) {
-    k_seg_items<<<blocks_for(d.n_items, 256), 256, 0, s>>>(d.slice_seg, n0, chunk, d.n_items,
+    k_seg_items<<<blocks_for(d.n_items, 256), 256, 0, s>>>(slice_units, n0, chunk, d.n_items,
                                                           d.item_pos);
     SPTTN_CUDA(cudaGetLastError());
   }
   SPTTN_CUDA(cudaMalloc(&d.part, std::max<int64_t>(1, d.n_items * 2 * tile) * sizeof(double)));
-  find_splits_and_absent(csf, d, true, s);
+  find_splits_and_absent(csf, d, slice_units, s);
 }
 
 void build_leaf_coords(const DevCsf& csf, int32_t** leaf_i, int32_t** leaf_j, cudaStream_t s) {
@@ -362,6 +374,12 @@ void free_decomp(Decomp& d) {
   cudaFree(d.chunk_hi);
   cudaFree(d.split_chunk);
   cudaFree(d.part2);
+  cudaFree(d.grp_hdr);
+  cudaFree(d.grp_node);
+  cudaFree(d.grp_node1);
+  cudaFree(d.pk);
+  cudaFree(d.pv);
+  cudaFree(d.slice_grp);
   cudaFree(d.slice_seg);
   d = Decomp{};
 }

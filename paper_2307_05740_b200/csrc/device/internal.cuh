@@ -80,6 +80,15 @@ struct Decomp {
   int32_t* chunk_hi = nullptr;
   int32_t* split_chunk = nullptr;  // [n_split+1] first chunk of each split slice
   double* part2 = nullptr;         // [n_chunk][tile]
+  // packed groups (pack.cu): header {leaf_base, len, nseg, slice} per group
+  int64_t n_groups = 0;
+  int64_t n_packed_leaves = 0;
+  int4* grp_hdr = nullptr;
+  int32_t* grp_node = nullptr;     // [n_groups][8] fiber coordinate per slot
+  int32_t* grp_node1 = nullptr;    // [n_groups][8] level-1 coordinate (order 4)
+  int32_t* pk = nullptr;           // interleaved leaf coordinates
+  double* pv = nullptr;            // interleaved leaf values
+  int32_t* slice_grp = nullptr;    // [n0+1] first group of each slice
   int32_t* slice_seg = nullptr;    // [n0+1]   segment offset of each slice
 };
 
@@ -100,6 +109,14 @@ struct RootOutArgs {
   const int32_t* seg_node;
   const int32_t* slice_seg;
   int64_t n_seg;
+  // packed groups
+  const int4* grp_hdr;
+  const int32_t* grp_node;
+  const int32_t* grp_node1;
+  const int32_t* pk;
+  const double* pv;
+  const int32_t* slice_grp;
+  int64_t n_groups;
 };
 
 void launch_mttkrp3(const RootOutArgs& a, cudaStream_t s);
@@ -122,7 +139,15 @@ int group_lanes_for(int R);
 // ---- plan-time helpers (decomp.cu) ----------------------------------------
 void build_leaf_items(const DevCsf& csf, int64_t chunk, Decomp& d, int64_t tile, cudaStream_t s);
 void build_segments(const DevCsf& csf, int unit_level, int seg_len, int64_t chunk, Decomp& d,
-                    int64_t tile, cudaStream_t s);
+                    int64_t tile, cudaStream_t s, bool make_items = true);
+// Items of `chunk` consecutive units (segments or packed groups) given the
+// first unit of every root slice; partial tiles, split slices, absent rows.
+void finish_unit_items(const DevCsf& csf, Decomp& d, const int32_t* slice_units, int64_t n_units,
+                       int64_t chunk, int64_t tile, cudaStream_t s);
+// Length-sorted packed groups of 8 segments (pack.cu); leaf_level = CSF level
+// of the streamed coordinates.
+constexpr int kPackSlots = 8;
+void build_packed(const DevCsf& csf, int leaf_level, Decomp& d, cudaStream_t s);
 constexpr int kFixChunk = 32;
 void build_fixup_chunks(Decomp& d, cudaStream_t s);
 void launch_fixup(const Decomp& d, const CsfView& t, double* out, cudaStream_t s);

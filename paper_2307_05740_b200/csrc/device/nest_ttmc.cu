@@ -728,6 +728,299 @@ __global__ void __launch_bounds__(kBlock, 3) k_ttmc3w(RootOutArgs a) {
   if (pending) flush(head ? 0 : 1);
 }
 
+// Packed variant (default): the warp walks length-sorted groups of 8
+// equal-length segments (pack.cu), so each of a group's n V-row gathers and
+// its U-row gather is a full 8-row 256-bit load with a warp-uniform trip
+// count. Group headers are prefetched two groups ahead and the leaf
+// coordinates of the next group one group ahead. Fragment mapping as in the
+// wide variant (slot = 4*ch + q, column quad c4, one xor-16 exchange).
+template <bool VECU, bool VECV>
+__global__ void __launch_bounds__(kBlock, 2) k_ttmc3pk(RootOutArgs a) {
+  const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
+  if (w >= a.n_items) return;  // warp-uniform
+  const int lane = threadIdx.x & 31;
+  const int q = lane & 3;
+  const int c4 = (lane >> 2) & 3;
+  const int ch = lane >> 4;
+  const int slot = ch * 4 + q;
+  const int h = lane >> 2;
+  const int R = a.R, S_ = a.S;
+  const CsfView& t = a.t;
+  const double* __restrict__ U = a.f[1];
+  const double* __restrict__ V = a.f[2];
+  const int4* __restrict__ hdr = a.grp_hdr;
+  const int32_t* __restrict__ gnode = a.grp_node;
+  const int32_t* __restrict__ pk = a.pk;
+  const double* __restrict__ pv = a.pv;
+  const int32_t* __restrict__ slice_grp = a.slice_grp;
+  const int32_t ng = static_cast<int32_t>(a.n_groups);
+
+  const int32_t cbeg = static_cast<int32_t>(w * a.chunk);
+  const int32_t cend = static_cast<int32_t>(min64(cbeg + a.chunk, a.n_groups));
+  int32_t sl = a.item_pos[w];
+  int32_t sl_end = slice_grp[sl + 1];
+  bool head = slice_grp[sl] < cbeg;
+  int32_t row = t.idx[0][sl];
+  int32_t nx_end = sl + 2 <= t.nlev[0] ? __ldg(slice_grp + sl + 2) : 0;
+  int32_t nx_row = sl + 1 < t.nlev[0] ? __ldg(t.idx[0] + sl + 1) : 0;
+  bool pending = false;
+  double acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.0;
+
+  auto flush = [&](int dslot) {
+    double* dst = dslot < 0 ? a.out + static_cast<int64_t>(row) * R * S_
+                            : a.part + (w * 2 + dslot) * static_cast<int64_t>(R) * S_;
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = 4 * (h & 3) + 2 * (h >> 2) + mt;
+          const int n = 2 * q + e;
+          const int s = 4 * (n & 3) + 2 * (n >> 2) + nt;
+          if (r < R && s < S_) dst[r * S_ + s] = acc[(mt * 2 + nt) * 2 + e];
+        }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = 0.0;
+  };
+  auto load_hdr = [&](int32_t g) { return g < ng ? __ldg(hdr + g) : make_int4(0, 0, 0, 0); };
+  auto load_k = [&](const int4& hh, int32_t* k) {
+#pragma unroll
+    for (int it = 0; it < 4; ++it) k[it] = it < hh.y ? __ldg(pk + hh.x + it * kPackSlots + slot) : 0;
+  };
+
+  int4 hc = load_hdr(cbeg), hn = load_hdr(cbeg + 1);
+  int32_t jc = cbeg < ng ? __ldg(gnode + static_cast<int64_t>(cbeg) * kPackSlots + slot) : 0;
+  int32_t kc[4];
+  load_k(hc, kc);
+  for (int32_t g = cbeg; g < cend; ++g) {
+    const int n = hc.y;  // warp-uniform segment length of this group
+    double4 vr[4];
+    double tt[4];
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      if (it < n) {
+        tt[it] = __ldg(pv + hc.x + it * kPackSlots + slot);
+        vr[it] = row4<VECV>(V + static_cast<int64_t>(kc[it]) * S_, 4 * c4, S_);
+      } else {
+        tt[it] = 0.0;
+        vr[it] = make_double4(0, 0, 0, 0);
+      }
+    }
+    const double4 ur = row4<VECU>(U + static_cast<int64_t>(jc) * R, 4 * c4, R);
+    // prefetch: header two groups ahead, coordinates of the next group
+    const int4 hnn = load_hdr(g + 2);
+    const int32_t jn = g + 1 < ng ? __ldg(gnode + static_cast<int64_t>(g + 1) * kPackSlots + slot) : 0;
+    int32_t kn[4];
+    load_k(hn, kn);
+    double4 x = make_double4(0, 0, 0, 0);
+#pragma unroll
+    for (int it = 0; it < 4; ++it) fma4(x, tt[it], vr[it]);  // X[s] += t * V[k,s]
+    const double sx0 = ch == 0 ? x.z : x.x, sx1 = ch == 0 ? x.w : x.y;
+    const double su0 = ch == 0 ? ur.z : ur.x, su1 = ch == 0 ? ur.w : ur.y;
+    const double rx0 = __shfl_xor_sync(0xffffffffu, sx0, 16);
+    const double rx1 = __shfl_xor_sync(0xffffffffu, sx1, 16);
+    const double ru0 = __shfl_xor_sync(0xffffffffu, su0, 16);
+    const double ru1 = __shfl_xor_sync(0xffffffffu, su1, 16);
+    const double bA0 = ch == 0 ? x.x : rx0, bA1 = ch == 0 ? x.y : rx1;
+    const double bB0 = ch == 0 ? rx0 : x.z, bB1 = ch == 0 ? rx1 : x.w;
+    const double aA0 = ch == 0 ? ur.x : ru0, aA1 = ch == 0 ? ur.y : ru1;
+    const double aB0 = ch == 0 ? ru0 : ur.z, aB1 = ch == 0 ? ru1 : ur.w;
+    dmma_8x8x4(acc[0], acc[1], aA0, bA0);
+    dmma_8x8x4(acc[2], acc[3], aA0, bA1);
+    dmma_8x8x4(acc[4], acc[5], aA1, bA0);
+    dmma_8x8x4(acc[6], acc[7], aA1, bA1);
+    dmma_8x8x4(acc[0], acc[1], aB0, bB0);
+    dmma_8x8x4(acc[2], acc[3], aB0, bB1);
+    dmma_8x8x4(acc[4], acc[5], aB1, bB0);
+    dmma_8x8x4(acc[6], acc[7], aB1, bB1);
+    pending = true;
+    hc = hn;
+    hn = hnn;
+    jc = jn;
+#pragma unroll
+    for (int it = 0; it < 4; ++it) kc[it] = kn[it];
+    if (g + 1 == sl_end) {
+      flush(head ? 0 : -1);
+      pending = false;
+      head = false;
+      if (g + 1 < cend) {
+        ++sl;
+        sl_end = nx_end;
+        row = nx_row;
+        nx_end = sl + 2 <= t.nlev[0] ? __ldg(slice_grp + sl + 2) : 0;
+        nx_row = sl + 1 < t.nlev[0] ? __ldg(t.idx[0] + sl + 1) : 0;
+      }
+    }
+  }
+  if (pending) flush(head ? 0 : 1);
+}
+
+// Packed + staged variant: packed groups (full 8-row gathers) whose stream
+// (headers, slot coordinates, interleaved leaf coordinates / values) is
+// copied into a per-warp shared-memory ring by cp.async kGW groups at a time,
+// headers two windows ahead and leaf data one window ahead, so only the
+// factor-row gathers remain on the critical path and registers hold no
+// prefetch state.
+constexpr int kGW = 4;                             // groups per window
+constexpr int kGWLeaves = kGW * kPackSlots * 4;    // leaves per window (len <= 4)
+
+struct StageP {
+  alignas(16) int4 hdr[3][kGW];
+  int32_t node[3][kGW * kPackSlots];
+  int32_t kk[2][kGWLeaves];
+  double tv[2][kGWLeaves];
+};
+
+template <bool VECU, bool VECV>
+__global__ void __launch_bounds__(kBlock, 3) k_ttmc3ps(RootOutArgs a) {
+  __shared__ StageP stage[kBlock / 32];
+  const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
+  if (w >= a.n_items) return;  // warp-uniform
+  StageP& S = stage[threadIdx.x / 32];
+  const int lane = threadIdx.x & 31;
+  const int q = lane & 3;
+  const int c4 = (lane >> 2) & 3;
+  const int ch = lane >> 4;
+  const int slot = ch * 4 + q;
+  const int h = lane >> 2;
+  const int R = a.R, S_ = a.S;
+  const CsfView& t = a.t;
+  const double* __restrict__ U = a.f[1];
+  const double* __restrict__ V = a.f[2];
+  const int32_t* __restrict__ slice_grp = a.slice_grp;
+
+  const int32_t cbeg = static_cast<int32_t>(w * a.chunk);
+  const int32_t cend = static_cast<int32_t>(min64(cbeg + a.chunk, a.n_groups));
+  int32_t sl = a.item_pos[w];
+  int32_t sl_end = slice_grp[sl + 1];
+  bool head = slice_grp[sl] < cbeg;
+  int32_t row = t.idx[0][sl];
+  int32_t nx_end = sl + 2 <= t.nlev[0] ? __ldg(slice_grp + sl + 2) : 0;
+  int32_t nx_row = sl + 1 < t.nlev[0] ? __ldg(t.idx[0] + sl + 1) : 0;
+  bool pending = false;
+  double acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.0;
+
+  auto flush = [&](int dslot) {
+    double* dst = dslot < 0 ? a.out + static_cast<int64_t>(row) * R * S_
+                            : a.part + (w * 2 + dslot) * static_cast<int64_t>(R) * S_;
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = 4 * (h & 3) + 2 * (h >> 2) + mt;
+          const int n = 2 * q + e;
+          const int s = 4 * (n & 3) + 2 * (n >> 2) + nt;
+          if (r < R && s < S_) dst[r * S_ + s] = acc[(mt * 2 + nt) * 2 + e];
+        }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = 0.0;
+  };
+  // window w covers groups [gs, min(gs + kGW, cend))
+  auto issue_meta = [&](int buf, int32_t gs) {
+    const int32_t nw = min(gs + kGW, cend) - gs;
+    if (lane < nw) cp_async16_cg(&S.hdr[buf][lane], a.grp_hdr + gs + lane, 16);
+    for (int i = lane; i < nw * kPackSlots; i += 32)
+      cp_async4(&S.node[buf][i], a.grp_node + static_cast<int64_t>(gs) * kPackSlots + i);
+  };
+  auto issue_leaves = [&](int lbuf, int mbuf, int32_t gs) {
+    const int32_t nw = min(gs + kGW, cend) - gs;
+    const int32_t L0 = S.hdr[mbuf][0].x;
+    const int32_t L1 = S.hdr[mbuf][nw - 1].x + kPackSlots * S.hdr[mbuf][nw - 1].y;
+    for (int32_t i = lane; i < L1 - L0; i += 32) {
+      cp_async4(&S.kk[lbuf][i], a.pk + L0 + i);
+      cp_async8(&S.tv[lbuf][i], a.pv + L0 + i);
+    }
+  };
+
+  const int32_t nwin = (cend - cbeg + kGW - 1) / kGW;
+  issue_meta(0, cbeg);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncwarp();
+  issue_leaves(0, 0, cbeg);
+  if (nwin > 1) issue_meta(1, cbeg + kGW);
+  cp_async_commit();
+  for (int32_t win = 0; win < nwin; ++win) {
+    cp_async_wait<0>();
+    __syncwarp();
+    const int mb = win % 3, lbf = win & 1;
+    const int32_t gs = cbeg + win * kGW;
+    if (win + 1 < nwin) issue_leaves((win + 1) & 1, (win + 1) % 3, gs + kGW);
+    if (win + 2 < nwin) issue_meta((win + 2) % 3, gs + 2 * kGW);
+    cp_async_commit();
+    const int32_t ge = min(gs + kGW, cend);
+    const int32_t L0 = S.hdr[mb][0].x;
+    for (int32_t g = gs; g < ge; ++g) {
+      const int4 hh = S.hdr[mb][g - gs];
+      const int n = hh.y;  // warp-uniform
+      const int32_t lbase = hh.x - L0 + slot;
+      // straight-line: read every index first, then issue all gathers
+      const int32_t j = S.node[mb][(g - gs) * kPackSlots + slot];
+      int32_t kk[4];
+      double tt[4];
+#pragma unroll
+      for (int it = 0; it < 4; ++it) {
+        kk[it] = S.kk[lbf][lbase + it * kPackSlots];
+        tt[it] = it < n ? S.tv[lbf][lbase + it * kPackSlots] : 0.0;
+      }
+      const double4 ur = row4<VECU>(U + static_cast<int64_t>(j) * R, 4 * c4, R);
+      double4 vr[4];
+#pragma unroll
+      for (int it = 0; it < 4; ++it) {
+        if (VECV) {
+          vr[it] = ld256_if(V + static_cast<int64_t>(kk[it]) * S_ + 4 * c4, it < n && 4 * c4 < S_);
+        } else {
+          vr[it] = it < n ? row4<false>(V + static_cast<int64_t>(kk[it]) * S_, 4 * c4, S_)
+                          : make_double4(0, 0, 0, 0);
+        }
+      }
+      double4 x = make_double4(0, 0, 0, 0);
+#pragma unroll
+      for (int it = 0; it < 4; ++it) fma4(x, tt[it], vr[it]);  // X[s] += t * V[k,s]
+      const double sx0 = ch == 0 ? x.z : x.x, sx1 = ch == 0 ? x.w : x.y;
+      const double su0 = ch == 0 ? ur.z : ur.x, su1 = ch == 0 ? ur.w : ur.y;
+      const double rx0 = __shfl_xor_sync(0xffffffffu, sx0, 16);
+      const double rx1 = __shfl_xor_sync(0xffffffffu, sx1, 16);
+      const double ru0 = __shfl_xor_sync(0xffffffffu, su0, 16);
+      const double ru1 = __shfl_xor_sync(0xffffffffu, su1, 16);
+      const double bA0 = ch == 0 ? x.x : rx0, bA1 = ch == 0 ? x.y : rx1;
+      const double bB0 = ch == 0 ? rx0 : x.z, bB1 = ch == 0 ? rx1 : x.w;
+      const double aA0 = ch == 0 ? ur.x : ru0, aA1 = ch == 0 ? ur.y : ru1;
+      const double aB0 = ch == 0 ? ru0 : ur.z, aB1 = ch == 0 ? ru1 : ur.w;
+      dmma_8x8x4(acc[0], acc[1], aA0, bA0);
+      dmma_8x8x4(acc[2], acc[3], aA0, bA1);
+      dmma_8x8x4(acc[4], acc[5], aA1, bA0);
+      dmma_8x8x4(acc[6], acc[7], aA1, bA1);
+      dmma_8x8x4(acc[0], acc[1], aB0, bB0);
+      dmma_8x8x4(acc[2], acc[3], aB0, bB1);
+      dmma_8x8x4(acc[4], acc[5], aB1, bB0);
+      dmma_8x8x4(acc[6], acc[7], aB1, bB1);
+      pending = true;
+      if (g + 1 == sl_end) {
+        flush(head ? 0 : -1);
+        pending = false;
+        head = false;
+        if (g + 1 < cend) {
+          ++sl;
+          sl_end = nx_end;
+          row = nx_row;
+          nx_end = sl + 2 <= t.nlev[0] ? __ldg(slice_grp + sl + 2) : 0;
+          nx_row = sl + 1 < t.nlev[0] ? __ldg(t.idx[0] + sl + 1) : 0;
+        }
+      }
+    }
+    __syncwarp();
+  }
+  if (pending) flush(head ? 0 : 1);
+}
+
 template <bool VECV>
 __global__ void __launch_bounds__(kBlock) k_ttmc4(RootOutArgs a) {
   const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
@@ -854,6 +1147,32 @@ void launch_ttmc3(const RootOutArgs& a, cudaStream_t s) {
   if (blocks == 0) return;
   const bool vu = a.vec & 1, vv = a.vec & 2;
   const int mode = a.flags >> 8;  // kernel variant chosen at plan time
+  if (mode == 7) {
+    const bool wu = a.vec & 4, wv = a.vec & 8;
+    if (wu && wv)
+      k_ttmc3ps<true, true><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
+    else if (wu)
+      k_ttmc3ps<true, false><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
+    else if (wv)
+      k_ttmc3ps<false, true><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
+    else
+      k_ttmc3ps<false, false><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
+    SPTTN_CUDA(cudaGetLastError());
+    return;
+  }
+  if (mode == 6) {
+    const bool wu = a.vec & 4, wv = a.vec & 8;
+    if (wu && wv)
+      k_ttmc3pk<true, true><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
+    else if (wu)
+      k_ttmc3pk<true, false><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
+    else if (wv)
+      k_ttmc3pk<false, true><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
+    else
+      k_ttmc3pk<false, false><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
+    SPTTN_CUDA(cudaGetLastError());
+    return;
+  }
   if (mode == 5) {
     // wide gathers need 32-byte aligned rows: R, S multiples of 4 (a.vec bits 4/8)
     const bool wu = a.vec & 4, wv = a.vec & 8;
