@@ -83,6 +83,7 @@ struct Decomp {
   // packed groups (pack.cu): header {leaf_base, len, nseg, slice} per group
   int64_t n_groups = 0;
   int64_t n_packed_leaves = 0;
+  int pack_slots = 0;
   int4* grp_hdr = nullptr;
   int32_t* grp_node = nullptr;     // [n_groups][8] fiber coordinate per slot
   int32_t* grp_node1 = nullptr;    // [n_groups][8] level-1 coordinate (order 4)
@@ -127,6 +128,7 @@ void launch_ttmc4(const RootOutArgs& a, cudaStream_t s);
 // Segment-form MTTKRP (R <= 32): order 3 units = level-1 fibers, order 4 =
 // level-2 fibers (seg_node1 carries the level-1 coordinate).
 void launch_mttkrp_seg(const RootOutArgs& a, const int32_t* seg_node1, int order, cudaStream_t s);
+void launch_mttkrp_pk(const RootOutArgs& a, int order, cudaStream_t s);
 void launch_tttp3_leaf(const RootOutArgs& a, const int32_t* leaf_i, const int32_t* leaf_j,
                        int batch, cudaStream_t s);
 // Per-leaf root / level-1 coordinates of an order-3 CSF (TTTP leaf kernel).
@@ -146,8 +148,9 @@ void finish_unit_items(const DevCsf& csf, Decomp& d, const int32_t* slice_units,
                        int64_t chunk, int64_t tile, cudaStream_t s);
 // Length-sorted packed groups of 8 segments (pack.cu); leaf_level = CSF level
 // of the streamed coordinates.
-constexpr int kPackSlots = 8;
-void build_packed(const DevCsf& csf, int leaf_level, Decomp& d, cudaStream_t s);
+constexpr int kPackSlots = 8;  // TTMc-3 groups (128-byte rows)
+void build_packed(const DevCsf& csf, int leaf_level, Decomp& d, cudaStream_t s,
+                  int slots = kPackSlots);
 constexpr int kFixChunk = 32;
 void build_fixup_chunks(Decomp& d, cudaStream_t s);
 void launch_fixup(const Decomp& d, const CsfView& t, double* out, cudaStream_t s);

@@ -152,7 +152,120 @@ __global__ void __launch_bounds__(kBlock, 2) k_mttkrp_seg(RootOutArgs a, const i
   if (pending) flush(head ? 0 : 1);
 }
 
+// Packed form (default for R <= 32): the warp walks length-sorted groups of 4
+// equal-length segments (pack.cu with 4 slots: a 256-byte row needs 8 lanes
+// of 32 bytes, so 4 rows fill one 256-bit warp gather). Lane L = (slot =
+// L/8, column quad c = 4*(L%8)). Every gather is issued in straight-line
+// code (predicated, no branches) so all of a group's rows are in flight
+// together; the group's segment length n is warp-uniform.
+template <int ORDER, bool VEC>
+__global__ void __launch_bounds__(kBlock, 3) k_mttkrp_pk(RootOutArgs a) {
+  const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
+  if (w >= a.n_items) return;  // warp-uniform
+  constexpr int kSlots = 4;
+  const int lane = threadIdx.x & 31;
+  const int slot = lane >> 3;
+  const int c = (lane & 7) * 4;
+  const int R = a.R;
+  const CsfView& t = a.t;
+  const double* __restrict__ Fleaf = a.f[ORDER - 1];
+  const double* __restrict__ Funit = a.f[ORDER - 2];
+  const double* __restrict__ Ftop = a.f[1];
+  const int4* __restrict__ hdr = a.grp_hdr;
+  const int32_t* __restrict__ gnode = a.grp_node;
+  const int32_t* __restrict__ gnode1 = a.grp_node1;
+  const int32_t* __restrict__ pk = a.pk;
+  const double* __restrict__ pv = a.pv;
+  const int32_t* __restrict__ slice_grp = a.slice_grp;
+
+  const int32_t cbeg = static_cast<int32_t>(w * a.chunk);
+  const int32_t cend = static_cast<int32_t>(min64(cbeg + a.chunk, a.n_groups));
+  int32_t sl = a.item_pos[w];
+  int32_t sl_end = slice_grp[sl + 1];
+  bool head = slice_grp[sl] < cbeg;
+  int32_t row = t.idx[0][sl];
+  bool pending = false;
+  double4 acc = make_double4(0, 0, 0, 0);
+  const bool colok = c < R;
+
+  auto flush = [&](int dslot) {
+    double v[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      v[e] += __shfl_xor_sync(0xffffffffu, v[e], 8);
+      v[e] += __shfl_xor_sync(0xffffffffu, v[e], 16);
+    }
+    if (slot == 0) {
+      double* dst = dslot < 0 ? a.out + static_cast<int64_t>(row) * R
+                              : a.part + (w * 2 + dslot) * static_cast<int64_t>(R);
+      store4(dst, c, R, make_double4(v[0], v[1], v[2], v[3]));
+    }
+    acc = make_double4(0, 0, 0, 0);
+  };
+  auto rowq = [&](const double* base, int32_t r, bool pred) {
+    if (VEC) return ld256_if(base + static_cast<int64_t>(r) * R + c, pred && colok);
+    return pred ? row4<false>(base + static_cast<int64_t>(r) * R, c, R) : make_double4(0, 0, 0, 0);
+  };
+
+  for (int32_t g = cbeg; g < cend; ++g) {
+    const int4 hh = __ldg(hdr + g);
+    const int n = hh.y;  // warp-uniform
+    const int64_t gs = static_cast<int64_t>(g) * kSlots + slot;
+    const int32_t u = __ldg(gnode + gs);
+    const int32_t j = ORDER == 4 ? __ldg(gnode1 + gs) : 0;
+    int32_t kk[4];
+    double tt[4];
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const bool on = it < n;
+      kk[it] = on ? __ldg(pk + hh.x + it * kSlots + slot) : 0;
+      tt[it] = on ? __ldg(pv + hh.x + it * kSlots + slot) : 0.0;
+    }
+    const double4 ur = rowq(Funit, u, true);
+    double4 tr = make_double4(0, 0, 0, 0);
+    if (ORDER == 4) tr = rowq(Ftop, j, true);
+    double4 rr[4];
+#pragma unroll
+    for (int it = 0; it < 4; ++it) rr[it] = rowq(Fleaf, kk[it], it < n);
+    double4 X = make_double4(0, 0, 0, 0);
+#pragma unroll
+    for (int it = 0; it < 4; ++it) fma4(X, tt[it], rr[it]);  // X += t * F_leaf[k]
+    if (ORDER == 3) {
+      fma4v(acc, X, ur);  // A[i] += X * B[j]
+    } else {
+      const double4 Y = make_double4(X.x * ur.x, X.y * ur.y, X.z * ur.z, X.w * ur.w);
+      fma4v(acc, Y, tr);  // A[i] += (X * C[k]) * B[j]
+    }
+    pending = true;
+    if (g + 1 == sl_end) {
+      flush(head ? 0 : -1);
+      pending = false;
+      head = false;
+      if (g + 1 < cend) {
+        ++sl;
+        sl_end = slice_grp[sl + 1];
+        row = t.idx[0][sl];
+      }
+    }
+  }
+  if (pending) flush(head ? 0 : 1);
+}
+
 }  // namespace
+
+void launch_mttkrp_pk(const RootOutArgs& a, int order, cudaStream_t s) {
+  const int64_t blocks = (a.n_items * 32 + kBlock - 1) / kBlock;
+  if (blocks == 0) return;
+  const unsigned b = static_cast<unsigned>(blocks);
+  if (order == 3) {
+    if (a.vec) k_mttkrp_pk<3, true><<<b, kBlock, 0, s>>>(a);
+    else k_mttkrp_pk<3, false><<<b, kBlock, 0, s>>>(a);
+  } else {
+    if (a.vec) k_mttkrp_pk<4, true><<<b, kBlock, 0, s>>>(a);
+    else k_mttkrp_pk<4, false><<<b, kBlock, 0, s>>>(a);
+  }
+  SPTTN_CUDA(cudaGetLastError());
+}
 
 void launch_mttkrp_seg(const RootOutArgs& a, const int32_t* seg_node1, int order, cudaStream_t s) {
   const int64_t blocks = (a.n_items * 32 + kBlock - 1) / kBlock;

@@ -1,14 +1,16 @@
 // Packed (length-sorted) segment layout — built once per plan.
 //
-// B200's L1 serves a warp-wide gather instruction in ~12-19 cycles per SM
-// almost regardless of how many of its lanes are active (tools/gather_probe.cu:
-// 1, 2, 4 or 8 rows per instruction cost the same), so a gather must carry a
-// full set of rows. Segments (fiber pieces of <= 4 leaves) of one root slice
-// are therefore regrouped by length: a *group* is 8 segments of the same
-// slice and the same length n, its leaves interleaved (leaf `it` of slot `s`
-// at base + 8*it + s), so the it-th gather of a group fetches 8 rows with no
-// predicated-off lanes and the loop trip count n is warp-uniform. Summing a
-// slice's segments in this fixed (sorted) order keeps results deterministic.
+// B200's L1 serves a warp-wide gather instruction at a cost set by the
+// instruction, not by how many of its lanes are active (tools/gather_probe.cu:
+// 1, 2, 4 or 8 rows per 256-bit instruction cost about the same), so a gather
+// must carry a full set of rows. Segments (fiber pieces of <= 4 leaves) of
+// one root slice are therefore regrouped by length: a *group* is `slots`
+// segments of the same slice and the same length n (8 for 128-byte factor
+// rows, 4 for 256-byte rows), with their leaves interleaved (leaf `it` of slot
+// `s` at base + slots*it + s), so the it-th gather of a group fetches a full
+// set of rows with no predicated-off lanes and the trip count n is
+// warp-uniform. Summing a slice's segments in this fixed (sorted) order keeps
+// results deterministic.
 #include <cub/cub.cuh>
 
 #include "internal.cuh"
@@ -41,28 +43,6 @@ __global__ void k_run_heads(const uint64_t* keys, int32_t n, int32_t* head) {
   head[p] = (p == 0 || keys[p] != keys[p - 1]) ? p : 0;
 }
 
-__global__ void k_group_flags(const int32_t* runstart, int32_t n, int32_t* flag) {
-  const int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n) return;
-  flag[p] = ((p - runstart[p]) % kPackSlots) == 0 ? 1 : 0;
-}
-
-// per group: n (len), slice, nseg; gleaves = 8*n for the leaf-base scan
-__global__ void k_group_headers(const uint64_t* keys, const int32_t* runstart, const int32_t* gid,
-                                const int32_t* seg_end_pos, int32_t n, int4* hdr,
-                                int32_t* gleaves) {
-  const int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n) return;
-  if ((p - runstart[p]) % kPackSlots != 0) return;
-  const int32_t g = gid[p] - 1;
-  const int32_t len = static_cast<int32_t>(keys[p] & 7);
-  const int32_t slice = static_cast<int32_t>(keys[p] >> 3);
-  const int32_t run_end = seg_end_pos[p];  // one past the last position of this run
-  const int32_t nseg = min(kPackSlots, run_end - p);
-  hdr[g] = make_int4(0, len, nseg, slice);
-  gleaves[g] = kPackSlots * len;
-}
-
 // one past the last sorted position of each run, stored at the run's start
 __global__ void k_run_ends(const uint64_t* keys, const int32_t* runstart, int32_t n,
                            int32_t* end_at_start) {
@@ -78,24 +58,46 @@ __global__ void k_run_end_of(const int32_t* runstart, const int32_t* end_at_star
   runend[p] = end_at_start[runstart[p]];
 }
 
+__global__ void k_group_flags(const int32_t* runstart, int32_t n, int slots, int32_t* flag) {
+  const int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  flag[p] = ((p - runstart[p]) % slots) == 0 ? 1 : 0;
+}
+
+// per group: len, slice, nseg; gleaves = slots * len for the leaf-base scan
+__global__ void k_group_headers(const uint64_t* keys, const int32_t* runstart, const int32_t* gid,
+                                const int32_t* runend, int32_t n, int slots, int4* hdr,
+                                int32_t* gleaves) {
+  const int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  if ((p - runstart[p]) % slots != 0) return;
+  const int32_t g = gid[p] - 1;
+  const int32_t len = static_cast<int32_t>(keys[p] & 7);
+  const int32_t slice = static_cast<int32_t>(keys[p] >> 3);
+  const int32_t nseg = min(slots, runend[p] - p);
+  hdr[g] = make_int4(0, len, nseg, slice);
+  gleaves[g] = slots * len;
+}
+
 __global__ void k_fill_groups(const int32_t* ids, const int32_t* runstart, const int32_t* gid,
                               const int32_t* leaf_off, const int32_t* seg_begin,
                               const int32_t* seg_node, const int32_t* seg_node1,
-                              const int32_t* kidx, const double* vals, int32_t n, int4* hdr,
-                              int32_t* gnode, int32_t* gnode1, int32_t* pk, double* pv) {
+                              const int32_t* kidx, const double* vals, int32_t n, int slots,
+                              int4* hdr, int32_t* gnode, int32_t* gnode1, int32_t* pk,
+                              double* pv) {
   const int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   const int32_t g = gid[p] - 1;
-  const int32_t slot = (p - runstart[p]) % kPackSlots;
+  const int32_t slot = (p - runstart[p]) % slots;
   const int32_t s = ids[p];
   const int32_t base = leaf_off[g];
   if (slot == 0) hdr[g].x = base;
-  gnode[g * kPackSlots + slot] = seg_node[s];
-  if (gnode1) gnode1[g * kPackSlots + slot] = seg_node1[s];
+  gnode[static_cast<int64_t>(g) * slots + slot] = seg_node[s];
+  if (gnode1) gnode1[static_cast<int64_t>(g) * slots + slot] = seg_node1[s];
   const int32_t b = seg_begin[s], len = seg_begin[s + 1] - b;
   for (int32_t it = 0; it < len; ++it) {
-    pk[base + it * kPackSlots + slot] = kidx[b + it];
-    pv[base + it * kPackSlots + slot] = vals[b + it];
+    pk[base + it * slots + slot] = kidx[b + it];
+    pv[base + it * slots + slot] = vals[b + it];
   }
 }
 
@@ -111,18 +113,21 @@ __global__ void k_slice_groups(const int4* hdr, int32_t ngroups, int32_t n0, int
 }
 
 template <class Op>
-void scan(int32_t* in, int32_t* out, int32_t n, Op op, bool inclusive, cudaStream_t s) {
+void scan_incl(int32_t* in, int32_t* out, int32_t n, Op op, cudaStream_t s) {
   size_t bytes = 0;
   void* tmp = nullptr;
-  if (inclusive) {
-    SPTTN_CUDA(cub::DeviceScan::InclusiveScan(nullptr, bytes, in, out, op, n, s));
-    SPTTN_CUDA(cudaMallocAsync(&tmp, bytes, s));
-    SPTTN_CUDA(cub::DeviceScan::InclusiveScan(tmp, bytes, in, out, op, n, s));
-  } else {
-    SPTTN_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, s));
-    SPTTN_CUDA(cudaMallocAsync(&tmp, bytes, s));
-    SPTTN_CUDA(cub::DeviceScan::ExclusiveSum(tmp, bytes, in, out, n, s));
-  }
+  SPTTN_CUDA(cub::DeviceScan::InclusiveScan(nullptr, bytes, in, out, op, n, s));
+  SPTTN_CUDA(cudaMallocAsync(&tmp, bytes, s));
+  SPTTN_CUDA(cub::DeviceScan::InclusiveScan(tmp, bytes, in, out, op, n, s));
+  SPTTN_CUDA(cudaFreeAsync(tmp, s));
+}
+
+void scan_excl_sum(int32_t* in, int32_t* out, int32_t n, cudaStream_t s) {
+  size_t bytes = 0;
+  void* tmp = nullptr;
+  SPTTN_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, s));
+  SPTTN_CUDA(cudaMallocAsync(&tmp, bytes, s));
+  SPTTN_CUDA(cub::DeviceScan::ExclusiveSum(tmp, bytes, in, out, n, s));
   SPTTN_CUDA(cudaFreeAsync(tmp, s));
 }
 
@@ -132,9 +137,10 @@ struct MaxOp {
 
 }  // namespace
 
-void build_packed(const DevCsf& csf, int leaf_level, Decomp& d, cudaStream_t s) {
+void build_packed(const DevCsf& csf, int leaf_level, Decomp& d, cudaStream_t s, int slots) {
   const int32_t nseg = static_cast<int32_t>(d.n_seg);
   const int32_t n0 = static_cast<int32_t>(csf.level_size[0]);
+  d.pack_slots = slots;
   if (nseg == 0) {
     d.n_groups = 0;
     SPTTN_CUDA(cudaMalloc(&d.slice_grp, (static_cast<int64_t>(n0) + 1) * sizeof(int32_t)));
@@ -142,8 +148,8 @@ void build_packed(const DevCsf& csf, int leaf_level, Decomp& d, cudaStream_t s) 
     return;
   }
   uint64_t *keys = nullptr, *keys2 = nullptr;
-  int32_t *ids = nullptr, *ids2 = nullptr, *head = nullptr, *runstart = nullptr, *tail = nullptr,
-          *runend = nullptr, *flag = nullptr, *gid = nullptr;
+  int32_t *ids = nullptr, *ids2 = nullptr, *head = nullptr, *runstart = nullptr,
+          *end_at_start = nullptr, *runend = nullptr, *flag = nullptr, *gid = nullptr;
   SPTTN_CUDA(cudaMallocAsync(&keys, nseg * sizeof(uint64_t), s));
   SPTTN_CUDA(cudaMallocAsync(&keys2, nseg * sizeof(uint64_t), s));
   SPTTN_CUDA(cudaMallocAsync(&ids, nseg * sizeof(int32_t), s));
@@ -162,16 +168,16 @@ void build_packed(const DevCsf& csf, int leaf_level, Decomp& d, cudaStream_t s) 
   SPTTN_CUDA(cudaFreeAsync(tmp, s));
   SPTTN_CUDA(cudaMallocAsync(&head, nseg * sizeof(int32_t), s));
   SPTTN_CUDA(cudaMallocAsync(&runstart, nseg * sizeof(int32_t), s));
-  SPTTN_CUDA(cudaMallocAsync(&tail, nseg * sizeof(int32_t), s));
+  SPTTN_CUDA(cudaMallocAsync(&end_at_start, nseg * sizeof(int32_t), s));
   SPTTN_CUDA(cudaMallocAsync(&runend, nseg * sizeof(int32_t), s));
   SPTTN_CUDA(cudaMallocAsync(&flag, nseg * sizeof(int32_t), s));
   SPTTN_CUDA(cudaMallocAsync(&gid, nseg * sizeof(int32_t), s));
   k_run_heads<<<nblk(nseg, 256), 256, 0, s>>>(keys2, nseg, head);
-  scan(head, runstart, nseg, MaxOp{}, true, s);
-  k_run_ends<<<nblk(nseg, 256), 256, 0, s>>>(keys2, runstart, nseg, tail);
-  k_run_end_of<<<nblk(nseg, 256), 256, 0, s>>>(runstart, tail, nseg, runend);
-  k_group_flags<<<nblk(nseg, 256), 256, 0, s>>>(runstart, nseg, flag);
-  scan(flag, gid, nseg, cub::Sum{}, true, s);
+  scan_incl(head, runstart, nseg, MaxOp{}, s);
+  k_run_ends<<<nblk(nseg, 256), 256, 0, s>>>(keys2, runstart, nseg, end_at_start);
+  k_run_end_of<<<nblk(nseg, 256), 256, 0, s>>>(runstart, end_at_start, nseg, runend);
+  k_group_flags<<<nblk(nseg, 256), 256, 0, s>>>(runstart, nseg, slots, flag);
+  scan_incl(flag, gid, nseg, cub::Sum{}, s);
   int32_t ngroups = 0;
   SPTTN_CUDA(cudaMemcpyAsync(&ngroups, gid + nseg - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   SPTTN_CUDA(cudaStreamSynchronize(s));
@@ -182,18 +188,19 @@ void build_packed(const DevCsf& csf, int leaf_level, Decomp& d, cudaStream_t s) 
   SPTTN_CUDA(cudaMallocAsync(&gleaves, (static_cast<int64_t>(ngroups) + 1) * sizeof(int32_t), s));
   SPTTN_CUDA(cudaMallocAsync(&leaf_off, (static_cast<int64_t>(ngroups) + 1) * sizeof(int32_t), s));
   SPTTN_CUDA(cudaMemsetAsync(gleaves, 0, (static_cast<int64_t>(ngroups) + 1) * sizeof(int32_t), s));
-  k_group_headers<<<nblk(nseg, 256), 256, 0, s>>>(keys2, runstart, gid, runend, nseg, d.grp_hdr,
-                                                  gleaves);
-  scan(gleaves, leaf_off, ngroups + 1, cub::Sum{}, false, s);
+  k_group_headers<<<nblk(nseg, 256), 256, 0, s>>>(keys2, runstart, gid, runend, nseg, slots,
+                                                  d.grp_hdr, gleaves);
+  scan_excl_sum(gleaves, leaf_off, ngroups + 1, s);
   int32_t nleaves = 0;
   SPTTN_CUDA(cudaMemcpyAsync(&nleaves, leaf_off + ngroups, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   SPTTN_CUDA(cudaStreamSynchronize(s));
   d.n_packed_leaves = nleaves;
-  SPTTN_CUDA(cudaMalloc(&d.grp_node, static_cast<int64_t>(ngroups) * kPackSlots * sizeof(int32_t)));
-  SPTTN_CUDA(cudaMemsetAsync(d.grp_node, 0, static_cast<int64_t>(ngroups) * kPackSlots * sizeof(int32_t), s));
+  const int64_t nslots = static_cast<int64_t>(ngroups) * slots;
+  SPTTN_CUDA(cudaMalloc(&d.grp_node, nslots * sizeof(int32_t)));
+  SPTTN_CUDA(cudaMemsetAsync(d.grp_node, 0, nslots * sizeof(int32_t), s));
   if (d.seg_node1) {
-    SPTTN_CUDA(cudaMalloc(&d.grp_node1, static_cast<int64_t>(ngroups) * kPackSlots * sizeof(int32_t)));
-    SPTTN_CUDA(cudaMemsetAsync(d.grp_node1, 0, static_cast<int64_t>(ngroups) * kPackSlots * sizeof(int32_t), s));
+    SPTTN_CUDA(cudaMalloc(&d.grp_node1, nslots * sizeof(int32_t)));
+    SPTTN_CUDA(cudaMemsetAsync(d.grp_node1, 0, nslots * sizeof(int32_t), s));
   }
   SPTTN_CUDA(cudaMalloc(&d.pk, std::max<int64_t>(1, nleaves) * sizeof(int32_t)));
   SPTTN_CUDA(cudaMalloc(&d.pv, std::max<int64_t>(1, nleaves) * sizeof(double)));
@@ -202,15 +209,15 @@ void build_packed(const DevCsf& csf, int leaf_level, Decomp& d, cudaStream_t s) 
   const CsfView t = csf.view();
   k_fill_groups<<<nblk(nseg, 256), 256, 0, s>>>(ids2, runstart, gid, leaf_off, d.seg_begin,
                                                 d.seg_node, d.seg_node1, t.idx[leaf_level],
-                                                t.vals, nseg, d.grp_hdr, d.grp_node, d.grp_node1,
-                                                d.pk, d.pv);
+                                                t.vals, nseg, slots, d.grp_hdr, d.grp_node,
+                                                d.grp_node1, d.pk, d.pv);
   SPTTN_CUDA(cudaMalloc(&d.slice_grp, (static_cast<int64_t>(n0) + 1) * sizeof(int32_t)));
   k_slice_groups<<<nblk(static_cast<int64_t>(ngroups) + 1, 256), 256, 0, s>>>(d.grp_hdr, ngroups,
                                                                             n0, d.slice_grp);
   SPTTN_CUDA(cudaGetLastError());
   for (void* p : {static_cast<void*>(keys), static_cast<void*>(keys2), static_cast<void*>(ids),
                   static_cast<void*>(ids2), static_cast<void*>(head),
-                  static_cast<void*>(runstart), static_cast<void*>(tail),
+                  static_cast<void*>(runstart), static_cast<void*>(end_at_start),
                   static_cast<void*>(runend), static_cast<void*>(flag), static_cast<void*>(gid),
                   static_cast<void*>(gleaves), static_cast<void*>(leaf_off)})
     SPTTN_CUDA(cudaFreeAsync(p, s));

@@ -85,6 +85,33 @@ def test_partition_independence(E, name, chunk, monkeypatch):
         assert plan.info()["split_slices"] > 0
 
 
+VARIANTS = [("SPTTN_TTMC3_MODE", m, ["ttmc3_small", "ttmc3_r16"]) for m in ("0", "3", "4", "5", "6", "7")] + \
+    [("SPTTN_MTTKRP_MODE", m, ["mttkrp3_small", "mttkrp3_r32", "mttkrp4_small", "mttkrp4_r32"])
+     for m in ("0", "1", "2")] + \
+    [("SPTTN_TTTP_MODE", m, ["tttp3_small", "tttp3_r64"]) for m in ("0", "1")]
+
+
+@pytest.mark.parametrize("env,mode,names", VARIANTS, ids=[f"{v[0]}={v[1]}" for v in VARIANTS])
+def test_kernel_variants_agree(E, env, mode, names, monkeypatch):
+    """Every kernel variant kept for A/B measurement stays within tolerance,
+    on the golden fixtures and on BASELINE-shaped inputs."""
+    from paper_2307_05740_b200.configs import make_workload
+    monkeypatch.setenv(env, mode)
+    for name in names:
+        m = [c for c in CASES if c["name"] == name][0]
+        csf, factors, z = load_case(m)
+        out, _, _ = run(E, m["kind"], csf, factors, m["ranks"])
+        _, norm = oracle_with_norm(m["kind"], csf, factors, m["ranks"])
+        assert_parity(out, z["fused"], norm, f"{name} {env}={mode}")
+    key = {"SPTTN_TTMC3_MODE": "ttmc3", "SPTTN_MTTKRP_MODE": "mttkrp4",
+           "SPTTN_TTTP_MODE": "tttp3"}[env]
+    w = make_workload(key, scale=2e-3)
+    c = w.cfg
+    out, _, _ = run(E, c.kind, w.csf, w.factors, c.ranks, E.FLAG_RESIDUAL if c.residual else 0)
+    want, norm = oracle_with_norm(c.kind, w.csf, w.factors, c.ranks, residual=c.residual)
+    assert_parity(out, want, norm, f"{key} {env}={mode}")
+
+
 @pytest.mark.parametrize("key", ["mttkrp3", "ttmc3", "tttp3", "mttkrp4", "ttmc4"])
 def test_baseline_shaped_reduced_scale(E, key):
     from paper_2307_05740_b200.configs import make_workload
