@@ -43,6 +43,8 @@ struct spttn_plan {
   const double** d_dense = nullptr;
   int64_t launches = 0;
   int64_t last_madds = -1;
+  void* arena = nullptr;                // GENERIC: one allocation for all plan state
+  std::vector<int64_t> last_counters;   // GENERIC: madds, resets, log cursor, overflow
 };
 
 namespace {
@@ -259,6 +261,13 @@ int64_t spttn_csf_device_bytes(const spttn_csf* c) { return c ? c->d.bytes : -1;
 int spttn_plan_destroy(spttn_plan* p) {
   return guarded([&] {
     if (!p) return;
+    if (p->arena) {  // GENERIC: everything lives in the arena
+      cudaFree(p->arena);
+      spttn_dev::free_decomp(p->dec);
+      delete p->prog;
+      delete p;
+      return;
+    }
     if (p->own_fac)
       for (int f = 0; f < p->nf; ++f) cudaFree(p->fac[f]);
     cudaFree(p->out);
@@ -354,6 +363,55 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
         fail(SPTTN_EINVAL, "unknown nest kind " + std::to_string(p->kind));
     }
 
+    if (p->kind == SPTTN_NEST_GENERIC) {
+      // One device arena per interpreter plan (tiny plans are dominated by
+      // allocation cost): [counters | buffers | out] (zeroed by one memset
+      // per execute), program, buffer offsets, dense pointer table, factor
+      // copies, observer log, leaf keys.
+      const spg_program& G = *p->prog;
+      const int nb = G.num_buffers;
+      std::vector<int64_t> off(nb + 1, 0);
+      for (int b = 0; b < nb; ++b) off[b + 1] = off[b] + G.buffer_size[b];
+      auto al = [](size_t x) { return (x + 255) & ~size_t{255}; };
+      const size_t n_cnt = (nb + 4) * sizeof(int64_t);
+      const size_t n_buf = static_cast<size_t>(std::max<int64_t>(1, off[nb])) * 8;
+      const size_t n_out = static_cast<size_t>(std::max<int64_t>(1, G.out_size)) * 8;
+      const bool lookup = G.need_leaf_lookup && nnz > 0;
+      size_t total = n_cnt + n_buf + n_out;  // contiguous, 8-byte aligned
+      total = al(total) + al(sizeof(spg_program)) + al((nb + 1) * sizeof(int64_t)) +
+              al(16 * sizeof(double*));
+      if (!on_dev)
+        for (int f = 0; f < p->nf; ++f) total += al(p->fac_size[f] * 8);
+      const int64_t log_bytes = G.observe ? G.observe_log_bytes : 0;
+      total += al(log_bytes);
+      if (lookup) total += 2 * al(nnz * sizeof(int64_t));
+      dev_malloc(&p->arena, total);
+      char* cur = static_cast<char*>(p->arena);
+      auto take = [&](size_t bytes) { char* r = cur; cur += al(bytes); return r; };
+      auto& g = p->gen;
+      g.counters = reinterpret_cast<int64_t*>(cur);
+      g.buffers = reinterpret_cast<double*>(cur + n_cnt);
+      p->out = reinterpret_cast<double*>(cur + n_cnt + n_buf);
+      g.zero_bytes = n_cnt + n_buf + n_out;
+      cur += al(g.zero_bytes);
+      g.total_buffer_elems = off[nb];
+      g.d_prog = reinterpret_cast<spg_program*>(take(sizeof(spg_program)));
+      g.buffer_off = reinterpret_cast<int64_t*>(take((nb + 1) * sizeof(int64_t)));
+      p->d_dense = reinterpret_cast<const double**>(take(16 * sizeof(double*)));
+      if (!on_dev)
+        for (int f = 0; f < p->nf; ++f) p->fac[f] = reinterpret_cast<double*>(take(p->fac_size[f] * 8));
+      g.log_bytes = log_bytes;
+      g.log = log_bytes > 0 ? reinterpret_cast<unsigned char*>(take(log_bytes)) : nullptr;
+      if (lookup) {
+        g.leaf_keys = reinterpret_cast<int64_t*>(take(nnz * sizeof(int64_t)));
+        g.leaf_pos = reinterpret_cast<int64_t*>(take(nnz * sizeof(int64_t)));
+        g.n_leaf_keys = nnz;
+      }
+      g.in_arena = true;
+      SPTTN_CUDA(cudaMemcpyAsync(g.d_prog, &G, sizeof(spg_program), cudaMemcpyHostToDevice, s));
+      SPTTN_CUDA(cudaMemcpyAsync(g.buffer_off, off.data(), off.size() * sizeof(int64_t),
+                                 cudaMemcpyHostToDevice, s));
+    }
     copy_factors(p, desc->factors, on_dev, s);
     bool facs_aligned32 = true, facs_aligned16 = true;
     for (int f = 0; f < p->nf; ++f) {
@@ -363,21 +421,15 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
 
     if (p->kind == SPTTN_NEST_GENERIC) {
       p->out_count = p->prog->out_size;
-      dev_malloc(reinterpret_cast<void**>(&p->out), std::max<int64_t>(1, p->out_count) * 8);
       const double* hp[16] = {nullptr};
       for (int f = 0; f < p->nf; ++f) hp[f + 1] = p->fac[f];
-      dev_malloc(reinterpret_cast<void**>(&p->d_dense), sizeof(hp));
       SPTTN_CUDA(cudaMemcpyAsync(p->d_dense, hp, sizeof(hp), cudaMemcpyHostToDevice, s));
-      spttn_dev::generic_prepare(*p->prog, D, p->gen, s);
-      if (p->prog->need_leaf_lookup && nnz > 0) {
-        dev_malloc(reinterpret_cast<void**>(&p->gen.leaf_keys), nnz * sizeof(int64_t));
-        dev_malloc(reinterpret_cast<void**>(&p->gen.leaf_pos), nnz * sizeof(int64_t));
-        p->gen.n_leaf_keys = nnz;
+      if (p->gen.n_leaf_keys > 0) {
         k_leaf_keys<<<static_cast<unsigned>((nnz + 255) / 256), 256, 0, s>>>(
             D.view(), p->gen.d_prog, p->gen.leaf_keys, p->gen.leaf_pos);
         SPTTN_CUDA(cudaGetLastError());
       }
-      p->launches = 4;
+      p->launches = 2;
     } else {
       const bool sparse_out = p->kind == SPTTN_NEST_TTTP3;
       p->out_count = sparse_out ? nnz : D.dims[0] * tile;
@@ -576,13 +628,14 @@ int spttn_read_output(spttn_plan* p, double* host_out, int64_t count, void* stre
     cudaStream_t s = as_stream(stream);
     if (count)
       SPTTN_CUDA(cudaMemcpyAsync(host_out, p->out, count * sizeof(double), cudaMemcpyDeviceToHost, s));
-    if (p->kind == SPTTN_NEST_GENERIC) {
-      int64_t madds = 0;
-      SPTTN_CUDA(cudaMemcpyAsync(&madds, p->gen.counters, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-      SPTTN_CUDA(cudaStreamSynchronize(s));
-      p->last_madds = madds;
+    if (p->kind == SPTTN_NEST_GENERIC) {  // counters travel with the output
+      p->last_counters.resize(p->prog->num_buffers + 4);
+      SPTTN_CUDA(cudaMemcpyAsync(p->last_counters.data(), p->gen.counters,
+                                 p->last_counters.size() * sizeof(int64_t),
+                                 cudaMemcpyDeviceToHost, s));
     }
     SPTTN_CUDA(cudaStreamSynchronize(s));
+    if (p->kind == SPTTN_NEST_GENERIC) p->last_madds = p->last_counters[0];
   });
 }
 
@@ -600,9 +653,8 @@ int spttn_generic_resets(const spttn_plan* p, int64_t* out, int n) {
   return guarded([&] {
     if (!p || p->kind != SPTTN_NEST_GENERIC) fail(SPTTN_EINVAL, "not a GENERIC plan");
     const int nb = p->prog->num_buffers;
-    std::vector<int64_t> h(nb + 3);
-    SPTTN_CUDA(cudaMemcpy(h.data(), p->gen.counters, (nb + 3) * sizeof(int64_t),
-                          cudaMemcpyDeviceToHost));
+    const auto& h = p->last_counters;  // filled by spttn_read_output
+    if (static_cast<int>(h.size()) < nb + 3) fail(SPTTN_EINVAL, "read the output first");
     for (int b = 0; b < n && b < nb; ++b) out[b] = h[1 + b];
     if (h[2 + nb]) fail(SPTTN_ENOMEM, "observer log overflowed");
   });
@@ -610,11 +662,9 @@ int spttn_generic_resets(const spttn_plan* p, int64_t* out, int n) {
 
 int64_t spttn_generic_log_bytes(const spttn_plan* p) {
   if (!p || p->kind != SPTTN_NEST_GENERIC || !p->prog->observe) return 0;
-  int64_t cur = 0;
-  if (cudaMemcpy(&cur, p->gen.counters + 1 + p->prog->num_buffers, sizeof(int64_t),
-                 cudaMemcpyDeviceToHost) != cudaSuccess)
-    return -1;
-  return cur;
+  const int nb = p->prog->num_buffers;
+  if (static_cast<int>(p->last_counters.size()) < nb + 2) return -1;
+  return p->last_counters[1 + nb];
 }
 
 int spttn_generic_read_log(spttn_plan* p, void* host_out, int64_t bytes, void* stream) {

@@ -149,9 +149,21 @@ __device__ void set_iter(Interp& I, const spg_node& nd, int64_t it) {
   }
 }
 
-__global__ void k_generic(Interp I) {
+// The program (~23 KB) is staged into shared memory by the whole block so the
+// interpreting thread reads node / operand / hook tables at shared-memory
+// latency instead of global-memory latency.
+__global__ void __launch_bounds__(256) k_generic(Interp I) {
+  extern __shared__ __align__(16) unsigned char prog_smem[];
+  {
+    const int4* src = reinterpret_cast<const int4*>(I.P);
+    int4* dst = reinterpret_cast<int4*>(prog_smem);
+    for (size_t w = threadIdx.x; w < sizeof(spg_program) / sizeof(int4); w += blockDim.x)
+      dst[w] = src[w];
+    __syncthreads();
+  }
   if (blockIdx.x != 0 || threadIdx.x != 0) return;
-  const spg_program* P = I.P;
+  const spg_program* P = reinterpret_cast<const spg_program*>(prog_smem);
+  I.P = P;
   for (int k = 0; k < SPG_MAX_IDX; ++k) I.ival[k] = 0;
   for (int k = 0; k < SPG_MAX_LEVELS; ++k) I.pos[k] = 0;
   I.madds = 0;
@@ -358,29 +370,10 @@ __global__ void k_unf_sparse(Unf u, const int32_t* leaf_parent /* unused */) {
 
 }  // namespace
 
-void generic_prepare(const spg_program& prog, const DevCsf& csf, GenericState& g,
-                     cudaStream_t s) {
-  SPTTN_CUDA(cudaMalloc(&g.d_prog, sizeof(spg_program)));
-  SPTTN_CUDA(cudaMemcpyAsync(g.d_prog, &prog, sizeof(spg_program), cudaMemcpyHostToDevice, s));
-  std::vector<int64_t> off(prog.num_buffers + 1, 0);
-  for (int b = 0; b < prog.num_buffers; ++b) off[b + 1] = off[b] + prog.buffer_size[b];
-  g.total_buffer_elems = off[prog.num_buffers];
-  SPTTN_CUDA(cudaMalloc(&g.buffers, std::max<int64_t>(1, g.total_buffer_elems) * sizeof(double)));
-  SPTTN_CUDA(cudaMalloc(&g.buffer_off, (prog.num_buffers + 1) * sizeof(int64_t)));
-  SPTTN_CUDA(cudaMemcpyAsync(g.buffer_off, off.data(), off.size() * sizeof(int64_t),
-                             cudaMemcpyHostToDevice, s));
-  SPTTN_CUDA(cudaMalloc(&g.counters, (prog.num_buffers + 4) * sizeof(int64_t)));
-  g.log_bytes = prog.observe ? prog.observe_log_bytes : 0;
-  if (g.log_bytes > 0) SPTTN_CUDA(cudaMalloc(&g.log, g.log_bytes));
-  SPTTN_CUDA(cudaStreamSynchronize(s));
-}
-
 void generic_execute(const spg_program& prog, const DevCsf& csf, const double* const* dense,
                      double* out, GenericState& g, cudaStream_t s) {
-  SPTTN_CUDA(cudaMemsetAsync(g.counters, 0, (prog.num_buffers + 4) * sizeof(int64_t), s));
-  SPTTN_CUDA(cudaMemsetAsync(g.buffers, 0,
-                             std::max<int64_t>(1, g.total_buffer_elems) * sizeof(double), s));
-  SPTTN_CUDA(cudaMemsetAsync(out, 0, std::max<int64_t>(1, prog.out_size) * sizeof(double), s));
+  // counters, buffers and output are contiguous in the plan arena
+  SPTTN_CUDA(cudaMemsetAsync(g.counters, 0, g.zero_bytes, s));
   Interp I{};
   I.P = g.d_prog;
   I.t = csf.view();
@@ -394,11 +387,17 @@ void generic_execute(const spg_program& prog, const DevCsf& csf, const double* c
   I.leaf_keys = g.leaf_keys;
   I.leaf_pos = g.leaf_pos;
   I.nkeys = g.n_leaf_keys;
-  k_generic<<<1, 1, 0, s>>>(I);
+  static_assert(sizeof(spg_program) % sizeof(int4) == 0, "program must be int4-copyable");
+  static_assert(sizeof(spg_program) <= 48 * 1024, "program must fit default shared memory");
+  k_generic<<<1, 256, sizeof(spg_program), s>>>(I);
   SPTTN_CUDA(cudaGetLastError());
 }
 
 void generic_free(GenericState& g) {
+  if (g.in_arena) {  // owned by the plan arena
+    g = GenericState{};
+    return;
+  }
   cudaFree(g.d_prog);
   cudaFree(g.buffers);
   cudaFree(g.buffer_off);

@@ -168,10 +168,9 @@ struct GenericState {
   int64_t* leaf_pos = nullptr;
   int64_t n_leaf_keys = 0;
   int64_t total_buffer_elems = 0;
+  size_t zero_bytes = 0;  // [counters | buffers | out] cleared by one memset
+  bool in_arena = false;  // all pointers live in the plan's arena
 };
-
-void generic_prepare(const spg_program& prog, const DevCsf& csf, GenericState& g,
-                     cudaStream_t s);
 void generic_execute(const spg_program& prog, const DevCsf& csf, const double* const* dense,
                      double* out, GenericState& g, cudaStream_t s);
 void generic_free(GenericState& g);

@@ -76,6 +76,7 @@ typedef struct {
   int64_t mode_key_stride[SPG_MAX_LEVELS];
   int32_t observe;                     /* log buffer snapshots on reset */
   int64_t observe_log_bytes;           /* capacity for the log          */
+  int64_t reserved;                    /* keeps sizeof a multiple of 16 */
 } spg_program;
 
 #endif

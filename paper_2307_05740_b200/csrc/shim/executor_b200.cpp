@@ -20,6 +20,7 @@
 #include <chrono>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <numeric>
 #include <stdexcept>
 #include <string>
@@ -226,7 +227,53 @@ struct DeviceCsfHandle {
   }
 };
 
+std::shared_ptr<DeviceCsfHandle> upload_csf_uncached(const CsfTensor& csf);
+
+// Device CSF cache: plans over the same host tensor (e.g. every admissible
+// order of one fixture, proj/tests/acceptance.cpp:248-274) share one device
+// copy. A hit requires the same CsfTensor object AND the same contents
+// (FNV-1a over every array), so a tensor mutated between plans is re-uploaded;
+// only tensors up to 1M leaves are fingerprinted (larger ones re-upload).
+uint64_t fingerprint(const CsfTensor& csf) {
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&](const void* p, size_t n) {
+    const unsigned char* c = static_cast<const unsigned char*>(p);
+    for (size_t i = 0; i < n; ++i) {
+      h ^= c[i];
+      h *= 1099511628211ull;
+    }
+  };
+  for (const auto& m : csf.modes) mix(&m.dim, sizeof(m.dim));
+  for (const auto& v : csf.idx) mix(v.data(), v.size() * sizeof(int64_t));
+  for (const auto& v : csf.ptr) mix(v.data(), v.size() * sizeof(int64_t));
+  mix(csf.values.data(), csf.values.size() * sizeof(double));
+  return h;
+}
+
 std::shared_ptr<DeviceCsfHandle> upload_csf(const CsfTensor& csf) {
+  constexpr int64_t kCacheMaxNnz = int64_t{1} << 20;
+  if (csf.nnz() > kCacheMaxNnz) return upload_csf_uncached(csf);
+  struct Entry {
+    const CsfTensor* key;
+    uint64_t fp;
+    std::weak_ptr<DeviceCsfHandle> dev;
+  };
+  static std::mutex mu;
+  static std::vector<Entry> cache;
+  const uint64_t fp = fingerprint(csf);
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& e : cache)
+    if (e.key == &csf && e.fp == fp)
+      if (auto d = e.dev.lock()) return d;
+  auto d = upload_csf_uncached(csf);
+  cache.erase(std::remove_if(cache.begin(), cache.end(),
+                             [&](const Entry& e) { return e.key == &csf || e.dev.expired(); }),
+              cache.end());
+  cache.push_back(Entry{&csf, fp, d});
+  return d;
+}
+
+std::shared_ptr<DeviceCsfHandle> upload_csf_uncached(const CsfTensor& csf) {
   const int d = static_cast<int>(csf.order());
   std::vector<int64_t> dims(d), sizes(d);
   std::vector<const int64_t*> idx(d), ptr(std::max(1, d - 1));
