@@ -457,7 +457,24 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
         const int64_t warps = static_cast<int64_t>(sms) * 32 * 2;
         int64_t chunk = env_int("SPTTN_CHUNK", 0);
         if (chunk <= 0) chunk = std::clamp<int64_t>((units + warps - 1) / warps, 8, 1024);
-        if (p->kind == SPTTN_NEST_TTMC3 && (p->mode == 6 || p->mode == 7)) {
+        if (p->kind == SPTTN_NEST_TTMC4)
+          p->mode = static_cast<int>(env_int("SPTTN_TTMC4_MODE", 1));  // 1 = packed (default)
+        if (p->kind == SPTTN_NEST_TTMC4 && p->mode == 1) {
+          // (i,j) pieces of <= 4 leaves, length-sorted groups of 8, with each
+          // leaf's level-2 (k) coordinate packed next to its level-3 (l) one
+          spttn_dev::build_segments(D, 1, std::clamp(seg_len, 1, 4), chunk, p->dec, tile, s,
+                                    false, true);
+          int32_t* leaf_k = nullptr;
+          dev_malloc(reinterpret_cast<void**>(&leaf_k), std::max<int64_t>(1, nnz) * sizeof(int32_t));
+          spttn_dev::expand_coords(D, 2, D.idx[2], leaf_k, s);
+          spttn_dev::build_packed(D, 3, p->dec, s, spttn_dev::kPackSlots, leaf_k);
+          cudaFree(leaf_k);
+          const int64_t w16 = static_cast<int64_t>(sms) * 16 * 2;
+          int64_t gchunk = env_int("SPTTN_GCHUNK", 0);
+          if (gchunk <= 0)
+            gchunk = std::clamp<int64_t>((p->dec.n_groups + w16 - 1) / w16, 4, 1024);
+          spttn_dev::finish_unit_items(D, p->dec, p->dec.slice_grp, p->dec.n_groups, gchunk, tile, s);
+        } else if (p->kind == SPTTN_NEST_TTMC3 && (p->mode == 6 || p->mode == 7)) {
           // packed length-sorted groups of 8 segments (pack.cu)
           spttn_dev::build_segments(D, 1, seg_len, chunk, p->dec, tile, s, false);
           spttn_dev::build_packed(D, 2, p->dec, s);
@@ -568,6 +585,7 @@ int spttn_execute_stage(spttn_plan* p, int stage, void* stream) {
     a.grp_node = p->dec.grp_node;
     a.grp_node1 = p->dec.grp_node1;
     a.pk = p->dec.pk;
+    a.pk2 = p->dec.pk2;
     a.pv = p->dec.pv;
     a.slice_grp = p->dec.slice_grp;
     a.n_groups = p->dec.n_groups;

@@ -67,20 +67,37 @@ __global__ void k_child_coord(const int32_t* ptr, const int32_t* coord, int32_t 
 }
 
 // Segment counts per unit node: ceil(children / seg_len).
-__global__ void k_seg_count(CsfView t, int unit_level, int seg_len, int32_t* cnt) {
-  const int32_t f = blockIdx.x * blockDim.x + threadIdx.x;
-  if (f >= t.nlev[unit_level]) return;
-  const int32_t n = t.ptr[unit_level][f + 1] - t.ptr[unit_level][f];
-  cnt[f] = (n + seg_len - 1) / seg_len;
+// Child range of unit node f: its direct children, or (leaf_space) its
+// leaves, found by following the child pointers down to the leaf level.
+__device__ __forceinline__ void child_range(const CsfView& t, int unit_level, int32_t f,
+                                            bool leaf_space, int32_t* b, int32_t* e) {
+  int32_t lo = t.ptr[unit_level][f], hi = t.ptr[unit_level][f + 1];
+  if (leaf_space)
+    for (int l = unit_level + 1; l + 1 < t.order; ++l) {
+      lo = t.ptr[l][lo];
+      hi = t.ptr[l][hi];
+    }
+  *b = lo;
+  *e = hi;
 }
 
-__global__ void k_seg_fill(CsfView t, int unit_level, int seg_len, const int32_t* off,
-                           const int32_t* unit_parent, int32_t* seg_begin, int32_t* seg_node,
-                           int32_t* seg_node1) {
+__global__ void k_seg_count(CsfView t, int unit_level, int seg_len, bool leaf_space,
+                            int32_t* cnt) {
+  const int32_t f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= t.nlev[unit_level]) return;
+  int32_t b, e;
+  child_range(t, unit_level, f, leaf_space, &b, &e);
+  cnt[f] = (e - b + seg_len - 1) / seg_len;
+}
+
+__global__ void k_seg_fill(CsfView t, int unit_level, int seg_len, bool leaf_space,
+                           const int32_t* off, const int32_t* unit_parent, int32_t* seg_begin,
+                           int32_t* seg_node, int32_t* seg_node1) {
   const int32_t f = blockIdx.x * blockDim.x + threadIdx.x;
   const int32_t nf = t.nlev[unit_level];
   if (f >= nf) return;
-  const int32_t b = t.ptr[unit_level][f], e = t.ptr[unit_level][f + 1];
+  int32_t b, e;
+  child_range(t, unit_level, f, leaf_space, &b, &e);
   const int32_t coord = t.idx[unit_level][f];
   const int32_t pc = unit_parent ? unit_parent[f] : 0;
   int32_t o = off[f];
@@ -193,7 +210,7 @@ void build_leaf_items(const DevCsf& csf, int64_t chunk, Decomp& d, int64_t tile,
 }
 
 void build_segments(const DevCsf& csf, int unit_level, int seg_len, int64_t chunk, Decomp& d,
-                    int64_t tile, cudaStream_t s, bool make_items) {
+                    int64_t tile, cudaStream_t s, bool make_items, bool leaf_space) {
   const CsfView t = csf.view();
   const int32_t nf = static_cast<int32_t>(csf.level_size[unit_level]);
   const int32_t n0 = static_cast<int32_t>(csf.level_size[0]);
@@ -204,7 +221,7 @@ void build_segments(const DevCsf& csf, int unit_level, int seg_len, int64_t chun
   SPTTN_CUDA(cudaMallocAsync(&off, (static_cast<int64_t>(nf) + 1) * sizeof(int32_t), s));
   SPTTN_CUDA(cudaMemsetAsync(off, 0, (static_cast<int64_t>(nf) + 1) * sizeof(int32_t), s));
   if (nf > 0) {
-    k_seg_count<<<blocks_for(nf, 256), 256, 0, s>>>(t, unit_level, seg_len, off);
+    k_seg_count<<<blocks_for(nf, 256), 256, 0, s>>>(t, unit_level, seg_len, leaf_space, off);
     SPTTN_CUDA(cudaGetLastError());
   }
   size_t temp_bytes = 0;
@@ -230,8 +247,9 @@ void build_segments(const DevCsf& csf, int unit_level, int seg_len, int64_t chun
       k_child_coord<<<blocks_for(n1, 256), 256, 0, s>>>(t.ptr[1], t.idx[1], n1, unit_parent);
   }
   if (nf > 0) {
-    k_seg_fill<<<blocks_for(nf, 256), 256, 0, s>>>(t, unit_level, seg_len, off, unit_parent,
-                                                   d.seg_begin, d.seg_node, d.seg_node1);
+    k_seg_fill<<<blocks_for(nf, 256), 256, 0, s>>>(t, unit_level, seg_len, leaf_space, off,
+                                                   unit_parent, d.seg_begin, d.seg_node,
+                                                   d.seg_node1);
     SPTTN_CUDA(cudaGetLastError());
   }
   if (unit_parent) SPTTN_CUDA(cudaFreeAsync(unit_parent, s));
@@ -256,6 +274,15 @@ void finish_unit_items(const DevCsf& csf, Decomp& d, const int32_t* slice_units,
   }
   SPTTN_CUDA(cudaMalloc(&d.part, std::max<int64_t>(1, d.n_items * 2 * tile) * sizeof(double)));
   find_splits_and_absent(csf, d, slice_units, s);
+}
+
+void expand_coords(const DevCsf& csf, int level, const int32_t* coords, int32_t* out,
+                   cudaStream_t s) {
+  const int32_t n = static_cast<int32_t>(csf.level_size[level]);
+  if (n > 0) {
+    k_child_coord<<<blocks_for(n, 256), 256, 0, s>>>(csf.ptr[level], coords, n, out);
+    SPTTN_CUDA(cudaGetLastError());
+  }
 }
 
 void build_leaf_coords(const DevCsf& csf, int32_t** leaf_i, int32_t** leaf_j, cudaStream_t s) {
@@ -378,6 +405,7 @@ void free_decomp(Decomp& d) {
   cudaFree(d.grp_node);
   cudaFree(d.grp_node1);
   cudaFree(d.pk);
+  cudaFree(d.pk2);
   cudaFree(d.pv);
   cudaFree(d.slice_grp);
   cudaFree(d.slice_seg);

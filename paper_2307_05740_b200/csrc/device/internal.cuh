@@ -88,6 +88,7 @@ struct Decomp {
   int32_t* grp_node = nullptr;     // [n_groups][8] fiber coordinate per slot
   int32_t* grp_node1 = nullptr;    // [n_groups][8] level-1 coordinate (order 4)
   int32_t* pk = nullptr;           // interleaved leaf coordinates
+  int32_t* pk2 = nullptr;          // interleaved second per-leaf coordinate (optional)
   double* pv = nullptr;            // interleaved leaf values
   int32_t* slice_grp = nullptr;    // [n0+1] first group of each slice
   int32_t* slice_seg = nullptr;    // [n0+1]   segment offset of each slice
@@ -115,6 +116,7 @@ struct RootOutArgs {
   const int32_t* grp_node;
   const int32_t* grp_node1;
   const int32_t* pk;
+  const int32_t* pk2;
   const double* pv;
   const int32_t* slice_grp;
   int64_t n_groups;
@@ -140,8 +142,15 @@ int group_lanes_for(int R);
 
 // ---- plan-time helpers (decomp.cu) ----------------------------------------
 void build_leaf_items(const DevCsf& csf, int64_t chunk, Decomp& d, int64_t tile, cudaStream_t s);
+// leaf_space: segments are cut in the unit's LEAF range (seg_begin in leaf
+// offsets) instead of its direct children.
 void build_segments(const DevCsf& csf, int unit_level, int seg_len, int64_t chunk, Decomp& d,
-                    int64_t tile, cudaStream_t s, bool make_items = true);
+                    int64_t tile, cudaStream_t s, bool make_items = true,
+                    bool leaf_space = false);
+// Coordinate of each node's ancestor one level up, broadcast to the node's
+// children (level `l` -> level `l+1`), into `out` (nlev[l+1] entries).
+void expand_coords(const DevCsf& csf, int level, const int32_t* coords, int32_t* out,
+                   cudaStream_t s);
 // Items of `chunk` consecutive units (segments or packed groups) given the
 // first unit of every root slice; partial tiles, split slices, absent rows.
 void finish_unit_items(const DevCsf& csf, Decomp& d, const int32_t* slice_units, int64_t n_units,
@@ -149,8 +158,10 @@ void finish_unit_items(const DevCsf& csf, Decomp& d, const int32_t* slice_units,
 // Length-sorted packed groups of 8 segments (pack.cu); leaf_level = CSF level
 // of the streamed coordinates.
 constexpr int kPackSlots = 8;  // TTMc-3 groups (128-byte rows)
+// leaf_coord2 (optional, per leaf) is packed alongside as pk2 (TTMc-4: the
+// leaf's level-2 coordinate).
 void build_packed(const DevCsf& csf, int leaf_level, Decomp& d, cudaStream_t s,
-                  int slots = kPackSlots);
+                  int slots = kPackSlots, const int32_t* leaf_coord2 = nullptr);
 constexpr int kFixChunk = 32;
 void build_fixup_chunks(Decomp& d, cudaStream_t s);
 void launch_fixup(const Decomp& d, const CsfView& t, double* out, cudaStream_t s);

@@ -1021,6 +1021,122 @@ __global__ void __launch_bounds__(kBlock, 3) k_ttmc3ps(RootOutArgs a) {
   if (pending) flush(head ? 0 : 1);
 }
 
+// TTMc-4, packed form (default). Units are (i,j) fiber pieces of <= 4 LEAVES
+// (the (i,j,k) level holds ~1 leaf at the BASELINE shape, so X[t] = v*W[l,t]
+// per leaf and Y[s,t] += V[k,s] * X[t] regroups the reference's per-(i,j,k)
+// sums), length-sorted into groups of 8 (pack.cu) with the leaf's level-3 and
+// level-2 coordinates interleaved. Lane L = (q = L%4, h = L/4) owns segments
+// q and q+4 (the two DMMA K-chunks) and holds Y[seg][s = 0..7][t = h] — which
+// is already the B fragment of tile s for the last stage, eight DMMA per
+// K-chunk: Out_i(R x ST) += U_J^T Y_J. Gathers: the V row is read by the 8
+// lanes of a slot (broadcast, 2 x 256-bit), W[l, h] per lane (8 rows per
+// 64-bit instruction), all issued in straight-line code.
+template <bool VECV>
+__global__ void __launch_bounds__(kBlock, 2) k_ttmc4pk(RootOutArgs a) {
+  const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
+  if (w >= a.n_items) return;  // warp-uniform
+  const int lane = threadIdx.x & 31;
+  const int q = lane & 3;
+  const int h = lane >> 2;
+  const int R = a.R, S = a.S, T = a.T;
+  const CsfView& t = a.t;
+  const double* __restrict__ U = a.f[1];
+  const double* __restrict__ V = a.f[2];
+  const double* __restrict__ W = a.f[3];
+  const int4* __restrict__ hdr = a.grp_hdr;
+  const int32_t* __restrict__ gnode = a.grp_node;
+  const int32_t* __restrict__ pl = a.pk;
+  const int32_t* __restrict__ pkk = a.pk2;
+  const double* __restrict__ pv = a.pv;
+  const int32_t* __restrict__ slice_grp = a.slice_grp;
+  const int64_t tile = static_cast<int64_t>(R) * S * T;
+
+  const int32_t cbeg = static_cast<int32_t>(w * a.chunk);
+  const int32_t cend = static_cast<int32_t>(min64(cbeg + a.chunk, a.n_groups));
+  int32_t sl = a.item_pos[w];
+  int32_t sl_end = slice_grp[sl + 1];
+  bool head = slice_grp[sl] < cbeg;
+  int32_t row = t.idx[0][sl];
+  bool pending = false;
+  double acc[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) acc[e] = 0.0;
+
+  auto flush = [&](int dslot) {
+    double* dst = dslot < 0 ? a.out + static_cast<int64_t>(row) * tile
+                            : a.part + (w * 2 + dslot) * tile;
+#pragma unroll
+    for (int s = 0; s < 8; ++s)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int tt = 2 * q + e;
+        if (h < R && s < S && tt < T) dst[(h * S + s) * T + tt] = acc[2 * s + e];
+      }
+#pragma unroll
+    for (int e = 0; e < 16; ++e) acc[e] = 0.0;
+  };
+  auto vrow = [&](int32_t k, bool on, double* vr) {
+    const double* p = V + static_cast<int64_t>(k) * S;
+    if (VECV) {
+      const double4 a0 = ld256_if(p, on), a1 = ld256_if(p + 4, on);
+      vr[0] = a0.x; vr[1] = a0.y; vr[2] = a0.z; vr[3] = a0.w;
+      vr[4] = a1.x; vr[5] = a1.y; vr[6] = a1.z; vr[7] = a1.w;
+    } else {
+#pragma unroll
+      for (int s = 0; s < 8; ++s) vr[s] = (on && s < S) ? __ldg(p + s) : 0.0;
+    }
+  };
+
+  for (int32_t g = cbeg; g < cend; ++g) {
+    const int4 hh = __ldg(hdr + g);
+    const int n = hh.y;  // warp-uniform leaves per segment
+    const int64_t gs = static_cast<int64_t>(g) * kPackSlots;
+    const int32_t jA = __ldg(gnode + gs + q), jB = __ldg(gnode + gs + 4 + q);
+    const double uA = h < R ? __ldg(U + static_cast<int64_t>(jA) * R + h) : 0.0;
+    const double uB = h < R ? __ldg(U + static_cast<int64_t>(jB) * R + h) : 0.0;
+    double YA[8], YB[8];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) YA[s] = YB[s] = 0.0;
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      if (it < n) {  // warp-uniform
+        const int32_t eA = hh.x + it * kPackSlots + q, eB = eA + 4;
+        const int32_t lA = __ldg(pl + eA), lB = __ldg(pl + eB);
+        const int32_t kA = __ldg(pkk + eA), kB = __ldg(pkk + eB);
+        const double vA = __ldg(pv + eA), vB = __ldg(pv + eB);
+        const double wA = h < T ? __ldg(W + static_cast<int64_t>(lA) * T + h) : 0.0;
+        const double wB = h < T ? __ldg(W + static_cast<int64_t>(lB) * T + h) : 0.0;
+        double vrA[8], vrB[8];
+        vrow(kA, true, vrA);
+        vrow(kB, true, vrB);
+        const double xA = vA * wA, xB = vB * wB;  // X[t] = t_ijkl * W[l,t]
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+          YA[s] = fma(vrA[s], xA, YA[s]);  // Y[s,t] += V[k,s] * X[t]
+          YB[s] = fma(vrB[s], xB, YB[s]);
+        }
+      }
+    }
+    // Out_i[r, s, t] += U[j, r] * Y[s, t] for both K-chunks
+#pragma unroll
+    for (int s = 0; s < 8; ++s) dmma_8x8x4(acc[2 * s], acc[2 * s + 1], uA, YA[s]);
+#pragma unroll
+    for (int s = 0; s < 8; ++s) dmma_8x8x4(acc[2 * s], acc[2 * s + 1], uB, YB[s]);
+    pending = true;
+    if (g + 1 == sl_end) {
+      flush(head ? 0 : -1);
+      pending = false;
+      head = false;
+      if (g + 1 < cend) {
+        ++sl;
+        sl_end = slice_grp[sl + 1];
+        row = t.idx[0][sl];
+      }
+    }
+  }
+  if (pending) flush(head ? 0 : 1);
+}
+
 template <bool VECV>
 __global__ void __launch_bounds__(kBlock) k_ttmc4(RootOutArgs a) {
   const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
@@ -1244,10 +1360,17 @@ void launch_ttmc3(const RootOutArgs& a, cudaStream_t s) {
 void launch_ttmc4(const RootOutArgs& a, cudaStream_t s) {
   const int64_t blocks = (a.n_items * 32 + kBlock - 1) / kBlock;
   if (blocks == 0) return;
-  if (a.vec & 2)
+  const int mode = a.flags >> 8;
+  if (mode == 1) {
+    if (a.vec & 2)
+      k_ttmc4pk<true><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
+    else
+      k_ttmc4pk<false><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
+  } else if (a.vec & 2) {
     k_ttmc4<true><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
-  else
+  } else {
     k_ttmc4<false><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
+  }
   SPTTN_CUDA(cudaGetLastError());
 }
 
