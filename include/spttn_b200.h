@@ -161,6 +161,10 @@ int spttn_unfactorized(const spttn_unfact_desc* desc, spttn_csf* csf, double* ho
 int spttn_device_info(int64_t* out, int n);
 /* Build identification string (arch, nvcc version). */
 const char* spttn_build_info(void);
+/* Device memory of CSF layouts and plans comes from a per-device
+ * stream-ordered pool that keeps freed pages mapped, so rebuilding plans is
+ * cheap. Returns the pools' cached (unused) pages to the driver. */
+int spttn_release_cached(void);
 
 #ifdef __cplusplus
 }

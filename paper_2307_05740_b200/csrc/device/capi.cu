@@ -72,14 +72,8 @@ void fail(int code, const std::string& msg) { throw Status(code, msg); }
 
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
-void dev_malloc(void** p, size_t bytes) {
-  const cudaError_t e = cudaMalloc(p, bytes ? bytes : 1);
-  if (e == cudaErrorMemoryAllocation) {
-    cudaGetLastError();
-    fail(SPTTN_ENOMEM, "device allocation of " + std::to_string(bytes) + " bytes failed");
-  }
-  if (e != cudaSuccess) fail(SPTTN_ECUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
-}
+// all device memory comes from the engine's pool (mem.cu)
+void dev_malloc(void** p, size_t bytes, cudaStream_t s) { spttn_dev::dmalloc_raw(p, bytes, s); }
 
 // int64 -> int32 narrowing with range / monotonicity checks.
 __global__ void k_narrow(const int64_t* src, int32_t* dst, int64_t n, int64_t limit,
@@ -133,7 +127,7 @@ void copy_factors(spttn_plan* p, const double* const* src, bool on_device, cudaS
     if (on_device) {
       p->fac[f] = const_cast<double*>(src[f]);
     } else {
-      if (!p->fac[f]) dev_malloc(reinterpret_cast<void**>(&p->fac[f]), p->fac_size[f] * sizeof(double));
+      if (!p->fac[f]) dev_malloc(reinterpret_cast<void**>(&p->fac[f]), p->fac_size[f] * sizeof(double), s);
       if (p->fac_size[f] > 0)
         SPTTN_CUDA(cudaMemcpyAsync(p->fac[f], src[f], p->fac_size[f] * sizeof(double),
                                    cudaMemcpyHostToDevice, s));
@@ -146,6 +140,13 @@ void copy_factors(spttn_plan* p, const double* const* src, bool on_device, cudaS
 extern "C" {
 
 const char* spttn_last_error(void) { return g_err.c_str(); }
+
+int spttn_release_cached(void) {
+  return guarded([] {
+    SPTTN_CUDA(cudaDeviceSynchronize());
+    spttn_dev::release_cached();
+  });
+}
 
 #define SPTTN_STR2(x) #x
 #define SPTTN_STR(x) SPTTN_STR2(x)
@@ -195,11 +196,11 @@ int spttn_csf_create(const spttn_csf_host* h, void* stream, spttn_csf** out) {
     }
     int64_t* stage = nullptr;
     int* err = nullptr;
-    dev_malloc(reinterpret_cast<void**>(&stage), maxn * sizeof(int64_t));
-    dev_malloc(reinterpret_cast<void**>(&err), sizeof(int));
+    dev_malloc(reinterpret_cast<void**>(&stage), maxn * sizeof(int64_t), s);
+    dev_malloc(reinterpret_cast<void**>(&err), sizeof(int), s);
     SPTTN_CUDA(cudaMemsetAsync(err, 0, sizeof(int), s));
     auto narrow = [&](const int64_t* src, int32_t** dst, int64_t n, int64_t limit, int mono) {
-      dev_malloc(reinterpret_cast<void**>(dst), std::max<int64_t>(1, n) * sizeof(int32_t));
+      dev_malloc(reinterpret_cast<void**>(dst), std::max<int64_t>(1, n) * sizeof(int32_t), s);
       D.bytes += n * sizeof(int32_t);
       if (n == 0) return;
       SPTTN_CUDA(cudaMemcpyAsync(stage, src, n * sizeof(int64_t), cudaMemcpyHostToDevice, s));
@@ -214,7 +215,7 @@ int spttn_csf_create(const spttn_csf_host* h, void* stream, spttn_csf** out) {
           narrow(h->ptr[l], &D.ptr[l], h->level_size[l] + 1, h->level_size[l + 1] + 1, 1);
       }
       const int64_t nnz = h->level_size[d - 1];
-      dev_malloc(reinterpret_cast<void**>(&D.vals), std::max<int64_t>(1, nnz) * sizeof(double));
+      dev_malloc(reinterpret_cast<void**>(&D.vals), std::max<int64_t>(1, nnz) * sizeof(double), s);
       D.bytes += nnz * sizeof(double);
       if (nnz > 0)
         SPTTN_CUDA(cudaMemcpyAsync(D.vals, h->values, nnz * sizeof(double),
@@ -225,17 +226,17 @@ int spttn_csf_create(const spttn_csf_host* h, void* stream, spttn_csf** out) {
       if (herr & 1) fail(SPTTN_EINVAL, "CSF coordinate or child pointer out of range");
       if (herr & 2) fail(SPTTN_EINVAL, "CSF child pointers are not monotone");
     } catch (...) {
-      cudaFree(stage);
-      cudaFree(err);
+      spttn_dev::dfree(stage, s);
+      spttn_dev::dfree(err, s);
       for (int l = 0; l < d; ++l) {
-        cudaFree(D.idx[l]);
-        cudaFree(D.ptr[l]);
+        spttn_dev::dfree(D.idx[l], s);
+        spttn_dev::dfree(D.ptr[l], s);
       }
-      cudaFree(D.vals);
+      spttn_dev::dfree(D.vals, s);
       throw;
     }
-    cudaFree(stage);
-    cudaFree(err);
+    spttn_dev::dfree(stage, s);
+    spttn_dev::dfree(err, s);
     *out = c.release();
   });
 }
@@ -243,11 +244,12 @@ int spttn_csf_create(const spttn_csf_host* h, void* stream, spttn_csf** out) {
 int spttn_csf_destroy(spttn_csf* c) {
   return guarded([&] {
     if (!c) return;
+    cudaDeviceSynchronize();  // as cudaFree would: no kernel may still read it
     for (int l = 0; l < c->d.order; ++l) {
-      cudaFree(c->d.idx[l]);
-      cudaFree(c->d.ptr[l]);
+      spttn_dev::dfree(c->d.idx[l]);
+      spttn_dev::dfree(c->d.ptr[l]);
     }
-    cudaFree(c->d.vals);
+    spttn_dev::dfree(c->d.vals);
     delete c;
   });
 }
@@ -261,19 +263,20 @@ int64_t spttn_csf_device_bytes(const spttn_csf* c) { return c ? c->d.bytes : -1;
 int spttn_plan_destroy(spttn_plan* p) {
   return guarded([&] {
     if (!p) return;
+    cudaDeviceSynchronize();  // as cudaFree would: no kernel may still use it
     if (p->arena) {  // GENERIC: everything lives in the arena
-      cudaFree(p->arena);
+      spttn_dev::dfree(p->arena);
       spttn_dev::free_decomp(p->dec);
       delete p->prog;
       delete p;
       return;
     }
     if (p->own_fac)
-      for (int f = 0; f < p->nf; ++f) cudaFree(p->fac[f]);
-    cudaFree(p->out);
-    cudaFree(p->d_dense);
-    cudaFree(p->leaf_i);
-    cudaFree(p->leaf_j);
+      for (int f = 0; f < p->nf; ++f) spttn_dev::dfree(p->fac[f]);
+    spttn_dev::dfree(p->out);
+    spttn_dev::dfree(p->d_dense);
+    spttn_dev::dfree(p->leaf_i);
+    spttn_dev::dfree(p->leaf_j);
     spttn_dev::free_decomp(p->dec);
     spttn_dev::generic_free(p->gen);
     delete p->prog;
@@ -385,7 +388,7 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
       const int64_t log_bytes = G.observe ? G.observe_log_bytes : 0;
       total += al(log_bytes);
       if (lookup) total += 2 * al(nnz * sizeof(int64_t));
-      dev_malloc(&p->arena, total);
+      dev_malloc(&p->arena, total, s);
       char* cur = static_cast<char*>(p->arena);
       auto take = [&](size_t bytes) { char* r = cur; cur += al(bytes); return r; };
       auto& g = p->gen;
@@ -412,7 +415,9 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
       SPTTN_CUDA(cudaMemcpyAsync(g.buffer_off, off.data(), off.size() * sizeof(int64_t),
                                  cudaMemcpyHostToDevice, s));
     }
+    spttn_dev::plan_trace("plan: setup", s);
     copy_factors(p, desc->factors, on_dev, s);
+    spttn_dev::plan_trace("plan: factors", s);
     bool facs_aligned32 = true, facs_aligned16 = true;
     for (int f = 0; f < p->nf; ++f) {
       facs_aligned32 &= aligned(p->fac[f], 32);
@@ -433,7 +438,7 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
     } else {
       const bool sparse_out = p->kind == SPTTN_NEST_TTTP3;
       p->out_count = sparse_out ? nnz : D.dims[0] * tile;
-      dev_malloc(reinterpret_cast<void**>(&p->out), std::max<int64_t>(1, p->out_count) * 8);
+      dev_malloc(reinterpret_cast<void**>(&p->out), std::max<int64_t>(1, p->out_count) * 8, s);
       const int sms = sm_count();
       if (p->kind == SPTTN_NEST_TTMC3 || p->kind == SPTTN_NEST_TTMC4) {
         const bool vu = (R % 2 == 0) && facs_aligned16;
@@ -465,10 +470,10 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
           spttn_dev::build_segments(D, 1, std::clamp(seg_len, 1, 4), chunk, p->dec, tile, s,
                                     false, true);
           int32_t* leaf_k = nullptr;
-          dev_malloc(reinterpret_cast<void**>(&leaf_k), std::max<int64_t>(1, nnz) * sizeof(int32_t));
+          dev_malloc(reinterpret_cast<void**>(&leaf_k), std::max<int64_t>(1, nnz) * sizeof(int32_t), s);
           spttn_dev::expand_coords(D, 2, D.idx[2], leaf_k, s);
           spttn_dev::build_packed(D, 3, p->dec, s, spttn_dev::kPackSlots, leaf_k);
-          cudaFree(leaf_k);
+          spttn_dev::dfree(leaf_k, s);
           const int64_t w16 = static_cast<int64_t>(sms) * 16 * 2;
           int64_t gchunk = env_int("SPTTN_GCHUNK", 0);
           if (gchunk <= 0)
@@ -525,6 +530,7 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
       }
       p->launches = 1 + (p->dec.n_split > 0) + (p->dec.n_absent > 0);
     }
+    spttn_dev::plan_trace("plan: decomposition", s);
     SPTTN_CUDA(cudaStreamSynchronize(s));
     *out = p;
     raw = nullptr;
@@ -709,19 +715,20 @@ int spttn_unfactorized(const spttn_unfact_desc* desc, spttn_csf* csf, double* ho
       int64_t n = 1;
       for (int k = 0; k < desc->factor_order[f]; ++k) n *= desc->dims[desc->factor_ids[f][k]];
       double* d = nullptr;
-      dev_malloc(reinterpret_cast<void**>(&d), n * sizeof(double));
+      dev_malloc(reinterpret_cast<void**>(&d), n * sizeof(double), s);
       tmp.push_back(d);
       SPTTN_CUDA(cudaMemcpyAsync(d, desc->factors[f], n * sizeof(double), cudaMemcpyHostToDevice, s));
       dptr[f] = d;
     }
-    dev_malloc(reinterpret_cast<void**>(&dout), std::max<int64_t>(1, out_count) * sizeof(double));
+    dev_malloc(reinterpret_cast<void**>(&dout), std::max<int64_t>(1, out_count) * sizeof(double), s);
     spttn_dev::unfactorized_run(desc, csf->d, dptr, dout, out_count, s);
     if (out_count)
       SPTTN_CUDA(cudaMemcpyAsync(host_out, dout, out_count * sizeof(double), cudaMemcpyDeviceToHost, s));
     SPTTN_CUDA(cudaStreamSynchronize(s));
   });
-  for (double* d : tmp) cudaFree(d);
-  cudaFree(dout);
+  cudaDeviceSynchronize();
+  for (double* d : tmp) spttn_dev::dfree(d);
+  spttn_dev::dfree(dout);
   return rc;
 }
 

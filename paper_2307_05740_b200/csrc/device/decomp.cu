@@ -2,6 +2,10 @@
 // deterministic fix-up epilogue for root slices split across work items.
 #include <cub/cub.cuh>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include "internal.cuh"
 
 namespace spttn_dev {
@@ -158,15 +162,15 @@ void find_splits_and_absent(const DevCsf& csf, Decomp& d, const int32_t* slice_u
   const int32_t n0 = static_cast<int32_t>(csf.level_size[0]);
   int32_t* counts = nullptr;
   unsigned char* present = nullptr;
-  SPTTN_CUDA(cudaMallocAsync(&counts, 2 * sizeof(int32_t), s));
+  dmalloc(&counts, 2 * sizeof(int32_t), s);
   SPTTN_CUDA(cudaMemsetAsync(counts, 0, 2 * sizeof(int32_t), s));
-  SPTTN_CUDA(cudaMallocAsync(&present, csf.dims[0], s));
+  dmalloc(&present, csf.dims[0], s);
   SPTTN_CUDA(cudaMemsetAsync(present, 0, csf.dims[0], s));
   const int64_t nsplit_cap = n0 > 0 ? n0 : 1;
-  SPTTN_CUDA(cudaMalloc(&d.split_node, nsplit_cap * sizeof(int32_t)));
-  SPTTN_CUDA(cudaMalloc(&d.split_first, nsplit_cap * sizeof(int32_t)));
-  SPTTN_CUDA(cudaMalloc(&d.split_last, nsplit_cap * sizeof(int32_t)));
-  SPTTN_CUDA(cudaMalloc(&d.absent_rows, csf.dims[0] * sizeof(int32_t)));
+  dmalloc(&d.split_node, nsplit_cap * sizeof(int32_t), s);
+  dmalloc(&d.split_first, nsplit_cap * sizeof(int32_t), s);
+  dmalloc(&d.split_last, nsplit_cap * sizeof(int32_t), s);
+  dmalloc(&d.absent_rows, csf.dims[0] * sizeof(int32_t), s);
   if (n0 > 0) {
     if (segments)
       k_seg_splits<<<blocks_for(n0, 256), 256, 0, s>>>(t, slice_units, d.chunk, d.split_node,
@@ -186,11 +190,26 @@ void find_splits_and_absent(const DevCsf& csf, Decomp& d, const int32_t* slice_u
   d.n_split = h[0];
   d.n_absent = h[1];
   build_fixup_chunks(d, s);
-  SPTTN_CUDA(cudaFreeAsync(counts, s));
-  SPTTN_CUDA(cudaFreeAsync(present, s));
+  dfree(counts, s);
+  dfree(present, s);
 }
 
 }  // namespace
+
+void plan_trace(const char* what, cudaStream_t s) {
+  static const bool on = [] {
+    const char* e = std::getenv("SPTTN_PLAN_TRACE");
+    return e && *e && *e != '0';
+  }();
+  if (!on) return;
+  using clk = std::chrono::steady_clock;
+  static clk::time_point last = clk::now();
+  cudaStreamSynchronize(s);
+  const clk::time_point now = clk::now();
+  std::fprintf(stderr, "[plan] %-28s %8.3f ms\n", what,
+               std::chrono::duration<double, std::milli>(now - last).count());
+  last = now;
+}
 
 void build_leaf_items(const DevCsf& csf, int64_t chunk, Decomp& d, int64_t tile, cudaStream_t s) {
   const int64_t nnz = csf.level_size[csf.order - 1];
@@ -198,13 +217,13 @@ void build_leaf_items(const DevCsf& csf, int64_t chunk, Decomp& d, int64_t tile,
   d.tile = tile;
   d.n_items = (nnz + chunk - 1) / chunk;
   const CsfView t = csf.view();
-  SPTTN_CUDA(cudaMalloc(&d.item_pos, std::max<int64_t>(1, d.n_items * csf.order) * sizeof(int32_t)));
+  dmalloc(&d.item_pos, std::max<int64_t>(1, d.n_items * csf.order) * sizeof(int32_t), s);
   if (d.n_items > 0) {
     k_leaf_items<<<blocks_for(d.n_items, 256), 256, 0, s>>>(t, chunk, d.n_items, d.item_pos);
     SPTTN_CUDA(cudaGetLastError());
   }
   if (tile > 0) {  // dense root-indexed output
-    SPTTN_CUDA(cudaMalloc(&d.part, std::max<int64_t>(1, d.n_items * 2 * tile) * sizeof(double)));
+    dmalloc(&d.part, std::max<int64_t>(1, d.n_items * 2 * tile) * sizeof(double), s);
     find_splits_and_absent(csf, d, nullptr, s);
   }
 }
@@ -218,7 +237,7 @@ void build_segments(const DevCsf& csf, int unit_level, int seg_len, int64_t chun
   d.chunk = chunk;
   d.tile = tile;
   int32_t* off = nullptr;
-  SPTTN_CUDA(cudaMallocAsync(&off, (static_cast<int64_t>(nf) + 1) * sizeof(int32_t), s));
+  dmalloc(&off, (static_cast<int64_t>(nf) + 1) * sizeof(int32_t), s);
   SPTTN_CUDA(cudaMemsetAsync(off, 0, (static_cast<int64_t>(nf) + 1) * sizeof(int32_t), s));
   if (nf > 0) {
     k_seg_count<<<blocks_for(nf, 256), 256, 0, s>>>(t, unit_level, seg_len, leaf_space, off);
@@ -227,21 +246,21 @@ void build_segments(const DevCsf& csf, int unit_level, int seg_len, int64_t chun
   size_t temp_bytes = 0;
   SPTTN_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp_bytes, off, off, nf + 1, s));
   void* temp = nullptr;
-  SPTTN_CUDA(cudaMallocAsync(&temp, temp_bytes, s));
+  dmalloc(&temp, temp_bytes, s);
   SPTTN_CUDA(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, off, off, nf + 1, s));
-  SPTTN_CUDA(cudaFreeAsync(temp, s));
+  dfree(temp, s);
   int32_t nseg = 0;
   SPTTN_CUDA(cudaMemcpyAsync(&nseg, off + nf, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   SPTTN_CUDA(cudaStreamSynchronize(s));
   d.n_seg = nseg;
-  SPTTN_CUDA(cudaMalloc(&d.seg_begin, (static_cast<int64_t>(nseg) + 1) * sizeof(int32_t)));
-  SPTTN_CUDA(cudaMalloc(&d.seg_node, std::max<int64_t>(1, nseg) * sizeof(int32_t)));
-  SPTTN_CUDA(cudaMalloc(&d.slice_seg, (static_cast<int64_t>(n0) + 1) * sizeof(int32_t)));
+  dmalloc(&d.seg_begin, (static_cast<int64_t>(nseg) + 1) * sizeof(int32_t), s);
+  dmalloc(&d.seg_node, std::max<int64_t>(1, nseg) * sizeof(int32_t), s);
+  dmalloc(&d.slice_seg, (static_cast<int64_t>(n0) + 1) * sizeof(int32_t), s);
   SPTTN_CUDA(cudaMemsetAsync(d.seg_begin, 0, sizeof(int32_t), s));
   int32_t* unit_parent = nullptr;  // level-1 coordinate of each unit node (unit_level 2)
   if (unit_level == 2) {
-    SPTTN_CUDA(cudaMalloc(&d.seg_node1, std::max<int64_t>(1, nseg) * sizeof(int32_t)));
-    SPTTN_CUDA(cudaMallocAsync(&unit_parent, std::max<int32_t>(1, nf) * sizeof(int32_t), s));
+    dmalloc(&d.seg_node1, std::max<int64_t>(1, nseg) * sizeof(int32_t), s);
+    dmalloc(&unit_parent, std::max<int32_t>(1, nf) * sizeof(int32_t), s);
     const int32_t n1 = static_cast<int32_t>(csf.level_size[1]);
     if (n1 > 0)
       k_child_coord<<<blocks_for(n1, 256), 256, 0, s>>>(t.ptr[1], t.idx[1], n1, unit_parent);
@@ -252,11 +271,12 @@ void build_segments(const DevCsf& csf, int unit_level, int seg_len, int64_t chun
                                                    d.seg_node1);
     SPTTN_CUDA(cudaGetLastError());
   }
-  if (unit_parent) SPTTN_CUDA(cudaFreeAsync(unit_parent, s));
+  if (unit_parent) dfree(unit_parent, s);
   k_slice_seg<<<blocks_for(static_cast<int64_t>(n0) + 1, 256), 256, 0, s>>>(t, unit_level, off,
                                                                           d.slice_seg);
   SPTTN_CUDA(cudaGetLastError());
-  SPTTN_CUDA(cudaFreeAsync(off, s));
+  dfree(off, s);
+  plan_trace("build_segments", s);
   if (make_items) finish_unit_items(csf, d, d.slice_seg, d.n_seg, chunk, tile, s);
 }
 
@@ -266,14 +286,16 @@ void finish_unit_items(const DevCsf& csf, Decomp& d, const int32_t* slice_units,
   d.chunk = chunk;
   d.tile = tile;
   d.n_items = (n_units + chunk - 1) / chunk;
-  SPTTN_CUDA(cudaMalloc(&d.item_pos, std::max<int64_t>(1, d.n_items) * sizeof(int32_t)));
+  dmalloc(&d.item_pos, std::max<int64_t>(1, d.n_items) * sizeof(int32_t), s);
   if (d.n_items > 0) {
     k_seg_items<<<blocks_for(d.n_items, 256), 256, 0, s>>>(slice_units, n0, chunk, d.n_items,
                                                           d.item_pos);
     SPTTN_CUDA(cudaGetLastError());
   }
-  SPTTN_CUDA(cudaMalloc(&d.part, std::max<int64_t>(1, d.n_items * 2 * tile) * sizeof(double)));
+  dmalloc(&d.part, std::max<int64_t>(1, d.n_items * 2 * tile) * sizeof(double), s);
+  plan_trace("unit items", s);
   find_splits_and_absent(csf, d, slice_units, s);
+  plan_trace("splits/absent/fixup chunks", s);
 }
 
 void expand_coords(const DevCsf& csf, int level, const int32_t* coords, int32_t* out,
@@ -288,9 +310,9 @@ void expand_coords(const DevCsf& csf, int level, const int32_t* coords, int32_t*
 void build_leaf_coords(const DevCsf& csf, int32_t** leaf_i, int32_t** leaf_j, cudaStream_t s) {
   const int64_t n0 = csf.level_size[0], n1 = csf.level_size[1], nnz = csf.level_size[2];
   int32_t* fib_i = nullptr;
-  SPTTN_CUDA(cudaMalloc(leaf_i, std::max<int64_t>(1, nnz) * sizeof(int32_t)));
-  SPTTN_CUDA(cudaMalloc(leaf_j, std::max<int64_t>(1, nnz) * sizeof(int32_t)));
-  SPTTN_CUDA(cudaMallocAsync(&fib_i, std::max<int64_t>(1, n1) * sizeof(int32_t), s));
+  dmalloc(leaf_i, std::max<int64_t>(1, nnz) * sizeof(int32_t), s);
+  dmalloc(leaf_j, std::max<int64_t>(1, nnz) * sizeof(int32_t), s);
+  dmalloc(&fib_i, std::max<int64_t>(1, n1) * sizeof(int32_t), s);
   if (n0 > 0)
     k_child_coord<<<blocks_for(n0, 256), 256, 0, s>>>(csf.ptr[0], csf.idx[0],
                                                       static_cast<int32_t>(n0), fib_i);
@@ -301,7 +323,7 @@ void build_leaf_coords(const DevCsf& csf, int32_t** leaf_i, int32_t** leaf_j, cu
                                                       static_cast<int32_t>(n1), *leaf_i);
   }
   SPTTN_CUDA(cudaGetLastError());
-  SPTTN_CUDA(cudaFreeAsync(fib_i, s));
+  dfree(fib_i, s);
 }
 
 namespace {
@@ -359,14 +381,14 @@ void build_fixup_chunks(Decomp& d, cudaStream_t s) {
   sc[d.n_split] = static_cast<int32_t>(cs.size());
   d.n_chunk = static_cast<int64_t>(cs.size());
   auto up = [&](int32_t** dst, const std::vector<int32_t>& v) {
-    SPTTN_CUDA(cudaMalloc(dst, std::max<size_t>(1, v.size()) * sizeof(int32_t)));
+    dmalloc(dst, std::max<size_t>(1, v.size()) * sizeof(int32_t), s);
     SPTTN_CUDA(cudaMemcpyAsync(*dst, v.data(), v.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
   };
   up(&d.chunk_split, cs);
   up(&d.chunk_lo, clo);
   up(&d.chunk_hi, chi);
   up(&d.split_chunk, sc);
-  SPTTN_CUDA(cudaMalloc(&d.part2, std::max<int64_t>(1, d.n_chunk * d.tile) * sizeof(double)));
+  dmalloc(&d.part2, std::max<int64_t>(1, d.n_chunk * d.tile) * sizeof(double), s);
   SPTTN_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -387,28 +409,28 @@ void launch_fixup(const Decomp& d, const CsfView& t, double* out, cudaStream_t s
 }
 
 void free_decomp(Decomp& d) {
-  cudaFree(d.item_pos);
-  cudaFree(d.part);
-  cudaFree(d.split_node);
-  cudaFree(d.split_first);
-  cudaFree(d.split_last);
-  cudaFree(d.absent_rows);
-  cudaFree(d.seg_begin);
-  cudaFree(d.seg_node);
-  cudaFree(d.seg_node1);
-  cudaFree(d.chunk_split);
-  cudaFree(d.chunk_lo);
-  cudaFree(d.chunk_hi);
-  cudaFree(d.split_chunk);
-  cudaFree(d.part2);
-  cudaFree(d.grp_hdr);
-  cudaFree(d.grp_node);
-  cudaFree(d.grp_node1);
-  cudaFree(d.pk);
-  cudaFree(d.pk2);
-  cudaFree(d.pv);
-  cudaFree(d.slice_grp);
-  cudaFree(d.slice_seg);
+  dfree(d.item_pos);
+  dfree(d.part);
+  dfree(d.split_node);
+  dfree(d.split_first);
+  dfree(d.split_last);
+  dfree(d.absent_rows);
+  dfree(d.seg_begin);
+  dfree(d.seg_node);
+  dfree(d.seg_node1);
+  dfree(d.chunk_split);
+  dfree(d.chunk_lo);
+  dfree(d.chunk_hi);
+  dfree(d.split_chunk);
+  dfree(d.part2);
+  dfree(d.grp_hdr);
+  dfree(d.grp_node);
+  dfree(d.grp_node1);
+  dfree(d.pk);
+  dfree(d.pk2);
+  dfree(d.pv);
+  dfree(d.slice_grp);
+  dfree(d.slice_seg);
   d = Decomp{};
 }
 

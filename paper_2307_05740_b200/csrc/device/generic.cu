@@ -398,13 +398,13 @@ void generic_free(GenericState& g) {
     g = GenericState{};
     return;
   }
-  cudaFree(g.d_prog);
-  cudaFree(g.buffers);
-  cudaFree(g.buffer_off);
-  cudaFree(g.counters);
-  cudaFree(g.log);
-  cudaFree(g.leaf_keys);
-  cudaFree(g.leaf_pos);
+  dfree(g.d_prog);
+  dfree(g.buffers);
+  dfree(g.buffer_off);
+  dfree(g.counters);
+  dfree(g.log);
+  dfree(g.leaf_keys);
+  dfree(g.leaf_pos);
   g = GenericState{};
 }
 

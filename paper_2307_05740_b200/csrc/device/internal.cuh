@@ -94,6 +94,16 @@ struct Decomp {
   int32_t* slice_seg = nullptr;    // [n0+1]   segment offset of each slice
 };
 
+// ---- device memory (mem.cu): one stream-ordered pool per device ---------
+void dmalloc_raw(void** p, size_t bytes, cudaStream_t s);
+template <class T>
+inline void dmalloc(T** p, size_t bytes, cudaStream_t s) {
+  dmalloc_raw(reinterpret_cast<void**>(p), bytes, s);
+}
+// Frees in stream order on `s`; owners free with s = 0 after synchronising.
+void dfree(void* p, cudaStream_t s = 0);
+void release_cached();
+
 // ---- kernel launchers (nest_*.cu) --------------------------------------
 struct RootOutArgs {
   CsfView t;
@@ -166,6 +176,9 @@ constexpr int kFixChunk = 32;
 void build_fixup_chunks(Decomp& d, cudaStream_t s);
 void launch_fixup(const Decomp& d, const CsfView& t, double* out, cudaStream_t s);
 void free_decomp(Decomp& d);
+// Plan-build tracing (env SPTTN_PLAN_TRACE=1): synchronises `s` and prints the
+// milliseconds since the previous mark to stderr. Development aid only.
+void plan_trace(const char* what, cudaStream_t s);
 
 // ---- generic interpreter (generic.cu) -------------------------------------
 struct GenericState {

@@ -119,18 +119,18 @@ void scan_incl(int32_t* in, int32_t* out, int32_t n, Op op, cudaStream_t s) {
   size_t bytes = 0;
   void* tmp = nullptr;
   SPTTN_CUDA(cub::DeviceScan::InclusiveScan(nullptr, bytes, in, out, op, n, s));
-  SPTTN_CUDA(cudaMallocAsync(&tmp, bytes, s));
+  dmalloc(&tmp, bytes, s);
   SPTTN_CUDA(cub::DeviceScan::InclusiveScan(tmp, bytes, in, out, op, n, s));
-  SPTTN_CUDA(cudaFreeAsync(tmp, s));
+  dfree(tmp, s);
 }
 
 void scan_excl_sum(int32_t* in, int32_t* out, int32_t n, cudaStream_t s) {
   size_t bytes = 0;
   void* tmp = nullptr;
   SPTTN_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, s));
-  SPTTN_CUDA(cudaMallocAsync(&tmp, bytes, s));
+  dmalloc(&tmp, bytes, s);
   SPTTN_CUDA(cub::DeviceScan::ExclusiveSum(tmp, bytes, in, out, n, s));
-  SPTTN_CUDA(cudaFreeAsync(tmp, s));
+  dfree(tmp, s);
 }
 
 struct MaxOp {
@@ -141,22 +141,23 @@ struct MaxOp {
 
 void build_packed(const DevCsf& csf, int leaf_level, Decomp& d, cudaStream_t s, int slots,
                   const int32_t* leaf_coord2) {
+  plan_trace("pack: enter", s);
   const int32_t nseg = static_cast<int32_t>(d.n_seg);
   const int32_t n0 = static_cast<int32_t>(csf.level_size[0]);
   d.pack_slots = slots;
   if (nseg == 0) {
     d.n_groups = 0;
-    SPTTN_CUDA(cudaMalloc(&d.slice_grp, (static_cast<int64_t>(n0) + 1) * sizeof(int32_t)));
+    dmalloc(&d.slice_grp, (static_cast<int64_t>(n0) + 1) * sizeof(int32_t), s);
     SPTTN_CUDA(cudaMemsetAsync(d.slice_grp, 0, (static_cast<int64_t>(n0) + 1) * sizeof(int32_t), s));
     return;
   }
   uint64_t *keys = nullptr, *keys2 = nullptr;
   int32_t *ids = nullptr, *ids2 = nullptr, *head = nullptr, *runstart = nullptr,
           *end_at_start = nullptr, *runend = nullptr, *flag = nullptr, *gid = nullptr;
-  SPTTN_CUDA(cudaMallocAsync(&keys, nseg * sizeof(uint64_t), s));
-  SPTTN_CUDA(cudaMallocAsync(&keys2, nseg * sizeof(uint64_t), s));
-  SPTTN_CUDA(cudaMallocAsync(&ids, nseg * sizeof(int32_t), s));
-  SPTTN_CUDA(cudaMallocAsync(&ids2, nseg * sizeof(int32_t), s));
+  dmalloc(&keys, nseg * sizeof(uint64_t), s);
+  dmalloc(&keys2, nseg * sizeof(uint64_t), s);
+  dmalloc(&ids, nseg * sizeof(int32_t), s);
+  dmalloc(&ids2, nseg * sizeof(int32_t), s);
   k_seg_keys<<<nblk(nseg, 256), 256, 0, s>>>(d.seg_begin, d.slice_seg, n0, nseg, keys, ids);
   SPTTN_CUDA(cudaGetLastError());
   int key_bits = 3;
@@ -165,16 +166,16 @@ void build_packed(const DevCsf& csf, int leaf_level, Decomp& d, cudaStream_t s, 
   SPTTN_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys, keys2, ids, ids2, nseg, 0,
                                              key_bits, s));
   void* tmp = nullptr;
-  SPTTN_CUDA(cudaMallocAsync(&tmp, bytes, s));
+  dmalloc(&tmp, bytes, s);
   SPTTN_CUDA(cub::DeviceRadixSort::SortPairs(tmp, bytes, keys, keys2, ids, ids2, nseg, 0, key_bits,
                                              s));
-  SPTTN_CUDA(cudaFreeAsync(tmp, s));
-  SPTTN_CUDA(cudaMallocAsync(&head, nseg * sizeof(int32_t), s));
-  SPTTN_CUDA(cudaMallocAsync(&runstart, nseg * sizeof(int32_t), s));
-  SPTTN_CUDA(cudaMallocAsync(&end_at_start, nseg * sizeof(int32_t), s));
-  SPTTN_CUDA(cudaMallocAsync(&runend, nseg * sizeof(int32_t), s));
-  SPTTN_CUDA(cudaMallocAsync(&flag, nseg * sizeof(int32_t), s));
-  SPTTN_CUDA(cudaMallocAsync(&gid, nseg * sizeof(int32_t), s));
+  dfree(tmp, s);
+  dmalloc(&head, nseg * sizeof(int32_t), s);
+  dmalloc(&runstart, nseg * sizeof(int32_t), s);
+  dmalloc(&end_at_start, nseg * sizeof(int32_t), s);
+  dmalloc(&runend, nseg * sizeof(int32_t), s);
+  dmalloc(&flag, nseg * sizeof(int32_t), s);
+  dmalloc(&gid, nseg * sizeof(int32_t), s);
   k_run_heads<<<nblk(nseg, 256), 256, 0, s>>>(keys2, nseg, head);
   scan_incl(head, runstart, nseg, MaxOp{}, s);
   k_run_ends<<<nblk(nseg, 256), 256, 0, s>>>(keys2, runstart, nseg, end_at_start);
@@ -182,14 +183,15 @@ void build_packed(const DevCsf& csf, int leaf_level, Decomp& d, cudaStream_t s, 
   k_group_flags<<<nblk(nseg, 256), 256, 0, s>>>(runstart, nseg, slots, flag);
   scan_incl(flag, gid, nseg, cub::Sum{}, s);
   int32_t ngroups = 0;
+  plan_trace("pack: sort + group ids", s);
   SPTTN_CUDA(cudaMemcpyAsync(&ngroups, gid + nseg - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   SPTTN_CUDA(cudaStreamSynchronize(s));
   d.n_groups = ngroups;
   int32_t* gleaves = nullptr;
   int32_t* leaf_off = nullptr;
-  SPTTN_CUDA(cudaMalloc(&d.grp_hdr, static_cast<int64_t>(ngroups) * sizeof(int4)));
-  SPTTN_CUDA(cudaMallocAsync(&gleaves, (static_cast<int64_t>(ngroups) + 1) * sizeof(int32_t), s));
-  SPTTN_CUDA(cudaMallocAsync(&leaf_off, (static_cast<int64_t>(ngroups) + 1) * sizeof(int32_t), s));
+  dmalloc(&d.grp_hdr, static_cast<int64_t>(ngroups) * sizeof(int4), s);
+  dmalloc(&gleaves, (static_cast<int64_t>(ngroups) + 1) * sizeof(int32_t), s);
+  dmalloc(&leaf_off, (static_cast<int64_t>(ngroups) + 1) * sizeof(int32_t), s);
   SPTTN_CUDA(cudaMemsetAsync(gleaves, 0, (static_cast<int64_t>(ngroups) + 1) * sizeof(int32_t), s));
   k_group_headers<<<nblk(nseg, 256), 256, 0, s>>>(keys2, runstart, gid, runend, nseg, slots,
                                                   d.grp_hdr, gleaves);
@@ -199,21 +201,21 @@ void build_packed(const DevCsf& csf, int leaf_level, Decomp& d, cudaStream_t s, 
   SPTTN_CUDA(cudaStreamSynchronize(s));
   d.n_packed_leaves = nleaves;
   const int64_t nslots = static_cast<int64_t>(ngroups) * slots;
-  SPTTN_CUDA(cudaMalloc(&d.grp_node, nslots * sizeof(int32_t)));
+  dmalloc(&d.grp_node, nslots * sizeof(int32_t), s);
   SPTTN_CUDA(cudaMemsetAsync(d.grp_node, 0, nslots * sizeof(int32_t), s));
   if (d.seg_node1) {
-    SPTTN_CUDA(cudaMalloc(&d.grp_node1, nslots * sizeof(int32_t)));
+    dmalloc(&d.grp_node1, nslots * sizeof(int32_t), s);
     SPTTN_CUDA(cudaMemsetAsync(d.grp_node1, 0, nslots * sizeof(int32_t), s));
   }
   // separate coordinate / value streams measured faster than 16-byte
   // {coord, coord2, value} records for TTMc-4 (750 vs 810 us)
   const int64_t nl = std::max<int64_t>(1, nleaves);
-  SPTTN_CUDA(cudaMalloc(&d.pk, nl * sizeof(int32_t)));
-  SPTTN_CUDA(cudaMalloc(&d.pv, nl * sizeof(double)));
+  dmalloc(&d.pk, nl * sizeof(int32_t), s);
+  dmalloc(&d.pv, nl * sizeof(double), s);
   SPTTN_CUDA(cudaMemsetAsync(d.pk, 0, nl * sizeof(int32_t), s));
   SPTTN_CUDA(cudaMemsetAsync(d.pv, 0, nl * sizeof(double), s));
   if (leaf_coord2) {
-    SPTTN_CUDA(cudaMalloc(&d.pk2, nl * sizeof(int32_t)));
+    dmalloc(&d.pk2, nl * sizeof(int32_t), s);
     SPTTN_CUDA(cudaMemsetAsync(d.pk2, 0, nl * sizeof(int32_t), s));
   }
   const CsfView t = csf.view();
@@ -221,7 +223,7 @@ void build_packed(const DevCsf& csf, int leaf_level, Decomp& d, cudaStream_t s, 
                                                 d.seg_node, d.seg_node1, t.idx[leaf_level],
                                                 leaf_coord2, t.vals, nseg, slots, d.grp_hdr,
                                                 d.grp_node, d.grp_node1, d.pk, d.pk2, d.pv);
-  SPTTN_CUDA(cudaMalloc(&d.slice_grp, (static_cast<int64_t>(n0) + 1) * sizeof(int32_t)));
+  dmalloc(&d.slice_grp, (static_cast<int64_t>(n0) + 1) * sizeof(int32_t), s);
   k_slice_groups<<<nblk(static_cast<int64_t>(ngroups) + 1, 256), 256, 0, s>>>(d.grp_hdr, ngroups,
                                                                             n0, d.slice_grp);
   SPTTN_CUDA(cudaGetLastError());
@@ -230,7 +232,7 @@ void build_packed(const DevCsf& csf, int leaf_level, Decomp& d, cudaStream_t s, 
                   static_cast<void*>(runstart), static_cast<void*>(end_at_start),
                   static_cast<void*>(runend), static_cast<void*>(flag), static_cast<void*>(gid),
                   static_cast<void*>(gleaves), static_cast<void*>(leaf_off)})
-    SPTTN_CUDA(cudaFreeAsync(p, s));
+    dfree(p, s);
   SPTTN_CUDA(cudaStreamSynchronize(s));
 }
 

@@ -68,6 +68,11 @@ def device_info() -> dict:
     return {"sm_count": out[0], "cc": out[1], "l2_bytes": out[2], "smem_optin": out[3]}
 
 
+def release_cached() -> None:
+    """spttn_release_cached: return the engine pool's unused device pages."""
+    _check(N.engine().spttn_release_cached())
+
+
 class DeviceCsf:
     """spttn_csf_create: copies a host Csf and builds the int32 device layout."""
 
