@@ -452,9 +452,9 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
         int seg_len = static_cast<int>(
             env_int("SPTTN_SEG_LEN", p->kind == SPTTN_NEST_TTMC3 ? 4 : 8));
         if (p->kind == SPTTN_NEST_TTMC3) {
-          // 4 = stream-staged kernel (default); 3 = pipelined direct loads;
-          // 0-2 = earlier variants kept for A/B measurements (tools/sweep.py)
-          p->mode = static_cast<int>(env_int("SPTTN_TTMC3_MODE", 4));
+          // 10 = packed, TMA-staged, row-contiguous gathers (default);
+          // 0-7 = earlier variants kept for A/B measurements (tools/sweep.py)
+          p->mode = static_cast<int>(env_int("SPTTN_TTMC3_MODE", 10));
           seg_len = std::clamp(seg_len, 1, p->mode == 0 ? 8 : 4);
         }
         seg_len = std::max(seg_len, 1);
@@ -479,7 +479,7 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
           if (gchunk <= 0)
             gchunk = std::clamp<int64_t>((p->dec.n_groups + w16 - 1) / w16, 4, 1024);
           spttn_dev::finish_unit_items(D, p->dec, p->dec.slice_grp, p->dec.n_groups, gchunk, tile, s);
-        } else if (p->kind == SPTTN_NEST_TTMC3 && (p->mode == 6 || p->mode == 7)) {
+        } else if (p->kind == SPTTN_NEST_TTMC3 && (p->mode == 6 || p->mode == 7 || p->mode == 10)) {
           // packed length-sorted groups of 8 segments (pack.cu)
           spttn_dev::build_segments(D, 1, seg_len, chunk, p->dec, tile, s, false);
           spttn_dev::build_packed(D, 2, p->dec, s);

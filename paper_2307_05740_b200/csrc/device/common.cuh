@@ -78,6 +78,44 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// TMA bulk copies (cp.async.bulk, SASS UBLKCP) completing on an mbarrier:
+// one elected lane stages a whole contiguous stream window into shared
+// memory with one instruction per array instead of one LDGSTS per lane and
+// element (the per-element form costs ~1 L1 data-pipe wavefront per thread).
+__device__ __forceinline__ void mbar_init(uint64_t* m, int count) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(m));
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* m, unsigned bytes) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(m));
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes)
+               : "memory");
+}
+// bytes and both addresses must be multiples of 16
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* m) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(m));
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
+      "l"(src), "r"(bytes), "r"(b)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* m, unsigned parity) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(m));
+  asm volatile(
+      "{\n .reg .pred p;\n W%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W%=;\n}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+// order this thread's earlier generic-proxy shared-memory accesses before
+// later async-proxy (bulk copy) writes to the same buffer
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 __device__ __forceinline__ int ldg_i32(const int32_t* p) { return __ldg(p); }
 __device__ __forceinline__ double ldg_f64(const double* p) { return __ldg(p); }
 

@@ -1021,6 +1021,211 @@ __global__ void __launch_bounds__(kBlock, 3) k_ttmc3ps(RootOutArgs a) {
   if (pending) flush(head ? 0 : 1);
 }
 
+// TMA-staged stream window: group headers, slot coordinates, interleaved leaf
+// coordinates and values — all contiguous and 32-byte aligned in the packed
+// layout — staged by lane 0 with one bulk copy per array, completing on a
+// per-stage mbarrier (instead of one LDGSTS per lane and element).
+struct StageT {
+  alignas(16) int4 hdr[3][kGW];
+  alignas(16) int32_t node[3][kGW * kPackSlots];
+  alignas(16) int32_t kk[2][kGWLeaves];
+  alignas(16) double tv[2][kGWLeaves];
+  uint64_t mbar_meta[3];
+  uint64_t mbar_leaf[2];
+};
+
+// Packed + TMA-staged + row-contiguous gathers (TTMc-3 default).
+//
+// The m8n8k4 fragment puts the contracted (segment) index at lane%4, so a
+// gather made directly in fragment layout has 4 consecutive lanes reading 4
+// different factor rows. ncu: such a 256-bit gather costs ~32 L1 data-pipe
+// wavefronts (one per 32-byte piece) instead of 8 (one per 128-byte row) —
+// every earlier variant sat at ~78 % of the data-pipe peak with 4x inflated
+// gather wavefronts. Here lane L gathers row slot = L/4, columns 4(L%4)..+3
+// (4 consecutive lanes per row), computes its X quad, and the X and U quads of
+// the group are transposed into fragment layout through a per-warp shared
+// tile: 16 B-aligned stores, column swizzle col ^ 4*(slot%4) ^ 2*(slot%2) so
+// both the 64-bit fragment reads and the 128-bit quad stores are
+// conflict-free. Tiles are double-buffered by
+// group parity, so one __syncwarp per group orders stores before loads.
+struct StageQ {
+  alignas(16) double xs[2][kPackSlots * 16];
+  alignas(16) double us[2][kPackSlots * 16];
+};
+
+constexpr size_t kPqSmem = (sizeof(StageT) + sizeof(StageQ)) * (kBlock / 32);
+
+template <bool VECU, bool VECV>
+__global__ void __launch_bounds__(kBlock, 3) k_ttmc3pq(RootOutArgs a) {
+  extern __shared__ __align__(16) unsigned char pq_smem[];  // kPqSmem bytes
+  StageT* stage = reinterpret_cast<StageT*>(pq_smem);
+  StageQ* tiles = reinterpret_cast<StageQ*>(pq_smem + sizeof(StageT) * (kBlock / 32));
+  const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
+  if (w >= a.n_items) return;  // warp-uniform
+  StageT& S = stage[threadIdx.x / 32];
+  StageQ& Q = tiles[threadIdx.x / 32];
+  const int lane = threadIdx.x & 31;
+  // gather role: row slot gs, column quad gc
+  const int gs = lane >> 2, gc = lane & 3;
+  // fragment role: K index fq (segment within a 4-chunk), M/N index fh
+  const int fq = lane & 3, fh = lane >> 2;
+  const int R = a.R, S_ = a.S;
+  const CsfView& t = a.t;
+  const double* __restrict__ U = a.f[1];
+  const double* __restrict__ V = a.f[2];
+  const int32_t* __restrict__ slice_grp = a.slice_grp;
+
+  const int32_t cbeg = static_cast<int32_t>(w * a.chunk);
+  const int32_t cend = static_cast<int32_t>(min64(cbeg + a.chunk, a.n_groups));
+  int32_t sl = a.item_pos[w];
+  int32_t sl_end = slice_grp[sl + 1];
+  bool head = slice_grp[sl] < cbeg;
+  int32_t row = t.idx[0][sl];
+  int32_t nx_end = sl + 2 <= t.nlev[0] ? __ldg(slice_grp + sl + 2) : 0;
+  int32_t nx_row = sl + 1 < t.nlev[0] ? __ldg(t.idx[0] + sl + 1) : 0;
+  bool pending = false;
+  double acc[8];  // tile (mt, nt) element e at acc[(mt*2+nt)*2+e]
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.0;
+
+  auto flush = [&](int dslot) {
+    double* dst = dslot < 0 ? a.out + static_cast<int64_t>(row) * R * S_
+                            : a.part + (w * 2 + dslot) * static_cast<int64_t>(R) * S_;
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = 8 * mt + fh;
+          const int s = 8 * nt + 2 * fq + e;
+          if (r < R && s < S_) dst[r * S_ + s] = acc[(mt * 2 + nt) * 2 + e];
+        }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = 0.0;
+  };
+  auto issue_meta = [&](int32_t wi) {
+    const int32_t g0 = cbeg + wi * kGW;
+    const int32_t nw = min(g0 + kGW, cend) - g0;
+    const int b = wi % 3;
+    const unsigned hb = nw * sizeof(int4), nb = nw * kPackSlots * sizeof(int32_t);
+    fence_proxy_async();
+    mbar_expect_tx(&S.mbar_meta[b], hb + nb);
+    bulk_g2s(&S.hdr[b][0], a.grp_hdr + g0, hb, &S.mbar_meta[b]);
+    bulk_g2s(&S.node[b][0], a.grp_node + static_cast<int64_t>(g0) * kPackSlots, nb, &S.mbar_meta[b]);
+  };
+  auto issue_leaves = [&](int32_t wi) {
+    const int32_t g0 = cbeg + wi * kGW;
+    const int32_t nw = min(g0 + kGW, cend) - g0;
+    const int b = wi % 3, lb = wi & 1;
+    mbar_wait(&S.mbar_meta[b], (wi / 3) & 1);
+    const int32_t L0 = S.hdr[b][0].x;
+    const int32_t L1 = S.hdr[b][nw - 1].x + kPackSlots * S.hdr[b][nw - 1].y;
+    const unsigned n = static_cast<unsigned>(L1 - L0);
+    fence_proxy_async();
+    mbar_expect_tx(&S.mbar_leaf[lb], n * 12u);
+    bulk_g2s(&S.kk[lb][0], a.pk + L0, n * 4u, &S.mbar_leaf[lb]);
+    bulk_g2s(&S.tv[lb][0], a.pv + L0, n * 8u, &S.mbar_leaf[lb]);
+  };
+
+  // swizzled tile: element (slot, col) at slot*16 + (col ^ 4*(slot&3) ^ 2*(slot&1))
+  const int st_off = gs * 16 + ((4 * gc) ^ (4 * (gs & 3)));
+  const int o_lo = st_off + 2 * (gs & 1), o_hi = st_off + 2 - 2 * (gs & 1);
+  int par = 0;
+
+  const int32_t nwin = (cend - cbeg + kGW - 1) / kGW;
+  if (lane == 0) {
+    for (int b = 0; b < 3; ++b) mbar_init(&S.mbar_meta[b], 1);
+    for (int b = 0; b < 2; ++b) mbar_init(&S.mbar_leaf[b], 1);
+    mbar_init_fence();
+    issue_meta(0);
+    if (nwin > 1) issue_meta(1);
+    issue_leaves(0);
+  }
+  __syncwarp();
+  for (int32_t win = 0; win < nwin; ++win) {
+    const int mb = win % 3, lbf = win & 1;
+    if (lane == 0) {
+      if (win + 1 < nwin) issue_leaves(win + 1);
+      if (win + 2 < nwin) issue_meta(win + 2);
+    }
+    mbar_wait(&S.mbar_meta[mb], (win / 3) & 1);
+    mbar_wait(&S.mbar_leaf[lbf], (win / 2) & 1);
+    const int32_t g0 = cbeg + win * kGW;
+    const int32_t ge = min(g0 + kGW, cend);
+    const int32_t L0 = S.hdr[mb][0].x;
+    for (int32_t g = g0; g < ge; ++g) {
+      const int4 hh = S.hdr[mb][g - g0];
+      const int n = hh.y;  // warp-uniform
+      const int32_t lbase = hh.x - L0 + gs;
+      const int32_t j = S.node[mb][(g - g0) * kPackSlots + gs];
+      int32_t kk[4];
+      double tt[4];
+#pragma unroll
+      for (int it = 0; it < 4; ++it) {
+        kk[it] = it < n ? S.kk[lbf][lbase + it * kPackSlots] : 0;
+        tt[it] = it < n ? S.tv[lbf][lbase + it * kPackSlots] : 0.0;
+      }
+      const double4 ur = row4<VECU>(U + static_cast<int64_t>(j) * R, 4 * gc, R);
+      double4 vr[4];
+#pragma unroll
+      for (int it = 0; it < 4; ++it) {
+        if (VECV) {
+          vr[it] = ld256_if(V + static_cast<int64_t>(kk[it]) * S_ + 4 * gc, it < n && 4 * gc < S_);
+        } else {
+          vr[it] = it < n ? row4<false>(V + static_cast<int64_t>(kk[it]) * S_, 4 * gc, S_)
+                          : make_double4(0, 0, 0, 0);
+        }
+      }
+      double4 x = make_double4(0, 0, 0, 0);
+#pragma unroll
+      for (int it = 0; it < 4; ++it) fma4(x, tt[it], vr[it]);  // X[s] += t * V[k,s]
+      // transpose X and U quads into fragment layout through the tile
+      double* xs = Q.xs[par];
+      double* us = Q.us[par];
+      *reinterpret_cast<double2*>(xs + o_lo) = make_double2(x.x, x.y);
+      *reinterpret_cast<double2*>(us + o_lo) = make_double2(ur.x, ur.y);
+      *reinterpret_cast<double2*>(xs + o_hi) = make_double2(x.z, x.w);
+      *reinterpret_cast<double2*>(us + o_hi) = make_double2(ur.z, ur.w);
+      __syncwarp();
+      double af[2][2], bf[2][2];  // [K chunk][m / n tile]
+#pragma unroll
+      for (int kc = 0; kc < 2; ++kc) {
+        const int seg = 4 * kc + fq;
+        const int sw = 4 * (seg & 3) ^ 2 * (seg & 1);
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          af[kc][mt] = us[seg * 16 + ((8 * mt + fh) ^ sw)];
+          bf[kc][mt] = xs[seg * 16 + ((8 * mt + fh) ^ sw)];
+        }
+      }
+#pragma unroll
+      for (int kc = 0; kc < 2; ++kc)
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt)
+            dmma_8x8x4(acc[(mt * 2 + nt) * 2], acc[(mt * 2 + nt) * 2 + 1], af[kc][mt], bf[kc][nt]);
+      par ^= 1;
+      pending = true;
+      if (g + 1 == sl_end) {
+        flush(head ? 0 : -1);
+        pending = false;
+        head = false;
+        if (g + 1 < cend) {
+          ++sl;
+          sl_end = nx_end;
+          row = nx_row;
+          nx_end = sl + 2 <= t.nlev[0] ? __ldg(slice_grp + sl + 2) : 0;
+          nx_row = sl + 1 < t.nlev[0] ? __ldg(t.idx[0] + sl + 1) : 0;
+        }
+      }
+    }
+    __syncwarp();  // stage buffers of this window are free after this point
+  }
+  if (pending) flush(head ? 0 : 1);
+}
+
 // TTMc-4, packed form (default). Units are (i,j) fiber pieces of <= 4 LEAVES
 // (the (i,j,k) level holds ~1 leaf at the BASELINE shape, so X[t] = v*W[l,t]
 // per leaf and Y[s,t] += V[k,s] * X[t] regroups the reference's per-(i,j,k)
@@ -1263,6 +1468,24 @@ void launch_ttmc3(const RootOutArgs& a, cudaStream_t s) {
   if (blocks == 0) return;
   const bool vu = a.vec & 1, vv = a.vec & 2;
   const int mode = a.flags >> 8;  // kernel variant chosen at plan time
+  if (mode == 10) {
+    const bool wu = a.vec & 4, wv = a.vec & 8;
+    auto go = [&](auto kern) {
+      SPTTN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(kPqSmem)));
+      kern<<<static_cast<unsigned>(blocks), kBlock, kPqSmem, s>>>(a);
+    };
+    if (wu && wv)
+      go(k_ttmc3pq<true, true>);
+    else if (wu)
+      go(k_ttmc3pq<true, false>);
+    else if (wv)
+      go(k_ttmc3pq<false, true>);
+    else
+      go(k_ttmc3pq<false, false>);
+    SPTTN_CUDA(cudaGetLastError());
+    return;
+  }
   if (mode == 7) {
     const bool wu = a.vec & 4, wv = a.vec & 8;
     if (wu && wv)
