@@ -445,6 +445,8 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
         const bool vv = p->kind == SPTTN_NEST_TTMC3 ? (S % 2 == 0 && facs_aligned16)
                                                     : (S == 8 && facs_aligned32);
         p->vec = (vu ? 1 : 0) | (vv ? 2 : 0);
+        if (p->kind == SPTTN_NEST_TTMC4)  // 128-bit W row pieces
+          p->vec |= (p->T % 2 == 0) && facs_aligned16 ? 4 : 0;
         if (p->kind == SPTTN_NEST_TTMC3)  // 256-bit row gathers (wide kernel)
           p->vec |= ((R % 4 == 0) && facs_aligned32 ? 4 : 0) | ((S % 4 == 0) && facs_aligned32 ? 8 : 0);
         // TTMc-3 stages a group's <= 4 segments of leaves in one warp-wide
@@ -463,8 +465,9 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
         int64_t chunk = env_int("SPTTN_CHUNK", 0);
         if (chunk <= 0) chunk = std::clamp<int64_t>((units + warps - 1) / warps, 8, 1024);
         if (p->kind == SPTTN_NEST_TTMC4)
-          p->mode = static_cast<int>(env_int("SPTTN_TTMC4_MODE", 1));  // 1 = packed (default)
-        if (p->kind == SPTTN_NEST_TTMC4 && p->mode == 1) {
+          // 2 = packed, TMA-staged, row-contiguous gathers (default); 1 = packed
+          p->mode = static_cast<int>(env_int("SPTTN_TTMC4_MODE", 2));
+        if (p->kind == SPTTN_NEST_TTMC4 && (p->mode == 1 || p->mode == 2)) {
           // (i,j) pieces of <= 4 leaves, length-sorted groups of 8, with each
           // leaf's level-2 (k) coordinate packed next to its level-3 (l) one
           spttn_dev::build_segments(D, 1, std::clamp(seg_len, 1, 4), chunk, p->dec, tile, s,

@@ -160,6 +160,17 @@ __device__ __forceinline__ double2 row2(const double* row, int c, int R) {
   }
 }
 
+// Two consecutive columns c, c+1 of a row of length n (zero beyond n). VEC
+// requires n even and a 16-byte aligned base.
+template <bool VEC>
+__device__ __forceinline__ double2 pair2(const double* row, int c, int n) {
+  if (VEC) return c < n ? ld128(row + c) : make_double2(0, 0);
+  double2 v;
+  v.x = c < n ? __ldg(row + c) : 0.0;
+  v.y = c + 1 < n ? __ldg(row + c + 1) : 0.0;
+  return v;
+}
+
 __device__ __forceinline__ void fma4(double4& acc, double s, const double4& v) {
   acc.x = fma(s, v.x, acc.x);
   acc.y = fma(s, v.y, acc.y);

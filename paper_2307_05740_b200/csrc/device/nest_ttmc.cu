@@ -1342,6 +1342,183 @@ __global__ void __launch_bounds__(kBlock, 2) k_ttmc4pk(RootOutArgs a) {
   if (pending) flush(head ? 0 : 1);
 }
 
+// TTMc-4 packed + TMA-staged (default): k_ttmc4pk's fragment mapping and
+// math, with (1) each window of kGW groups (headers, slot coordinates and the
+// three interleaved leaf streams l, k, value) staged into shared memory by
+// lane 0 with bulk copies two (meta) / one (leaves) windows ahead, and (2) the
+// V and W rows of an iteration's 8 leaves gathered row-contiguously (4 lanes
+// per 64-byte row, one 128-bit load each) into small per-warp row tiles, from
+// which each lane reads its segment's V row (broadcast) and W[l, t=h].
+// ncu on k_ttmc4pk: the fragment-order gathers (8 lanes broadcast-reading one
+// row with 256-bit loads, W[l_q, h] with 64-bit loads) cost ~110 L1
+// data-pipe wavefronts per 8-leaf iteration and bound the kernel at 84 %.
+struct StageT4 {
+  alignas(16) double vs[kPackSlots][10];  // this iteration's V rows (padded)
+  alignas(16) double ws[kPackSlots][10];  // this iteration's W rows
+  alignas(16) int4 hdr[3][kGW];
+  alignas(16) int32_t node[3][kGW * kPackSlots];
+  alignas(16) int32_t ll[2][kGWLeaves];
+  alignas(16) int32_t kk[2][kGWLeaves];
+  alignas(16) double tv[2][kGWLeaves];
+  uint64_t mbar_meta[3];
+  uint64_t mbar_leaf[2];
+};
+
+template <bool VECV, bool VECW>
+__global__ void __launch_bounds__(kBlock, 2) k_ttmc4pq(RootOutArgs a) {
+  __shared__ StageT4 stage[kBlock / 32];
+  const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
+  if (w >= a.n_items) return;  // warp-uniform
+  StageT4& S = stage[threadIdx.x / 32];
+  const int lane = threadIdx.x & 31;
+  const int q = lane & 3;   // fragment role: segment (K) index
+  const int h = lane >> 2;  //   and r / t index
+  const int gs = lane >> 2, gc = lane & 3;  // gather role: row slot, column pair
+  const int R = a.R, S_ = a.S, T = a.T;
+  const CsfView& t = a.t;
+  const double* __restrict__ U = a.f[1];
+  const double* __restrict__ V = a.f[2];
+  const double* __restrict__ W = a.f[3];
+  const int32_t* __restrict__ slice_grp = a.slice_grp;
+  const int64_t tile = static_cast<int64_t>(R) * S_ * T;
+
+  const int32_t cbeg = static_cast<int32_t>(w * a.chunk);
+  const int32_t cend = static_cast<int32_t>(min64(cbeg + a.chunk, a.n_groups));
+  int32_t sl = a.item_pos[w];
+  int32_t sl_end = slice_grp[sl + 1];
+  bool head = slice_grp[sl] < cbeg;
+  int32_t row = t.idx[0][sl];
+  int32_t nx_end = sl + 2 <= t.nlev[0] ? __ldg(slice_grp + sl + 2) : 0;
+  int32_t nx_row = sl + 1 < t.nlev[0] ? __ldg(t.idx[0] + sl + 1) : 0;
+  bool pending = false;
+  double acc[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) acc[e] = 0.0;
+
+  auto flush = [&](int dslot) {
+    double* dst = dslot < 0 ? a.out + static_cast<int64_t>(row) * tile
+                            : a.part + (w * 2 + dslot) * tile;
+#pragma unroll
+    for (int s = 0; s < 8; ++s)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int tt = 2 * q + e;
+        if (h < R && s < S_ && tt < T) dst[(h * S_ + s) * T + tt] = acc[2 * s + e];
+      }
+#pragma unroll
+    for (int e = 0; e < 16; ++e) acc[e] = 0.0;
+  };
+  auto issue_meta = [&](int32_t wi) {
+    const int32_t g0 = cbeg + wi * kGW;
+    const int32_t nw = min(g0 + kGW, cend) - g0;
+    const int b = wi % 3;
+    const unsigned hb = nw * sizeof(int4), nb = nw * kPackSlots * sizeof(int32_t);
+    fence_proxy_async();
+    mbar_expect_tx(&S.mbar_meta[b], hb + nb);
+    bulk_g2s(&S.hdr[b][0], a.grp_hdr + g0, hb, &S.mbar_meta[b]);
+    bulk_g2s(&S.node[b][0], a.grp_node + static_cast<int64_t>(g0) * kPackSlots, nb, &S.mbar_meta[b]);
+  };
+  auto issue_leaves = [&](int32_t wi) {
+    const int32_t g0 = cbeg + wi * kGW;
+    const int32_t nw = min(g0 + kGW, cend) - g0;
+    const int b = wi % 3, lb = wi & 1;
+    mbar_wait(&S.mbar_meta[b], (wi / 3) & 1);
+    const int32_t L0 = S.hdr[b][0].x;
+    const int32_t L1 = S.hdr[b][nw - 1].x + kPackSlots * S.hdr[b][nw - 1].y;
+    const unsigned n = static_cast<unsigned>(L1 - L0);
+    fence_proxy_async();
+    mbar_expect_tx(&S.mbar_leaf[lb], n * 16u);
+    bulk_g2s(&S.ll[lb][0], a.pk + L0, n * 4u, &S.mbar_leaf[lb]);
+    bulk_g2s(&S.kk[lb][0], a.pk2 + L0, n * 4u, &S.mbar_leaf[lb]);
+    bulk_g2s(&S.tv[lb][0], a.pv + L0, n * 8u, &S.mbar_leaf[lb]);
+  };
+
+  const int32_t nwin = (cend - cbeg + kGW - 1) / kGW;
+  if (lane == 0) {
+    for (int b = 0; b < 3; ++b) mbar_init(&S.mbar_meta[b], 1);
+    for (int b = 0; b < 2; ++b) mbar_init(&S.mbar_leaf[b], 1);
+    mbar_init_fence();
+    issue_meta(0);
+    if (nwin > 1) issue_meta(1);
+    issue_leaves(0);
+  }
+  __syncwarp();
+  for (int32_t win = 0; win < nwin; ++win) {
+    const int mb = win % 3, lbf = win & 1;
+    if (lane == 0) {
+      if (win + 1 < nwin) issue_leaves(win + 1);
+      if (win + 2 < nwin) issue_meta(win + 2);
+    }
+    mbar_wait(&S.mbar_meta[mb], (win / 3) & 1);
+    mbar_wait(&S.mbar_leaf[lbf], (win / 2) & 1);
+    const int32_t g0 = cbeg + win * kGW;
+    const int32_t ge = min(g0 + kGW, cend);
+    const int32_t L0 = S.hdr[mb][0].x;
+    for (int32_t g = g0; g < ge; ++g) {
+      const int4 hh = S.hdr[mb][g - g0];
+      const int n = hh.y;  // warp-uniform leaves per segment
+      const int32_t jA = S.node[mb][(g - g0) * kPackSlots + q];
+      const int32_t jB = S.node[mb][(g - g0) * kPackSlots + 4 + q];
+      const double uA = h < R ? __ldg(U + static_cast<int64_t>(jA) * R + h) : 0.0;
+      const double uB = h < R ? __ldg(U + static_cast<int64_t>(jB) * R + h) : 0.0;
+      double YA[8], YB[8];
+#pragma unroll
+      for (int s = 0; s < 8; ++s) YA[s] = YB[s] = 0.0;
+#pragma unroll
+      for (int it = 0; it < 4; ++it) {
+        if (it < n) {  // warp-uniform
+          // row-contiguous gathers: lane (gs, gc) fetches columns 2gc, 2gc+1
+          // of slot gs's V and W rows into the per-warp row tiles
+          const int32_t eg = hh.x - L0 + it * kPackSlots + gs;
+          const double2 vg = pair2<VECV>(V + static_cast<int64_t>(S.kk[lbf][eg]) * S_, 2 * gc, S_);
+          const double2 wg = pair2<VECW>(W + static_cast<int64_t>(S.ll[lbf][eg]) * T, 2 * gc, T);
+          *reinterpret_cast<double2*>(&S.vs[gs][2 * gc]) = vg;
+          *reinterpret_cast<double2*>(&S.ws[gs][2 * gc]) = wg;
+          __syncwarp();
+          const int32_t eA = hh.x - L0 + it * kPackSlots + q, eB = eA + 4;
+          const double vA = S.tv[lbf][eA], vB = S.tv[lbf][eB];
+          const double wA = S.ws[q][h], wB = S.ws[q + 4][h];
+          double vrA[8], vrB[8];
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            const double2 a2 = *reinterpret_cast<const double2*>(&S.vs[q][2 * m]);
+            const double2 b2 = *reinterpret_cast<const double2*>(&S.vs[q + 4][2 * m]);
+            vrA[2 * m] = a2.x; vrA[2 * m + 1] = a2.y;
+            vrB[2 * m] = b2.x; vrB[2 * m + 1] = b2.y;
+          }
+          __syncwarp();  // row tiles are rewritten by the next iteration
+          const double xA = vA * wA, xB = vB * wB;  // X[t] = t_ijkl * W[l,t]
+#pragma unroll
+          for (int s = 0; s < 8; ++s) {
+            YA[s] = fma(vrA[s], xA, YA[s]);  // Y[s,t] += V[k,s] * X[t]
+            YB[s] = fma(vrB[s], xB, YB[s]);
+          }
+        }
+      }
+      // Out_i[r, s, t] += U[j, r] * Y[s, t] for both K-chunks
+#pragma unroll
+      for (int s = 0; s < 8; ++s) dmma_8x8x4(acc[2 * s], acc[2 * s + 1], uA, YA[s]);
+#pragma unroll
+      for (int s = 0; s < 8; ++s) dmma_8x8x4(acc[2 * s], acc[2 * s + 1], uB, YB[s]);
+      pending = true;
+      if (g + 1 == sl_end) {
+        flush(head ? 0 : -1);
+        pending = false;
+        head = false;
+        if (g + 1 < cend) {
+          ++sl;
+          sl_end = nx_end;
+          row = nx_row;
+          nx_end = sl + 2 <= t.nlev[0] ? __ldg(slice_grp + sl + 2) : 0;
+          nx_row = sl + 1 < t.nlev[0] ? __ldg(t.idx[0] + sl + 1) : 0;
+        }
+      }
+    }
+    __syncwarp();  // stage buffers of this window are free after this point
+  }
+  if (pending) flush(head ? 0 : 1);
+}
+
 template <bool VECV>
 __global__ void __launch_bounds__(kBlock) k_ttmc4(RootOutArgs a) {
   const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
@@ -1584,7 +1761,17 @@ void launch_ttmc4(const RootOutArgs& a, cudaStream_t s) {
   const int64_t blocks = (a.n_items * 32 + kBlock - 1) / kBlock;
   if (blocks == 0) return;
   const int mode = a.flags >> 8;
-  if (mode == 1) {
+  if (mode == 2) {
+    const bool vv = a.vec & 2, vw = a.vec & 4;
+    if (vv && vw)
+      k_ttmc4pq<true, true><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
+    else if (vv)
+      k_ttmc4pq<true, false><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
+    else if (vw)
+      k_ttmc4pq<false, true><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
+    else
+      k_ttmc4pq<false, false><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
+  } else if (mode == 1) {
     if (a.vec & 2)
       k_ttmc4pk<true><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
     else

@@ -7,13 +7,14 @@
 #include <cstdio>
 #include <cuda_runtime.h>
 
-template <int WIDTH, bool SMEM>
+template <int WIDTH, bool SMEM, bool FRAG = false>
 __global__ void k_gather(const double* __restrict__ table, int rows, int iters, double* out, int active) {
   extern __shared__ double sh[];
   const int lane = threadIdx.x & 31;
   constexpr int LPR = 128 / WIDTH;      // lanes per row
-  const int slot = lane / LPR;
-  const int col = (lane % LPR) * (WIDTH / 8);
+  // FRAG: DMMA fragment order — row = lane % 4, 8-byte column = lane / 4
+  const int slot = FRAG ? (lane & 3) : lane / LPR;
+  const int col = FRAG ? (lane >> 2) : (lane % LPR) * (WIDTH / 8);
   if (SMEM) {
     for (int i = threadIdx.x; i < rows * 16; i += blockDim.x) sh[i] = table[i];
     __syncthreads();
@@ -52,24 +53,25 @@ __global__ void k_gather(const double* __restrict__ table, int rows, int iters, 
   if (acc == 1234.5) out[0] = acc;
 }
 
-template <int WIDTH, bool SMEM>
+template <int WIDTH, bool SMEM, bool FRAG = false>
 void run(const double* table, int rows, double* out, int sms, int active = 32) {
   const int iters = 4096, threads = 256, blocks = sms * 4;
   const size_t smem = SMEM ? rows * 16 * sizeof(double) : 0;
-  if (SMEM) cudaFuncSetAttribute(k_gather<WIDTH, SMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (SMEM) cudaFuncSetAttribute(k_gather<WIDTH, SMEM, FRAG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  k_gather<WIDTH, SMEM><<<blocks, threads, smem>>>(table, rows, iters, out, active);
+  k_gather<WIDTH, SMEM, FRAG><<<blocks, threads, smem>>>(table, rows, iters, out, active);
   cudaEventRecord(a);
-  k_gather<WIDTH, SMEM><<<blocks, threads, smem>>>(table, rows, iters, out, active);
+  k_gather<WIDTH, SMEM, FRAG><<<blocks, threads, smem>>>(table, rows, iters, out, active);
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   float ms;
   cudaEventElapsedTime(&ms, a, b);
-  const int lpr = 128 / WIDTH; const int act = active < 32 / lpr ? active : 32 / lpr;
+  const int lpr = FRAG ? 8 : 128 / WIDTH; const int act = active < 32 / lpr ? active : 32 / lpr;
   const double bytes = double(blocks) * threads / 32 * act * lpr * iters * WIDTH;
-  printf("width %2d B/lane %-6s rows %5d active-rows %2d : %8.2f TB/s  (%.1f B/clk/SM @1.9GHz)  err=%s\n", WIDTH,
+  printf("%s width %2d B/lane %-6s rows %5d active-rows %2d : %8.2f TB/s  (%.1f B/clk/SM @1.9GHz)  err=%s\n",
+         FRAG ? "frag" : "rows", WIDTH,
          SMEM ? "smem" : "global", rows, act, bytes / (ms * 1e-3) / 1e12,
          bytes / (ms * 1e-3) / sms / 1.9e9, cudaGetErrorString(cudaGetLastError()));
 }
@@ -82,6 +84,10 @@ int main() {
   cudaMalloc(&table, maxrows * 16 * sizeof(double));
   cudaMemset(table, 0, maxrows * 16 * sizeof(double));
   cudaMalloc(&out, 8);
+  for (int rows : {1024, 20000}) {
+    run<8, false, true>(table, rows, out, sms);
+    run<8, true, true>(table, rows < 1024 ? rows : 512, out, sms);
+  }
   for (int rows : {256, 1024, 20000}) {
     run<8, false>(table, rows, out, sms);
     run<16, false>(table, rows, out, sms);
