@@ -531,7 +531,8 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
         else
           spttn_dev::build_leaf_items(D, chunk, p->dec, sparse_out ? 0 : tile, s);
       }
-      p->launches = 1 + (p->dec.n_split > 0) + (p->dec.n_absent > 0);
+      p->launches = 1 + ((p->dec.n_split > 0 || p->dec.n_absent > 0) ? 1 : 0) +
+                    (p->dec.n_multi > 0 ? 1 : 0);
     }
     spttn_dev::plan_trace("plan: decomposition", s);
     SPTTN_CUDA(cudaStreamSynchronize(s));

@@ -145,12 +145,6 @@ __global__ void k_seg_splits(CsfView t, const int32_t* slice_seg, int64_t chunk,
   present[t.idx[0][s]] = 1;
 }
 
-__global__ void k_zero_rows(const int32_t* rows, int64_t n, int64_t tile, double* out) {
-  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (e >= n * tile) return;
-  out[static_cast<int64_t>(rows[e / tile]) * tile + e % tile] = 0.0;
-}
-
 unsigned blocks_for(int64_t n, int b) { return static_cast<unsigned>((n + b - 1) / b); }
 
 // slice_units: first work unit (segment / packed group) of every root slice,
@@ -333,29 +327,124 @@ namespace {
 // partial tiles (TAIL of the slice's first item, HEAD of the others) in item
 // order; level 2: one block per split slice sums its chunk tiles in chunk
 // order. Both orders are fixed by the plan, so results are deterministic.
-__global__ void k_fix1(const int32_t* chunk_split, const int32_t* chunk_lo,
-                       const int32_t* chunk_hi, const int32_t* split_first, const double* part,
-                       int64_t tile, double* part2) {
-  const int32_t c = blockIdx.x;
-  const int32_t first = split_first[chunk_split[c]];
-  const int32_t lo = chunk_lo[c], hi = chunk_hi[c];
-  for (int64_t e = threadIdx.x; e < tile; e += blockDim.x) {
-    double sum = 0.0;
-    for (int32_t it = lo; it <= hi; ++it)
-      sum += part[(static_cast<int64_t>(it) * 2 + (it == first ? 1 : 0)) * tile + e];
-    part2[static_cast<int64_t>(c) * tile + e] = sum;
+// Epilogue, pass 1 — one warp per work unit. Warps [0, n_chunk) each sum one
+// chunk of <= kFixChunk items of a split root slice (the first item's TAIL
+// tile, the other items' HEAD tiles, in item order; lanes stride the tile
+// with 256-bit loads, 8 item tiles in flight). A slice with one chunk is
+// written straight to the output, otherwise the chunk sum goes to part2 for
+// pass 2. Warps past n_chunk zero absent rows.
+template <bool V4>
+__global__ void __launch_bounds__(256) k_fix1(
+    const int32_t* chunk_split, const int32_t* chunk_lo, const int32_t* chunk_hi,
+    const int32_t* split_first, const int32_t* split_chunk, const int32_t* split_node,
+    const int32_t* idx0, const double* part, int64_t tile, int64_t n_chunk, double* part2,
+    const int32_t* absent_rows, int64_t n_absent, double* out) {
+  const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  if (wid >= n_chunk) {  // absent root rows: zero their output tiles
+    const int64_t zw = nwarps - n_chunk;
+    for (int64_t z = (wid - n_chunk) * 32 + lane; z < n_absent * tile; z += zw * 32)
+      out[static_cast<int64_t>(absent_rows[z / tile]) * tile + z % tile] = 0.0;
+    return;
+  }
+  const int32_t sidx = chunk_split[wid];
+  const int32_t first = split_first[sidx];
+  const int32_t lo = chunk_lo[wid], hi = chunk_hi[wid];
+  const bool single = split_chunk[sidx + 1] - split_chunk[sidx] == 1;
+  double* dst = single ? out + static_cast<int64_t>(idx0[split_node[sidx]]) * tile : part2 + wid * tile;
+  const int64_t nv = V4 ? tile / 4 : tile;
+  for (int64_t e = lane; e < nv; e += 32) {
+    double4 sum = make_double4(0, 0, 0, 0);
+    for (int32_t it = lo; it <= hi; it += 8) {
+      double4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int32_t i = it + u;
+        const double* src = part + (static_cast<int64_t>(i) * 2 + (i == first ? 1 : 0)) * tile;
+        if (V4)
+          v[u] = i <= hi ? reinterpret_cast<const double4*>(src)[e] : make_double4(0, 0, 0, 0);
+        else
+          v[u] = make_double4(i <= hi ? src[e] : 0.0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (it + u <= hi) {
+          sum.x += v[u].x;
+          sum.y += v[u].y;
+          sum.z += v[u].z;
+          sum.w += v[u].w;
+        }
+    }
+    if (V4)
+      reinterpret_cast<double4*>(dst)[e] = sum;
+    else
+      dst[e] = sum.x;
   }
 }
 
-__global__ void k_fix2(const int32_t* split_node, const int32_t* split_chunk, const int32_t* idx0,
-                       const double* part2, int64_t tile, double* out) {
-  const int32_t sidx = blockIdx.x;
+// Epilogue, pass 2 — one block per slice split into several chunks (the
+// heavy root slices of skewed tensors). The block's threads form G groups of
+// tile/4 (or tile) threads; group g adds chunk sums c0+g, c0+g+G, ... in
+// order (8 loads in flight), then the G group sums are added in group order
+// through shared memory. Fixed order: deterministic.
+template <bool V4>
+__global__ void __launch_bounds__(256) k_fix2(const int32_t* multi, const int32_t* split_chunk,
+                                              const int32_t* split_node, const int32_t* idx0,
+                                              const double* part2, int64_t tile, double* out) {
+  __shared__ double4 ws[256];
+  const int32_t sidx = multi[blockIdx.x];
   const int32_t c0 = split_chunk[sidx], c1 = split_chunk[sidx + 1];
   const int64_t row = idx0[split_node[sidx]];
-  for (int64_t e = threadIdx.x; e < tile; e += blockDim.x) {
-    double sum = part2[static_cast<int64_t>(c0) * tile + e];
-    for (int32_t c = c0 + 1; c < c1; ++c) sum += part2[static_cast<int64_t>(c) * tile + e];
-    out[row * tile + e] = sum;
+  const int64_t nv = V4 ? tile / 4 : tile;  // vector elements per tile
+  // piece of the tile handled per pass: up to 256 elements, G = 256 / piece groups
+  const int64_t piece = nv < 256 ? nv : 256;
+  const int G = static_cast<int>(256 / piece);
+  const int g = threadIdx.x / static_cast<int>(piece);
+  const int64_t el = threadIdx.x % piece;
+  for (int64_t p0 = 0; p0 < nv; p0 += piece) {
+    const int64_t e = p0 + el;
+    const bool act = g < G && e < nv;
+    double4 sum = make_double4(0, 0, 0, 0);
+    if (act) {
+      for (int32_t c = c0 + g; c < c1; c += 8 * G) {
+        double4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int32_t k = c + u * G;
+          const double* src = part2 + static_cast<int64_t>(k) * tile;
+          if (V4)
+            v[u] = k < c1 ? reinterpret_cast<const double4*>(src)[e] : make_double4(0, 0, 0, 0);
+          else
+            v[u] = make_double4(k < c1 ? src[e] : 0.0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (c + u * G < c1) {
+            sum.x += v[u].x;
+            sum.y += v[u].y;
+            sum.z += v[u].z;
+            sum.w += v[u].w;
+          }
+      }
+    }
+    ws[threadIdx.x] = sum;
+    __syncthreads();
+    if (g == 0 && e < nv) {
+      double4 t = ws[el];
+      for (int k = 1; k < G; ++k) {
+        const double4 o = ws[k * piece + el];
+        t.x += o.x;
+        t.y += o.y;
+        t.z += o.z;
+        t.w += o.w;
+      }
+      if (V4)
+        reinterpret_cast<double4*>(out + row * tile)[e] = t;
+      else
+        out[row * tile + e] = t.x;
+    }
+    __syncthreads();
   }
 }
 
@@ -369,7 +458,7 @@ void build_fixup_chunks(Decomp& d, cudaStream_t s) {
   SPTTN_CUDA(cudaMemcpyAsync(last.data(), d.split_last, d.n_split * sizeof(int32_t),
                              cudaMemcpyDeviceToHost, s));
   SPTTN_CUDA(cudaStreamSynchronize(s));
-  std::vector<int32_t> cs, clo, chi, sc(d.n_split + 1, 0);
+  std::vector<int32_t> cs, clo, chi, sc(d.n_split + 1, 0), multi;
   for (int64_t k = 0; k < d.n_split; ++k) {
     sc[k] = static_cast<int32_t>(cs.size());
     for (int32_t lo = first[k]; lo <= last[k]; lo += kFixChunk) {
@@ -377,6 +466,7 @@ void build_fixup_chunks(Decomp& d, cudaStream_t s) {
       clo.push_back(lo);
       chi.push_back(std::min(last[k], lo + kFixChunk - 1));
     }
+    if (static_cast<int32_t>(cs.size()) - sc[k] > 1) multi.push_back(static_cast<int32_t>(k));
   }
   sc[d.n_split] = static_cast<int32_t>(cs.size());
   d.n_chunk = static_cast<int64_t>(cs.size());
@@ -388,24 +478,34 @@ void build_fixup_chunks(Decomp& d, cudaStream_t s) {
   up(&d.chunk_lo, clo);
   up(&d.chunk_hi, chi);
   up(&d.split_chunk, sc);
+  up(&d.multi_split, multi);
+  d.n_multi = static_cast<int64_t>(multi.size());
   dmalloc(&d.part2, std::max<int64_t>(1, d.n_chunk * d.tile) * sizeof(double), s);
   SPTTN_CUDA(cudaStreamSynchronize(s));
 }
 
 void launch_fixup(const Decomp& d, const CsfView& t, double* out, cudaStream_t s) {
-  if (d.n_split > 0) {
-    const int threads = d.tile >= 256 ? 256 : (d.tile >= 128 ? 128 : (d.tile >= 64 ? 64 : 32));
-    k_fix1<<<static_cast<unsigned>(d.n_chunk), threads, 0, s>>>(
-        d.chunk_split, d.chunk_lo, d.chunk_hi, d.split_first, d.part, d.tile, d.part2);
-    k_fix2<<<static_cast<unsigned>(d.n_split), threads, 0, s>>>(d.split_node, d.split_chunk,
-                                                                 t.idx[0], d.part2, d.tile, out);
-    SPTTN_CUDA(cudaGetLastError());
+  if (d.n_split == 0 && d.n_absent == 0) return;
+  const int64_t zero_warps =
+      d.n_absent > 0 ? std::min<int64_t>((d.n_absent * d.tile + 31) / 32, 148 * 64) : 0;
+  const unsigned blocks = blocks_for((d.n_chunk + zero_warps) * 32, 256);
+  if (d.tile % 4 == 0)
+    k_fix1<true><<<blocks, 256, 0, s>>>(d.chunk_split, d.chunk_lo, d.chunk_hi, d.split_first,
+                                         d.split_chunk, d.split_node, t.idx[0], d.part, d.tile,
+                                         d.n_chunk, d.part2, d.absent_rows, d.n_absent, out);
+  else
+    k_fix1<false><<<blocks, 256, 0, s>>>(d.chunk_split, d.chunk_lo, d.chunk_hi, d.split_first,
+                                          d.split_chunk, d.split_node, t.idx[0], d.part, d.tile,
+                                          d.n_chunk, d.part2, d.absent_rows, d.n_absent, out);
+  if (d.n_multi > 0) {
+    if (d.tile % 4 == 0)
+      k_fix2<true><<<static_cast<unsigned>(d.n_multi), 256, 0, s>>>(
+          d.multi_split, d.split_chunk, d.split_node, t.idx[0], d.part2, d.tile, out);
+    else
+      k_fix2<false><<<static_cast<unsigned>(d.n_multi), 256, 0, s>>>(
+          d.multi_split, d.split_chunk, d.split_node, t.idx[0], d.part2, d.tile, out);
   }
-  if (d.n_absent > 0) {
-    k_zero_rows<<<blocks_for(d.n_absent * d.tile, 256), 256, 0, s>>>(d.absent_rows, d.n_absent,
-                                                                     d.tile, out);
-    SPTTN_CUDA(cudaGetLastError());
-  }
+  SPTTN_CUDA(cudaGetLastError());
 }
 
 void free_decomp(Decomp& d) {
@@ -423,6 +523,7 @@ void free_decomp(Decomp& d) {
   dfree(d.chunk_hi);
   dfree(d.split_chunk);
   dfree(d.part2);
+  dfree(d.multi_split);
   dfree(d.grp_hdr);
   dfree(d.grp_node);
   dfree(d.grp_node1);

@@ -80,6 +80,8 @@ struct Decomp {
   int32_t* chunk_hi = nullptr;
   int32_t* split_chunk = nullptr;  // [n_split+1] first chunk of each split slice
   double* part2 = nullptr;         // [n_chunk][tile]
+  int64_t n_multi = 0;
+  int32_t* multi_split = nullptr;  // split slices with more than one chunk (pass 2)
   // packed groups (pack.cu): header {leaf_base, len, nseg, slice} per group
   int64_t n_groups = 0;
   int64_t n_packed_leaves = 0;
@@ -172,7 +174,7 @@ constexpr int kPackSlots = 8;  // TTMc-3 groups (128-byte rows)
 // leaf's level-2 coordinate).
 void build_packed(const DevCsf& csf, int leaf_level, Decomp& d, cudaStream_t s,
                   int slots = kPackSlots, const int32_t* leaf_coord2 = nullptr);
-constexpr int kFixChunk = 32;
+constexpr int kFixChunk = 8;  // items per pass-1 chunk (one batch of loads)
 void build_fixup_chunks(Decomp& d, cudaStream_t s);
 void launch_fixup(const Decomp& d, const CsfView& t, double* out, cudaStream_t s);
 void free_decomp(Decomp& d);
