@@ -66,6 +66,18 @@ def parse():
     return ap.parse_args()
 
 
+def _load_traffic():
+    """Per-launch DRAM traffic of each config's dominant kernel, from the
+    committed ncu --set full summaries (profiles/traffic.json)."""
+    try:
+        return json.loads((ROOT / "profiles" / "traffic.json").read_text())
+    except (OSError, ValueError):
+        return {}
+
+
+TRAFFIC = _load_traffic()
+
+
 def measured_peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -363,6 +375,11 @@ def main():
                     "unit": "TFLOP/s"}
         roof["frac"] = roof["achieved"] / roof["peak"]
         roof["traffic"] = None
+        tr = TRAFFIC.get(key)
+        if tr:  # dram read+write bytes of one launch of this config's kernel (ncu --set full)
+            roof["traffic"] = tr["traffic_bytes"]
+            roof["traffic_kernel"] = tr["kernel"]
+            roof["traffic_source"] = tr["source"]
         roof["peak_source"] = (f"{peak_src} MEASURED_PEAKS.json hbm_gbs" if bound == "hbm" else
                                "fp64 " + ("DMMA" if fp_peak == fp64["dmma_tflops"] else "DFMA") +
                                " probe measured by bench.py (MEASURED_PEAKS.json has no fp64)")

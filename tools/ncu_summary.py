@@ -17,7 +17,10 @@ RAW = ["dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_sectors_srcunit_
        "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active",
        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
        "l1tex__data_pipe_lsu_wavefronts.sum.pct_of_peak_sustained_elapsed",
-       "lts__throughput.avg.pct_of_peak_sustained_elapsed"]
+       "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+       "SM_A.TriageCompute.l1tex__data_pipe_lsu_wavefronts_mem_lgds.avg",
+       "SM_A.TriageCompute.l1tex__data_pipe_lsu_wavefronts_mem_shared.avg",
+       "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
 
 
 def ncu(rep, *args):
