@@ -494,9 +494,11 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
           spttn_dev::build_segments(D, 1, seg_len, chunk, p->dec, tile, s);
         }
       } else if (!sparse_out && R <= 32 && env_int("SPTTN_MTTKRP_MODE", 2) >= 1) {
-        // segment-form MTTKRP (R <= 32): 2 = packed length-sorted groups
-        // (default), 1 = plain segments
-        p->mode = static_cast<int>(env_int("SPTTN_MTTKRP_MODE", 2));
+        // segment-form MTTKRP (R <= 32): 3 = packed length-sorted groups with
+        // TMA-staged streams (default for order 4), 2 = packed (default for
+        // order 3: items hold too few windows to amortise the staging
+        // prologue), 1 = plain segments
+        p->mode = static_cast<int>(env_int("SPTTN_MTTKRP_MODE", D.order == 4 ? 3 : 2));
         p->vec = (R % 4 == 0) && facs_aligned32 ? 1 : 0;
         const int seg_len = static_cast<int>(std::clamp<int64_t>(env_int("SPTTN_SEG_LEN", 4), 1, 4));
         const int unit_level = D.order - 2;
@@ -504,13 +506,14 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
         const int64_t warps = static_cast<int64_t>(sms) * 16 * 2;
         int64_t chunk = env_int("SPTTN_CHUNK", 0);
         if (chunk <= 0) chunk = std::clamp<int64_t>((units + warps - 1) / warps, 8, 1024);
-        if (p->mode == 2) {
+        if (p->mode == 2 || p->mode == 3) {
           spttn_dev::build_segments(D, unit_level, seg_len, chunk, p->dec, tile, s, false);
           spttn_dev::build_packed(D, D.order - 1, p->dec, s, 4);
           const int64_t w24 = static_cast<int64_t>(sms) * 24 * 2;
           int64_t gchunk = env_int("SPTTN_GCHUNK", 0);
           if (gchunk <= 0)
-            gchunk = std::clamp<int64_t>((p->dec.n_groups + w24 - 1) / w24, 4, 1024);
+            gchunk = std::clamp<int64_t>((p->dec.n_groups + w24 - 1) / w24, 4,
+                                         p->mode == 3 ? 64 : 1024);
           spttn_dev::finish_unit_items(D, p->dec, p->dec.slice_grp, p->dec.n_groups, gchunk, tile, s);
         } else {
           spttn_dev::build_segments(D, unit_level, seg_len, chunk, p->dec, tile, s);
@@ -603,7 +606,9 @@ int spttn_execute_stage(spttn_plan* p, int stage, void* stream) {
       case SPTTN_NEST_MTTKRP3:
         a.f[1] = p->fac[0];
         a.f[2] = p->fac[1];
-        if (p->mode == 2)
+        if (p->mode == 3)
+          spttn_dev::launch_mttkrp_pq(a, 3, s);
+        else if (p->mode == 2)
           spttn_dev::launch_mttkrp_pk(a, 3, s);
         else if (p->mode == 1)
           spttn_dev::launch_mttkrp_seg(a, nullptr, 3, s);
@@ -614,7 +619,9 @@ int spttn_execute_stage(spttn_plan* p, int stage, void* stream) {
         a.f[1] = p->fac[0];
         a.f[2] = p->fac[1];
         a.f[3] = p->fac[2];
-        if (p->mode == 2)
+        if (p->mode == 3)
+          spttn_dev::launch_mttkrp_pq(a, 4, s);
+        else if (p->mode == 2)
           spttn_dev::launch_mttkrp_pk(a, 4, s);
         else if (p->mode == 1)
           spttn_dev::launch_mttkrp_seg(a, p->dec.seg_node1, 4, s);
