@@ -28,7 +28,7 @@ probe: $(LIB)/libspttn_probe.so
 datagen: $(LIB)/libspttn_datagen.so
 HAVE_HOST := $(and $(wildcard $(REF)/src/loop_nest.cpp),$(wildcard $(PKG)/csrc/shim/executor_b200.cpp))
 ifneq ($(HAVE_HOST),)
-host: $(LIB)/libspttn_b200_host.so build/tests/test_executor_b200 build/tests/acceptance_b200 build/tests/plan_overhead
+host: $(LIB)/libspttn_b200_host.so build/tests/test_executor_b200 build/tests/acceptance_b200 build/tests/plan_overhead build/tests/generic_scale
 else
 host:
 	@echo "reference sources absent: keeping prebuilt host shim"
@@ -86,6 +86,11 @@ clean:
 .PHONY: all device datagen probe host oracle clean
 
 build/tests/plan_overhead: tests/cpp/plan_overhead.cpp $(LIB)/libspttn_b200_host.so
+	@mkdir -p $(dir $@)
+	$(CXX) $(HOSTFLAGS) -I$(REF)/tests $< -L$(LIB) -lspttn_b200_host -lspttn_b200 \
+	  -Wl,-rpath,'$$ORIGIN/../../$(LIB)' -o $@
+
+build/tests/generic_scale: tests/cpp/generic_scale.cpp $(LIB)/libspttn_b200_host.so
 	@mkdir -p $(dir $@)
 	$(CXX) $(HOSTFLAGS) -I$(REF)/tests $< -L$(LIB) -lspttn_b200_host -lspttn_b200 \
 	  -Wl,-rpath,'$$ORIGIN/../../$(LIB)' -o $@

@@ -376,11 +376,49 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
       std::vector<int64_t> off(nb + 1, 0);
       for (int b = 0; b < nb; ++b) off[b + 1] = off[b] + G.buffer_size[b];
       auto al = [](size_t x) { return (x + 255) & ~size_t{255}; };
-      const size_t n_cnt = (nb + 4) * sizeof(int64_t);
-      const size_t n_buf = static_cast<size_t>(std::max<int64_t>(1, off[nb])) * 8;
+      // Parallel interpretation over root slices (generic.cu k_generic_par)
+      // when the single root is the CSF level-0 loop without resets of its
+      // own; outputs indexed by the root mode (or sparse) are written
+      // directly (mode 1), any other dense output goes through per-worker
+      // copies reduced in worker order (mode 2). Replicas are capped at
+      // 512 MB. SPTTN_GENERIC_PAR=0 forces the sequential walk.
+      auto& g = p->gen;
+      {
+        const int64_t n0 = D.level_size[0];
+        const spg_node* rootn = G.num_roots == 1 ? &G.nodes[G.roots[0]] : nullptr;
+        const bool par_ok = env_int("SPTTN_GENERIC_PAR", 1) != 0 && !G.observe && rootn &&
+                            rootn->kind == SPG_SPARSE && rootn->csf_level == 0 &&
+                            rootn->reset_count == 0 && n0 >= 2;
+        if (par_ok) {
+          bool disjoint = true;
+          for (int t = 0; t < G.num_terms; ++t) {
+            const spg_access& o = G.out[t];
+            if (o.kind != SPG_OP_OUT_DENSE) continue;
+            bool has_root = false;
+            for (int k = 0; k < o.naddr; ++k)
+              has_root |= o.ids[k] == rootn->index && o.strides[k] != 0;
+            disjoint &= has_root;
+          }
+          const int64_t budget = int64_t{512} << 20;
+          const int64_t per_buf = std::max<int64_t>(8, off[nb] * 8);
+          const int64_t per_out = disjoint ? 0 : std::max<int64_t>(8, G.out_size * 8);
+          int64_t W = std::min<int64_t>(n0, static_cast<int64_t>(sm_count()) * (disjoint ? 128 : 32));
+          W = std::min<int64_t>(W, budget / (per_buf + per_out));
+          if (W >= 2) {
+            g.par_mode = disjoint ? 1 : 2;
+            g.workers = W;
+            g.out_size = G.out_size;
+          }
+        }
+      }
+      const int64_t reps = g.workers;
+      const size_t n_cnt = (nb + 5) * sizeof(int64_t);  // + slice counter (mode 1)
+      const size_t n_buf = static_cast<size_t>(std::max<int64_t>(1, off[nb]) * reps) * 8;
       const size_t n_out = static_cast<size_t>(std::max<int64_t>(1, G.out_size)) * 8;
+      const size_t n_priv =
+          g.par_mode == 2 ? static_cast<size_t>(std::max<int64_t>(1, G.out_size) * reps) * 8 : 0;
       const bool lookup = G.need_leaf_lookup && nnz > 0;
-      size_t total = n_cnt + n_buf + n_out;  // contiguous, 8-byte aligned
+      size_t total = n_cnt + n_buf + n_out + n_priv;  // contiguous, 8-byte aligned
       total = al(total) + al(sizeof(spg_program)) + al((nb + 1) * sizeof(int64_t)) +
               al(16 * sizeof(double*));
       if (!on_dev)
@@ -391,11 +429,11 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
       dev_malloc(&p->arena, total, s);
       char* cur = static_cast<char*>(p->arena);
       auto take = [&](size_t bytes) { char* r = cur; cur += al(bytes); return r; };
-      auto& g = p->gen;
       g.counters = reinterpret_cast<int64_t*>(cur);
       g.buffers = reinterpret_cast<double*>(cur + n_cnt);
       p->out = reinterpret_cast<double*>(cur + n_cnt + n_buf);
-      g.zero_bytes = n_cnt + n_buf + n_out;
+      if (g.par_mode == 2) g.priv_out = reinterpret_cast<double*>(cur + n_cnt + n_buf + n_out);
+      g.zero_bytes = n_cnt + n_buf + n_out + n_priv;
       cur += al(g.zero_bytes);
       g.total_buffer_elems = off[nb];
       g.d_prog = reinterpret_cast<spg_program*>(take(sizeof(spg_program)));
@@ -434,7 +472,7 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
             D.view(), p->gen.d_prog, p->gen.leaf_keys, p->gen.leaf_pos);
         SPTTN_CUDA(cudaGetLastError());
       }
-      p->launches = 2;
+      p->launches = 2 + (p->gen.par_mode == 2 ? 1 : 0);
     } else {
       const bool sparse_out = p->kind == SPTTN_NEST_TTTP3;
       p->out_count = sparse_out ? nnz : D.dims[0] * tile;

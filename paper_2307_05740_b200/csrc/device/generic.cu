@@ -115,7 +115,7 @@ struct Interp {
       double* buf = bufs + boff[b];
       const int64_t n = P->buffer_size[b];
       for (int64_t i = 0; i < n; ++i) buf[i] = 0.0;
-      counters[1 + b] += 1;
+      atomicAdd(reinterpret_cast<unsigned long long*>(&counters[1 + b]), 1ull);
       if (P->observe) {
         int64_t* cursor = &counters[1 + P->num_buffers];
         const int64_t need = 16 + 8 * n;
@@ -149,74 +149,138 @@ __device__ void set_iter(Interp& I, const spg_node& nd, int64_t it) {
   }
 }
 
-// The program (~23 KB) is staged into shared memory by the whole block so the
-// interpreting thread reads node / operand / hook tables at shared-memory
-// latency instead of global-memory latency.
+// Walks root node `root` of the forest like exec_node; a sparse level-0 root
+// may be restricted to the iteration range [rlo, rhi) (parallel mode).
+__device__ void walk(Interp& I, const spg_program* P, int root, int64_t rlo, int64_t rhi) {
+  Frame st[SPG_MAX_IDX + 2];
+  int sp = 0;
+  int pending = root;
+  bool top = true;
+  for (;;) {
+    if (pending >= 0) {
+      const spg_node& nd = P->nodes[pending];
+      I.resets(nd);
+      if (nd.kind == SPG_LEAF) {
+        I.leaf(nd.term);
+      } else if (nd.hook >= 0) {
+        I.hook(P->hooks[nd.hook]);
+      } else {
+        int64_t lo = 0, hi = 0;
+        if (nd.kind == SPG_SPARSE) {
+          if (nd.csf_level == 0) {
+            hi = I.t.nlev[0];
+            if (top && rlo >= 0) {
+              lo = rlo;
+              hi = rhi;
+            }
+          } else {
+            lo = I.t.ptr[nd.csf_level - 1][I.pos[nd.csf_level - 1]];
+            hi = I.t.ptr[nd.csf_level - 1][I.pos[nd.csf_level - 1] + 1];
+          }
+        } else {
+          hi = P->dims[nd.index];
+        }
+        if (lo < hi) {
+          st[sp++] = Frame{pending, 0, lo, hi};
+          set_iter(I, nd, lo);
+        }
+      }
+      pending = -1;
+      top = false;
+    }
+    if (sp == 0) break;
+    Frame& f = st[sp - 1];
+    const spg_node& fn = P->nodes[f.node];
+    if (f.child < fn.child_count) {
+      pending = P->children[fn.child_begin + f.child];
+      ++f.child;
+      continue;
+    }
+    ++f.it;
+    if (f.it < f.end) {
+      f.child = 0;
+      set_iter(I, fn, f.it);
+    } else {
+      --sp;
+    }
+  }
+}
+
+__device__ void stage_program(const spg_program* src_prog, unsigned char* smem) {
+  const int4* src = reinterpret_cast<const int4*>(src_prog);
+  int4* dst = reinterpret_cast<int4*>(smem);
+  for (size_t w = threadIdx.x; w < sizeof(spg_program) / sizeof(int4); w += blockDim.x)
+    dst[w] = src[w];
+  __syncthreads();
+}
+
+// Sequential interpreter: the program (~23 KB) is staged into shared memory by
+// the whole block so the interpreting thread reads node / operand / hook
+// tables at shared-memory latency instead of global-memory latency.
 __global__ void __launch_bounds__(256) k_generic(Interp I) {
   extern __shared__ __align__(16) unsigned char prog_smem[];
-  {
-    const int4* src = reinterpret_cast<const int4*>(I.P);
-    int4* dst = reinterpret_cast<int4*>(prog_smem);
-    for (size_t w = threadIdx.x; w < sizeof(spg_program) / sizeof(int4); w += blockDim.x)
-      dst[w] = src[w];
-    __syncthreads();
-  }
+  stage_program(I.P, prog_smem);
   if (blockIdx.x != 0 || threadIdx.x != 0) return;
   const spg_program* P = reinterpret_cast<const spg_program*>(prog_smem);
   I.P = P;
   for (int k = 0; k < SPG_MAX_IDX; ++k) I.ival[k] = 0;
   for (int k = 0; k < SPG_MAX_LEVELS; ++k) I.pos[k] = 0;
   I.madds = 0;
-  Frame st[SPG_MAX_IDX + 2];
-  int sp = 0;
-  for (int ri = 0; ri < P->num_roots; ++ri) {
-    // enter(root) then run the frame stack
-    int pending = P->roots[ri];
-    for (;;) {
-      if (pending >= 0) {
-        const spg_node& nd = P->nodes[pending];
-        I.resets(nd);
-        if (nd.kind == SPG_LEAF) {
-          I.leaf(nd.term);
-        } else if (nd.hook >= 0) {
-          I.hook(P->hooks[nd.hook]);
-        } else {
-          int64_t lo = 0, hi = 0;
-          if (nd.kind == SPG_SPARSE) {
-            if (nd.csf_level == 0) {
-              hi = I.t.nlev[0];
-            } else {
-              lo = I.t.ptr[nd.csf_level - 1][I.pos[nd.csf_level - 1]];
-              hi = I.t.ptr[nd.csf_level - 1][I.pos[nd.csf_level - 1] + 1];
-            }
-          } else {
-            hi = P->dims[nd.index];
-          }
-          if (lo < hi) {
-            st[sp++] = Frame{pending, 0, lo, hi};
-            set_iter(I, nd, lo);
-          }
-        }
-        pending = -1;
-      }
-      if (sp == 0) break;
-      Frame& f = st[sp - 1];
-      const spg_node& fn = P->nodes[f.node];
-      if (f.child < fn.child_count) {
-        pending = P->children[fn.child_begin + f.child];
-        ++f.child;
-        continue;
-      }
-      ++f.it;
-      if (f.it < f.end) {
-        f.child = 0;
-        set_iter(I, fn, f.it);
-      } else {
-        --sp;
-      }
-    }
-  }
+  for (int ri = 0; ri < P->num_roots; ++ri) walk(I, P, P->roots[ri], -1, -1);
   I.counters[0] = I.madds;
+}
+
+// Parallel interpreter over the root slices of a forest whose single root is
+// the CSF level-0 loop with no resets of its own (so iterations share no
+// buffer state). Every thread is a worker with private buffers.
+//  mode 1 (outputs disjoint across root slices: indexed by the root mode, or
+//          sparse): workers take root slices dynamically and write the output
+//          directly — each slice is computed exactly as in the sequential
+//          walk, so results are bit-identical to it.
+//  mode 2 (dense output not indexed by the root mode, e.g. MTTKRP for mode
+//          j): worker w walks the fixed root range [w*n0/W, (w+1)*n0/W) into
+//          a private output copy; k_generic_reduce adds the copies in worker
+//          order (deterministic; grouping differs from the sequential sum).
+__global__ void __launch_bounds__(256) k_generic_par(Interp I0, int mode, int64_t workers,
+                                                     int64_t buf_elems, double* priv,
+                                                     int64_t out_size) {
+  extern __shared__ __align__(16) unsigned char prog_smem[];
+  stage_program(I0.P, prog_smem);
+  const int64_t w = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (w >= workers) return;
+  const spg_program* P = reinterpret_cast<const spg_program*>(prog_smem);
+  Interp I = I0;
+  I.P = P;
+  I.bufs = I0.bufs + w * buf_elems;
+  if (mode == 2) I.out = priv + w * out_size;
+  for (int k = 0; k < SPG_MAX_IDX; ++k) I.ival[k] = 0;
+  for (int k = 0; k < SPG_MAX_LEVELS; ++k) I.pos[k] = 0;
+  I.madds = 0;
+  const int root = P->roots[0];
+  const int64_t n0 = I.t.nlev[0];
+  if (mode == 1) {
+    unsigned long long* next =
+        reinterpret_cast<unsigned long long*>(&I.counters[P->num_buffers + 3]);
+    for (;;) {
+      const int64_t sl = static_cast<int64_t>(atomicAdd(next, 1ull));
+      if (sl >= n0) break;
+      walk(I, P, root, sl, sl + 1);
+    }
+  } else {
+    const int64_t lo = w * n0 / workers, hi = (w + 1) * n0 / workers;
+    if (lo < hi) walk(I, P, root, lo, hi);
+  }
+  atomicAdd(reinterpret_cast<unsigned long long*>(&I.counters[0]),
+            static_cast<unsigned long long>(I.madds));
+}
+
+__global__ void k_generic_reduce(const double* priv, int64_t workers, int64_t out_size,
+                                 double* out) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= out_size) return;
+  double sum = 0.0;
+  for (int64_t w = 0; w < workers; ++w) sum += priv[w * out_size + e];
+  out[e] = sum;
 }
 
 // ---- unfactorized ---------------------------------------------------------
@@ -389,7 +453,17 @@ void generic_execute(const spg_program& prog, const DevCsf& csf, const double* c
   I.nkeys = g.n_leaf_keys;
   static_assert(sizeof(spg_program) % sizeof(int4) == 0, "program must be int4-copyable");
   static_assert(sizeof(spg_program) <= 48 * 1024, "program must fit default shared memory");
-  k_generic<<<1, 256, sizeof(spg_program), s>>>(I);
+  if (g.par_mode == 0) {
+    k_generic<<<1, 256, sizeof(spg_program), s>>>(I);
+  } else {
+    const unsigned blocks = static_cast<unsigned>((g.workers + 127) / 128);
+    k_generic_par<<<blocks, 128, sizeof(spg_program), s>>>(I, g.par_mode, g.workers,
+                                                           g.total_buffer_elems, g.priv_out,
+                                                           g.out_size);
+    if (g.par_mode == 2)
+      k_generic_reduce<<<static_cast<unsigned>((g.out_size + 255) / 256), 256, 0, s>>>(
+          g.priv_out, g.workers, g.out_size, out);
+  }
   SPTTN_CUDA(cudaGetLastError());
 }
 

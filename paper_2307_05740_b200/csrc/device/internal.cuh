@@ -195,8 +195,14 @@ struct GenericState {
   int64_t* leaf_pos = nullptr;
   int64_t n_leaf_keys = 0;
   int64_t total_buffer_elems = 0;
-  size_t zero_bytes = 0;  // [counters | buffers | out] cleared by one memset
+  size_t zero_bytes = 0;  // [counters | buffers | out | private outs] cleared by one memset
   bool in_arena = false;  // all pointers live in the plan's arena
+  // parallel interpreter (generic.cu k_generic_par): 0 = sequential,
+  // 1 = root slices to workers with disjoint outputs, 2 = private outputs
+  int par_mode = 0;
+  int64_t workers = 1;
+  double* priv_out = nullptr;  // mode 2: [workers][out_size]
+  int64_t out_size = 0;
 };
 void generic_execute(const spg_program& prog, const DevCsf& csf, const double* const* dense,
                      double* out, GenericState& g, cudaStream_t s);
