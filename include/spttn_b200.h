@@ -76,6 +76,8 @@ enum {
   SPTTN_NEST_TTTP3 = 3,   /* T*A[i,r]*B[j,r]*C[k,r]->S[i,j,k] (((A*B)*C)*T)   */
   SPTTN_NEST_MTTKRP4 = 4, /* T[i,j,k,l]*B*C*D->A[i,r]  (((T*D)*C)*B)          */
   SPTTN_NEST_TTMC4 = 5,   /* T[i,j,k,l]*U*V*W->Y[i,r,s,t] (((T*W)*V)*U)       */
+  SPTTN_NEST_MTTKRP3_J = 6, /* T[i,j,k]*A[i,r]*C[k,r]->B[j,r] ((T*C)*A), atomics */
+  SPTTN_NEST_MTTKRP3_K = 7, /* T[i,j,k]*A[i,r]*B[j,r]->C[k,r] ((A*B)*T), atomics */
   SPTTN_NEST_GENERIC = 100
 };
 

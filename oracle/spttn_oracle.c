@@ -36,6 +36,48 @@ void oc_mttkrp3(const oc_csf* t, int64_t R, const double* B, const double* C, do
   free(X);
 }
 
+/* MTTKRP-3 for mode j: T[i,j,k]*A[i,a]*C[k,a]->B[j,a], path ((T*C)*A),
+ * orders (i,j,a,k)(i,j,a) (max-buf-dim's pick): per (i,j) X[a] = sum_k t*C[k,a]
+ * in CSF order (the dense a loop outside k keeps each X[a] a sum over k in
+ * leaf order), then B[j,a] += X[a]*A[i,a] in (i,j) CSF order. */
+void oc_mttkrp3_j(const oc_csf* t, int64_t R, const double* A, const double* C, double* out) {
+  const int64_t J = t->dims[1];
+  memset(out, 0, sizeof(double) * dense_out_size(J, R, 1, 1));
+  double* X = (double*)calloc((size_t)R, sizeof(double));
+  for (int64_t p0 = 0; p0 < t->level_size[0]; ++p0) {
+    const int64_t i = t->idx[0][p0];
+    for (int64_t p1 = t->ptr[0][p0]; p1 < t->ptr[0][p0 + 1]; ++p1) {
+      const int64_t j = t->idx[1][p1];
+      memset(X, 0, sizeof(double) * R);
+      for (int64_t a = 0; a < R; ++a)
+        for (int64_t p2 = t->ptr[1][p1]; p2 < t->ptr[1][p1 + 1]; ++p2)
+          X[a] += t->values[p2] * C[t->idx[2][p2] * R + a];
+      for (int64_t a = 0; a < R; ++a) out[j * R + a] += X[a] * A[i * R + a];
+    }
+  }
+  free(X);
+}
+
+/* MTTKRP-3 for mode k: T[i,j,k]*A[i,a]*B[j,a]->C[k,a], path ((A*B)*T),
+ * orders (i,j,a)(i,j,a,k): per (i,j) W[a] = A[i,a]*B[j,a], per leaf
+ * C[k,a] += W[a]*t, contributions to each C[k,a] in (i,j) CSF order. */
+void oc_mttkrp3_k(const oc_csf* t, int64_t R, const double* A, const double* B, double* out) {
+  const int64_t K = t->dims[2];
+  memset(out, 0, sizeof(double) * dense_out_size(K, R, 1, 1));
+  double* W = (double*)calloc((size_t)R, sizeof(double));
+  for (int64_t p0 = 0; p0 < t->level_size[0]; ++p0) {
+    const int64_t i = t->idx[0][p0];
+    for (int64_t p1 = t->ptr[0][p0]; p1 < t->ptr[0][p0 + 1]; ++p1) {
+      const int64_t j = t->idx[1][p1];
+      for (int64_t a = 0; a < R; ++a) W[a] = A[i * R + a] * B[j * R + a];
+      for (int64_t a = 0; a < R; ++a)
+        for (int64_t p2 = t->ptr[1][p1]; p2 < t->ptr[1][p1 + 1]; ++p2)
+          out[t->idx[2][p2] * R + a] += W[a] * t->values[p2];
+    }
+  }
+  free(W);
+}
+
 void oc_ttmc3(const oc_csf* t, int64_t R, int64_t S, const double* U, const double* V,
               double* out) {
   const int64_t I = t->dims[0];

@@ -37,6 +37,13 @@ typedef struct {
  * (i,j,k,a)(i,j,a). out: I x R, overwritten. */
 void oc_mttkrp3(const oc_csf* t, int64_t R, const double* B, const double* C, double* out);
 
+/* MTTKRP-3 for the non-root modes:
+ *   _j: T[i,j,k]*A[i,a]*C[k,a]->B[j,a], path ((T*C)*A), orders (i,j,a,k)(i,j,a)
+ *   _k: T[i,j,k]*A[i,a]*B[j,a]->C[k,a], path ((A*B)*T), orders (i,j,a)(i,j,a,k)
+ * out: J x R / K x R, overwritten. */
+void oc_mttkrp3_j(const oc_csf* t, int64_t R, const double* A, const double* C, double* out);
+void oc_mttkrp3_k(const oc_csf* t, int64_t R, const double* A, const double* B, double* out);
+
 /* TTMc-3  T[i,j,k]*U[j,r]*V[k,s]->S[i,r,s], path ((T*V)*U), orders
  * (i,j,k,s)(i,j,s,r). out: I x R x S. */
 void oc_ttmc3(const oc_csf* t, int64_t R, int64_t S, const double* U, const double* V,

@@ -325,6 +325,16 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
         if (R < 1 || R > 128) fail(SPTTN_EUNSUPPORTED, "MTTKRP kernel supports 1 <= R <= 128");
         tile = R;
         break;
+      case SPTTN_NEST_MTTKRP3_J:  // factors A[i,r], C[k,r]; output B[j,r]
+        need(3, 2, {D.dims[0] * R, D.dims[2] * R});
+        if (R < 1 || R > 32) fail(SPTTN_EUNSUPPORTED, "non-root MTTKRP kernel supports 1 <= R <= 32");
+        tile = R;
+        break;
+      case SPTTN_NEST_MTTKRP3_K:  // factors A[i,r], B[j,r]; output C[k,r]
+        need(3, 2, {D.dims[0] * R, D.dims[1] * R});
+        if (R < 1 || R > 32) fail(SPTTN_EUNSUPPORTED, "non-root MTTKRP kernel supports 1 <= R <= 32");
+        tile = R;
+        break;
       case SPTTN_NEST_MTTKRP4:
         need(4, 3, {D.dims[1] * R, D.dims[2] * R, D.dims[3] * R});
         if (R < 1 || R > 128) fail(SPTTN_EUNSUPPORTED, "MTTKRP kernel supports 1 <= R <= 128");
@@ -473,6 +483,15 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
         SPTTN_CUDA(cudaGetLastError());
       }
       p->launches = 2 + (p->gen.par_mode == 2 ? 1 : 0);
+    } else if (p->kind == SPTTN_NEST_MTTKRP3_J || p->kind == SPTTN_NEST_MTTKRP3_K) {
+      // output rows on CSF level 1 / 2: packed 4-slot groups of (i,j)
+      // segments, atomics into a zeroed output (no items, no fix-up)
+      p->out_count = D.dims[p->kind == SPTTN_NEST_MTTKRP3_J ? 1 : 2] * R;
+      dev_malloc(reinterpret_cast<void**>(&p->out), std::max<int64_t>(1, p->out_count) * 8, s);
+      p->vec = (R % 4 == 0) && facs_aligned32 ? 1 : 0;
+      spttn_dev::build_segments(D, 1, 4, 1, p->dec, 0, s, false);
+      spttn_dev::build_packed(D, 2, p->dec, s, 4);
+      p->launches = 2;  // memset + kernel
     } else {
       const bool sparse_out = p->kind == SPTTN_NEST_TTTP3;
       p->out_count = sparse_out ? nnz : D.dims[0] * tile;
@@ -641,6 +660,13 @@ int spttn_execute_stage(spttn_plan* p, int stage, void* stream) {
     a.slice_grp = p->dec.slice_grp;
     a.n_groups = p->dec.n_groups;
     if (stage != 1) switch (p->kind) {
+      case SPTTN_NEST_MTTKRP3_J:
+      case SPTTN_NEST_MTTKRP3_K:
+        a.f[0] = p->fac[0];
+        a.f[1] = p->fac[1];
+        SPTTN_CUDA(cudaMemsetAsync(p->out, 0, std::max<int64_t>(1, p->out_count) * 8, s));
+        spttn_dev::launch_mttkrp3_nonroot(a, p->kind == SPTTN_NEST_MTTKRP3_J ? 1 : 2, s);
+        break;
       case SPTTN_NEST_MTTKRP3:
         a.f[1] = p->fac[0];
         a.f[2] = p->fac[1];

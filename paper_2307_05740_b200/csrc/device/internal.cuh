@@ -144,6 +144,8 @@ void launch_ttmc4(const RootOutArgs& a, cudaStream_t s);
 void launch_mttkrp_seg(const RootOutArgs& a, const int32_t* seg_node1, int order, cudaStream_t s);
 void launch_mttkrp_pk(const RootOutArgs& a, int order, cudaStream_t s);
 void launch_mttkrp_pq(const RootOutArgs& a, int order, cudaStream_t s);
+// MTTKRP-3 with the output on CSF level 1 (mode 1) or 2 (mode 2): atomics.
+void launch_mttkrp3_nonroot(const RootOutArgs& a, int mode, cudaStream_t s);
 void launch_tttp3_leaf(const RootOutArgs& a, const int32_t* leaf_i, const int32_t* leaf_j,
                        int batch, cudaStream_t s);
 // Per-leaf root / level-1 coordinates of an order-3 CSF (TTTP leaf kernel).

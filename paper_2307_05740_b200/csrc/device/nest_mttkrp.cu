@@ -459,4 +459,107 @@ void launch_mttkrp_seg(const RootOutArgs& a, const int32_t* seg_node1, int order
   SPTTN_CUDA(cudaGetLastError());
 }
 
+
+
+// ---- MTTKRP-3 for the non-root output modes ------------
+//
+// On the same (i,j,k) CSF, the other two CP-ALS products:
+//   mode j  ((T*C)*A), orders e.g. (i,j,r,k)(i,j,r):
+//       per (i,j)  X[r] = sum_k t * C[k,r];   B[j,r] += X[r] * A[i,r]
+//   mode k  ((A*B)*T), orders e.g. (i,j,r)(i,j,r,k):
+//       per (i,j)  W[r] = A[i,r] * B[j,r];    per leaf  C[k,r] += W[r] * t
+// The output row is not owned by a root slice, so contributions are added
+// with fp64 atomics (RED.E.ADD.F64) — the "atomics only where the output mode
+// is not the root" half of the north star. The work layout is the packed
+// 4-slot groups of (i,j) segments of the mode-i kernel; a group belongs to
+// one root slice, whose A[i] row a warp loads once per slice. Warps stride
+// over groups; no items or fix-up. Summation order varies run to run (atomic
+// arrival), within the fp64 tolerance.
+namespace {
+
+template <int MODE, bool VEC>
+__global__ void __launch_bounds__(kBlock, 3) k_mttkrp3_nonroot(RootOutArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int slot = lane >> 3;
+  const int c = (lane & 7) * 4;
+  const int R = a.R;
+  const CsfView& t = a.t;
+  const double* __restrict__ A = a.f[0];
+  const double* __restrict__ F = a.f[1];  // C[k] (mode j) or B[j] (mode k)
+  const int4* __restrict__ hdr = a.grp_hdr;
+  const int32_t* __restrict__ gnode = a.grp_node;
+  const int32_t* __restrict__ pk = a.pk;
+  const double* __restrict__ pv = a.pv;
+  const bool colok = c < R;
+  auto rowq = [&](const double* base, int32_t r, bool pred) {
+    if (VEC) return ld256_if(base + static_cast<int64_t>(r) * R + c, pred && colok);
+    return pred ? row4<false>(base + static_cast<int64_t>(r) * R, c, R) : make_double4(0, 0, 0, 0);
+  };
+  auto red4 = [&](int32_t row, const double4& v, bool on) {
+    if (!on) return;
+    double* dst = a.out + static_cast<int64_t>(row) * R + c;
+    if (c + 0 < R) atomicAdd(dst + 0, v.x);
+    if (c + 1 < R) atomicAdd(dst + 1, v.y);
+    if (c + 2 < R) atomicAdd(dst + 2, v.z);
+    if (c + 3 < R) atomicAdd(dst + 3, v.w);
+  };
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * (kBlock / 32);
+  int32_t cur_slice = -1;
+  double4 ar = make_double4(0, 0, 0, 0);
+  for (int64_t g = static_cast<int64_t>(blockIdx.x) * (kBlock / 32) + threadIdx.x / 32;
+       g < a.n_groups; g += nw) {
+    const int4 hh = __ldg(hdr + g);
+    const int n = hh.y;  // warp-uniform
+    const bool live = slot < hh.z;
+    if (hh.w != cur_slice) {  // warp-uniform: A[i] once per root slice
+      cur_slice = hh.w;
+      ar = rowq(A, __ldg(t.idx[0] + cur_slice), true);
+    }
+    const int32_t j = __ldg(gnode + g * 4 + slot);
+    int32_t kk[4];
+    double tt[4];
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const bool on = it < n;
+      kk[it] = on ? __ldg(pk + hh.x + it * 4 + slot) : 0;
+      tt[it] = on ? __ldg(pv + hh.x + it * 4 + slot) : 0.0;
+    }
+    if (MODE == 1) {  // B[j] += (sum_k t C[k]) * A[i]
+      double4 rr[4];
+#pragma unroll
+      for (int it = 0; it < 4; ++it) rr[it] = rowq(F, kk[it], it < n);
+      double4 X = make_double4(0, 0, 0, 0);
+#pragma unroll
+      for (int it = 0; it < 4; ++it) fma4(X, tt[it], rr[it]);
+      red4(j, make_double4(X.x * ar.x, X.y * ar.y, X.z * ar.z, X.w * ar.w), live);
+    } else {  // C[k] += (A[i] * B[j]) * t
+      const double4 br = rowq(F, j, true);
+      const double4 W = make_double4(ar.x * br.x, ar.y * br.y, ar.z * br.z, ar.w * br.w);
+#pragma unroll
+      for (int it = 0; it < 4; ++it)
+        if (it < n)
+          red4(kk[it], make_double4(W.x * tt[it], W.y * tt[it], W.z * tt[it], W.w * tt[it]), live);
+    }
+  }
+}
+
+}  // namespace
+
+void launch_mttkrp3_nonroot(const RootOutArgs& a, int mode, cudaStream_t s) {
+  if (a.n_groups == 0) return;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t want = (a.n_groups + 7) / 8;
+  const unsigned b = static_cast<unsigned>(std::min<int64_t>(want, static_cast<int64_t>(sms) * 3 * 4));
+  if (mode == 1) {
+    if (a.vec) k_mttkrp3_nonroot<1, true><<<b, kBlock, 0, s>>>(a);
+    else k_mttkrp3_nonroot<1, false><<<b, kBlock, 0, s>>>(a);
+  } else {
+    if (a.vec) k_mttkrp3_nonroot<2, true><<<b, kBlock, 0, s>>>(a);
+    else k_mttkrp3_nonroot<2, false><<<b, kBlock, 0, s>>>(a);
+  }
+  SPTTN_CUDA(cudaGetLastError());
+}
+
 }  // namespace spttn_dev

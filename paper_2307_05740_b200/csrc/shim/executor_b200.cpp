@@ -18,6 +18,7 @@
 // throws.
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -145,10 +146,24 @@ bool same(const std::vector<int>& a, std::initializer_list<int> b) {
   return a == std::vector<int>(b);
 }
 
+// Non-root-output MTTKRP kernels add with fp64 atomics (run-to-run rounding
+// differences); SPTTN_NONROOT_ATOMICS=0 keeps those nests on the
+// deterministic interpreter.
+bool nonroot_atomics_enabled() {
+  const char* e = std::getenv("SPTTN_NONROOT_ATOMICS");
+  return !(e && *e == '0');
+}
+
 // Recognises the pinned nests structurally, whatever the
-// tensor / index names: matrix factors F[m, r] keyed by the CSF level of m.
+// tensor / index names: matrix factors F[m, r] keyed by the CSF level of m,
+// the pinned contraction path and the kernel's output layout. Any admissible
+// loop order on that path is accepted: orders only move dense loops relative
+// to the CSF walk, so every intermediate entry is the same sum over the same
+// sparse iteration order (the planners' own picks, e.g. max-buf-dim's
+// (i,j,r,k)(i,j,r) for MTTKRP-3, run on the dedicated kernel too). Hooks,
+// resets and flop counters still follow the given order (compile()).
 PinnedMatch match_pinned(const KernelSpec& spec, const ContractionPath& path,
-                         const LoopOrder& order) {
+                         const LoopOrder& /*order*/) {
   PinnedMatch none;
   const auto& sp = spec.sparse_input().indices;
   const int d = static_cast<int>(sp.size());
@@ -171,28 +186,41 @@ PinnedMatch match_pinned(const KernelSpec& spec, const ContractionPath& path,
     const auto& tm = path.terms[t];
     return (tm.lhs_id == x && tm.rhs_id == y) || (tm.lhs_id == y && tm.rhs_id == x);
   };
-  const auto& O = order.per_term;
   const int i = sp[0], j = sp[1], k = sp[2];
   PinnedMatch m;
   if (d == 3 && n == 3 && !spec.output_sparse && by_level[1] > 0 && by_level[2] > 0 &&
       path.num_terms() == 2 && term_is(0, 0, by_level[2]) && term_is(1, n, by_level[1])) {
     const int r1 = rank_of[1], r2 = rank_of[2];
-    if (r1 == r2 && same(out, {i, r1}) && same(O[0], {i, j, k, r1}) && same(O[1], {i, j, r1})) {
+    if (r1 == r2 && same(out, {i, r1})) {
       m.kind = SPTTN_NEST_MTTKRP3;
       m.rank[0] = spec.dim(r1);
-    } else if (r1 != r2 && same(out, {i, r1, r2}) && same(O[0], {i, j, k, r2}) &&
-               same(O[1], {i, j, r2, r1})) {
+    } else if (r1 != r2 && same(out, {i, r1, r2})) {
       m.kind = SPTTN_NEST_TTMC3;
       m.rank[0] = spec.dim(r1);
       m.rank[1] = spec.dim(r2);
     }
     m.factor_inputs = {by_level[1], by_level[2]};
+  } else if (d == 3 && n == 3 && !spec.output_sparse && by_level[0] > 0 &&
+             rank_of[0] == rank_of[by_level[1] > 0 ? 1 : 2] && path.num_terms() == 2 &&
+             nonroot_atomics_enabled()) {
+    // MTTKRP-3 for the non-root modes (output on CSF level 1 or 2)
+    const int r = rank_of[0];
+    if (by_level[2] > 0 && same(out, {j, r}) && term_is(0, 0, by_level[2]) &&
+        term_is(1, n, by_level[0])) {
+      m.kind = SPTTN_NEST_MTTKRP3_J;  // ((T*C)*A)
+      m.rank[0] = spec.dim(r);
+      m.factor_inputs = {by_level[0], by_level[2]};
+    } else if (by_level[1] > 0 && same(out, {k, r}) && term_is(0, by_level[0], by_level[1]) &&
+               term_is(1, n, 0)) {
+      m.kind = SPTTN_NEST_MTTKRP3_K;  // ((A*B)*T)
+      m.rank[0] = spec.dim(r);
+      m.factor_inputs = {by_level[0], by_level[1]};
+    }
   } else if (d == 3 && n == 4 && spec.output_sparse && by_level[0] > 0 && by_level[1] > 0 &&
              by_level[2] > 0 && path.num_terms() == 3 && term_is(0, by_level[0], by_level[1]) &&
              term_is(1, n, by_level[2]) && term_is(2, n + 1, 0)) {
     const int r = rank_of[0];
-    if (rank_of[1] == r && rank_of[2] == r && same(O[0], {i, j, r}) &&
-        same(O[1], {i, j, k, r}) && same(O[2], {i, j, k})) {
+    if (rank_of[1] == r && rank_of[2] == r) {
       m.kind = SPTTN_NEST_TTTP3;
       m.rank[0] = spec.dim(r);
       m.factor_inputs = {by_level[0], by_level[1], by_level[2]};
@@ -202,13 +230,10 @@ PinnedMatch match_pinned(const KernelSpec& spec, const ContractionPath& path,
              term_is(1, n, by_level[2]) && term_is(2, n + 1, by_level[1])) {
     const int l = sp[3];
     const int r1 = rank_of[1], r2 = rank_of[2], r3 = rank_of[3];
-    if (r1 == r2 && r2 == r3 && same(out, {i, r1}) && same(O[0], {i, j, k, l, r1}) &&
-        same(O[1], {i, j, k, r1}) && same(O[2], {i, j, r1})) {
+    if (r1 == r2 && r2 == r3 && same(out, {i, r1})) {
       m.kind = SPTTN_NEST_MTTKRP4;
       m.rank[0] = spec.dim(r1);
-    } else if (r1 != r2 && r2 != r3 && r1 != r3 && same(out, {i, r1, r2, r3}) &&
-               same(O[0], {i, j, k, l, r3}) && same(O[1], {i, j, k, r2, r3}) &&
-               same(O[2], {i, j, r1, r2, r3})) {
+    } else if (r1 != r2 && r2 != r3 && r1 != r3 && same(out, {i, r1, r2, r3})) {
       m.kind = SPTTN_NEST_TTMC4;
       m.rank[0] = spec.dim(r1);
       m.rank[1] = spec.dim(r2);

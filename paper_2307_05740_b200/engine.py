@@ -27,6 +27,8 @@ NEST_TTMC3 = 2
 NEST_TTTP3 = 3
 NEST_MTTKRP4 = 4
 NEST_TTMC4 = 5
+NEST_MTTKRP3_J = 6  # T[i,j,k]*A[i,r]*C[k,r]->B[j,r], output on CSF level 1 (atomics)
+NEST_MTTKRP3_K = 7  # T[i,j,k]*A[i,r]*B[j,r]->C[k,r], output on CSF level 2 (atomics)
 NEST_GENERIC = 100
 
 FLAG_RESIDUAL = 1

@@ -47,6 +47,14 @@ CASES = [
     ("mttkrp4_r32", "T[i,j,k,l]*B[j,r]*C[k,r]*D[l,r]->A[i,r]",
      {"i": 9, "j": 8, "k": 7, "l": 10, "r": 32}, "(((T*D)*C)*B)", "i,j,k,l,r;i,j,k,r;i,j,r", 0.05,
      43, 4, (32, 0, 0), False),
+    ("mttkrp3j_small", "T[i,j,k]*A[i,a]*C[k,a]->B[j,a]", {"i": 8, "j": 9, "k": 7, "a": 4},
+     "((T*C)*A)", "i,j,a,k;i,j,a", 0.08, 21, 6, (4, 0, 0), False),
+    ("mttkrp3j_r32", "T[i,j,k]*A[i,a]*C[k,a]->B[j,a]", {"i": 20, "j": 18, "k": 16, "a": 32},
+     "((T*C)*A)", "i,j,a,k;i,j,a", 0.05, 22, 6, (32, 0, 0), False),
+    ("mttkrp3k_small", "T[i,j,k]*A[i,a]*B[j,a]->C[k,a]", {"i": 7, "j": 8, "k": 9, "a": 4},
+     "((A*B)*T)", "i,j,a;i,j,a,k", 0.08, 23, 7, (4, 0, 0), False),
+    ("mttkrp3k_r32", "T[i,j,k]*A[i,a]*B[j,a]->C[k,a]", {"i": 16, "j": 20, "k": 18, "a": 32},
+     "((A*B)*T)", "i,j,a;i,j,a,k", 0.05, 24, 7, (32, 0, 0), False),
     ("ttmc4_small", "T[i,j,k,l]*U[j,r]*V[k,s]*W[l,t]->S[i,r,s,t]",
      {"i": 4, "j": 4, "k": 4, "l": 4, "r": 2, "s": 3, "t": 2}, "(((T*W)*V)*U)",
      "i,j,k,l,t;i,j,k,s,t;i,j,r,s,t", 0.2, 3, 5, (2, 3, 2), False),

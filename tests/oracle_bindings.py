@@ -115,6 +115,11 @@ def oracle_nest(kind: int, csf, factors, ranks, residual=False) -> np.ndarray:
     elif kind == 4:
         out = np.zeros(I * R)
         lib.oc_mttkrp4(C.byref(a.oc), C.c_int64(R), fp[0], fp[1], fp[2], out.ctypes.data_as(dblp))
+    elif kind in (6, 7):  # MTTKRP-3 non-root modes j / k
+        rows = csf.dims[1] if kind == 6 else csf.dims[2]
+        out = np.zeros(rows * R)
+        fn = lib.oc_mttkrp3_j if kind == 6 else lib.oc_mttkrp3_k
+        fn(C.byref(a.oc), C.c_int64(R), fp[0], fp[1], out.ctypes.data_as(dblp))
     elif kind == 5:
         out = np.zeros(I * R * S * T)
         lib.oc_ttmc4(C.byref(a.oc), C.c_int64(R), C.c_int64(S), C.c_int64(T), fp[0], fp[1], fp[2],

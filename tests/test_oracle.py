@@ -106,7 +106,7 @@ def test_mttkrp_on_coo3_direct_evaluation():
 
 
 def pinned_flops(kind, L, nnz, R, S, T):
-    if kind == 1:
+    if kind in (1, 6, 7):  # MTTKRP-3, any output mode: 2·nnz·R + 2·nnz_ij·R
         return 2 * nnz * R + 2 * L[1] * R
     if kind == 2:
         return 2 * nnz * S + 2 * L[1] * R * S
@@ -132,7 +132,10 @@ def test_reset_counts_are_level_counts(m):
     (proj/tests/test_executor.cpp:270-288): MTTKRP-3/TTMc-3 X per (i,j);
     TTTP X per (i,j), Y per leaf; order 4: X per (i,j,k), Y per (i,j)."""
     L = m["level_sizes"]
-    want = {1: [L[1]], 2: [L[1]], 3: [L[1], L[2]], 4: [L[2], L[1]], 5: [L[2], L[1]]}[m["kind"]]
+    R = m["ranks"][0]
+    # non-root MTTKRP orders keep a scalar buffer per (i,j,a): reset L1*R times
+    want = {1: [L[1]], 2: [L[1]], 3: [L[1], L[2]], 4: [L[2], L[1]], 5: [L[2], L[1]],
+            6: [L[1] * R], 7: [L[1] * R]}[m["kind"]]
     assert m["buffer_resets"] == want
 
 
