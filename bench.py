@@ -45,7 +45,7 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 HEADLINE = "ttmc3"
-ORDER = ["mttkrp3", "ttmc3", "tttp3", "mttkrp4", "ttmc4"]
+ORDER = ["mttkrp3", "ttmc3", "tttp3", "mttkrp4", "ttmc4", "mttkrp3_j", "mttkrp3_k"]
 L2_FLUSH_BYTES = 256 << 20
 
 
@@ -226,7 +226,8 @@ def e2e_config(P, w, steps, stream):
 def ref_args(w):
     c = w.cfg
     dims = dict(zip(c.mode_names, w.dims))
-    rank_names = {1: ["r"], 2: ["r", "s"], 3: ["r"], 4: ["r"], 5: ["r", "s", "t"]}[c.kind]
+    rank_names = {1: ["r"], 2: ["r", "s"], 3: ["r"], 4: ["r"], 5: ["r", "s", "t"], 6: ["r"],
+                  7: ["r"]}[c.kind]
     for n, r in zip(rank_names, c.ranks):
         dims[n] = r
     return c.kernel, dims, c.path, c.order_text
@@ -335,6 +336,8 @@ def main():
     head_clocks = None
     for key in keys:
         strong = args.shard and world > 1
+        if strong and key.startswith("mttkrp3_"):
+            continue  # non-root outputs: root-slice shards would need an output all-reduce
         w = make_workload(key, seed_offset=0 if strong else rank)
         job_nnz = w.csf.nnz if strong else w.csf.nnz * world
         if strong:  # this rank's nnz-balanced root range (no data-path collective)

@@ -52,6 +52,14 @@ CONFIGS = {
                       "(((T*D)*C)*B)", "i,j,k,l,r;i,j,k,r;i,j,r", ("i", "j", "k", "l"),
                       (5000, 5000, 5000, 5000), 20_000_000, 1.1, (32, 0, 0), ("B", "C", "D"),
                       (1, 2, 3), (0, 0, 0), 1.0),
+    # §8f-2: MTTKRP-3 for the non-root modes on the mttkrp3 tensor (same seed),
+    # the planners' (max-buf-dim) orders; not BASELINE configs
+    "mttkrp3_j": Config("mttkrp3_j", 1, E.NEST_MTTKRP3_J, "T[i,j,k]*A[i,r]*C[k,r]->B[j,r]",
+                        "((T*C)*A)", "i,j,r,k;i,j,r", ("i", "j", "k"), (1000, 1000, 1000),
+                        1_000_000, 0.0, (32, 0, 0), ("A", "C"), (0, 2), (0, 0), 1.0),
+    "mttkrp3_k": Config("mttkrp3_k", 1, E.NEST_MTTKRP3_K, "T[i,j,k]*A[i,r]*B[j,r]->C[k,r]",
+                        "((A*B)*T)", "i,j,r;i,j,r,k", ("i", "j", "k"), (1000, 1000, 1000),
+                        1_000_000, 0.0, (32, 0, 0), ("A", "B"), (0, 1), (0, 0), 1.0),
     "ttmc4": Config("ttmc4", 5, E.NEST_TTMC4, "T[i,j,k,l]*U[j,r]*V[k,s]*W[l,t]->Y[i,r,s,t]",
                     "(((T*W)*V)*U)", "i,j,k,l,t;i,j,k,s,t;i,j,r,s,t", ("i", "j", "k", "l"),
                     (2000, 2000, 2000, 2000), 10_000_000, 0.0, (8, 8, 8), ("U", "V", "W"),
@@ -73,6 +81,8 @@ class Workload:
         if c.kind == E.NEST_TTTP3:
             return self.csf.nnz
         R, S, T = c.ranks
+        if c.kind in (E.NEST_MTTKRP3_J, E.NEST_MTTKRP3_K):  # output rows on level 1 / 2
+            return self.dims[1 if c.kind == E.NEST_MTTKRP3_J else 2] * R
         return self.dims[0] * R * max(S, 1) * max(T, 1)
 
 
@@ -115,7 +125,7 @@ def algorithmic_flops(w: Workload) -> int:
     L = csf.level_sizes()
     R, S, T = w.cfg.ranks
     k = w.cfg.kind
-    if k == E.NEST_MTTKRP3:
+    if k in (E.NEST_MTTKRP3, E.NEST_MTTKRP3_J, E.NEST_MTTKRP3_K):
         return 2 * csf.nnz * R + 2 * L[1] * R
     if k == E.NEST_TTMC3:
         return 2 * csf.nnz * S + 2 * L[1] * R * S
@@ -137,6 +147,10 @@ def gather_bytes(w: Workload) -> int:
     k = w.cfg.kind
     if k == E.NEST_MTTKRP3:
         return 8 * R * (csf.nnz + L[1])
+    if k == E.NEST_MTTKRP3_J:  # C row per leaf, A row per slice, B row atomics per (i,j)
+        return 8 * R * (csf.nnz + L[0] + L[1])
+    if k == E.NEST_MTTKRP3_K:  # A row per slice, B row per (i,j), C row atomics per leaf
+        return 8 * R * (L[0] + L[1] + csf.nnz)
     if k == E.NEST_TTMC3:
         return 8 * (S * csf.nnz + R * L[1])
     if k == E.NEST_TTTP3:
