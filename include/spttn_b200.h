@@ -161,6 +161,11 @@ int spttn_unfactorized(const spttn_unfact_desc* desc, spttn_csf* csf, double* ho
 /* [0] SM count, [1] compute capability major*10+minor, [2] L2 bytes,
  * [3] max shared memory per block (opt-in). */
 int spttn_device_info(int64_t* out, int n);
+/* Creates the CUDA context and the engine's memory pool up front (the C++
+ * drop-in calls it when it is loaded, so the first prepare() does not pay for
+ * context creation; SPTTN_LAZY_INIT=1 skips that). SPTTN_ECUDA without a
+ * device. */
+int spttn_init(void);
 /* Build identification string (arch, nvcc version). */
 const char* spttn_build_info(void);
 /* Device memory of CSF layouts and plans comes from a per-device

@@ -69,7 +69,7 @@ ENGINE_SYMBOLS = [
     "spttn_plan_set_factors", "spttn_execute", "spttn_execute_stage", "spttn_output_count", "spttn_output_device",
     "spttn_read_output", "spttn_plan_info", "spttn_generic_resets", "spttn_generic_log_bytes",
     "spttn_generic_read_log", "spttn_unfactorized", "spttn_device_info", "spttn_build_info",
-    "spttn_release_cached",
+    "spttn_release_cached", "spttn_init",
 ]
 
 _engine = None

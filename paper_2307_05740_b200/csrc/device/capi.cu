@@ -154,6 +154,21 @@ const char* spttn_build_info(void) {
   return "spttn_b200 sm_100a nvcc " SPTTN_STR(__CUDACC_VER_MAJOR__) "." SPTTN_STR(__CUDACC_VER_MINOR__);
 }
 
+int spttn_init(void) {
+  return guarded([] {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+      cudaGetLastError();
+      fail(SPTTN_ECUDA, "no CUDA device");
+    }
+    SPTTN_CUDA(cudaFree(nullptr));  // creates the primary context
+    void* p = nullptr;              // and the engine's memory pool
+    spttn_dev::dmalloc_raw(&p, 256, nullptr);
+    spttn_dev::dfree(p, nullptr);
+    SPTTN_CUDA(cudaStreamSynchronize(nullptr));
+  });
+}
+
 int spttn_device_info(int64_t* out, int n) {
   return guarded([&] {
     int dev = 0;
