@@ -18,6 +18,7 @@
 // throws.
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -275,41 +276,53 @@ std::shared_ptr<DeviceCsfHandle> upload_csf_uncached(const CsfTensor& csf);
 // (FNV-1a over every array), so a tensor mutated between plans is re-uploaded;
 // only tensors up to 1M leaves are fingerprinted (larger ones re-upload).
 uint64_t fingerprint(const CsfTensor& csf) {
-  uint64_t h = 1469598103934665603ull;
-  auto mix = [&](const void* p, size_t n) {
-    const unsigned char* c = static_cast<const unsigned char*>(p);
-    for (size_t i = 0; i < n; ++i) {
-      h ^= c[i];
-      h *= 1099511628211ull;
+  // 64-bit words (every array is int64 / fp64): multiply-xorshift mixing
+  uint64_t h = 0x9E3779B97F4A7C15ull;
+  auto mix = [&](const void* p, size_t words) {
+    const uint64_t* w = static_cast<const uint64_t*>(p);
+    for (size_t i = 0; i < words; ++i) {
+      h = (h ^ w[i]) * 0xBF58476D1CE4E5B9ull;
+      h ^= h >> 31;
     }
   };
-  for (const auto& m : csf.modes) mix(&m.dim, sizeof(m.dim));
-  for (const auto& v : csf.idx) mix(v.data(), v.size() * sizeof(int64_t));
-  for (const auto& v : csf.ptr) mix(v.data(), v.size() * sizeof(int64_t));
-  mix(csf.values.data(), csf.values.size() * sizeof(double));
+  for (const auto& m : csf.modes) mix(&m.dim, 1);
+  for (const auto& v : csf.idx) mix(v.data(), v.size());
+  for (const auto& v : csf.ptr) mix(v.data(), v.size());
+  mix(csf.values.data(), csf.values.size());
   return h;
 }
 
+// Device CSFs of small tensors are cached by (tensor address, content
+// fingerprint) so re-planning the same tensor (every order of a study, every
+// sweep of a solver) does not re-upload it; the most recent kCsfKeep stay
+// resident after their plans are gone.
 std::shared_ptr<DeviceCsfHandle> upload_csf(const CsfTensor& csf) {
   constexpr int64_t kCacheMaxNnz = int64_t{1} << 20;
+  constexpr size_t kCsfKeep = 4;
   if (csf.nnz() > kCacheMaxNnz) return upload_csf_uncached(csf);
   struct Entry {
     const CsfTensor* key;
     uint64_t fp;
-    std::weak_ptr<DeviceCsfHandle> dev;
+    std::shared_ptr<DeviceCsfHandle> dev;
   };
   static std::mutex mu;
-  static std::vector<Entry> cache;
+  // most recent last; intentionally leaked: no device frees at process exit
+  static std::vector<Entry>& cache = *new std::vector<Entry>;
   const uint64_t fp = fingerprint(csf);
   std::lock_guard<std::mutex> lock(mu);
-  for (auto& e : cache)
-    if (e.key == &csf && e.fp == fp)
-      if (auto d = e.dev.lock()) return d;
+  for (size_t e = 0; e < cache.size(); ++e)
+    if (cache[e].key == &csf && cache[e].fp == fp) {
+      Entry hit = cache[e];
+      cache.erase(cache.begin() + static_cast<std::ptrdiff_t>(e));
+      cache.push_back(hit);
+      return hit.dev;
+    }
   auto d = upload_csf_uncached(csf);
   cache.erase(std::remove_if(cache.begin(), cache.end(),
-                             [&](const Entry& e) { return e.key == &csf || e.dev.expired(); }),
+                             [&](const Entry& e) { return e.key == &csf; }),
               cache.end());
   cache.push_back(Entry{&csf, fp, d});
+  if (cache.size() > kCsfKeep) cache.erase(cache.begin());
   return d;
 }
 
@@ -659,6 +672,33 @@ void run_observer(ExecPlanImpl& P) {
 
 }  // namespace
 
+namespace {
+// Development aid (SPTTN_SHIM_TRACE=1): per-phase wall time of prepare /
+// execute, printed at exit.
+struct ShimTrace {
+  bool on = false;
+  double t[8] = {0};
+  int64_t n[8] = {0};
+  ShimTrace() {
+    const char* e = std::getenv("SPTTN_SHIM_TRACE");
+    on = e && *e == '1';
+  }
+  ~ShimTrace() {
+    if (!on) return;
+    static const char* names[8] = {"host compile", "csf upload/cache", "plan create",
+                                   "set factors", "execute launch", "read output", "", ""};
+    for (int k = 0; k < 6; ++k)
+      if (n[k]) std::fprintf(stderr, "[shim] %-18s %8.1f us mean over %lld\n", names[k],
+                             1e6 * t[k] / n[k], static_cast<long long>(n[k]));
+  }
+  void add(int k, Clock::time_point a) {
+    if (!on) return;
+    t[k] += std::chrono::duration<double>(Clock::now() - a).count();
+    ++n[k];
+  }
+} g_trace;
+}  // namespace
+
 ExecPlan prepare(const KernelSpec& spec, const ContractionPath& path, const LoopOrder& order,
                  const ExecInputs& inputs, const ExecOptions& opts) {
   validate_inputs(spec, inputs);
@@ -673,11 +713,16 @@ ExecPlan prepare(const KernelSpec& spec, const ContractionPath& path, const Loop
   P.order = order;
   P.inputs = inputs;
   P.opts = opts;
+  auto tc = Clock::now();
   P.forest = build_forest(spec, path, order);
   compile(P);
   P.flops = forest_flops(spec, path, P.forest, *inputs.sparse);
+  g_trace.add(0, tc);
 
+  tc = Clock::now();
   P.csf = upload_csf(*inputs.sparse);
+  g_trace.add(1, tc);
+  tc = Clock::now();
   spttn_plan_desc desc{};
   desc.buffer_limit_bytes = opts.buffer_limit_bytes;
   P.pinned = match_pinned(spec, path, order);
@@ -711,6 +756,7 @@ ExecPlan prepare(const KernelSpec& spec, const ContractionPath& path, const Loop
     desc.program_bytes = sizeof(spg_program);
     check(spttn_plan_create(&desc, P.csf->h, nullptr, &P.plan), "prepare");
   }
+  g_trace.add(2, tc);
   ExecPlan plan;
   plan.impl = std::move(impl);
   return plan;
@@ -723,12 +769,18 @@ ExecResult execute(ExecPlan& plan) {
   // (executor.cpp:373-387): refresh the device copies.
   std::vector<const double*> f(P.factor_inputs.size());
   for (size_t k = 0; k < f.size(); ++k) f[k] = P.inputs.dense[P.factor_inputs[k] - 1]->values.data();
+  auto tc = Clock::now();
   check(spttn_plan_set_factors(P.plan, f.data(), 0, nullptr), "execute");
+  g_trace.add(3, tc);
+  tc = Clock::now();
   check(spttn_execute(P.plan, nullptr), "execute");
+  g_trace.add(4, tc);
+  tc = Clock::now();
   ExecResult res;
   const int64_t count = spttn_output_count(P.plan);
   std::vector<double> out(static_cast<size_t>(count));
   check(spttn_read_output(P.plan, out.data(), count, nullptr), "execute");
+  g_trace.add(5, tc);
   res.stats.buffer_resets = P.reset_count;
   res.stats.multiply_adds = P.flops;
   if (P.pinned.kind == 0) {
