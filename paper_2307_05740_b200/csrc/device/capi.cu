@@ -45,6 +45,7 @@ struct spttn_plan {
   int64_t last_madds = -1;
   void* arena = nullptr;                // GENERIC: one allocation for all plan state
   std::vector<int64_t> last_counters;   // GENERIC: madds, resets, log cursor, overflow
+  alignas(64) unsigned char tmap[2][128];  // TTMc-3 mode 11: U / V gather4 tensor maps
 };
 
 namespace {
@@ -529,6 +530,8 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
           // 10 = packed, TMA-staged, row-contiguous gathers (default);
           // 0-7 = earlier variants kept for A/B measurements (tools/sweep.py)
           p->mode = static_cast<int>(env_int("SPTTN_TTMC3_MODE", 10));
+          if (p->mode == 11 && !spttn_dev::ttmc3_tma_supported(static_cast<int>(R), static_cast<int>(S)))
+            p->mode = 10;
           seg_len = std::clamp(seg_len, 1, p->mode == 0 ? 8 : 4);
         }
         seg_len = std::max(seg_len, 1);
@@ -554,7 +557,7 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
           if (gchunk <= 0)
             gchunk = std::clamp<int64_t>((p->dec.n_groups + w16 - 1) / w16, 4, 1024);
           spttn_dev::finish_unit_items(D, p->dec, p->dec.slice_grp, p->dec.n_groups, gchunk, tile, s);
-        } else if (p->kind == SPTTN_NEST_TTMC3 && (p->mode == 6 || p->mode == 7 || p->mode == 10)) {
+        } else if (p->kind == SPTTN_NEST_TTMC3 && (p->mode == 6 || p->mode == 7 || p->mode == 10 || p->mode == 11)) {
           // packed length-sorted groups of 8 segments (pack.cu)
           spttn_dev::build_segments(D, 1, seg_len, chunk, p->dec, tile, s, false);
           spttn_dev::build_packed(D, 2, p->dec, s);
@@ -719,7 +722,13 @@ int spttn_execute_stage(spttn_plan* p, int stage, void* stream) {
       case SPTTN_NEST_TTMC3:
         a.f[1] = p->fac[0];
         a.f[2] = p->fac[1];
-        spttn_dev::launch_ttmc3(a, s);
+        if (p->mode == 11) {  // tensor maps follow the current factor pointers
+          spttn_dev::make_row_map(p->tmap[0], p->fac[0], p->fac_size[0] / 16);
+          spttn_dev::make_row_map(p->tmap[1], p->fac[1], p->fac_size[1] / 16);
+          spttn_dev::launch_ttmc3_tma(a, p->tmap[0], p->tmap[1], s);
+        } else {
+          spttn_dev::launch_ttmc3(a, s);
+        }
         break;
       case SPTTN_NEST_TTMC4:
         a.f[1] = p->fac[0];

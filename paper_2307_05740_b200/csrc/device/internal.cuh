@@ -139,6 +139,10 @@ void launch_mttkrp4(const RootOutArgs& a, cudaStream_t s);
 void launch_tttp3(const RootOutArgs& a, cudaStream_t s);
 void launch_ttmc3(const RootOutArgs& a, cudaStream_t s);
 void launch_ttmc4(const RootOutArgs& a, cudaStream_t s);
+// TTMc-3 with TMA gather4 row loads (nest_ttmc3_tma.cu): needs R = S = 16.
+bool ttmc3_tma_supported(int R, int S);
+void make_row_map(void* map128, const double* base, int64_t rows);
+void launch_ttmc3_tma(const RootOutArgs& a, const void* mapU, const void* mapV, cudaStream_t s);
 // Segment-form MTTKRP (R <= 32): order 3 units = level-1 fibers, order 4 =
 // level-2 fibers (seg_node1 carries the level-1 coordinate).
 void launch_mttkrp_seg(const RootOutArgs& a, const int32_t* seg_node1, int order, cudaStream_t s);
