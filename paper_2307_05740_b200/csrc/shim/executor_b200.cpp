@@ -813,6 +813,55 @@ int spttn_b200_plan_device_kind(const spttn::ExecPlan& plan) {
   return plan.impl->pinned.kind != 0 ? plan.impl->pinned.kind : SPTTN_NEST_GENERIC;
 }
 
+spttn::CsfTensor spttn_b200_build_csf(const spttn::CooTensor& coo,
+                                      const std::vector<std::string>& mode_order) {
+  const int d = static_cast<int>(coo.order());
+  if (static_cast<int>(mode_order.size()) != d)
+    throw std::invalid_argument("mode_order size does not match tensor order");
+  std::vector<int> perm(d, -1);
+  std::vector<bool> used(d, false);
+  for (int l = 0; l < d; ++l) {
+    for (int s = 0; s < d; ++s)
+      if (coo.indices[s].name == mode_order[l]) perm[l] = s;
+    if (perm[l] == -1 || used[perm[l]])
+      throw std::invalid_argument("mode_order is not a permutation of tensor indices: " +
+                                  mode_order[l]);
+    used[perm[l]] = true;
+  }
+  const int64_t nnz = static_cast<int64_t>(coo.entries.size());
+  std::vector<int64_t> dims(d), coords(static_cast<size_t>(nnz * d));
+  std::vector<double> vals(static_cast<size_t>(nnz));
+  for (int l = 0; l < d; ++l) dims[l] = coo.indices[perm[l]].dim;
+  for (int64_t e = 0; e < nnz; ++e) {
+    for (int l = 0; l < d; ++l) coords[e * d + l] = coo.entries[e].first[perm[l]];
+    vals[e] = coo.entries[e].second;
+  }
+  spttn_csf* h = nullptr;
+  const int rc = spttn_csf_from_coo(d, dims.data(), nnz, coords.data(), vals.data(), nullptr, &h);
+  if (rc == SPTTN_EINVAL)
+    throw std::invalid_argument(std::string("build_csf: ") + spttn_last_error());
+  spttn::check(rc, "build_csf");
+  spttn::CsfTensor csf;
+  csf.modes.resize(d);
+  for (int l = 0; l < d; ++l) csf.modes[l] = coo.indices[perm[l]];
+  csf.idx.resize(d);
+  csf.ptr.resize(d > 0 ? d - 1 : 0);
+  std::vector<int64_t*> ip(d), pp(std::max(1, d - 1), nullptr);
+  for (int l = 0; l < d; ++l) {
+    csf.idx[l].resize(static_cast<size_t>(spttn_csf_level_size(h, l)));
+    ip[l] = csf.idx[l].data();
+    if (l + 1 < d) {
+      csf.ptr[l].resize(static_cast<size_t>(spttn_csf_level_size(h, l) + 1));
+      pp[l] = csf.ptr[l].data();
+    }
+  }
+  csf.values.resize(static_cast<size_t>(d > 0 ? spttn_csf_level_size(h, d - 1) : 0));
+  const int rc2 = spttn_csf_download(h, ip.data(), pp.data(), csf.values.data(), nullptr);
+  spttn_csf_destroy(h);
+  spttn::check(rc2, "build_csf");
+  return csf;
+}
+
 namespace spttn {
 
 ExecResult execute_unfactorized(const KernelSpec& spec, const ExecInputs& inputs) {

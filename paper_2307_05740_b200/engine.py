@@ -94,6 +94,52 @@ class DeviceCsf:
         self.handle = h
         self._keep = None
 
+    @classmethod
+    def from_coo(cls, dims, coords: np.ndarray, values: np.ndarray, stream=None) -> "DeviceCsf":
+        """spttn_csf_from_coo: normalize + build_csf on the GPU (rows in CSF
+        mode order, nnz x order int64); the host Csf is not materialised."""
+        lib = N.engine()
+        coords = np.ascontiguousarray(coords, np.int64).reshape(-1, len(dims))
+        values = np.ascontiguousarray(values, np.float64)
+        if coords.shape[0] != values.shape[0]:
+            raise ValueError("coords / values length mismatch")
+        dd = (C.c_int64 * len(dims))(*dims)
+        h = C.c_void_p()
+        _check(lib.spttn_csf_from_coo(len(dims), dd, int(values.shape[0]),
+                                      coords.ctypes.data_as(N.c_i64_p),
+                                      values.ctypes.data_as(N.c_dbl_p), _stream_ptr(stream),
+                                      C.byref(h)))
+        self = cls.__new__(cls)
+        self.csf = None
+        self.handle = h
+        self._keep = None
+        return self
+
+    def level_sizes(self):
+        lib = N.engine()
+        sizes = []
+        for l in range(8):
+            n = int(lib.spttn_csf_level_size(self.handle, l))
+            if n < 0:
+                break
+            sizes.append(n)
+        return sizes
+
+    def download(self, stream=None) -> Csf:
+        """spttn_csf_download: the reference's int64 CSF arrays back on the host."""
+        lib = N.engine()
+        sizes = self.level_sizes()
+        d = len(sizes)
+        dims = [int(lib.spttn_csf_dim(self.handle, l)) for l in range(d)]
+        idx = [np.empty(n, np.int64) for n in sizes]
+        ptr = [np.empty(sizes[l] + 1, np.int64) for l in range(d - 1)]
+        vals = np.empty(sizes[-1] if sizes else 0, np.float64)
+        ip = (N.c_i64_p * d)(*[a.ctypes.data_as(N.c_i64_p) for a in idx])
+        pp = (N.c_i64_p * max(1, d - 1))(*[a.ctypes.data_as(N.c_i64_p) for a in ptr])
+        _check(lib.spttn_csf_download(self.handle, ip, pp, vals.ctypes.data_as(N.c_dbl_p),
+                                      _stream_ptr(stream)))
+        return Csf(dims, idx, ptr, vals)
+
     def device_bytes(self) -> int:
         return int(N.engine().spttn_csf_device_bytes(self.handle))
 

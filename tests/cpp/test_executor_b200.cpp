@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstring>
 #include <functional>
+#include <set>
 #include <string>
 
 #include "fixtures.hpp"
@@ -345,6 +346,37 @@ int main() {
         ++n;
       }
     CHECK(n > 0);
+  });
+
+  run_case("device build_csf equals the reference build_csf (any mode order)", [] {
+    CooTensor coo;
+    coo.indices = {{"i", 23}, {"j", 17}, {"k", 29}};
+    uint64_t x = 88172645463325252ull;
+    auto next = [&](int64_t m) {
+      x ^= x << 13; x ^= x >> 7; x ^= x << 17;
+      return static_cast<int64_t>(x % static_cast<uint64_t>(m));
+    };
+    std::set<std::vector<int64_t>> seen;  // distinct rows, then duplicate PAIRS only:
+    while (coo.entries.size() < 2500) {   // (a+b == b+a; the order std::sort gives 3+
+      std::vector<int64_t> c{next(23), next(17), next(29)};  // duplicates is unspecified)
+      if (seen.insert(c).second) coo.entries.push_back({c, (next(2000) - 1000) / 997.0});
+    }
+    for (int e = 0; e < 300; ++e)
+      coo.entries.push_back({coo.entries[e].first, (next(2000) - 1000) / 991.0});
+    for (const auto& order : std::vector<std::vector<std::string>>{{"i", "j", "k"}, {"k", "i", "j"}}) {
+      CooTensor norm = coo;
+      norm.normalize();
+      CsfTensor want = build_csf(norm, order);
+      CsfTensor got = spttn_b200_build_csf(coo, order);
+      CHECK(got.idx == want.idx);
+      CHECK(got.ptr == want.ptr);
+      CHECK(got.values == want.values);
+      CHECK(got.modes.size() == want.modes.size() && got.modes[0].name == want.modes[0].name);
+    }
+    CooTensor bad = coo;
+    bad.entries.push_back({{23, 0, 0}, 1.0});
+    CHECK(throws_as<std::invalid_argument>([&] { spttn_b200_build_csf(bad, {"i", "j", "k"}); }));
+    CHECK(throws_as<std::invalid_argument>([&] { spttn_b200_build_csf(coo, {"i", "j", "j"}); }));
   });
 
   run_case("pinned nests at BASELINE ranks run on their kernels and match", [] {
