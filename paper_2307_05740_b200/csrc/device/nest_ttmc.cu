@@ -1364,7 +1364,7 @@ struct StageT4 {
   uint64_t mbar_leaf[2];
 };
 
-template <bool VECV, bool VECW>
+template <bool VECV, bool VECW, bool BLK>
 __global__ void __launch_bounds__(kBlock, 2) k_ttmc4pq(RootOutArgs a) {
   __shared__ StageT4 stage[kBlock / 32];
   const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
@@ -1399,11 +1399,15 @@ __global__ void __launch_bounds__(kBlock, 2) k_ttmc4pq(RootOutArgs a) {
     double* dst = dslot < 0 ? a.out + static_cast<int64_t>(row) * tile
                             : a.part + (w * 2 + dslot) * tile;
 #pragma unroll
-    for (int s = 0; s < 8; ++s)
+    for (int nb = 0; nb < 8; ++nb)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int tt = 2 * q + e;
-        if (h < R && s < S_ && tt < T) dst[(h * S_ + s) * T + tt] = acc[2 * s + e];
+        // n-tile nb, n index c = 2q + e: BLK maps it to the (s, t) of the
+        // 4 x 2 block lane-column c owns, otherwise to (s = nb, t = c)
+        const int c = 2 * q + e;
+        const int ss = BLK ? 4 * (c & 1) + (nb >> 1) : nb;
+        const int tt = BLK ? 2 * (c >> 1) + (nb & 1) : c;
+        if (h < R && ss < S_ && tt < T) dst[(h * S_ + ss) * T + tt] = acc[2 * nb + e];
       }
 #pragma unroll
     for (int e = 0; e < 16; ++e) acc[e] = 0.0;
@@ -1472,26 +1476,53 @@ __global__ void __launch_bounds__(kBlock, 2) k_ttmc4pq(RootOutArgs a) {
           const int32_t eg = hh.x - L0 + it * kPackSlots + gs;
           const double2 vg = pair2<VECV>(V + static_cast<int64_t>(S.kk[lbf][eg]) * S_, 2 * gc, S_);
           const double2 wg = pair2<VECW>(W + static_cast<int64_t>(S.ll[lbf][eg]) * T, 2 * gc, T);
-          *reinterpret_cast<double2*>(&S.vs[gs][2 * gc]) = vg;
+          // BLK: 64-byte rows, 16-byte chunk c stored at c ^ ((row >> 1) & 1)
+          *reinterpret_cast<double2*>(BLK ? &S.vs[0][0] + gs * 8 + 2 * (gc ^ ((gs >> 1) & 1))
+                                          : &S.vs[gs][2 * gc]) = vg;
           *reinterpret_cast<double2*>(&S.ws[gs][2 * gc]) = wg;
           __syncwarp();
           const int32_t eA = hh.x - L0 + it * kPackSlots + q, eB = eA + 4;
           const double vA = S.tv[lbf][eA], vB = S.tv[lbf][eB];
-          const double wA = S.ws[q][h], wB = S.ws[q + 4][h];
-          double vrA[8], vrB[8];
+          if (BLK) {
+            // lane (q, h) owns Y[s = 4sb + i][t = 2tb + j] (i < 4, j < 2):
+            // 4 V and 2 W values per leaf and K-chunk
+            const int sb = h & 1, tb = h >> 1;
+            const int sw = (q >> 1) & 1;
+            const double* vsf = &S.vs[0][0];  // BLK: rows of 8 doubles
+            const double2 a0 = *reinterpret_cast<const double2*>(vsf + q * 8 + 2 * ((2 * sb) ^ sw));
+            const double2 a1 = *reinterpret_cast<const double2*>(vsf + q * 8 + 2 * ((2 * sb + 1) ^ sw));
+            const double2 b0 = *reinterpret_cast<const double2*>(vsf + (q + 4) * 8 + 2 * ((2 * sb) ^ sw));
+            const double2 b1 =
+                *reinterpret_cast<const double2*>(vsf + (q + 4) * 8 + 2 * ((2 * sb + 1) ^ sw));
+            const double2 wa = *reinterpret_cast<const double2*>(&S.ws[q][2 * tb]);
+            const double2 wb = *reinterpret_cast<const double2*>(&S.ws[q + 4][2 * tb]);
+            __syncwarp();  // row tiles are rewritten by the next iteration
+            const double va[4] = {a0.x, a0.y, a1.x, a1.y}, vb[4] = {b0.x, b0.y, b1.x, b1.y};
+            const double xa[2] = {vA * wa.x, vA * wa.y}, xb[2] = {vB * wb.x, vB * wb.y};
 #pragma unroll
-          for (int m = 0; m < 4; ++m) {
-            const double2 a2 = *reinterpret_cast<const double2*>(&S.vs[q][2 * m]);
-            const double2 b2 = *reinterpret_cast<const double2*>(&S.vs[q + 4][2 * m]);
-            vrA[2 * m] = a2.x; vrA[2 * m + 1] = a2.y;
-            vrB[2 * m] = b2.x; vrB[2 * m + 1] = b2.y;
-          }
-          __syncwarp();  // row tiles are rewritten by the next iteration
-          const double xA = vA * wA, xB = vB * wB;  // X[t] = t_ijkl * W[l,t]
+            for (int i2 = 0; i2 < 4; ++i2)
 #pragma unroll
-          for (int s = 0; s < 8; ++s) {
-            YA[s] = fma(vrA[s], xA, YA[s]);  // Y[s,t] += V[k,s] * X[t]
-            YB[s] = fma(vrB[s], xB, YB[s]);
+              for (int j2 = 0; j2 < 2; ++j2) {
+                YA[2 * i2 + j2] = fma(va[i2], xa[j2], YA[2 * i2 + j2]);  // Y[s,t] += V[k,s] * X[t]
+                YB[2 * i2 + j2] = fma(vb[i2], xb[j2], YB[2 * i2 + j2]);
+              }
+          } else {
+            const double wA = S.ws[q][h], wB = S.ws[q + 4][h];
+            double vrA[8], vrB[8];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+              const double2 a2 = *reinterpret_cast<const double2*>(&S.vs[q][2 * m]);
+              const double2 b2 = *reinterpret_cast<const double2*>(&S.vs[q + 4][2 * m]);
+              vrA[2 * m] = a2.x; vrA[2 * m + 1] = a2.y;
+              vrB[2 * m] = b2.x; vrB[2 * m + 1] = b2.y;
+            }
+            __syncwarp();  // row tiles are rewritten by the next iteration
+            const double xA = vA * wA, xB = vB * wB;  // X[t] = t_ijkl * W[l,t]
+#pragma unroll
+            for (int s = 0; s < 8; ++s) {
+              YA[s] = fma(vrA[s], xA, YA[s]);  // Y[s,t] += V[k,s] * X[t]
+              YB[s] = fma(vrB[s], xB, YB[s]);
+            }
           }
         }
       }
@@ -1761,16 +1792,20 @@ void launch_ttmc4(const RootOutArgs& a, cudaStream_t s) {
   const int64_t blocks = (a.n_items * 32 + kBlock - 1) / kBlock;
   if (blocks == 0) return;
   const int mode = a.flags >> 8;
-  if (mode == 2) {
+  if (mode == 2 || mode == 3) {
     const bool vv = a.vec & 2, vw = a.vec & 4;
-    if (vv && vw)
-      k_ttmc4pq<true, true><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
-    else if (vv)
-      k_ttmc4pq<true, false><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
-    else if (vw)
-      k_ttmc4pq<false, true><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
-    else
-      k_ttmc4pq<false, false><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
+    const unsigned b = static_cast<unsigned>(blocks);
+    if (mode == 3) {  // 4 x 2 (s, t) blocks per lane
+      if (vv && vw) k_ttmc4pq<true, true, true><<<b, kBlock, 0, s>>>(a);
+      else if (vv) k_ttmc4pq<true, false, true><<<b, kBlock, 0, s>>>(a);
+      else if (vw) k_ttmc4pq<false, true, true><<<b, kBlock, 0, s>>>(a);
+      else k_ttmc4pq<false, false, true><<<b, kBlock, 0, s>>>(a);
+    } else {
+      if (vv && vw) k_ttmc4pq<true, true, false><<<b, kBlock, 0, s>>>(a);
+      else if (vv) k_ttmc4pq<true, false, false><<<b, kBlock, 0, s>>>(a);
+      else if (vw) k_ttmc4pq<false, true, false><<<b, kBlock, 0, s>>>(a);
+      else k_ttmc4pq<false, false, false><<<b, kBlock, 0, s>>>(a);
+    }
   } else if (mode == 1) {
     if (a.vec & 2)
       k_ttmc4pk<true><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);

@@ -93,7 +93,7 @@ VARIANTS = [("SPTTN_TTMC3_MODE", m, ["ttmc3_small", "ttmc3_r16"]) for m in ("0",
     [("SPTTN_MTTKRP_MODE", m, ["mttkrp3_small", "mttkrp3_r32", "mttkrp4_small", "mttkrp4_r32"])
      for m in ("0", "1", "2", "3")] + \
     [("SPTTN_TTTP_MODE", m, ["tttp3_small", "tttp3_r64"]) for m in ("0", "1")] + \
-    [("SPTTN_TTMC4_MODE", m, ["ttmc4_small", "ttmc4_r8"]) for m in ("0", "1", "2")]
+    [("SPTTN_TTMC4_MODE", m, ["ttmc4_small", "ttmc4_r8"]) for m in ("0", "1", "2", "3")]
 
 
 @pytest.mark.parametrize("env,mode,names", VARIANTS, ids=[f"{v[0]}={v[1]}" for v in VARIANTS])
