@@ -16,6 +16,12 @@ needs no data-path collective:
     ranges), replacing the paper's CTF reduction + redistribution
     (PAPER.md:1106-1115).
 
+Outputs NOT indexed by the root mode (MTTKRP for modes j / k,
+SPTTN_NEST_MTTKRP3_J / _K) are the one place the path has a real exchange:
+every shard adds into every output row, so the full output is the sum of the
+ranks' outputs (`reduce_dense_output`, one all_reduce — NCCL over NVLink on a
+GPU job).
+
 bench.py runs N independent full-size tensors (weak scaling, one per rank);
 `--shard` runs one tensor split with these helpers (strong scaling).
 """
@@ -122,3 +128,17 @@ def gather_sparse_leaves(local_out: np.ndarray, leaf_begin: int, nnz: int) -> np
         b, n = int(m[0]), int(m[1])
         full[b:b + n] = v.numpy()[:n]
     return full
+
+
+def reduce_dense_output(local_out) -> "np.ndarray":
+    """Sum of every rank's full-size output (non-root output modes). Accepts a
+    numpy array (host, any backend) or a torch tensor (reduced in place, e.g.
+    a CUDA tensor over NCCL); returns the summed array / tensor."""
+    import torch
+    import torch.distributed as dist
+    if isinstance(local_out, torch.Tensor):
+        dist.all_reduce(local_out, op=dist.ReduceOp.SUM)
+        return local_out
+    t = torch.from_numpy(np.ascontiguousarray(local_out, dtype=np.float64)).clone()
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return t.numpy()

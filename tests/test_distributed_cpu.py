@@ -43,6 +43,13 @@ def _worker(rank, world, port, key, result_q):
         if c.kind == 3:
             lb, _ = D.leaf_range_of_roots(w.csf, r0, r1)
             full = D.gather_sparse_leaves(local, lb, w.csf.nnz)
+        elif c.kind in (6, 7):  # non-root output: every shard adds into every row
+            full = D.reduce_dense_output(local)
+            want = OB.oracle_nest(c.kind, w.csf, w.factors, c.ranks)
+            scale = OB.oracle_nest(c.kind, w.csf.abs(), [np.abs(f) for f in w.factors], c.ranks)
+            ok = bool(np.all(np.abs(full - want) <= 1e-12 * scale + 1e-300))
+            result_q.put((rank, ok, [p[1] - p[0] for p in parts], shard.nnz))
+            return
         else:
             tile = int(np.prod([r for r in c.ranks if r]))
             full = D.gather_dense_rows(local, D.owned_rows(shard), tile, w.dims[0])
@@ -53,7 +60,8 @@ def _worker(rank, world, port, key, result_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("key", ["mttkrp3", "ttmc3", "tttp3", "mttkrp4", "ttmc4"])
+@pytest.mark.parametrize("key", ["mttkrp3", "ttmc3", "tttp3", "mttkrp4", "ttmc4", "mttkrp3_j",
+                                 "mttkrp3_k"])
 def test_sharded_equals_whole_world2(key):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
