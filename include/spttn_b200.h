@@ -73,6 +73,10 @@ int spttn_csf_from_coo(int order, const int64_t* dims, int64_t nnz, const int64_
 int spttn_csf_download(const spttn_csf* csf, int64_t* const* idx, int64_t* const* ptr,
                        double* values, void* stream);
 int64_t spttn_csf_dim(const spttn_csf* csf, int level);
+/* The same tensor with its levels reordered on the device (new level l =
+ * source level order[l]) — re-rooting a CSF so an output on a non-root mode
+ * becomes root-indexed (owner computes, no atomics). */
+int spttn_csf_permute(const spttn_csf* src, const int* order, void* stream, spttn_csf** out);
 int64_t spttn_csf_level_size(const spttn_csf* csf, int level);
 int64_t spttn_csf_device_bytes(const spttn_csf* csf);
 

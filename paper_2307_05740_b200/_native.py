@@ -70,7 +70,7 @@ ENGINE_SYMBOLS = [
     "spttn_read_output", "spttn_plan_info", "spttn_generic_resets", "spttn_generic_log_bytes",
     "spttn_generic_read_log", "spttn_unfactorized", "spttn_device_info", "spttn_build_info",
     "spttn_release_cached", "spttn_init", "spttn_csf_from_coo", "spttn_csf_download",
-    "spttn_csf_dim",
+    "spttn_csf_dim", "spttn_csf_permute",
 ]
 
 _engine = None
@@ -120,6 +120,7 @@ def engine() -> C.CDLL:
                                            C.POINTER(P)]
         lib.spttn_csf_download.argtypes = [P, C.POINTER(c_i64_p), C.POINTER(c_i64_p), c_dbl_p, P]
         lib.spttn_csf_dim.argtypes = [P, C.c_int]
+        lib.spttn_csf_permute.argtypes = [P, C.POINTER(C.c_int), P, C.POINTER(P)]
         lib.spttn_csf_dim.restype = c_i64
         _engine = lib
     return _engine

@@ -197,6 +197,24 @@ int spttn_csf_from_coo(int order, const int64_t* dims, int64_t nnz, const int64_
   });
 }
 
+int spttn_csf_permute(const spttn_csf* src, const int* order, void* stream, spttn_csf** out) {
+  return guarded([&] {
+    if (!src || !order || !out) fail(SPTTN_EINVAL, "spttn_csf_permute: null argument");
+    *out = nullptr;
+    const int d = src->d.order;
+    bool seen[spttn_dev::kMaxOrder] = {false};
+    for (int l = 0; l < d; ++l) {
+      if (order[l] < 0 || order[l] >= d || seen[order[l]])
+        fail(SPTTN_EINVAL, "spttn_csf_permute: order is not a permutation of the levels");
+      seen[order[l]] = true;
+    }
+    auto c = std::make_unique<spttn_csf>();
+    SPTTN_CUDA(cudaGetDevice(&c->d.device));
+    spttn_dev::csf_permute(src->d, order, c->d, as_stream(stream));
+    *out = c.release();
+  });
+}
+
 int spttn_csf_download(const spttn_csf* c, int64_t* const* idx, int64_t* const* ptr,
                        double* values, void* stream) {
   return guarded([&] {

@@ -40,22 +40,43 @@ __global__ void k_iota(int32_t* v, int64_t n) {
   if (e < n) v[e] = static_cast<int32_t>(e);
 }
 
-__global__ void k_gather_keys(const int64_t* coords, int d, int l, const int32_t* perm, int64_t n,
-                              uint32_t* out) {
+// per-level coordinates, SoA int32 (device)
+struct Soa {
+  const int32_t* c[kMaxOrder];
+};
+
+__global__ void k_aos_to_soa(const int64_t* coords, int64_t nnz, int d, Soa out) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= nnz) return;
+  for (int l = 0; l < d; ++l) const_cast<int32_t*>(out.c[l])[e] = static_cast<int32_t>(coords[e * d + l]);
+}
+
+__global__ void k_gather_keys(Soa co, int l, const int32_t* perm, int64_t n, uint32_t* out) {
   const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (r < n) out[r] = static_cast<uint32_t>(coords[static_cast<int64_t>(perm[r]) * d + l]);
+  if (r < n) out[r] = static_cast<uint32_t>(co.c[l][perm[r]]);
+}
+
+// parent coordinate broadcast to every child, one thread per child (binary
+// search of the child's parent: balanced for any fan-out)
+__global__ void k_expand_parent(const int32_t* ptr, int32_t nparent, const int32_t* pcoord,
+                                int64_t nchild, int32_t* out) {
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= nchild) return;
+  int32_t lo = 0, hi = nparent;  // largest p with ptr[p] <= c
+  while (hi - lo > 1) {
+    const int32_t mid = (lo + hi) >> 1;
+    if (ptr[mid] <= c) lo = mid; else hi = mid;
+  }
+  out[c] = pcoord[lo];
 }
 
 // run heads: row r of the sorted order starts a new distinct coordinate tuple
-__global__ void k_run_heads(const int64_t* coords, int d, const int32_t* perm, int64_t n,
-                            int32_t* head) {
+__global__ void k_run_heads(Soa co, int d, const int32_t* perm, int64_t n, int32_t* head) {
   const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (r >= n) return;
   int h = r == 0;
-  if (!h) {
-    const int64_t a = static_cast<int64_t>(perm[r]) * d, b = static_cast<int64_t>(perm[r - 1]) * d;
-    for (int l = 0; l < d; ++l) h |= coords[a + l] != coords[b + l];
-  }
+  if (!h)
+    for (int l = 0; l < d; ++l) h |= co.c[l][perm[r]] != co.c[l][perm[r - 1]];
   head[r] = h;
 }
 
@@ -72,27 +93,24 @@ __global__ void k_merge_runs(const int32_t* head, const int32_t* run_id, const i
 }
 
 // new node at level l for unique row u: its prefix [0, l] differs from u-1
-__global__ void k_node_flags(const int64_t* coords, int d, int l, const int32_t* urow, int64_t nu,
-                             int32_t* flag) {
+__global__ void k_node_flags(Soa co, int l, const int32_t* urow, int64_t nu, int32_t* flag) {
   const int64_t u = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (u >= nu) return;
   int f = u == 0;
-  if (!f) {
-    const int64_t a = static_cast<int64_t>(urow[u]) * d, b = static_cast<int64_t>(urow[u - 1]) * d;
-    for (int m = 0; m <= l; ++m) f |= coords[a + m] != coords[b + m];
-  }
+  if (!f)
+    for (int m = 0; m <= l; ++m) f |= co.c[m][urow[u]] != co.c[m][urow[u - 1]];
   flag[u] = f;
 }
 
 // nid_l = inclusive scan of the level-l flags (1-based); for level l < d-1
 // the first child of node nid_l[u]-1 is node nid_{l+1}[u]-1
-__global__ void k_emit_level(const int64_t* coords, int d, int l, const int32_t* urow,
-                             const int32_t* flag, const int32_t* nid, const int32_t* nid_next,
-                             int64_t nu, int32_t* idx, int32_t* ptr) {
+__global__ void k_emit_level(Soa co, int l, const int32_t* urow, const int32_t* flag,
+                             const int32_t* nid, const int32_t* nid_next, int64_t nu,
+                             int32_t* idx, int32_t* ptr) {
   const int64_t u = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (u >= nu || !flag[u]) return;
   const int32_t node = nid[u] - 1;
-  idx[node] = static_cast<int32_t>(coords[static_cast<int64_t>(urow[u]) * d + l]);
+  idx[node] = co.c[l][urow[u]];
   if (ptr) ptr[node] = nid_next[u] - 1;
 }
 
@@ -124,44 +142,26 @@ int bits_for(int64_t dim) {
 
 }  // namespace
 
-void csf_from_coo(DevCsf& D, int d, const int64_t* dims, int64_t nnz, const int64_t* h_coords,
-                  const double* h_vals, cudaStream_t s) {
-  if (nnz >= INT32_MAX) throw Status(SPTTN_EINVAL, "COO exceeds the int32 device layout");
+namespace {
+
+// The build proper: device SoA coordinates (co.c[l], CSF level order) and
+// values -> D (sorted rows, duplicates summed in order, levels emitted).
+void build_from_soa(DevCsf& D, int d, const int64_t* dims, int64_t nnz, const Soa& co,
+                    const double* vals, cudaStream_t s) {
   D.order = d;
-  for (int l = 0; l < d; ++l) {
-    if (dims[l] < 1 || dims[l] > INT32_MAX) throw Status(SPTTN_EINVAL, "mode size must be in [1, 2^31)");
-    D.dims[l] = dims[l];
-  }
-  int64_t* coords = scratch<int64_t>(nnz * d, s);
-  double* vals = scratch<double>(nnz, s);
-  int* err = scratch<int>(1, s);
-  SPTTN_CUDA(cudaMemsetAsync(err, 0, sizeof(int), s));
-  if (nnz > 0) {
-    SPTTN_CUDA(cudaMemcpyAsync(coords, h_coords, nnz * d * sizeof(int64_t), cudaMemcpyHostToDevice, s));
-    SPTTN_CUDA(cudaMemcpyAsync(vals, h_vals, nnz * sizeof(double), cudaMemcpyHostToDevice, s));
-  }
-  // bounds check
-  uint32_t* key = scratch<uint32_t>(nnz, s);
-  for (int l = 0; l < d && nnz > 0; ++l)
-    k_level_keys<<<nb(nnz, 256), 256, 0, s>>>(coords, nnz, d, l, dims[l], key, err);
-  int herr = 0;
-  SPTTN_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, s));
-  SPTTN_CUDA(cudaStreamSynchronize(s));
-  if (herr) {
-    dfree(coords, s); dfree(vals, s); dfree(err, s); dfree(key, s);
-    throw Status(SPTTN_EINVAL, "COO coordinate out of bounds");
-  }
+  for (int l = 0; l < d; ++l) D.dims[l] = dims[l];
   // 1. LSD radix sort of the row permutation, last level first
+  uint32_t* key = scratch<uint32_t>(nnz, s);
+  uint32_t* key2 = scratch<uint32_t>(nnz, s);
   int32_t* perm = scratch<int32_t>(nnz, s);
   int32_t* perm2 = scratch<int32_t>(nnz, s);
-  uint32_t* key2 = scratch<uint32_t>(nnz, s);
   if (nnz > 0) k_iota<<<nb(nnz, 256), 256, 0, s>>>(perm, nnz);
   size_t tbytes = 0;
   SPTTN_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tbytes, key, key2, perm, perm2,
                                              static_cast<int>(nnz), 0, 32, s));
   void* ttmp = scratch<unsigned char>(static_cast<int64_t>(tbytes), s);
   for (int l = d - 1; l >= 0 && nnz > 0; --l) {
-    k_gather_keys<<<nb(nnz, 256), 256, 0, s>>>(coords, d, l, perm, nnz, key);
+    k_gather_keys<<<nb(nnz, 256), 256, 0, s>>>(co, l, perm, nnz, key);
     SPTTN_CUDA(cub::DeviceRadixSort::SortPairs(ttmp, tbytes, key, key2, perm, perm2,
                                                static_cast<int>(nnz), 0, bits_for(dims[l]), s));
     std::swap(perm, perm2);
@@ -172,7 +172,7 @@ void csf_from_coo(DevCsf& D, int d, const int64_t* dims, int64_t nnz, const int6
   int32_t* run_id = scratch<int32_t>(nnz, s);
   int32_t nu = 0;
   if (nnz > 0) {
-    k_run_heads<<<nb(nnz, 256), 256, 0, s>>>(coords, d, perm, nnz, head);
+    k_run_heads<<<nb(nnz, 256), 256, 0, s>>>(co, d, perm, nnz, head);
     scan_incl_sum(head, run_id, nnz, s);
     SPTTN_CUDA(cudaMemcpyAsync(&nu, run_id + nnz - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     SPTTN_CUDA(cudaStreamSynchronize(s));
@@ -188,7 +188,7 @@ void csf_from_coo(DevCsf& D, int d, const int64_t* dims, int64_t nnz, const int6
     flag[l] = scratch<int32_t>(nu, s);
     nid[l] = scratch<int32_t>(nu, s);
     if (nu > 0) {
-      k_node_flags<<<nb(nu, 256), 256, 0, s>>>(coords, d, l, urow, nu, flag[l]);
+      k_node_flags<<<nb(nu, 256), 256, 0, s>>>(co, l, urow, nu, flag[l]);
       scan_incl_sum(flag[l], nid[l], nu, s);
       SPTTN_CUDA(cudaMemcpyAsync(&count[l], nid[l] + nu - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     }
@@ -207,7 +207,7 @@ void csf_from_coo(DevCsf& D, int d, const int64_t* dims, int64_t nnz, const int6
                                  cudaMemcpyHostToDevice, s));
     }
     if (nu > 0)
-      k_emit_level<<<nb(nu, 256), 256, 0, s>>>(coords, d, l, urow, flag[l], nid[l],
+      k_emit_level<<<nb(nu, 256), 256, 0, s>>>(co, l, urow, flag[l], nid[l],
                                                l + 1 < d ? nid[l + 1] : nullptr, nu, D.idx[l],
                                                l + 1 < d ? D.ptr[l] : nullptr);
   }
@@ -216,12 +216,84 @@ void csf_from_coo(DevCsf& D, int d, const int64_t* dims, int64_t nnz, const int6
     dfree(flag[l], s);
     dfree(nid[l], s);
   }
-  for (void* p : {static_cast<void*>(coords), static_cast<void*>(vals), static_cast<void*>(err),
-                  static_cast<void*>(key), static_cast<void*>(key2), static_cast<void*>(perm),
+  for (void* p : {static_cast<void*>(key), static_cast<void*>(key2), static_cast<void*>(perm),
                   static_cast<void*>(perm2), static_cast<void*>(head), static_cast<void*>(run_id),
                   static_cast<void*>(urow)})
     dfree(p, s);
   SPTTN_CUDA(cudaGetLastError());
+}
+
+}  // namespace
+
+void csf_from_coo(DevCsf& D, int d, const int64_t* dims, int64_t nnz, const int64_t* h_coords,
+                  const double* h_vals, cudaStream_t s) {
+  if (nnz >= INT32_MAX) throw Status(SPTTN_EINVAL, "COO exceeds the int32 device layout");
+  for (int l = 0; l < d; ++l)
+    if (dims[l] < 1 || dims[l] > INT32_MAX) throw Status(SPTTN_EINVAL, "mode size must be in [1, 2^31)");
+  int64_t* coords = scratch<int64_t>(nnz * d, s);
+  double* vals = scratch<double>(nnz, s);
+  int* err = scratch<int>(1, s);
+  SPTTN_CUDA(cudaMemsetAsync(err, 0, sizeof(int), s));
+  if (nnz > 0) {
+    SPTTN_CUDA(cudaMemcpyAsync(coords, h_coords, nnz * d * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    SPTTN_CUDA(cudaMemcpyAsync(vals, h_vals, nnz * sizeof(double), cudaMemcpyHostToDevice, s));
+  }
+  uint32_t* key = scratch<uint32_t>(nnz, s);
+  for (int l = 0; l < d && nnz > 0; ++l)  // bounds check
+    k_level_keys<<<nb(nnz, 256), 256, 0, s>>>(coords, nnz, d, l, dims[l], key, err);
+  int herr = 0;
+  SPTTN_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SPTTN_CUDA(cudaStreamSynchronize(s));
+  dfree(key, s);
+  dfree(err, s);
+  if (herr) {
+    dfree(coords, s);
+    dfree(vals, s);
+    throw Status(SPTTN_EINVAL, "COO coordinate out of bounds");
+  }
+  Soa co{};
+  std::vector<int32_t*> cols(d);
+  for (int l = 0; l < d; ++l) {
+    cols[l] = scratch<int32_t>(nnz, s);
+    co.c[l] = cols[l];
+  }
+  if (nnz > 0) k_aos_to_soa<<<nb(nnz, 256), 256, 0, s>>>(coords, nnz, d, co);
+  dfree(coords, s);
+  build_from_soa(D, d, dims, nnz, co, vals, s);
+  for (int l = 0; l < d; ++l) dfree(cols[l], s);
+  dfree(vals, s);
+}
+
+void csf_permute(const DevCsf& src, const int* order, DevCsf& D, cudaStream_t s) {
+  const int d = src.order;
+  const int64_t nnz = src.level_size[d - 1];
+  // every leaf's coordinate at every level (parents broadcast downwards)
+  std::vector<int32_t*> leafc(d, nullptr);
+  for (int l = 0; l < d; ++l) {
+    if (l == d - 1) {
+      leafc[l] = src.idx[l];
+      continue;
+    }
+    int32_t* cur = nullptr;  // coordinate of level l at the nodes of level m
+    for (int m = l + 1; m < d; ++m) {
+      int32_t* next = scratch<int32_t>(src.level_size[m], s);
+      if (src.level_size[m] > 0)
+        k_expand_parent<<<nb(src.level_size[m], 256), 256, 0, s>>>(
+            src.ptr[m - 1], static_cast<int32_t>(src.level_size[m - 1]), m == l + 1 ? src.idx[l] : cur,
+            src.level_size[m], next);
+      if (cur) dfree(cur, s);
+      cur = next;
+    }
+    leafc[l] = cur;
+  }
+  Soa co{};
+  int64_t dims[kMaxOrder];
+  for (int l = 0; l < d; ++l) {
+    co.c[l] = leafc[order[l]];
+    dims[l] = src.dims[order[l]];
+  }
+  build_from_soa(D, d, dims, nnz, co, src.vals, s);
+  for (int l = 0; l + 1 < d; ++l) dfree(leafc[l], s);
 }
 
 void csf_download(const DevCsf& D, int64_t* const* idx, int64_t* const* ptr, double* values,

@@ -164,6 +164,9 @@ int group_lanes_for(int R);
 // semantics straight into the int32 device layout.
 void csf_from_coo(DevCsf& D, int d, const int64_t* dims, int64_t nnz, const int64_t* h_coords,
                   const double* h_vals, cudaStream_t s);
+// The same tensor with its levels reordered (new level l = source level
+// order[l]), built on the device from the source layout.
+void csf_permute(const DevCsf& src, const int* order, DevCsf& dst, cudaStream_t s);
 // int32 device layout -> the reference's int64 idx / ptr arrays + values (host).
 void csf_download(const DevCsf& D, int64_t* const* idx, int64_t* const* ptr, double* values,
                   cudaStream_t s);

@@ -178,10 +178,12 @@ bool nonroot_atomics_enabled() {
 // sparse iteration order (the planners' own picks, e.g. max-buf-dim's
 // (i,j,r,k)(i,j,r) for MTTKRP-3, run on the dedicated kernel too). Hooks,
 // resets and flop counters still follow the given order (compile()).
+// `levels` = the sparse tensor's indices in CSF level order (the spec's own
+// order, or a re-rooted one: see prepare()).
 PinnedMatch match_pinned(const KernelSpec& spec, const ContractionPath& path,
-                         const LoopOrder& /*order*/) {
+                         const std::vector<int>& levels) {
   PinnedMatch none;
-  const auto& sp = spec.sparse_input().indices;
+  const auto& sp = levels;
   const int d = static_cast<int>(sp.size());
   const int n = spec.num_inputs();
   if (d != 3 && d != 4) return none;
@@ -323,6 +325,35 @@ std::shared_ptr<DeviceCsfHandle> upload_csf(const CsfTensor& csf) {
               cache.end());
   cache.push_back(Entry{&csf, fp, d});
   if (cache.size() > kCsfKeep) cache.erase(cache.begin());
+  return d;
+}
+
+// The device tensor re-rooted to `order` (spttn_csf_permute), cached like
+// the uploads: (tensor, fingerprint, order) -> handle, the last kCsfKeep kept.
+std::shared_ptr<DeviceCsfHandle> rerooted_csf(const CsfTensor& csf,
+                                              const std::shared_ptr<DeviceCsfHandle>& base,
+                                              const std::vector<int>& order) {
+  constexpr size_t kCsfKeep = 4;
+  struct Entry {
+    const CsfTensor* key;
+    uint64_t fp;
+    std::vector<int> order;
+    std::shared_ptr<DeviceCsfHandle> dev;
+  };
+  static std::mutex mu;
+  static std::vector<Entry>& cache = *new std::vector<Entry>;  // leaked: no frees at exit
+  const bool small = csf.nnz() <= (int64_t{1} << 20);
+  const uint64_t fp = small ? fingerprint(csf) : 0;
+  std::lock_guard<std::mutex> lock(mu);
+  if (small)
+    for (const auto& e : cache)
+      if (e.key == &csf && e.fp == fp && e.order == order) return e.dev;
+  auto d = std::make_shared<DeviceCsfHandle>();
+  check(spttn_csf_permute(base->h, order.data(), nullptr, &d->h), "prepare (re-rooted CSF)");
+  if (small) {
+    cache.push_back(Entry{&csf, fp, order, d});
+    if (cache.size() > kCsfKeep) cache.erase(cache.begin());
+  }
   return d;
 }
 
@@ -725,7 +756,36 @@ ExecPlan prepare(const KernelSpec& spec, const ContractionPath& path, const Loop
   tc = Clock::now();
   spttn_plan_desc desc{};
   desc.buffer_limit_bytes = opts.buffer_limit_bytes;
-  P.pinned = match_pinned(spec, path, order);
+  P.pinned = match_pinned(spec, path, spec.sparse_input().indices);
+  const std::shared_ptr<DeviceCsfHandle> base_csf = P.csf;  // the interpreter walks this one
+  // A dense output on a non-root mode m: re-root the tensor on the device
+  // (level order m, then the rest) so the nest becomes a root-output pinned
+  // nest — owner computes, deterministic. Preferred over the atomic
+  // non-root MTTKRP kernels unless SPTTN_NONROOT=atomics.
+  if (opts.observer == nullptr && !spec.output_sparse && !spec.output().indices.empty() &&
+      (P.pinned.kind == 0 || P.pinned.kind == SPTTN_NEST_MTTKRP3_J ||
+       P.pinned.kind == SPTTN_NEST_MTTKRP3_K)) {
+    const auto& sp = spec.sparse_input().indices;
+    const auto it = std::find(sp.begin(), sp.end(), spec.output().indices[0]);
+    const char* pref = std::getenv("SPTTN_NONROOT");
+    const bool atomics = pref && std::string(pref) == "atomics" && P.pinned.kind != 0;
+    if (it != sp.end() && it != sp.begin() && !atomics) {
+      const int m = static_cast<int>(it - sp.begin());
+      std::vector<int> rr{sp[m]};
+      std::vector<int> order_lv{m};
+      for (int l = 0; l < static_cast<int>(sp.size()); ++l)
+        if (l != m) {
+          rr.push_back(sp[l]);
+          order_lv.push_back(l);
+        }
+      PinnedMatch m2 = match_pinned(spec, path, rr);
+      if (m2.kind >= SPTTN_NEST_MTTKRP3 && m2.kind <= SPTTN_NEST_TTMC4 &&
+          m2.kind != SPTTN_NEST_TTTP3) {
+        P.pinned = m2;
+        P.csf = rerooted_csf(*inputs.sparse, P.csf, order_lv);
+      }
+    }
+  }
   int rc = SPTTN_EUNSUPPORTED;
   if (P.pinned.kind != 0 && opts.observer == nullptr) {
     desc.kind = P.pinned.kind;
@@ -742,6 +802,7 @@ ExecPlan prepare(const KernelSpec& spec, const ContractionPath& path, const Loop
   }
   if (rc != SPTTN_OK) {  // any other admissible order: device forest interpreter
     P.pinned = PinnedMatch{};
+    P.csf = base_csf;
     desc = spttn_plan_desc{};
     desc.kind = SPTTN_NEST_GENERIC;
     desc.buffer_limit_bytes = opts.buffer_limit_bytes;

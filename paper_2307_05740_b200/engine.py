@@ -115,6 +115,19 @@ class DeviceCsf:
         self._keep = None
         return self
 
+    def permute(self, order, stream=None) -> "DeviceCsf":
+        """spttn_csf_permute: the same tensor with levels in `order` (new level
+        l = current level order[l]), rebuilt on the device."""
+        lib = N.engine()
+        o = (C.c_int * len(order))(*order)
+        h = C.c_void_p()
+        _check(lib.spttn_csf_permute(self.handle, o, _stream_ptr(stream), C.byref(h)))
+        out = DeviceCsf.__new__(DeviceCsf)
+        out.csf = None
+        out.handle = h
+        out._keep = None
+        return out
+
     def level_sizes(self):
         lib = N.engine()
         sizes = []

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstring>
 #include <functional>
+#include <map>
 #include <set>
 #include <string>
 
@@ -346,6 +347,45 @@ int main() {
         ++n;
       }
     CHECK(n > 0);
+  });
+
+  run_case("non-root outputs are re-rooted on the device onto the pinned kernels", [] {
+    struct Case {
+      const char* kernel;
+      std::map<std::string, int64_t> dims;
+      const char* path;
+      int kind;
+    };
+    const std::vector<Case> cases = {
+        {"T[i,j,k]*A[i,a]*C[k,a]->B[j,a]", {{"i", 9}, {"j", 8}, {"k", 7}, {"a", 4}}, "((T*C)*A)",
+         SPTTN_NEST_MTTKRP3},
+        {"T[i,j,k]*U[i,r]*V[k,s]->Y[j,r,s]", {{"i", 9}, {"j", 8}, {"k", 7}, {"r", 3}, {"s", 2}},
+         "((T*V)*U)", SPTTN_NEST_TTMC3},
+        {"T[i,j,k]*U[i,r]*V[j,s]->Y[k,r,s]", {{"i", 9}, {"j", 8}, {"k", 7}, {"r", 3}, {"s", 2}},
+         "((T*V)*U)", SPTTN_NEST_TTMC3},
+        {"T[i,j,k,l]*A[i,r]*B[j,r]*C[k,r]->D[l,r]",
+         {{"i", 5}, {"j", 4}, {"k", 6}, {"l", 5}, {"r", 4}}, "(((T*C)*B)*A)", SPTTN_NEST_MTTKRP4},
+    };
+    for (const auto& c : cases) {
+      KernelSpec spec = parse_kernel(c.kernel, c.dims);
+      Tensors t = make_tensors(spec, random_coo(spec, 0.2, 17));
+      auto in = t.inputs();
+      ExecResult oracle = execute_unfactorized(spec, in);
+      int routed = 0, n = 0;
+      for (const auto& path : filter_min_depth(enumerate_paths(spec))) {
+        if (path.describe(spec) != c.path) continue;
+        for (const auto& order : enumerate_orders(spec, path, default_csf_order(spec))) {
+          ExecPlan plan = prepare(spec, path, order, in);
+          routed += spttn_b200_plan_device_kind(plan) == c.kind;
+          ExecResult r = execute(plan);
+          CHECK(close(r, oracle));
+          CHECK(r.stats.multiply_adds == flops_estimate(spec, path, order, t.csf));
+          ++n;
+        }
+      }
+      CHECK(n > 0);
+      CHECK(routed == n);
+    }
   });
 
   run_case("device build_csf equals the reference build_csf (any mode order)", [] {

@@ -334,3 +334,29 @@ def test_device_csf_from_coo_errors_and_empty(E):
     got = dev.download()
     assert got.level_sizes() == [0, 0, 0]
     assert [p.tolist() for p in got.ptr] == [[0], [0]]
+
+
+def test_device_csf_permute_reroots(E):
+    """spttn_csf_permute: the (j, i, k) CSF of a tensor equals the host build
+    of its COO in that mode order, and the re-rooted MTTKRP-3 kernel then gives
+    the mode-j product (owner computes, no atomics)."""
+    from paper_2307_05740_b200.configs import make_workload
+    from paper_2307_05740_b200.tensor import Csf
+    w = make_workload("mttkrp3", scale=2e-2)
+    dev = E.DeviceCsf(w.csf)
+    rr = dev.permute([1, 0, 2])
+    coo, vals = w.csf.to_coo()
+    want = Csf.from_coo([w.csf.dims[1], w.csf.dims[0], w.csf.dims[2]], coo[:, [1, 0, 2]], vals)
+    got = rr.download()
+    for a, b in zip(got.idx + got.ptr, want.idx + want.ptr):
+        assert np.array_equal(a, b)
+    assert np.array_equal(got.values, want.values)
+    rng = np.random.default_rng(3)
+    R = 32
+    A = rng.standard_normal((w.csf.dims[0], R))
+    Cf = rng.standard_normal((w.csf.dims[2], R))
+    plan = E.Plan(E.NEST_MTTKRP3, rr, [A, Cf], ranks=(R, 0, 0))  # level-1 factor = A
+    plan.execute()
+    out = plan.read_output()
+    ref, norm = oracle_with_norm(6, w.csf, [A, Cf], (R, 0, 0))
+    assert_parity(out, ref, norm, "re-rooted mode-j MTTKRP")
