@@ -61,14 +61,35 @@ __global__ void k_absent(const unsigned char* present, int64_t dim0, int32_t* ro
   if (!present[i]) rows[atomicAdd(count, 1)] = static_cast<int32_t>(i);
 }
 
-// Parent coordinate broadcast one level down: child c of node n gets idx[n].
-__global__ void k_child_coord(const int32_t* ptr, const int32_t* coord, int32_t n,
-                              int32_t* child_coord) {
+// Parent coordinate broadcast one level down (child c of node n gets
+// coord[n]), balanced for any fan-out: every parent with children marks its
+// first child, an inclusive max-scan carries the parent id across its
+// children, a gather reads the coordinate — three streaming passes, so a root
+// slice with a million children costs no more than a million small fibers.
+__global__ void k_mark_first_child(const int32_t* ptr, int32_t nparent, int32_t* mark) {
+  const int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= nparent) return;
+  if (ptr[p] < ptr[p + 1]) mark[ptr[p]] = p;
+}
+
+__global__ void k_gather_parent(const int32_t* parent, const int32_t* coord, int64_t n,
+                                int32_t* out) {
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c < n) out[c] = coord[parent[c]];
+}
+
+// one thread per parent: for levels whose fan-out is ~1 (fibers of one leaf)
+__global__ void k_child_coord_loop(const int32_t* ptr, const int32_t* coord, int32_t n,
+                                   int32_t* child_coord) {
   const int32_t node = blockIdx.x * blockDim.x + threadIdx.x;
   if (node >= n) return;
   const int32_t v = coord[node];
   for (int32_t c = ptr[node]; c < ptr[node + 1]; ++c) child_coord[c] = v;
 }
+
+struct MaxI32 {
+  __device__ __forceinline__ int32_t operator()(int32_t a, int32_t b) const { return a > b ? a : b; }
+};
 
 // Segment counts per unit node: ceil(children / seg_len).
 // Child range of unit node f: its direct children, or (leaf_space) its
@@ -146,6 +167,31 @@ __global__ void k_seg_splits(CsfView t, const int32_t* slice_seg, int64_t chunk,
 }
 
 unsigned blocks_for(int64_t n, int b) { return static_cast<unsigned>((n + b - 1) / b); }
+
+void child_coords(const int32_t* ptr, int32_t nparent, const int32_t* coord, int64_t nchild,
+                  int32_t* out, cudaStream_t s) {
+  if (nchild == 0 || nparent == 0) return;
+  if (nchild <= 4 * static_cast<int64_t>(nparent)) {  // small fan-out: a loop per parent
+    k_child_coord_loop<<<blocks_for(nparent, 256), 256, 0, s>>>(ptr, coord, nparent, out);
+    SPTTN_CUDA(cudaGetLastError());
+    return;
+  }
+  int32_t* mark = nullptr;
+  dmalloc(&mark, nchild * sizeof(int32_t), s);
+  SPTTN_CUDA(cudaMemsetAsync(mark, 0, nchild * sizeof(int32_t), s));
+  k_mark_first_child<<<blocks_for(nparent, 256), 256, 0, s>>>(ptr, nparent, mark);
+  size_t bytes = 0;
+  SPTTN_CUDA(cub::DeviceScan::InclusiveScan(nullptr, bytes, mark, mark, MaxI32{},
+                                            static_cast<int>(nchild), s));
+  void* tmp = nullptr;
+  dmalloc(&tmp, std::max<size_t>(1, bytes), s);
+  SPTTN_CUDA(cub::DeviceScan::InclusiveScan(tmp, bytes, mark, mark, MaxI32{},
+                                            static_cast<int>(nchild), s));
+  k_gather_parent<<<blocks_for(nchild, 256), 256, 0, s>>>(mark, coord, nchild, out);
+  SPTTN_CUDA(cudaGetLastError());
+  dfree(tmp, s);
+  dfree(mark, s);
+}
 
 // slice_units: first work unit (segment / packed group) of every root slice,
 // or nullptr when items are leaf ranges.
@@ -257,7 +303,7 @@ void build_segments(const DevCsf& csf, int unit_level, int seg_len, int64_t chun
     dmalloc(&unit_parent, std::max<int32_t>(1, nf) * sizeof(int32_t), s);
     const int32_t n1 = static_cast<int32_t>(csf.level_size[1]);
     if (n1 > 0)
-      k_child_coord<<<blocks_for(n1, 256), 256, 0, s>>>(t.ptr[1], t.idx[1], n1, unit_parent);
+      child_coords(t.ptr[1], n1, t.idx[1], nf, unit_parent, s);
   }
   if (nf > 0) {
     k_seg_fill<<<blocks_for(nf, 256), 256, 0, s>>>(t, unit_level, seg_len, leaf_space, off,
@@ -296,7 +342,7 @@ void expand_coords(const DevCsf& csf, int level, const int32_t* coords, int32_t*
                    cudaStream_t s) {
   const int32_t n = static_cast<int32_t>(csf.level_size[level]);
   if (n > 0) {
-    k_child_coord<<<blocks_for(n, 256), 256, 0, s>>>(csf.ptr[level], coords, n, out);
+    child_coords(csf.ptr[level], n, coords, csf.level_size[level + 1], out, s);
     SPTTN_CUDA(cudaGetLastError());
   }
 }
@@ -307,15 +353,9 @@ void build_leaf_coords(const DevCsf& csf, int32_t** leaf_i, int32_t** leaf_j, cu
   dmalloc(leaf_i, std::max<int64_t>(1, nnz) * sizeof(int32_t), s);
   dmalloc(leaf_j, std::max<int64_t>(1, nnz) * sizeof(int32_t), s);
   dmalloc(&fib_i, std::max<int64_t>(1, n1) * sizeof(int32_t), s);
-  if (n0 > 0)
-    k_child_coord<<<blocks_for(n0, 256), 256, 0, s>>>(csf.ptr[0], csf.idx[0],
-                                                      static_cast<int32_t>(n0), fib_i);
-  if (n1 > 0) {
-    k_child_coord<<<blocks_for(n1, 256), 256, 0, s>>>(csf.ptr[1], csf.idx[1],
-                                                      static_cast<int32_t>(n1), *leaf_j);
-    k_child_coord<<<blocks_for(n1, 256), 256, 0, s>>>(csf.ptr[1], fib_i,
-                                                      static_cast<int32_t>(n1), *leaf_i);
-  }
+  child_coords(csf.ptr[0], static_cast<int32_t>(n0), csf.idx[0], n1, fib_i, s);
+  child_coords(csf.ptr[1], static_cast<int32_t>(n1), csf.idx[1], nnz, *leaf_j, s);
+  child_coords(csf.ptr[1], static_cast<int32_t>(n1), fib_i, nnz, *leaf_i, s);
   SPTTN_CUDA(cudaGetLastError());
   dfree(fib_i, s);
 }
