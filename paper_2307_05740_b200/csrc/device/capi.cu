@@ -573,8 +573,12 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
             env_int("SPTTN_SEG_LEN", p->kind == SPTTN_NEST_TTMC3 ? 4 : 8));
         if (p->kind == SPTTN_NEST_TTMC3) {
           // 10 = packed, TMA-staged, row-contiguous gathers (default);
-          // 0-7 = earlier variants kept for A/B measurements (tools/sweep.py)
+          // 0, 4, 6, 7 = earlier variants, 11 = TMA gather4 rows, kept for
+          // A/B measurements (tools/sweep.py)
           p->mode = static_cast<int>(env_int("SPTTN_TTMC3_MODE", 10));
+          if (p->mode != 0 && p->mode != 4 && p->mode != 6 && p->mode != 7 && p->mode != 10 &&
+              p->mode != 11)
+            p->mode = 10;
           if (p->mode == 11 && !spttn_dev::ttmc3_tma_supported(static_cast<int>(R), static_cast<int>(S)))
             p->mode = 10;
           seg_len = std::clamp(seg_len, 1, p->mode == 0 ? 8 : 4);

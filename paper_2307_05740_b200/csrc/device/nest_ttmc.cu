@@ -167,256 +167,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_ttmc3(RootOutArgs a) {
   if (pending) flush(head ? 0 : 1);
 }
 
-// Direct-load variant: seg_len <= 4, fully unrolled leaf loop (no
-// data-dependent trip counts), each lane loads its slot's leaf indices /
-// values itself (4 distinct addresses per instruction, broadcast within the
-// 8 lanes of a slot); NG groups of 4 segments are in flight per step.
-template <bool VECU, bool VECV, int NG>
-__global__ void __launch_bounds__(kBlock, NG == 1 ? 4 : 3) k_ttmc3d(RootOutArgs a) {
-  const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
-  if (w >= a.n_items) return;  // warp-uniform
-  const int lane = threadIdx.x & 31;
-  const int q = lane & 3;
-  const int h = lane >> 2;
-  const int R = a.R, S = a.S;
-  const CsfView& t = a.t;
-  const double* __restrict__ U = a.f[1];
-  const double* __restrict__ V = a.f[2];
-  const int32_t* __restrict__ kidx = t.idx[2];
-  const double* __restrict__ vals = t.vals;
-  const int32_t* __restrict__ seg_begin = a.seg_begin;
-  const int32_t* __restrict__ seg_node = a.seg_node;
-  const int32_t n_seg = static_cast<int32_t>(a.n_seg);
-
-  int32_t c = static_cast<int32_t>(w * a.chunk);
-  const int32_t cend = static_cast<int32_t>(min64(c + a.chunk, a.n_seg));
-  int32_t sl = a.item_pos[w];
-  int32_t sl_end = a.slice_seg[sl + 1];
-  bool head = a.slice_seg[sl] < c;
-  int32_t row = t.idx[0][sl];
-  bool pending = false;
-  double acc[8];
-#pragma unroll
-  for (int e = 0; e < 8; ++e) acc[e] = 0.0;
-
-  auto flush = [&](int slot) {
-    double* dst = slot < 0 ? a.out + static_cast<int64_t>(row) * R * S
-                           : a.part + (w * 2 + slot) * static_cast<int64_t>(R) * S;
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int r = 2 * h + mt;
-          const int s = 2 * (2 * q + e) + nt;
-          if (r < R && s < S) dst[r * S + s] = acc[(mt * 2 + nt) * 2 + e];
-        }
-#pragma unroll
-    for (int e = 0; e < 8; ++e) acc[e] = 0.0;
-  };
-
-  while (c < cend) {
-    const int32_t wb = c;
-    const int32_t wend = min(wb + 32, cend);
-    const int32_t sb = wb + lane <= n_seg ? __ldg(seg_begin + wb + lane) : 0;
-    const int32_t sb32 = __ldg(seg_begin + min(wb + 32, n_seg));
-    const int32_t sn = wb + lane < n_seg ? __ldg(seg_node + wb + lane) : 0;
-    while (c < wend) {
-      const int32_t lim = min(wend, sl_end);
-      int32_t lb[NG], n[NG], nv[NG];
-      double2 u[NG];
-      int32_t cg = c;
-#pragma unroll
-      for (int g = 0; g < NG; ++g) {
-        nv[g] = max(0, min(4, lim - cg));
-        const int rq = cg - wb + q;
-        const bool valid = q < nv[g];
-        const int32_t b = __shfl_sync(0xffffffffu, sb, min(rq, 31));
-        const int32_t ea = __shfl_sync(0xffffffffu, sb, min(rq + 1, 31));
-        const int32_t jj = __shfl_sync(0xffffffffu, sn, min(rq, 31));
-        const int32_t e = rq + 1 < 32 ? ea : sb32;
-        lb[g] = valid ? b : 0;
-        n[g] = valid ? e - b : 0;
-        u[g] = valid ? row2<VECU>(U + static_cast<int64_t>(jj) * R, 2 * h, R)
-                     : make_double2(0, 0);
-        cg += nv[g];
-      }
-      int32_t kk[NG][4];
-      double tt[NG][4];
-#pragma unroll
-      for (int g = 0; g < NG; ++g)
-#pragma unroll
-        for (int it = 0; it < 4; ++it) {
-          kk[g][it] = it < n[g] ? __ldg(kidx + lb[g] + it) : 0;
-          tt[g][it] = it < n[g] ? __ldg(vals + lb[g] + it) : 0.0;
-        }
-      double2 vr[NG][4];
-#pragma unroll
-      for (int g = 0; g < NG; ++g)
-#pragma unroll
-        for (int it = 0; it < 4; ++it)
-          vr[g][it] = it < n[g] ? row2<VECV>(V + static_cast<int64_t>(kk[g][it]) * S, 2 * h, S)
-                                : make_double2(0, 0);
-#pragma unroll
-      for (int g = 0; g < NG; ++g) {
-        double x0 = 0.0, x1 = 0.0;
-#pragma unroll
-        for (int it = 0; it < 4; ++it) {
-          x0 = fma(tt[g][it], vr[g][it].x, x0);  // X[s] += t * V[k,s]
-          x1 = fma(tt[g][it], vr[g][it].y, x1);
-        }
-        dmma_8x8x4(acc[0], acc[1], u[g].x, x0);
-        dmma_8x8x4(acc[2], acc[3], u[g].x, x1);
-        dmma_8x8x4(acc[4], acc[5], u[g].y, x0);
-        dmma_8x8x4(acc[6], acc[7], u[g].y, x1);
-      }
-      pending = true;
-      c = cg;
-      if (c == sl_end) {
-        flush(head ? 0 : -1);
-        pending = false;
-        head = false;
-        if (c < cend) {
-          ++sl;
-          sl_end = a.slice_seg[sl + 1];
-          row = t.idx[0][sl];
-        }
-      }
-    }
-  }
-  if (pending) flush(head ? 0 : 1);
-}
-
-// Pipelined direct-load variant (seg_len <= 4). Groups are speculated to be
-// the next 4 segments: segment metadata is loaded two groups ahead and leaf
-// coordinates one group ahead, so the only round trip on a group's critical
-// path is its V-row gather (issued together with its values and U rows).
-// A group shortened by a slice / item end falls back to direct loads.
-struct SegMeta {
-  int32_t lb, n, j;
-};
-
-__device__ __forceinline__ SegMeta load_meta(const RootOutArgs& a, int32_t base, int q,
-                                             int32_t n_seg) {
-  SegMeta m{0, 0, 0};
-  const int32_t seg = base + q;
-  if (seg < n_seg) {
-    m.lb = __ldg(a.seg_begin + seg);
-    m.n = __ldg(a.seg_begin + seg + 1) - m.lb;
-    m.j = __ldg(a.seg_node + seg);
-  }
-  return m;
-}
-
-template <bool VECU, bool VECV>
-__global__ void __launch_bounds__(kBlock, 3) k_ttmc3p(RootOutArgs a) {
-  const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
-  if (w >= a.n_items) return;  // warp-uniform
-  const int lane = threadIdx.x & 31;
-  const int q = lane & 3;
-  const int h = lane >> 2;
-  const int R = a.R, S = a.S;
-  const CsfView& t = a.t;
-  const double* __restrict__ U = a.f[1];
-  const double* __restrict__ V = a.f[2];
-  const int32_t* __restrict__ kidx = t.idx[2];
-  const double* __restrict__ vals = t.vals;
-  const int32_t n_seg = static_cast<int32_t>(a.n_seg);
-
-  int32_t c = static_cast<int32_t>(w * a.chunk);
-  const int32_t cend = static_cast<int32_t>(min64(c + a.chunk, a.n_seg));
-  int32_t sl = a.item_pos[w];
-  int32_t sl_end = a.slice_seg[sl + 1];
-  bool head = a.slice_seg[sl] < c;
-  int32_t row = t.idx[0][sl];
-  bool pending = false;
-  double acc[8];
-#pragma unroll
-  for (int e = 0; e < 8; ++e) acc[e] = 0.0;
-
-  auto flush = [&](int slot) {
-    double* dst = slot < 0 ? a.out + static_cast<int64_t>(row) * R * S
-                           : a.part + (w * 2 + slot) * static_cast<int64_t>(R) * S;
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int r = 2 * h + mt;
-          const int s = 2 * (2 * q + e) + nt;
-          if (r < R && s < S) dst[r * S + s] = acc[(mt * 2 + nt) * 2 + e];
-        }
-#pragma unroll
-    for (int e = 0; e < 8; ++e) acc[e] = 0.0;
-  };
-  auto load_k = [&](const SegMeta& m, int32_t* k) {
-#pragma unroll
-    for (int it = 0; it < 4; ++it) k[it] = it < m.n ? __ldg(kidx + m.lb + it) : 0;
-  };
-
-  SegMeta mc = load_meta(a, c, q, n_seg);
-  SegMeta mn = load_meta(a, c + 4, q, n_seg);
-  int32_t kc[4];
-  load_k(mc, kc);
-  while (c < cend) {
-    const int32_t lim = min(cend, sl_end);
-    const int nv = min(4, lim - c);
-    const bool valid = q < nv;
-    const int n = valid ? mc.n : 0;
-    double tt[4];
-    double2 vr[4];
-#pragma unroll
-    for (int it = 0; it < 4; ++it) {
-      tt[it] = it < n ? __ldg(vals + mc.lb + it) : 0.0;
-      vr[it] = it < n ? row2<VECV>(V + static_cast<int64_t>(kc[it]) * S, 2 * h, S)
-                      : make_double2(0, 0);
-    }
-    const double2 u = valid ? row2<VECU>(U + static_cast<int64_t>(mc.j) * R, 2 * h, R)
-                            : make_double2(0, 0);
-    // speculative prefetch: next group = the next 4 segments
-    const SegMeta mnn = load_meta(a, c + 8, q, n_seg);
-    int32_t kn[4];
-    load_k(mn, kn);
-    double x0 = 0.0, x1 = 0.0;
-#pragma unroll
-    for (int it = 0; it < 4; ++it) {
-      x0 = fma(tt[it], vr[it].x, x0);  // X[s] += t * V[k,s]
-      x1 = fma(tt[it], vr[it].y, x1);
-    }
-    dmma_8x8x4(acc[0], acc[1], u.x, x0);
-    dmma_8x8x4(acc[2], acc[3], u.x, x1);
-    dmma_8x8x4(acc[4], acc[5], u.y, x0);
-    dmma_8x8x4(acc[6], acc[7], u.y, x1);
-    pending = true;
-    const int32_t cn = c + nv;
-    if (nv == 4) {
-      mc = mn;
-      mn = mnn;
-#pragma unroll
-      for (int it = 0; it < 4; ++it) kc[it] = kn[it];
-    } else {  // group cut by a slice / item end: restart the pipeline
-      mc = load_meta(a, cn, q, n_seg);
-      mn = load_meta(a, cn + 4, q, n_seg);
-      load_k(mc, kc);
-    }
-    c = cn;
-    if (c == sl_end) {
-      flush(head ? 0 : -1);
-      pending = false;
-      head = false;
-      if (c < cend) {
-        ++sl;
-        sl_end = a.slice_seg[sl + 1];
-        row = t.idx[0][sl];
-      }
-    }
-  }
-  if (pending) flush(head ? 0 : 1);
-}
-
-// Stream-staged variant (default). The warp's CSF stream — segment metadata
+// Stream-staged variant (mode 4). The warp's CSF stream — segment metadata
 // and the leaves' coordinates / values — is copied into a per-warp shared
 // memory ring with cp.async (LDGSTS) one 32-segment window ahead (metadata
 // two windows ahead, since a window's leaf range comes from its metadata),
@@ -568,172 +319,13 @@ __global__ void __launch_bounds__(kBlock, 3) k_ttmc3s(RootOutArgs a) {
   if (pending) flush(head ? 0 : 1);
 }
 
-// Wide-gather variant (default): 8 segments per warp step as two DMMA
-// K-chunks. Lane L = (q = L%4, c4 = (L/4)%4, ch = L/16) handles segment
-// ch*4+q and the 4 rank columns [4*c4, 4*c4+4) of its factor rows, so every
-// gather is one 256-bit load (4 lanes per 128-byte row, 8 rows per
-// instruction) — measured 123 B/clk/SM from L1 against 84 B/clk/SM for
-// 16-byte lanes (tools/gather_probe.cu). One xor-16 exchange of two doubles
-// then turns the per-lane column quads into the DMMA fragments of both
-// K-chunks, with rows / columns interleaved as r|s = 4(h%4) + 2(h/4) + t.
-template <bool VECU, bool VECV>
-__global__ void __launch_bounds__(kBlock, 3) k_ttmc3w(RootOutArgs a) {
-  __shared__ Stage3 stage[kBlock / 32];
-  const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
-  if (w >= a.n_items) return;  // warp-uniform
-  Stage3& S = stage[threadIdx.x / 32];
-  const int lane = threadIdx.x & 31;
-  const int q = lane & 3;
-  const int c4 = (lane >> 2) & 3;
-  const int ch = lane >> 4;
-  const int slot = ch * 4 + q;
-  const int h = lane >> 2;
-  const int R = a.R, S_ = a.S;
-  const CsfView& t = a.t;
-  const double* __restrict__ U = a.f[1];
-  const double* __restrict__ V = a.f[2];
-  const int32_t* __restrict__ kidx = t.idx[2];
-  const double* __restrict__ vals = t.vals;
-  const int32_t* __restrict__ seg_begin = a.seg_begin;
-  const int32_t* __restrict__ seg_node = a.seg_node;
-  const int32_t* __restrict__ slice_seg = a.slice_seg;
-
-  const int32_t cbeg = static_cast<int32_t>(w * a.chunk);
-  const int32_t cend = static_cast<int32_t>(min64(cbeg + a.chunk, a.n_seg));
-  int32_t sl = a.item_pos[w];
-  int32_t sl_end = slice_seg[sl + 1];
-  bool head = slice_seg[sl] < cbeg;
-  int32_t row = t.idx[0][sl];
-  int32_t nx_end = sl + 2 <= t.nlev[0] ? __ldg(slice_seg + sl + 2) : 0;
-  int32_t nx_row = sl + 1 < t.nlev[0] ? __ldg(t.idx[0] + sl + 1) : 0;
-  bool pending = false;
-  double acc[8];
-#pragma unroll
-  for (int e = 0; e < 8; ++e) acc[e] = 0.0;
-
-  auto flush = [&](int dslot) {
-    double* dst = dslot < 0 ? a.out + static_cast<int64_t>(row) * R * S_
-                            : a.part + (w * 2 + dslot) * static_cast<int64_t>(R) * S_;
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int r = 4 * (h & 3) + 2 * (h >> 2) + mt;
-          const int n = 2 * q + e;
-          const int s = 4 * (n & 3) + 2 * (n >> 2) + nt;
-          if (r < R && s < S_) dst[r * S_ + s] = acc[(mt * 2 + nt) * 2 + e];
-        }
-#pragma unroll
-    for (int e = 0; e < 8; ++e) acc[e] = 0.0;
-  };
-  auto issue_meta = [&](int buf, int32_t ws) {
-    const int32_t nsw = min(ws + kWin, cend) - ws;
-    if (lane <= nsw) cp_async4(&S.sb[buf][lane], seg_begin + ws + lane);
-    if (lane == 0 && nsw == kWin) cp_async4(&S.sb[buf][kWin], seg_begin + ws + kWin);
-    if (lane < nsw) cp_async4(&S.sn[buf][lane], seg_node + ws + lane);
-  };
-  auto issue_leaves = [&](int lbuf, int mbuf, int32_t ws) {
-    const int32_t nsw = min(ws + kWin, cend) - ws;
-    const int32_t L0 = S.sb[mbuf][0];
-    const int32_t nl = S.sb[mbuf][nsw] - L0;
-    for (int32_t i = lane; i < nl; i += 32) {
-      cp_async4(&S.kk[lbuf][i], kidx + L0 + i);
-      cp_async8(&S.tv[lbuf][i], vals + L0 + i);
-    }
-  };
-
-  const int32_t nwin = (cend - cbeg + kWin - 1) / kWin;
-  issue_meta(0, cbeg);
-  cp_async_commit();
-  cp_async_wait<0>();
-  __syncwarp();
-  issue_leaves(0, 0, cbeg);
-  if (nwin > 1) issue_meta(1, cbeg + kWin);
-  cp_async_commit();
-  int32_t cs = cbeg;
-  for (int32_t win = 0; win < nwin; ++win) {
-    cp_async_wait<0>();
-    __syncwarp();
-    const int mb = win % 3, lbf = win & 1;
-    const int32_t ws = cbeg + win * kWin;
-    if (win + 1 < nwin) issue_leaves((win + 1) & 1, (win + 1) % 3, ws + kWin);
-    if (win + 2 < nwin) issue_meta((win + 2) % 3, ws + 2 * kWin);
-    cp_async_commit();
-    const int32_t we = min(ws + kWin, cend);
-    const int32_t L0 = S.sb[mb][0];
-    while (cs < we) {
-      const int32_t lim = min(we, sl_end);
-      const int nv = min(8, lim - cs);
-      const int r = cs - ws + slot;
-      const bool valid = slot < nv;
-      int32_t lb = 0, n = 0, j = 0;
-      if (valid) {
-        lb = S.sb[mb][r] - L0;
-        n = S.sb[mb][r + 1] - S.sb[mb][r];
-        j = S.sn[mb][r];
-      }
-      double4 vr[4];
-      double tt[4];
-#pragma unroll
-      for (int it = 0; it < 4; ++it) {
-        const int32_t k = it < n ? S.kk[lbf][lb + it] : 0;
-        tt[it] = it < n ? S.tv[lbf][lb + it] : 0.0;
-        vr[it] = it < n ? row4<VECV>(V + static_cast<int64_t>(k) * S_, 4 * c4, S_)
-                        : make_double4(0, 0, 0, 0);
-      }
-      const double4 ur = valid ? row4<VECU>(U + static_cast<int64_t>(j) * R, 4 * c4, R)
-                               : make_double4(0, 0, 0, 0);
-      double4 x = make_double4(0, 0, 0, 0);
-#pragma unroll
-      for (int it = 0; it < 4; ++it) fma4(x, tt[it], vr[it]);  // X[s] += t * V[k,s]
-      // column quads -> fragments of both K-chunks (one xor-16 exchange)
-      const double sx0 = ch == 0 ? x.z : x.x, sx1 = ch == 0 ? x.w : x.y;
-      const double su0 = ch == 0 ? ur.z : ur.x, su1 = ch == 0 ? ur.w : ur.y;
-      const double rx0 = __shfl_xor_sync(0xffffffffu, sx0, 16);
-      const double rx1 = __shfl_xor_sync(0xffffffffu, sx1, 16);
-      const double ru0 = __shfl_xor_sync(0xffffffffu, su0, 16);
-      const double ru1 = __shfl_xor_sync(0xffffffffu, su1, 16);
-      const double bA0 = ch == 0 ? x.x : rx0, bA1 = ch == 0 ? x.y : rx1;
-      const double bB0 = ch == 0 ? rx0 : x.z, bB1 = ch == 0 ? rx1 : x.w;
-      const double aA0 = ch == 0 ? ur.x : ru0, aA1 = ch == 0 ? ur.y : ru1;
-      const double aB0 = ch == 0 ? ru0 : ur.z, aB1 = ch == 0 ? ru1 : ur.w;
-      // rank-1 updates of 8 segments: two K-chunks into the same 16x16 tile
-      dmma_8x8x4(acc[0], acc[1], aA0, bA0);
-      dmma_8x8x4(acc[2], acc[3], aA0, bA1);
-      dmma_8x8x4(acc[4], acc[5], aA1, bA0);
-      dmma_8x8x4(acc[6], acc[7], aA1, bA1);
-      dmma_8x8x4(acc[0], acc[1], aB0, bB0);
-      dmma_8x8x4(acc[2], acc[3], aB0, bB1);
-      dmma_8x8x4(acc[4], acc[5], aB1, bB0);
-      dmma_8x8x4(acc[6], acc[7], aB1, bB1);
-      pending = true;
-      cs += nv;
-      if (cs == sl_end) {
-        flush(head ? 0 : -1);
-        pending = false;
-        head = false;
-        if (cs < cend) {
-          ++sl;
-          sl_end = nx_end;
-          row = nx_row;
-          nx_end = sl + 2 <= t.nlev[0] ? __ldg(slice_seg + sl + 2) : 0;
-          nx_row = sl + 1 < t.nlev[0] ? __ldg(t.idx[0] + sl + 1) : 0;
-        }
-      }
-    }
-    __syncwarp();
-  }
-  if (pending) flush(head ? 0 : 1);
-}
-
-// Packed variant (default): the warp walks length-sorted groups of 8
+// Packed variant (mode 6): the warp walks length-sorted groups of 8
 // equal-length segments (pack.cu), so each of a group's n V-row gathers and
 // its U-row gather is a full 8-row 256-bit load with a warp-uniform trip
 // count. Group headers are prefetched two groups ahead and the leaf
-// coordinates of the next group one group ahead. Fragment mapping as in the
-// wide variant (slot = 4*ch + q, column quad c4, one xor-16 exchange).
+// coordinates of the next group one group ahead. Lane L = (q = L%4,
+// c4 = (L/4)%4, ch = L/16) gathers slot 4*ch + q, columns [4*c4, 4*c4+4) of
+// its rows (fragment order), one xor-16 exchange builds both K-chunks.
 template <bool VECU, bool VECV>
 __global__ void __launch_bounds__(kBlock, 2) k_ttmc3pk(RootOutArgs a) {
   const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
@@ -1720,20 +1312,6 @@ void launch_ttmc3(const RootOutArgs& a, cudaStream_t s) {
     SPTTN_CUDA(cudaGetLastError());
     return;
   }
-  if (mode == 5) {
-    // wide gathers need 32-byte aligned rows: R, S multiples of 4 (a.vec bits 4/8)
-    const bool wu = a.vec & 4, wv = a.vec & 8;
-    if (wu && wv)
-      k_ttmc3w<true, true><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
-    else if (wu)
-      k_ttmc3w<true, false><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
-    else if (wv)
-      k_ttmc3w<false, true><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
-    else
-      k_ttmc3w<false, false><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
-    SPTTN_CUDA(cudaGetLastError());
-    return;
-  }
   if (mode == 4) {
     if (vu && vv)
       k_ttmc3s<true, true><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
@@ -1743,37 +1321,6 @@ void launch_ttmc3(const RootOutArgs& a, cudaStream_t s) {
       k_ttmc3s<false, true><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
     else
       k_ttmc3s<false, false><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
-    SPTTN_CUDA(cudaGetLastError());
-    return;
-  }
-  if (mode == 3) {
-    if (vu && vv)
-      k_ttmc3p<true, true><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
-    else if (vu)
-      k_ttmc3p<true, false><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
-    else if (vv)
-      k_ttmc3p<false, true><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
-    else
-      k_ttmc3p<false, false><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
-    SPTTN_CUDA(cudaGetLastError());
-    return;
-  }
-  if (mode == 1 || mode == 2) {
-#define SPTTN_TTMC3D(NG)                                                                  \
-  if (vu && vv)                                                                           \
-    k_ttmc3d<true, true, NG><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);         \
-  else if (vu)                                                                            \
-    k_ttmc3d<true, false, NG><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);        \
-  else if (vv)                                                                            \
-    k_ttmc3d<false, true, NG><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);        \
-  else                                                                                    \
-    k_ttmc3d<false, false, NG><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
-    if (mode == 1) {
-      SPTTN_TTMC3D(1)
-    } else {
-      SPTTN_TTMC3D(2)
-    }
-#undef SPTTN_TTMC3D
     SPTTN_CUDA(cudaGetLastError());
     return;
   }
