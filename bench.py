@@ -102,8 +102,14 @@ class Clocks:
             self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=self.f, stderr=subprocess.DEVNULL)
+            # nvidia-smi needs ~0.1-0.3 s to start: wait for its first sample so
+            # even short timed regions are covered (that pre-region sample is
+            # dropped from the summary when later ones exist)
+            t0 = time.time()
+            while time.time() - t0 < 3.0 and not Path(self.f.name).read_text().strip():
+                time.sleep(0.01)
         except Exception:
             self.proc = None
         return self
@@ -127,6 +133,8 @@ class Clocks:
                 rows.append(parts)
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        if len(rows) > 1:
+            rows = rows[1:]  # the first sample predates the timed region
         sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
