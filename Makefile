@@ -38,9 +38,15 @@ build/device/%.o: $(PKG)/csrc/device/%.cu $(DEV_HDR)
 	@mkdir -p $(dir $@)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
+# the forest interpreter follows the reference's host arithmetic exactly
+# (separate multiply and add): no FMA contraction in this file
+build/device/generic.o: $(PKG)/csrc/device/generic.cu $(DEV_HDR)
+	@mkdir -p $(dir $@)
+	$(NVCC) $(NVFLAGS) -fmad=false -c $< -o $@
+
 $(LIB)/libspttn_b200.so: $(DEV_OBJS)
 	@mkdir -p $(LIB)
-	$(NVCC) $(ARCH) -shared $^ -o $@
+	$(NVCC) $(ARCH) -shared $^ -o $@ -lnvrtc -Xlinker -rpath,/usr/local/cuda/lib64
 
 $(LIB)/libspttn_probe.so: $(PKG)/csrc/probe/fp64_peak.cu
 	@mkdir -p $(LIB)

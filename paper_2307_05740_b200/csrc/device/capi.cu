@@ -544,6 +544,14 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
         SPTTN_CUDA(cudaGetLastError());
       }
       p->launches = 2 + (p->gen.par_mode == 2 ? 1 : 0);
+      // Specialised kernel for this forest (jit.cu) when the tensor is large
+      // enough to amortise an NVRTC compile (cached per distinct nest):
+      // SPTTN_GENERIC_JIT=1 always, 0 never, default from 65536 nonzeros.
+      const int64_t jit_env = env_int("SPTTN_GENERIC_JIT", -1);
+      const bool want_jit = !p->prog->observe &&
+                            (jit_env == 1 || (jit_env < 0 && nnz >= (int64_t{1} << 16)));
+      if (want_jit && spttn_dev::jit_available())
+        p->gen.jit_kernel = spttn_dev::jit_prepare(*p->prog, p->gen);
     } else if (p->kind == SPTTN_NEST_MTTKRP3_J || p->kind == SPTTN_NEST_MTTKRP3_K) {
       // output rows on CSF level 1 / 2: packed 4-slot groups of (i,j)
       // segments, atomics into a zeroed output (no items, no fix-up)
@@ -700,7 +708,12 @@ int spttn_execute_stage(spttn_plan* p, int stage, void* stream) {
     cudaStream_t s = as_stream(stream);
     const auto& D = p->csf->d;
     if (p->kind == SPTTN_NEST_GENERIC) {
-      if (stage != 1) spttn_dev::generic_execute(*p->prog, D, p->d_dense, p->out, p->gen, s);
+      if (stage != 1) {
+        if (p->gen.jit_kernel)
+          spttn_dev::jit_execute(p->gen.jit_kernel, *p->prog, D, p->d_dense, p->out, p->gen, s);
+        else
+          spttn_dev::generic_execute(*p->prog, D, p->d_dense, p->out, p->gen, s);
+      }
       return;
     }
     spttn_dev::RootOutArgs a{};

@@ -467,6 +467,12 @@ void generic_execute(const spg_program& prog, const DevCsf& csf, const double* c
   SPTTN_CUDA(cudaGetLastError());
 }
 
+void generic_reduce(const GenericState& g, double* out, cudaStream_t s) {
+  k_generic_reduce<<<static_cast<unsigned>((g.out_size + 255) / 256), 256, 0, s>>>(
+      g.priv_out, g.workers, g.out_size, out);
+  SPTTN_CUDA(cudaGetLastError());
+}
+
 void generic_free(GenericState& g) {
   if (g.in_arena) {  // owned by the plan arena
     g = GenericState{};

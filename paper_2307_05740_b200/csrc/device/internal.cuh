@@ -221,10 +221,21 @@ struct GenericState {
   int64_t workers = 1;
   double* priv_out = nullptr;  // mode 2: [workers][out_size]
   int64_t out_size = 0;
+  void* jit_kernel = nullptr;  // specialised kernel (jit.cu), or the interpreter
 };
 void generic_execute(const spg_program& prog, const DevCsf& csf, const double* const* dense,
                      double* out, GenericState& g, cudaStream_t s);
 void generic_free(GenericState& g);
+// mode 2: out = sum of the per-worker output copies, in worker order
+void generic_reduce(const GenericState& g, double* out, cudaStream_t s);
+
+// ---- fused-nest JIT (jit.cu) -----------------------------------------------
+bool jit_available();
+// compiles (or fetches from the process cache) the specialised kernel of a
+// program for g's parallel mode; returns a cudaKernel_t
+void* jit_prepare(const spg_program& prog, const GenericState& g);
+void jit_execute(void* kernel, const spg_program& prog, const DevCsf& csf,
+                 const double* const* dense, double* out, GenericState& g, cudaStream_t s);
 
 struct UnfactArgs;
 void unfactorized_run(const void* desc, const DevCsf& csf, const double* const* dense,

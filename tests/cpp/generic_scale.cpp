@@ -136,6 +136,32 @@ int main(int argc, char** argv) {
     bad += run("mode k, max-buf-dim order", s3, t3, "((A*B)*T)", "i,j,a;i,j,a,k", &want3);
     (void)in2;
   }
+  {
+    // TTTc-4 through the JIT-compiled nest vs the
+    // interpreter, on the max-buf-dim planner's path / order
+    KernelSpec spec = tttc4(60, 8);
+    Tensors t = make_tensors(spec, random_coo(spec, 0.02, 31));
+    std::printf("TTTc-4 60^4 R=8 nnz %lld\n", static_cast<long long>(t.csf.nnz()));
+    auto in = t.inputs();
+    auto model = max_buffer_dim_model();
+    auto [path, result] = joint_search(spec, *model);
+    auto timed = [&](const char* jit) {
+      setenv("SPTTN_GENERIC_JIT", jit, 1);
+      auto t0 = std::chrono::steady_clock::now();
+      ExecPlan plan = prepare(spec, path, result.best.order, in);
+      const double tp = seconds_since(t0);
+      unsetenv("SPTTN_GENERIC_JIT");
+      execute(plan);
+      t0 = std::chrono::steady_clock::now();
+      ExecResult r = execute(plan);
+      std::printf("  %-12s prepare %8.2f ms  execute %9.2f ms\n", jit[0] == '1' ? "JIT" : "interpreter",
+                  tp * 1e3, seconds_since(t0) * 1e3);
+      return r.dense_out.values;
+    };
+    const std::vector<double> a = timed("1"), b = timed("0");
+    std::printf("  bit-identical: %s\n", a == b ? "yes" : "NO");
+    bad += a != b;
+  }
   std::printf("%s\n", bad ? "FAILED" : "all match");
   return bad ? 1 : 0;
 }

@@ -388,6 +388,42 @@ int main() {
     }
   });
 
+  run_case("JIT-compiled nests equal the interpreter bit for bit (TTTc-4, sparse out, other paths)", [] {
+    struct Case {
+      KernelSpec spec;
+      double density;
+      int max_orders;
+    };
+    std::vector<Case> cases;
+    cases.push_back({tttc4(5, 3), 0.3, 12});
+    cases.push_back({mttkrp3(12, 11, 10, 4), 0.2, 12});
+    cases.push_back({tttp3(7, 6, 5, 3), 0.3, 12});
+    for (auto& c : cases) {
+      Tensors t = make_tensors(c.spec, random_coo(c.spec, c.density, 29));
+      auto in = t.inputs();
+      ExecResult oracle = execute_unfactorized(c.spec, in);
+      int n = 0;
+      for (const auto& path : filter_min_depth(enumerate_paths(c.spec)))
+        for (const auto& order : enumerate_orders(c.spec, path, default_csf_order(c.spec))) {
+          if (n >= c.max_orders) break;
+          setenv("SPTTN_GENERIC_JIT", "1", 1);
+          ExecPlan pj = prepare(c.spec, path, order, in);
+          setenv("SPTTN_GENERIC_JIT", "0", 1);
+          ExecPlan pi = prepare(c.spec, path, order, in);
+          unsetenv("SPTTN_GENERIC_JIT");
+          if (spttn_b200_plan_device_kind(pj) != SPTTN_NEST_GENERIC) continue;
+          ExecResult rj = execute(pj), ri = execute(pi);
+          CHECK(rj.dense_out.values == ri.dense_out.values);
+          CHECK(rj.sparse_out_values == ri.sparse_out_values);
+          CHECK(rj.stats.multiply_adds == ri.stats.multiply_adds);
+          CHECK(rj.stats.buffer_resets == ri.stats.buffer_resets);
+          CHECK(close(rj, oracle));
+          ++n;
+        }
+      CHECK(n > 0);
+    }
+  });
+
   run_case("device build_csf equals the reference build_csf (any mode order)", [] {
     CooTensor coo;
     coo.indices = {{"i", 23}, {"j", 17}, {"k", 29}};
