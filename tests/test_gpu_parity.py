@@ -360,3 +360,30 @@ def test_device_csf_permute_reroots(E):
     out = plan.read_output()
     ref, norm = oracle_with_norm(6, w.csf, [A, Cf], (R, 0, 0))
     assert_parity(out, ref, norm, "re-rooted mode-j MTTKRP")
+
+
+def test_device_csf_permute_edge_cases(E):
+    """Re-rooting an empty tensor, a 4-D tensor in every rotation, and the
+    order-1 / order-2 device builds."""
+    from paper_2307_05740_b200.tensor import Csf
+    empty = E.DeviceCsf.from_coo([4, 5, 6], np.zeros((0, 3), np.int64), np.zeros(0))
+    assert empty.permute([2, 0, 1]).download().level_sizes() == [0, 0, 0]
+    rng = np.random.default_rng(11)
+    dims = [7, 6, 5, 8]
+    coords = np.unique(np.stack([rng.integers(0, d, 400) for d in dims], axis=1), axis=0)
+    vals = rng.uniform(-1, 1, coords.shape[0])
+    dev = E.DeviceCsf.from_coo(dims, coords, vals)
+    for order in ([1, 0, 2, 3], [3, 2, 1, 0], [2, 3, 0, 1]):
+        got = dev.permute(order).download()
+        want = Csf.from_coo([dims[o] for o in order], coords[:, order], vals)
+        for a, b in zip(got.idx + got.ptr, want.idx + want.ptr):
+            assert np.array_equal(a, b)
+        assert np.array_equal(got.values, want.values)
+    for d in (1, 2):
+        c = np.unique(rng.integers(0, 9, (30, d)), axis=0)
+        v = rng.uniform(-1, 1, c.shape[0])
+        got = E.DeviceCsf.from_coo([9] * d, c, v).download()
+        want = Csf.from_coo([9] * d, c, v)
+        for a, b in zip(got.idx + got.ptr, want.idx + want.ptr):
+            assert np.array_equal(a, b)
+        assert np.array_equal(got.values, want.values)
