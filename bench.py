@@ -258,6 +258,43 @@ def _ref_run(w, sub, threads, repeats=1):
     return secs
 
 
+def csf_build_config(P, w, stream, ref_sample=1_000_000):
+    """the headline tensor's CSF built on the GPU from its
+    COO (shuffled rows in pinned host memory; H2D + radix-sort build, through
+    spttn_csf_from_coo) vs the reference's CooTensor::normalize + build_csf
+    (oracle/_ref, host) on a bounded sample of the same rows."""
+    import torch
+    coo, vals = w.csf.to_coo()
+    perm = np.random.default_rng(1).permutation(vals.shape[0])
+    pc = pinned_copy(np.ascontiguousarray(coo[perm]))
+    pv = pinned_copy(np.ascontiguousarray(vals[perm]))
+    ts = []
+    for it in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        dev = P.DeviceCsf.from_coo(w.csf.dims, pc.numpy(), pv.numpy(), stream=stream)
+        torch.cuda.synchronize()
+        if it:
+            ts.append(time.perf_counter() - t0)
+        dev.close()
+    out = {"device_ms": 1e3 * min(ts), "nnz": int(vals.shape[0]),
+           "device_nnz_per_s": vals.shape[0] / min(ts)}
+    try:
+        sys.path.insert(0, str(ROOT / "tests"))
+        import oracle_bindings as OB  # the reference build (test infrastructure)
+        if OB.ref_available():
+            n = min(ref_sample, vals.shape[0])
+            names = list(w.cfg.mode_names)
+            t0 = time.perf_counter()
+            OB.ref_build_csf(names, list(w.csf.dims), coo[perm][:n], vals[perm][:n], names)
+            tr = time.perf_counter() - t0
+            out.update({"reference_sample_nnz": int(n), "reference_s": tr,
+                        "reference_nnz_per_s": n / tr, "reference_cores": 1})
+    except Exception as e:  # noqa: BLE001
+        out["reference"] = f"unavailable: {e}"
+    return out
+
+
 def cpu_sample(w, seconds, threads):
     """Every k-th root slice of the tensor, k calibrated on a ~1/64 probe so
     the reference executor needs about `seconds`."""
@@ -423,6 +460,8 @@ def main():
                         "breakdown_ms": e["breakdown_ms"]}
         if rank == 0 and world == 1 and not args.no_cpu:
             r["cpu_baseline"] = cpu_reference(w, args.cpu_seconds, 1)
+            if key == HEADLINE:
+                r["csf_build"] = csf_build_config(P, w, stream)
         if key == HEADLINE:
             head_clocks = clk.summary()
         else:
