@@ -454,6 +454,12 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
       // copies reduced in worker order (mode 2). Replicas are capped at
       // 512 MB. SPTTN_GENERIC_PAR=0 forces the sequential walk.
       auto& g = p->gen;
+      // Specialised kernel for this forest (jit.cu) when the tensor is large
+      // enough to amortise an NVRTC compile (cached per distinct nest):
+      // SPTTN_GENERIC_JIT=1 always, 0 never, default from 65536 nonzeros.
+      const int64_t jit_env = env_int("SPTTN_GENERIC_JIT", -1);
+      const bool want_jit = !G.observe && spttn_dev::jit_available() &&
+                            (jit_env == 1 || (jit_env < 0 && nnz >= (int64_t{1} << 16)));
       {
         const int64_t n0 = D.level_size[0];
         const spg_node* rootn = G.num_roots == 1 ? &G.nodes[G.roots[0]] : nullptr;
@@ -479,6 +485,39 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
             g.par_mode = disjoint ? 1 : 2;
             g.workers = W;
             g.out_size = G.out_size;
+            g.priv = !disjoint;
+          }
+        }
+        // The JIT kernel admits more decompositions (jit.cu jit_analyze):
+        // level-1 fibers as work units (few heavy root slices), and forests
+        // whose root loop accumulates into buffers reset once before it and
+        // consumed by later roots (TTTc-like chains): per-worker
+        // accumulators summed in worker order, then the later roots.
+        if (want_jit && env_int("SPTTN_GENERIC_PAR", 1) != 0 && n0 >= 2) {
+          const spttn_dev::JitSplit js = spttn_dev::jit_analyze(G);
+          const int64_t n1 = D.order > 1 ? D.level_size[1] : 0;
+          const bool fiber = js.ok && js.fiber_ok && n1 >= 4 * n0;
+          if (js.ok && (js.tail || fiber)) {
+            const bool disjoint = fiber ? js.disjoint_fiber : js.disjoint_slice;
+            const bool priv = js.writes_out && !disjoint;
+            const int64_t budget = int64_t{512} << 20;
+            const int64_t per = std::max<int64_t>(8, off[nb] * 8) +
+                                (priv ? std::max<int64_t>(8, G.out_size * 8) : 0);
+            int64_t W = fiber ? std::min<int64_t>(n1, static_cast<int64_t>(sm_count()) * 64)
+                              : std::min<int64_t>(n0, static_cast<int64_t>(sm_count()) * 32);
+            W = std::min<int64_t>(W, budget / per);
+            if (W >= 2) {
+              g.par_mode = fiber ? 3 : 2;
+              g.workers = W;
+              g.out_size = G.out_size;
+              g.priv = priv;
+              g.tail = js.tail;
+              g.n_tail_bufs = js.n_rset;
+              for (int i = 0; i < js.n_rset; ++i) {
+                g.tail_off[i] = off[js.rset[i]];
+                g.tail_len[i] = G.buffer_size[js.rset[i]];
+              }
+            }
           }
         }
       }
@@ -487,7 +526,7 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
       const size_t n_buf = static_cast<size_t>(std::max<int64_t>(1, off[nb]) * reps) * 8;
       const size_t n_out = static_cast<size_t>(std::max<int64_t>(1, G.out_size)) * 8;
       const size_t n_priv =
-          g.par_mode == 2 ? static_cast<size_t>(std::max<int64_t>(1, G.out_size) * reps) * 8 : 0;
+          g.priv ? static_cast<size_t>(std::max<int64_t>(1, G.out_size) * reps) * 8 : 0;
       const bool lookup = G.need_leaf_lookup && nnz > 0;
       size_t total = n_cnt + n_buf + n_out + n_priv;  // contiguous, 8-byte aligned
       total = al(total) + al(sizeof(spg_program)) + al((nb + 1) * sizeof(int64_t)) +
@@ -503,7 +542,7 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
       g.counters = reinterpret_cast<int64_t*>(cur);
       g.buffers = reinterpret_cast<double*>(cur + n_cnt);
       p->out = reinterpret_cast<double*>(cur + n_cnt + n_buf);
-      if (g.par_mode == 2) g.priv_out = reinterpret_cast<double*>(cur + n_cnt + n_buf + n_out);
+      if (g.priv) g.priv_out = reinterpret_cast<double*>(cur + n_cnt + n_buf + n_out);
       g.zero_bytes = n_cnt + n_buf + n_out + n_priv;
       cur += al(g.zero_bytes);
       g.total_buffer_elems = off[nb];
@@ -543,14 +582,10 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
             D.view(), p->gen.d_prog, p->gen.leaf_keys, p->gen.leaf_pos);
         SPTTN_CUDA(cudaGetLastError());
       }
-      p->launches = 2 + (p->gen.par_mode == 2 ? 1 : 0);
-      // Specialised kernel for this forest (jit.cu) when the tensor is large
-      // enough to amortise an NVRTC compile (cached per distinct nest):
-      // SPTTN_GENERIC_JIT=1 always, 0 never, default from 65536 nonzeros.
-      const int64_t jit_env = env_int("SPTTN_GENERIC_JIT", -1);
-      const bool want_jit = !p->prog->observe &&
-                            (jit_env == 1 || (jit_env < 0 && nnz >= (int64_t{1} << 16)));
-      if (want_jit && spttn_dev::jit_available())
+      p->launches = 2 + (p->gen.priv ? 1 : 0) + (p->gen.tail ? p->gen.n_tail_bufs + 1 : 0);
+      const int64_t jit_env2 = env_int("SPTTN_GENERIC_JIT", -1);
+      if (!p->prog->observe && spttn_dev::jit_available() &&
+          (jit_env2 == 1 || (jit_env2 < 0 && nnz >= (int64_t{1} << 16))))
         p->gen.jit_kernel = spttn_dev::jit_prepare(*p->prog, p->gen);
     } else if (p->kind == SPTTN_NEST_MTTKRP3_J || p->kind == SPTTN_NEST_MTTKRP3_K) {
       // output rows on CSF level 1 / 2: packed 4-slot groups of (i,j)

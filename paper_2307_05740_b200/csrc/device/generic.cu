@@ -453,6 +453,7 @@ void generic_execute(const spg_program& prog, const DevCsf& csf, const double* c
   I.nkeys = g.n_leaf_keys;
   static_assert(sizeof(spg_program) % sizeof(int4) == 0, "program must be int4-copyable");
   static_assert(sizeof(spg_program) <= 48 * 1024, "program must fit default shared memory");
+  if (g.tail || g.par_mode > 2) throw Status(SPTTN_EINVAL, "JIT-only decomposition without a JIT kernel");
   if (g.par_mode == 0) {
     k_generic<<<1, 256, sizeof(spg_program), s>>>(I);
   } else {
@@ -470,6 +471,25 @@ void generic_execute(const spg_program& prog, const DevCsf& csf, const double* c
 void generic_reduce(const GenericState& g, double* out, cudaStream_t s) {
   k_generic_reduce<<<static_cast<unsigned>((g.out_size + 255) / 256), 256, 0, s>>>(
       g.priv_out, g.workers, g.out_size, out);
+  SPTTN_CUDA(cudaGetLastError());
+}
+
+// worker 0's copy of each accumulator = sum over workers, in worker order
+__global__ void k_buffer_reduce(double* bufs, int64_t workers, int64_t stride, int64_t off,
+                                int64_t n) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  double sum = 0.0;
+  for (int64_t w = 0; w < workers; ++w) sum += bufs[w * stride + off + e];
+  bufs[off + e] = sum;
+}
+
+void generic_reduce_buffers(const GenericState& g, cudaStream_t s) {
+  for (int i = 0; i < g.n_tail_bufs; ++i) {
+    if (g.tail_len[i] <= 0) continue;
+    k_buffer_reduce<<<static_cast<unsigned>((g.tail_len[i] + 127) / 128), 128, 0, s>>>(
+        g.buffers, g.workers, g.total_buffer_elems, g.tail_off[i], g.tail_len[i]);
+  }
   SPTTN_CUDA(cudaGetLastError());
 }
 

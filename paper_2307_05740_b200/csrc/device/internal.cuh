@@ -222,7 +222,29 @@ struct GenericState {
   double* priv_out = nullptr;  // mode 2: [workers][out_size]
   int64_t out_size = 0;
   void* jit_kernel = nullptr;  // specialised kernel (jit.cu), or the interpreter
+  // JIT-only extensions (jit.cu): mode 3 = level-1 fibers to workers;
+  // `priv` = the root loop's dense output goes through per-worker copies;
+  // `tail` = buffers the root loop accumulates across slices (reset once,
+  // before it) are summed over workers in worker order, then the remaining
+  // roots run on one thread (phase 1)
+  bool priv = false;
+  bool tail = false;
+  int n_tail_bufs = 0;
+  int64_t tail_off[16] = {}, tail_len[16] = {};
 };
+// Which JIT parallel decompositions a forest admits (jit.cu).
+struct JitSplit {
+  bool ok = false;           // root 0 is the CSF level-0 loop, accumulators are safe
+  bool fiber_ok = false;     // root 0 encloses only the level-1 loop, no resets on either
+  bool writes_out = false;   // root 0 writes the output
+  bool disjoint_slice = false, disjoint_fiber = false;
+  bool tail = false;         // more roots, or root-level accumulators
+  int n_rset = 0;
+  int rset[16] = {};
+};
+JitSplit jit_analyze(const spg_program& prog);
+// phase-1 input: per-worker accumulator copies summed into worker 0's
+void generic_reduce_buffers(const GenericState& g, cudaStream_t s);
 void generic_execute(const spg_program& prog, const DevCsf& csf, const double* const* dense,
                      double* out, GenericState& g, cudaStream_t s);
 void generic_free(GenericState& g);

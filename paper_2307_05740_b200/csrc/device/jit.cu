@@ -23,7 +23,10 @@
 #include <mutex>
 #include <sstream>
 #include <string>
+#include <cstdlib>
+#include <cstdio>
 #include <unordered_map>
+#include <vector>
 
 #include "../../../include/spttn_b200.h"
 #include "internal.cuh"
@@ -48,11 +51,12 @@ struct JitArgs {
   const int64_t* leaf_keys;
   const int64_t* leaf_pos;
   int64_t nkeys;
+  int64_t phase;
 };
 
 class Gen {
  public:
-  Gen(const spg_program& P, int par_mode) : P_(P), mode_(par_mode) {}
+  Gen(const spg_program& P, const GenericState& g) : P_(P), mode_(g.par_mode), g_(g) {}
 
   std::string source() {
     std::ostringstream o;
@@ -60,7 +64,8 @@ class Gen {
          "struct JitArgs { const int32_t* idx[8]; const int32_t* ptr[8]; int32_t nlev[8];\n"
          "  const double* vals; const double* const* dense; double* out; double* bufs;\n"
          "  int64_t buf_elems; double* priv; int64_t out_size; int64_t workers;\n"
-         "  int64_t* counters; const int64_t* leaf_keys; const int64_t* leaf_pos; int64_t nkeys; };\n"
+         "  int64_t* counters; const int64_t* leaf_keys; const int64_t* leaf_pos; int64_t nkeys;\n"
+         "  int64_t phase; };\n"
          "extern \"C\" __global__ void __launch_bounds__(128) spg_nest(JitArgs a) {\n"
          "  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;\n"
          "  if (w >= a.workers) return;\n";
@@ -69,7 +74,10 @@ class Gen {
     for (int l = 0; l + 1 < P_.csf_order; ++l)
       o << "  const int32_t* __restrict__ ptr" << l << " = a.ptr[" << l << "];\n";
     o << "  const double* __restrict__ vals = a.vals;\n";
-    o << "  double* out = " << (mode_ == 2 ? "a.priv + w * a.out_size" : "a.out") << ";\n";
+    if (g_.priv && g_.tail)
+      o << "  double* out = a.phase == 0 ? a.priv + w * a.out_size : a.out;\n";
+    else
+      o << "  double* out = " << (g_.priv ? "a.priv + w * a.out_size" : "a.out") << ";\n";
     int64_t off = 0;
     for (int b = 0; b < P_.num_buffers; ++b) {
       o << "  double* B" << b << " = a.bufs + w * a.buf_elems + " << off << "LL;\n";
@@ -87,23 +95,16 @@ class Gen {
     for (int l = 0; l < P_.csf_order; ++l) o << (l ? ", " : "") << "p" << l << " = 0";
     o << ";\n";
     o << "  (void)vals; (void)out;\n";
-    const bool par = mode_ != 0;
-    if (par) {
-      const spg_node& root = P_.nodes[P_.roots[0]];
-      if (mode_ == 1) {
-        o << "  for (;;) {\n"
-             "    const int64_t r = (int64_t)atomicAdd((unsigned long long*)&a.counters["
-          << P_.num_buffers + 3 << "], 1ULL);\n"
-             "    if (r >= a.nlev[0]) break;\n"
-             "    const int64_t rlo = r, rhi = r + 1;\n";
-      } else {
-        o << "  {\n    const int64_t rlo = w * a.nlev[0] / a.workers, rhi = (w + 1) * a.nlev[0] / a.workers;\n";
-      }
-      emit_node(o, P_.roots[0], 2, true);
-      o << "  }\n";
-      (void)root;
-    } else {
+    if (mode_ == 0) {
       for (int r = 0; r < P_.num_roots; ++r) emit_node(o, P_.roots[r], 1, false);
+    } else {
+      if (g_.tail) o << "  if (a.phase == 0) {\n";
+      emit_parallel_root(o);
+      if (g_.tail) {
+        o << "  } else {\n";
+        for (int r = 1; r < P_.num_roots; ++r) emit_node(o, P_.roots[r], 2, false);
+        o << "  }\n";
+      }
     }
     o << "  atomicAdd((unsigned long long*)&a.counters[0], (unsigned long long)madds);\n";
     for (int b = 0; b < P_.num_buffers; ++b)
@@ -116,6 +117,55 @@ class Gen {
  private:
   const spg_program& P_;
   int mode_;
+  const GenericState& g_;
+
+  // Root 0 restricted to this worker's work units: atomically claimed root
+  // slices (mode 1), a static range of slices (mode 2) or of level-1
+  // fibers (mode 3, p0 follows along). Root-level resets zero each worker's
+  // private accumulators; only worker 0 counts them (they happen once in
+  // the sequential walk).
+  void emit_parallel_root(std::ostringstream& o) {
+    const spg_node& root = P_.nodes[P_.roots[0]];
+    if (mode_ == 3) {
+      const spg_node& l1 = P_.nodes[P_.children[root.child_begin]];
+      emit_resets(o, root, 1, true);
+      o << "  {\n"
+           "    const int64_t n1 = a.nlev[1];\n"
+           "    const int64_t flo = w * n1 / a.workers, fhi = (w + 1) * n1 / a.workers;\n"
+           "    if (flo < fhi) {\n"
+           "      int64_t lo = 0, hi = a.nlev[0];\n"
+           "      while (hi - lo > 1) { const int64_t mid = (lo + hi) >> 1;"
+           " if (ptr0[mid] <= flo) lo = mid; else hi = mid; }\n"
+           "      p0 = lo;\n"
+           "      v" << root.index << " = idx0[p0];\n"
+           "      for (p1 = flo; p1 < fhi; ++p1) {\n"
+           "        while (ptr0[p0 + 1] <= p1) { ++p0; v" << root.index << " = idx0[p0]; }\n"
+           "        v" << l1.index << " = idx1[p1];\n";
+      for (int c = 0; c < l1.child_count; ++c) emit_node(o, P_.children[l1.child_begin + c], 4, false);
+      o << "      }\n    }\n  }\n";
+      return;
+    }
+    if (mode_ == 1) {
+      o << "  for (;;) {\n"
+           "    const int64_t r = (int64_t)atomicAdd((unsigned long long*)&a.counters["
+        << P_.num_buffers + 3 << "], 1ULL);\n"
+           "    if (r >= a.nlev[0]) break;\n"
+           "    const int64_t rlo = r, rhi = r + 1;\n";
+    } else {
+      o << "  {\n    const int64_t rlo = w * a.nlev[0] / a.workers, rhi = (w + 1) * a.nlev[0] / a.workers;\n";
+    }
+    emit_node(o, P_.roots[0], 2, true);
+    o << "  }\n";
+  }
+
+  void emit_resets(std::ostringstream& o, const spg_node& nd, int d, bool once) {
+    for (int r = 0; r < nd.reset_count; ++r) {
+      const int b = P_.resets[nd.reset_begin + r];
+      o << ind(d) << "for (int64_t e = 0; e < " << P_.buffer_size[b] << "LL; ++e) B" << b
+        << "[e] = 0.0;\n"
+        << ind(d) << (once ? "if (w == 0) " : "") << "++rs" << b << ";\n";
+    }
+  }
 
   static std::string ind(int d) { return std::string(2 * d, ' '); }
 
@@ -143,12 +193,7 @@ class Gen {
 
   void emit_node(std::ostringstream& o, int v, int d, bool top) {
     const spg_node& nd = P_.nodes[v];
-    for (int r = 0; r < nd.reset_count; ++r) {
-      const int b = P_.resets[nd.reset_begin + r];
-      o << ind(d) << "for (int64_t e = 0; e < " << P_.buffer_size[b] << "LL; ++e) B" << b
-        << "[e] = 0.0;\n"
-        << ind(d) << "++rs" << b << ";\n";
-    }
+    emit_resets(o, nd, d, top);
     if (nd.kind == SPG_LEAF) {
       emit_leaf(o, nd.term, d);
       return;
@@ -285,8 +330,12 @@ bool jit_available() {
 }
 
 void* jit_prepare(const spg_program& prog, const GenericState& g) {
-  Gen gen(prog, g.par_mode);
-  return reinterpret_cast<void*>(compile(gen.source()));
+  Gen gen(prog, g);
+  const std::string src = gen.source();
+  if (const char* d = std::getenv("SPTTN_JIT_DUMP"); d && *d && *d != '0')
+    std::fprintf(stderr, "// ---- spttn JIT nest (mode %d, %lld workers) ----\n%s\n", g.par_mode,
+                 static_cast<long long>(g.workers), src.c_str());
+  return reinterpret_cast<void*>(compile(src));
 }
 
 void jit_execute(void* kernel, const spg_program& P, const DevCsf& csf,
@@ -311,11 +360,90 @@ void jit_execute(void* kernel, const spg_program& P, const DevCsf& csf,
   a.leaf_keys = g.leaf_keys;
   a.leaf_pos = g.leaf_pos;
   a.nkeys = g.n_leaf_keys;
+  a.phase = 0;
   void* args[] = {&a};
   const unsigned blocks = static_cast<unsigned>((a.workers + 127) / 128);
   SPTTN_CUDA(cudaLaunchKernel(kernel, dim3(blocks), dim3(128), args, 0, s));
   (void)P;
-  if (g.par_mode == 2) generic_reduce(g, out, s);
+  if (g.priv) generic_reduce(g, out, s);
+  if (g.tail) {
+    generic_reduce_buffers(g, s);
+    a.phase = 1;
+    a.workers = 1;
+    SPTTN_CUDA(cudaLaunchKernel(kernel, dim3(1), dim3(128), args, 0, s));
+  }
+}
+
+JitSplit jit_analyze(const spg_program& G) {
+  JitSplit js;
+  if (G.observe || G.num_roots < 1) return js;
+  const spg_node& r = G.nodes[G.roots[0]];
+  if (r.kind != SPG_SPARSE || r.csf_level != 0 || r.hook >= 0) return js;
+  bool in_r[SPG_MAX_BUFFERS] = {};
+  for (int k = 0; k < r.reset_count; ++k) {
+    const int b = G.resets[r.reset_begin + k];
+    if (!in_r[b] && js.n_rset < 16) js.rset[js.n_rset++] = b;
+    in_r[b] = true;
+  }
+  const spg_node* l1 = nullptr;
+  if (r.child_count == 1) {
+    const spg_node& c = G.nodes[G.children[r.child_begin]];
+    if (c.kind == SPG_SPARSE && c.csf_level == 1 && c.reset_count == 0 && c.hook < 0) l1 = &c;
+  }
+  auto term_of = [&](const spg_node& n) {
+    if (n.kind == SPG_LEAF) return static_cast<int>(n.term);
+    return n.hook >= 0 ? static_cast<int>(G.hooks[n.hook].term) : -1;
+  };
+  auto has = [](const spg_access& a, int id) {
+    for (int k = 0; k < a.naddr; ++k)
+      if (a.ids[k] == id && a.strides[k] != 0) return true;
+    return false;
+  };
+  bool ok = true, ds = true, df = l1 != nullptr;
+  std::vector<int> st(G.children + r.child_begin, G.children + r.child_begin + r.child_count);
+  while (!st.empty()) {
+    const spg_node& n = G.nodes[st.back()];
+    st.pop_back();
+    for (int k = 0; k < n.reset_count; ++k) ok &= !in_r[G.resets[n.reset_begin + k]];
+    const int t = term_of(n);
+    if (t >= 0) {
+      for (const spg_access* a : {&G.lhs[t], &G.rhs[t]})
+        ok &= !(a->kind == SPG_OP_BUFFER && in_r[a->slot]);
+      const spg_access& o = G.out[t];
+      if (o.kind == SPG_OP_OUT_DENSE || o.kind == SPG_OP_OUT_SPARSE) js.writes_out = true;
+      if (o.kind == SPG_OP_OUT_DENSE) {
+        ds &= has(o, r.index);
+        df &= l1 && has(o, r.index) && has(o, l1->index);
+      }
+    }
+    if (n.kind != SPG_LEAF && n.hook < 0)
+      for (int c = 0; c < n.child_count; ++c) st.push_back(G.children[n.child_begin + c]);
+  }
+  // later roots run sequentially after the accumulators are summed: every
+  // buffer they read is one of those or is reset among them
+  bool reset_tail[SPG_MAX_BUFFERS] = {};
+  std::vector<int> tail;
+  for (int q = 1; q < G.num_roots; ++q) st.push_back(G.roots[q]);
+  while (!st.empty()) {
+    const spg_node& n = G.nodes[st.back()];
+    st.pop_back();
+    tail.push_back(static_cast<int>(&n - G.nodes));
+    for (int k = 0; k < n.reset_count; ++k) reset_tail[G.resets[n.reset_begin + k]] = true;
+    if (n.kind != SPG_LEAF && n.hook < 0)
+      for (int c = 0; c < n.child_count; ++c) st.push_back(G.children[n.child_begin + c]);
+  }
+  for (int v : tail) {
+    const int t = term_of(G.nodes[v]);
+    if (t < 0) continue;
+    for (const spg_access* a : {&G.lhs[t], &G.rhs[t]})
+      ok &= !(a->kind == SPG_OP_BUFFER && !in_r[a->slot] && !reset_tail[a->slot]);
+  }
+  js.ok = ok;
+  js.fiber_ok = l1 != nullptr;
+  js.disjoint_slice = ds;
+  js.disjoint_fiber = df;
+  js.tail = G.num_roots > 1 || js.n_rset > 0;
+  return js;
 }
 
 }  // namespace spttn_dev

@@ -145,22 +145,31 @@ int main(int argc, char** argv) {
     auto in = t.inputs();
     auto model = max_buffer_dim_model();
     auto [path, result] = joint_search(spec, *model);
-    auto timed = [&](const char* jit) {
+    auto timed = [&](const char* what, const char* jit, const char* par) {
       setenv("SPTTN_GENERIC_JIT", jit, 1);
+      setenv("SPTTN_GENERIC_PAR", par, 1);
       auto t0 = std::chrono::steady_clock::now();
       ExecPlan plan = prepare(spec, path, result.best.order, in);
       const double tp = seconds_since(t0);
       unsetenv("SPTTN_GENERIC_JIT");
+      unsetenv("SPTTN_GENERIC_PAR");
       execute(plan);
       t0 = std::chrono::steady_clock::now();
       ExecResult r = execute(plan);
-      std::printf("  %-12s prepare %8.2f ms  execute %9.2f ms\n", jit[0] == '1' ? "JIT" : "interpreter",
-                  tp * 1e3, seconds_since(t0) * 1e3);
+      std::printf("  %-22s prepare %8.2f ms  execute %9.2f ms\n", what, tp * 1e3,
+                  seconds_since(t0) * 1e3);
       return r.dense_out.values;
     };
-    const std::vector<double> a = timed("1"), b = timed("0");
-    std::printf("  bit-identical: %s\n", a == b ? "yes" : "NO");
-    bad += a != b;
+    const std::vector<double> a = timed("JIT (parallel)", "1", "1"), c = timed("JIT (sequential)", "1", "0"),
+                              b = timed("interpreter", "0", "1");
+    double err = 0, mag = 0;
+    for (size_t e = 0; e < a.size(); ++e) {
+      err = std::max(err, std::abs(a[e] - b[e]));
+      mag = std::max(mag, std::abs(b[e]));
+    }
+    std::printf("  sequential JIT bit-identical to interpreter: %s; parallel JIT max rel err %.2e\n",
+                c == b ? "yes" : "NO", err / std::max(mag, 1e-300));
+    bad += c != b || err > 1e-12 * mag;
   }
   std::printf("%s\n", bad ? "FAILED" : "all match");
   return bad ? 1 : 0;

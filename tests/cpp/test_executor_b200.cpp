@@ -388,7 +388,8 @@ int main() {
     }
   });
 
-  run_case("JIT-compiled nests equal the interpreter bit for bit (TTTc-4, sparse out, other paths)", [] {
+  run_case("JIT-compiled nests: sequential JIT equals the interpreter bit for bit, parallel JIT "
+           "decompositions (slices, fibers, accumulator tails) match (TTTc-4, sparse out, other paths)", [] {
     struct Case {
       KernelSpec spec;
       double density;
@@ -396,6 +397,7 @@ int main() {
     };
     std::vector<Case> cases;
     cases.push_back({tttc4(5, 3), 0.3, 12});
+    cases.push_back({tttc4(9, 2), 0.5, 6});
     cases.push_back({mttkrp3(12, 11, 10, 4), 0.2, 12});
     cases.push_back({tttp3(7, 6, 5, 3), 0.3, 12});
     for (auto& c : cases) {
@@ -406,18 +408,24 @@ int main() {
       for (const auto& path : filter_min_depth(enumerate_paths(c.spec)))
         for (const auto& order : enumerate_orders(c.spec, path, default_csf_order(c.spec))) {
           if (n >= c.max_orders) break;
-          setenv("SPTTN_GENERIC_JIT", "1", 1);
-          ExecPlan pj = prepare(c.spec, path, order, in);
-          setenv("SPTTN_GENERIC_JIT", "0", 1);
-          ExecPlan pi = prepare(c.spec, path, order, in);
-          unsetenv("SPTTN_GENERIC_JIT");
+          auto plan = [&](const char* jit, const char* par) {
+            setenv("SPTTN_GENERIC_JIT", jit, 1);
+            setenv("SPTTN_GENERIC_PAR", par, 1);
+            ExecPlan p = prepare(c.spec, path, order, in);
+            unsetenv("SPTTN_GENERIC_JIT");
+            unsetenv("SPTTN_GENERIC_PAR");
+            return p;
+          };
+          ExecPlan pj = plan("1", "1"), pjs = plan("1", "0"), pis = plan("0", "0"), pi = plan("0", "1");
           if (spttn_b200_plan_device_kind(pj) != SPTTN_NEST_GENERIC) continue;
-          ExecResult rj = execute(pj), ri = execute(pi);
-          CHECK(rj.dense_out.values == ri.dense_out.values);
-          CHECK(rj.sparse_out_values == ri.sparse_out_values);
-          CHECK(rj.stats.multiply_adds == ri.stats.multiply_adds);
-          CHECK(rj.stats.buffer_resets == ri.stats.buffer_resets);
-          CHECK(close(rj, oracle));
+          ExecResult rj = execute(pj), rjs = execute(pjs), ris = execute(pis), ri = execute(pi);
+          CHECK(rjs.dense_out.values == ris.dense_out.values);
+          CHECK(rjs.sparse_out_values == ris.sparse_out_values);
+          for (const ExecResult* r : {&rj, &rjs, &ri}) {
+            CHECK(r->stats.multiply_adds == ris.stats.multiply_adds);
+            CHECK(r->stats.buffer_resets == ris.stats.buffer_resets);
+            CHECK(close(*r, oracle));
+          }
           ++n;
         }
       CHECK(n > 0);
