@@ -192,4 +192,34 @@ __device__ __forceinline__ void store4(double* row, int c, int R, const double4&
   if (c + 3 < R) row[c + 3] = v.w;
 }
 
+
+// Programmatic dependent launch (sm_90+): a grid launched with launch_pdl may
+// start while the previous kernel in the stream drains; grid_dependency_wait()
+// blocks until that kernel has completed and its memory operations are
+// visible.
+__device__ __forceinline__ void grid_dependency_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+// lets the next grid's CTAs be scheduled once every CTA of this grid has
+// started (they still wait for its completion in grid_dependency_wait)
+__device__ __forceinline__ void grid_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, cudaStream_t s,
+                       Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 }  // namespace spttn_dev

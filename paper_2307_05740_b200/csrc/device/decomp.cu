@@ -229,7 +229,7 @@ void find_splits_and_absent(const DevCsf& csf, Decomp& d, const int32_t* slice_u
   SPTTN_CUDA(cudaStreamSynchronize(s));
   d.n_split = h[0];
   d.n_absent = h[1];
-  build_fixup_chunks(d, s);
+  build_fixup_chunks(d, t.idx[0], s);
   dfree(counts, s);
   dfree(present, s);
 }
@@ -374,25 +374,27 @@ namespace {
 // written straight to the output, otherwise the chunk sum goes to part2 for
 // pass 2. Warps past n_chunk zero absent rows.
 template <bool V4>
-__global__ void __launch_bounds__(256) k_fix1(
-    const int32_t* chunk_split, const int32_t* chunk_lo, const int32_t* chunk_hi,
-    const int32_t* split_first, const int32_t* split_chunk, const int32_t* split_node,
-    const int32_t* idx0, const double* part, int64_t tile, int64_t n_chunk, double* part2,
-    const int32_t* absent_rows, int64_t n_absent, double* out) {
+__global__ void __launch_bounds__(256) k_fix1(const int4* __restrict__ meta,
+                                              const double* __restrict__ part, int64_t tile,
+                                              int64_t n_chunk, double* part2,
+                                              const int32_t* absent_rows, int64_t n_absent,
+                                              double* out) {
   const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   if (wid >= n_chunk) {  // absent root rows: zero their output tiles
+    grid_dependency_wait();
     const int64_t zw = nwarps - n_chunk;
     for (int64_t z = (wid - n_chunk) * 32 + lane; z < n_absent * tile; z += zw * 32)
       out[static_cast<int64_t>(absent_rows[z / tile]) * tile + z % tile] = 0.0;
     return;
   }
-  const int32_t sidx = chunk_split[wid];
-  const int32_t first = split_first[sidx];
-  const int32_t lo = chunk_lo[wid], hi = chunk_hi[wid];
-  const bool single = split_chunk[sidx + 1] - split_chunk[sidx] == 1;
-  double* dst = single ? out + static_cast<int64_t>(idx0[split_node[sidx]]) * tile : part2 + wid * tile;
+  // one dependent metadata load per chunk (built at plan time, so it is
+  // read before waiting for the nest kernel under programmatic launch)
+  const int4 m = meta[wid];
+  grid_dependency_wait();
+  const int32_t lo = m.x, hi = m.y, first = m.z;
+  double* dst = m.w >= 0 ? out + static_cast<int64_t>(m.w) * tile : part2 + wid * tile;
   const int64_t nv = V4 ? tile / 4 : tile;
   for (int64_t e = lane; e < nv; e += 32) {
     double4 sum = make_double4(0, 0, 0, 0);
@@ -423,6 +425,18 @@ __global__ void __launch_bounds__(256) k_fix1(
   }
 }
 
+__global__ void k_chunk_meta(const int32_t* chunk_split, const int32_t* chunk_lo,
+                             const int32_t* chunk_hi, const int32_t* split_first,
+                             const int32_t* split_chunk, const int32_t* split_node,
+                             const int32_t* idx0, int64_t n_chunk, int4* meta) {
+  const int64_t w = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (w >= n_chunk) return;
+  const int32_t sidx = chunk_split[w];
+  const bool single = split_chunk[sidx + 1] - split_chunk[sidx] == 1;
+  meta[w] = make_int4(chunk_lo[w], chunk_hi[w], split_first[sidx],
+                      single ? idx0[split_node[sidx]] : -1);
+}
+
 // Epilogue, pass 2 — one block per slice split into several chunks (the
 // heavy root slices of skewed tensors). The block's threads form G groups of
 // tile/4 (or tile) threads; group g adds chunk sums c0+g, c0+g+G, ... in
@@ -436,6 +450,7 @@ __global__ void __launch_bounds__(256) k_fix2(const int32_t* multi, const int32_
   const int32_t sidx = multi[blockIdx.x];
   const int32_t c0 = split_chunk[sidx], c1 = split_chunk[sidx + 1];
   const int64_t row = idx0[split_node[sidx]];
+  grid_dependency_wait();
   const int64_t nv = V4 ? tile / 4 : tile;  // vector elements per tile
   // piece of the tile handled per pass: up to 256 elements, G = 256 / piece groups
   const int64_t piece = nv < 256 ? nv : 256;
@@ -490,7 +505,7 @@ __global__ void __launch_bounds__(256) k_fix2(const int32_t* multi, const int32_
 
 }  // namespace
 
-void build_fixup_chunks(Decomp& d, cudaStream_t s) {
+void build_fixup_chunks(Decomp& d, const int32_t* idx0, cudaStream_t s) {
   if (d.n_split == 0) return;
   std::vector<int32_t> first(d.n_split), last(d.n_split);
   SPTTN_CUDA(cudaMemcpyAsync(first.data(), d.split_first, d.n_split * sizeof(int32_t),
@@ -521,6 +536,13 @@ void build_fixup_chunks(Decomp& d, cudaStream_t s) {
   up(&d.multi_split, multi);
   d.n_multi = static_cast<int64_t>(multi.size());
   dmalloc(&d.part2, std::max<int64_t>(1, d.n_chunk * d.tile) * sizeof(double), s);
+  dmalloc(&d.chunk_meta, std::max<int64_t>(1, d.n_chunk) * sizeof(int4), s);
+  if (d.n_chunk > 0)
+    k_chunk_meta<<<blocks_for(d.n_chunk, 256), 256, 0, s>>>(d.chunk_split, d.chunk_lo, d.chunk_hi,
+                                                           d.split_first, d.split_chunk,
+                                                           d.split_node, idx0, d.n_chunk,
+                                                           d.chunk_meta);
+  SPTTN_CUDA(cudaGetLastError());
   SPTTN_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -529,21 +551,22 @@ void launch_fixup(const Decomp& d, const CsfView& t, double* out, cudaStream_t s
   const int64_t zero_warps =
       d.n_absent > 0 ? std::min<int64_t>((d.n_absent * d.tile + 31) / 32, 148 * 64) : 0;
   const unsigned blocks = blocks_for((d.n_chunk + zero_warps) * 32, 256);
+  // programmatic dependent launch: the fix-up grids are scheduled while the
+  // previous kernel drains and wait in griddepcontrol.wait for its results
   if (d.tile % 4 == 0)
-    k_fix1<true><<<blocks, 256, 0, s>>>(d.chunk_split, d.chunk_lo, d.chunk_hi, d.split_first,
-                                         d.split_chunk, d.split_node, t.idx[0], d.part, d.tile,
-                                         d.n_chunk, d.part2, d.absent_rows, d.n_absent, out);
+    launch_pdl(k_fix1<true>, blocks, 256, s, d.chunk_meta, d.part, d.tile, d.n_chunk, d.part2,
+               d.absent_rows, d.n_absent, out);
   else
-    k_fix1<false><<<blocks, 256, 0, s>>>(d.chunk_split, d.chunk_lo, d.chunk_hi, d.split_first,
-                                          d.split_chunk, d.split_node, t.idx[0], d.part, d.tile,
-                                          d.n_chunk, d.part2, d.absent_rows, d.n_absent, out);
+    launch_pdl(k_fix1<false>, blocks, 256, s, d.chunk_meta, d.part, d.tile, d.n_chunk, d.part2,
+               d.absent_rows, d.n_absent, out);
   if (d.n_multi > 0) {
+    const unsigned nb = static_cast<unsigned>(d.n_multi);
     if (d.tile % 4 == 0)
-      k_fix2<true><<<static_cast<unsigned>(d.n_multi), 256, 0, s>>>(
-          d.multi_split, d.split_chunk, d.split_node, t.idx[0], d.part2, d.tile, out);
+      launch_pdl(k_fix2<true>, nb, 256, s, d.multi_split, d.split_chunk, d.split_node, t.idx[0],
+                 d.part2, d.tile, out);
     else
-      k_fix2<false><<<static_cast<unsigned>(d.n_multi), 256, 0, s>>>(
-          d.multi_split, d.split_chunk, d.split_node, t.idx[0], d.part2, d.tile, out);
+      launch_pdl(k_fix2<false>, nb, 256, s, d.multi_split, d.split_chunk, d.split_node, t.idx[0],
+                 d.part2, d.tile, out);
   }
   SPTTN_CUDA(cudaGetLastError());
 }
@@ -558,6 +581,7 @@ void free_decomp(Decomp& d) {
   dfree(d.seg_begin);
   dfree(d.seg_node);
   dfree(d.seg_node1);
+  dfree(d.chunk_meta);
   dfree(d.chunk_split);
   dfree(d.chunk_lo);
   dfree(d.chunk_hi);

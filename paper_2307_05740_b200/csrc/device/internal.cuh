@@ -75,6 +75,7 @@ struct Decomp {
   int32_t* seg_node1 = nullptr;    // [n_seg]  level-1 coordinate (unit level 2 only)
   // two-level fix-up: chunks of <= kFixChunk items per split slice
   int64_t n_chunk = 0;
+  int4* chunk_meta = nullptr;  // per chunk {lo, hi, first item, out row or -(1 + part2 slot)}
   int32_t* chunk_split = nullptr;
   int32_t* chunk_lo = nullptr;
   int32_t* chunk_hi = nullptr;
@@ -194,7 +195,7 @@ constexpr int kPackSlots = 8;  // TTMc-3 groups (128-byte rows)
 void build_packed(const DevCsf& csf, int leaf_level, Decomp& d, cudaStream_t s,
                   int slots = kPackSlots, const int32_t* leaf_coord2 = nullptr);
 constexpr int kFixChunk = 8;  // items per pass-1 chunk (one batch of loads)
-void build_fixup_chunks(Decomp& d, cudaStream_t s);
+void build_fixup_chunks(Decomp& d, const int32_t* idx0, cudaStream_t s);
 void launch_fixup(const Decomp& d, const CsfView& t, double* out, cudaStream_t s);
 void free_decomp(Decomp& d);
 // Plan-build tracing (env SPTTN_PLAN_TRACE=1): synchronises `s` and prints the

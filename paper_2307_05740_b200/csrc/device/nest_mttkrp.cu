@@ -160,6 +160,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_mttkrp_seg(RootOutArgs a, const i
 // together; the group's segment length n is warp-uniform.
 template <int ORDER, bool VEC>
 __global__ void __launch_bounds__(kBlock, 3) k_mttkrp_pk(RootOutArgs a) {
+  grid_launch_dependents();
   const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
   if (w >= a.n_items) return;  // warp-uniform
   constexpr int kSlots = 4;
@@ -275,6 +276,7 @@ struct StageM {
 
 template <int ORDER, bool VEC>
 __global__ void __launch_bounds__(kBlock, 3) k_mttkrp_pq(RootOutArgs a) {
+  grid_launch_dependents();
   __shared__ StageM stage[kBlock / 32];
   const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
   if (w >= a.n_items) return;  // warp-uniform

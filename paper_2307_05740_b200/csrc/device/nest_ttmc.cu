@@ -649,6 +649,7 @@ constexpr size_t kPqSmem = (sizeof(StageT) + sizeof(StageQ)) * (kBlock / 32);
 
 template <bool VECU, bool VECV>
 __global__ void __launch_bounds__(kBlock, 3) k_ttmc3pq(RootOutArgs a) {
+  grid_launch_dependents();
   extern __shared__ __align__(16) unsigned char pq_smem[];  // kPqSmem bytes
   StageT* stage = reinterpret_cast<StageT*>(pq_smem);
   StageQ* tiles = reinterpret_cast<StageQ*>(pq_smem + sizeof(StageT) * (kBlock / 32));
@@ -958,6 +959,7 @@ struct StageT4 {
 
 template <bool VECV, bool VECW, bool BLK>
 __global__ void __launch_bounds__(kBlock, 2) k_ttmc4pq(RootOutArgs a) {
+  grid_launch_dependents();
   __shared__ StageT4 stage[kBlock / 32];
   const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
   if (w >= a.n_items) return;  // warp-uniform

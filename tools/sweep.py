@@ -56,7 +56,17 @@ def main():
                 plan.execute_stage(1, s)
                 e2.record(s)
                 ts.append((e0, e1, e2))
+        whole = []
+        with torch.cuda.stream(s):
+            for _ in range(10):
+                flush.zero_()
+                e0, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
+                e0.record(s)
+                plan.execute(s)
+                e2.record(s)
+                whole.append((e0, e2))
         torch.cuda.synchronize()
+        step = statistics.median(a.elapsed_time(b) for a, b in whole)
         ms = [a.elapsed_time(b) for a, b, _ in ts]
         epi = statistics.median(b.elapsed_time(c) for _, b, c in ts)
         out = plan.read_output(s)
@@ -66,7 +76,7 @@ def main():
         else:
             err = float(np.max(np.abs(out - ref)) / max(1e-300, np.max(np.abs(ref))))
         info = plan.info()
-        print(f"{key} [{v}] kernel {statistics.median(ms)*1e3:8.1f} us (min {min(ms)*1e3:.1f}) epi {epi*1e3:6.1f} us"
+        print(f"{key} [{v}] kernel {statistics.median(ms)*1e3:8.1f} us (min {min(ms)*1e3:.1f}) epi {epi*1e3:6.1f} us step {step*1e3:7.1f} us"
               f"  {flops/statistics.median(ms)/1e9:6.2f} TF/s  items {info['items']} "
               f"segs {info['segments']} split {info['split_slices']}  relerr {err:.2e}",
               flush=True)
