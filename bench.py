@@ -44,6 +44,9 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
+METRIC = "SpTTN nnz/s (MTTKRP, TTMc, TTTP) + % of HBM/fp64 roofline on 1 B200"
+WORKLOAD = ("ttmc3: BASELINE configs[1] Order-3 TTMc 20000^3, 1e7 nnz Zipf(1.1), U,V 20000x16 "
+            "N(0,1), pinned nest ((T*V)*U)")
 HEADLINE = "ttmc3"
 ORDER = ["mttkrp3", "ttmc3", "tttp3", "mttkrp4", "ttmc4", "mttkrp3_j", "mttkrp3_k"]
 L2_FLUSH_BYTES = 256 << 20
@@ -358,11 +361,12 @@ def run_reference_impl(args, rank, world):
         if step >= args.warmup:
             vals.append(res["value"])
     v = statistics.median(vals)
-    line = {"impl": "reference", "metric": "SpTTN nnz/s (TTMc-3 Zipf 1e7, fused nest)",
+    line = {"impl": "reference", "metric": METRIC,
             "value": v, "unit": "nnz/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": res["seconds"] * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": "ttmc3 (BASELINE configs[1])"},
+            "data": "synthetic", "config": {"workload": WORKLOAD,
+                                            "threads": threads},
             "cpu_baseline": {"value": v, "unit": "nnz/s", "cores": threads, "kind": "reference",
                              "sample": res["sample"]},
             "e2e": {"value": v, "unit": "nnz/s", "h2d_bytes_per_step": 0,
@@ -488,13 +492,12 @@ def main():
 
     h = results[HEADLINE]
     line = {
-        "metric": "SpTTN nnz/s (MTTKRP, TTMc, TTTP) + % of HBM/fp64 roofline on 1 B200",
+        "metric": METRIC,
         "value": h["value"], "unit": "nnz/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": h["ms_per_step"], "higher_is_better": True,
         "scaling": "strong" if (args.shard and world > 1) else "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "ttmc3: BASELINE configs[1] Order-3 TTMc 20000^3, 1e7 nnz "
-                               "Zipf(1.1), U,V 20000x16 N(0,1), pinned nest ((T*V)*U)",
+        "config": {"workload": WORKLOAD,
                    "l2": "256 MB L2 flush write between timed steps",
                    "parallelism": (f"root-slice shards x{world} of one tensor"
                                    if (args.shard and world > 1) else
