@@ -677,9 +677,11 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
         if (p->mode == 2 || p->mode == 3) {
           spttn_dev::build_segments(D, unit_level, seg_len, chunk, p->dec, tile, s, false);
           spttn_dev::build_packed(D, D.order - 1, p->dec, s, 4);
-          // order 3: ~24 items per SM keeps a root slice within one fix-up
-          // chunk (one fix-up kernel); order 4 wants two waves for balance
-          const int64_t w24 = static_cast<int64_t>(sms) * 24 * (D.order == 3 ? 1 : 2);
+          // order 3: one item per resident warp (k_mttkrp_pk: 4 CTAs of 8
+          // warps per SM) — a single wave, and root slices stay within one
+          // fix-up chunk (one fix-up kernel); order 4 wants two waves of the
+          // 24-warp k_mttkrp_pq for balance
+          const int64_t w24 = static_cast<int64_t>(sms) * (D.order == 3 ? 32 : 48);
           int64_t gchunk = env_int("SPTTN_GCHUNK", 0);
           if (gchunk <= 0)
             gchunk = std::clamp<int64_t>((p->dec.n_groups + w24 - 1) / w24, 4,

@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_mttkrp_seg(RootOutArgs a, const i
 // code (predicated, no branches) so all of a group's rows are in flight
 // together; the group's segment length n is warp-uniform.
 template <int ORDER, bool VEC>
-__global__ void __launch_bounds__(kBlock, 3) k_mttkrp_pk(RootOutArgs a) {
+__global__ void __launch_bounds__(kBlock, 4) k_mttkrp_pk(RootOutArgs a) {
   grid_launch_dependents();
   const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
   if (w >= a.n_items) return;  // warp-uniform
