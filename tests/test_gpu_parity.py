@@ -243,6 +243,32 @@ def test_device_factors_and_set_factors(E):
     assert_parity(hplan.read_output(), want2, norm2, "set_factors")
 
 
+@pytest.mark.parametrize("name", ["mttkrp3_r32", "ttmc3_r16", "tttp3_r64", "mttkrp4_r32",
+                                  "ttmc4_r8"])
+def test_device_factors_at_unaligned_addresses(E, name):
+    """Device-resident factors that start 8 bytes past a 32-byte boundary (a
+    caller's tensor view) take the scalar-load paths (no 128/256-bit
+    gathers); results must not change."""
+    import torch
+    m = [c for c in CASES if c["name"] == name][0]
+    csf, factors, _ = load_case(m)
+    dev = E.DeviceCsf(csf)
+    views, keep = [], []
+    for f in factors:
+        flat = np.ascontiguousarray(f).ravel()
+        buf = torch.zeros(flat.size + 4, dtype=torch.float64, device="cuda")
+        buf[1:1 + flat.size] = torch.from_numpy(flat).cuda()
+        keep.append(buf)
+        views.append(buf[1:1 + flat.size])
+    assert all(v.data_ptr() % 32 == 8 for v in views)
+    plan = E.Plan(m["kind"], dev, [v.data_ptr() for v in views], ranks=m["ranks"],
+                  on_device=True, factor_sizes=[v.numel() for v in views])
+    plan.execute()
+    out = plan.read_output()
+    want, norm = oracle_with_norm(m["kind"], csf, factors, m["ranks"])
+    assert_parity(out, want, norm, name + " unaligned device factors")
+
+
 def test_unit_values_tttp_equals_residual_flow(E):
     """rho = T - S(unit values): the residual flag equals the oracle flow the
     survey prescribes."""
