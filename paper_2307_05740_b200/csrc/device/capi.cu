@@ -123,6 +123,13 @@ int sm_count() {
 
 bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 
+int smem_optin_bytes() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&n, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  return n;
+}
+
 void copy_factors(spttn_plan* p, const double* const* src, bool on_device, cudaStream_t s) {
   for (int f = 0; f < p->nf; ++f) {
     if (on_device) {
@@ -344,6 +351,44 @@ int spttn_plan_destroy(spttn_plan* p) {
     delete p;
   });
 }
+
+namespace {
+
+// k_mttkrp3_smf work split: cut the packed group sequence into one range per
+// CTA at root-slice boundaries, balanced by groups. False when a slice is too
+// heavy for that (Zipf hubs): the plan then uses the item / fix-up kernels.
+bool smf_ranges(spttn_plan* p, const spttn_dev::DevCsf& D, int sms, int64_t tile, cudaStream_t s) {
+  auto& d = p->dec;
+  const int nq = static_cast<int>(p->R / 16);
+  const int nc = std::max(1, sms / nq);
+  const int64_t n0 = D.level_size[0];
+  const int64_t G = d.n_groups;
+  std::vector<int32_t> sg(n0 + 1, 0);
+  SPTTN_CUDA(cudaMemcpyAsync(sg.data(), d.slice_grp, (n0 + 1) * sizeof(int32_t),
+                             cudaMemcpyDeviceToHost, s));
+  SPTTN_CUDA(cudaStreamSynchronize(s));
+  std::vector<int32_t> cg(nc + 1, 0);
+  cg[nc] = static_cast<int32_t>(G);
+  int64_t widest = 0;
+  for (int c = 1; c < nc; ++c) {
+    const int64_t target = G * c / nc;
+    const auto it = std::lower_bound(sg.begin(), sg.end(), static_cast<int32_t>(target));
+    cg[c] = std::max(cg[c - 1], it == sg.end() ? static_cast<int32_t>(G) : *it);
+  }
+  for (int c = 0; c < nc; ++c) widest = std::max<int64_t>(widest, cg[c + 1] - cg[c]);
+  const int64_t fair = (G + nc - 1) / nc;
+  if (env_int("SPTTN_SMF_FORCE", 0) == 0 && G > 0 && widest > fair + fair / 4 + 64) return false;
+  // absent root rows (zeroed by the kernel); one item, so no split slices
+  spttn_dev::finish_unit_items(D, d, d.slice_grp, G, std::max<int64_t>(1, G), tile, s);
+  d.n_cta = nc;
+  spttn_dev::dmalloc(&d.cta_grp, (nc + 1) * sizeof(int32_t), s);
+  SPTTN_CUDA(cudaMemcpyAsync(d.cta_grp, cg.data(), (nc + 1) * sizeof(int32_t),
+                             cudaMemcpyHostToDevice, s));
+  SPTTN_CUDA(cudaStreamSynchronize(s));
+  return true;
+}
+
+}  // namespace
 
 int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
                       spttn_plan** out) {
@@ -666,14 +711,33 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
         // TMA-staged streams (default for order 4), 2 = packed (default for
         // order 3: items hold too few windows to amortise the staging
         // prologue), 1 = plain segments
-        p->mode = static_cast<int>(env_int("SPTTN_MTTKRP_MODE", D.order == 4 ? 3 : 2));
+        // 4 = factor column blocks resident in shared memory (order 3,
+        // default when they fit and the slices balance over the CTAs)
         p->vec = (R % 4 == 0) && facs_aligned32 ? 1 : 0;
+        const int64_t rows_b = R > 0 ? p->fac_size[0] / R : 0;
+        const int64_t rows_c = R > 0 ? p->fac_size[1] / R : 0;
+        const bool smf_fits = D.order == 3 && R % 16 == 0 && facs_aligned16 &&
+                              rows_b * R < (int64_t{1} << 31) && D.level_size[0] < (1 << 27) &&
+                              spttn_dev::mttkrp3_smf_smem(rows_c) <=
+                                  static_cast<size_t>(smem_optin_bytes());
+        p->mode = static_cast<int>(env_int("SPTTN_MTTKRP_MODE", D.order == 4 ? 3 : (smf_fits ? 4 : 2)));
+        if (p->mode == 4 && !smf_fits) p->mode = 2;
         const int seg_len = static_cast<int>(std::clamp<int64_t>(env_int("SPTTN_SEG_LEN", 4), 1, 4));
         const int unit_level = D.order - 2;
         const int64_t units = D.level_size[unit_level];
         const int64_t warps = static_cast<int64_t>(sms) * 16 * 2;
         int64_t chunk = env_int("SPTTN_CHUNK", 0);
         if (chunk <= 0) chunk = std::clamp<int64_t>((units + warps - 1) / warps, 8, 1024);
+        if (p->mode == 4) {
+          spttn_dev::build_segments(D, unit_level, seg_len, chunk, p->dec, tile, s, false);
+          spttn_dev::build_packed(D, D.order - 1, p->dec, s, 8);
+          if (smf_ranges(p, D, sms, tile, s)) {
+            spttn_dev::mttkrp3_smf_prepare(p->dec, static_cast<int>(R), s);
+          } else {
+            spttn_dev::free_decomp(p->dec);
+            p->mode = 2;
+          }
+        }
         if (p->mode == 2 || p->mode == 3) {
           spttn_dev::build_segments(D, unit_level, seg_len, chunk, p->dec, tile, s, false);
           spttn_dev::build_packed(D, D.order - 1, p->dec, s, 4);
@@ -687,7 +751,7 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
             gchunk = std::clamp<int64_t>((p->dec.n_groups + w24 - 1) / w24, 4,
                                          p->mode == 3 ? 64 : 1024);
           spttn_dev::finish_unit_items(D, p->dec, p->dec.slice_grp, p->dec.n_groups, gchunk, tile, s);
-        } else {
+        } else if (p->mode != 4) {
           spttn_dev::build_segments(D, unit_level, seg_len, chunk, p->dec, tile, s);
         }
       } else {
@@ -708,6 +772,7 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
       }
       p->launches = 1 + ((p->dec.n_split > 0 || p->dec.n_absent > 0) ? 1 : 0) +
                     (p->dec.n_multi > 0 ? 1 : 0);
+      if (p->kind == SPTTN_NEST_MTTKRP3 && p->mode == 4) p->launches = 1;  // no fix-up pass
     }
     spttn_dev::plan_trace("plan: decomposition", s);
     SPTTN_CUDA(cudaStreamSynchronize(s));
@@ -790,7 +855,17 @@ int spttn_execute_stage(spttn_plan* p, int stage, void* stream) {
       case SPTTN_NEST_MTTKRP3:
         a.f[1] = p->fac[0];
         a.f[2] = p->fac[1];
-        if (p->mode == 3)
+        if (p->mode == 4) {
+          spttn_dev::SmfArgs x{};
+          x.nq = static_cast<int>(p->R / 16);
+          x.n_cta = static_cast<int>(p->dec.n_cta);
+          x.rows_c = static_cast<int32_t>(p->fac_size[1] / p->R);
+          x.cta_grp = p->dec.cta_grp;
+          x.hdr2 = p->dec.hdr2;
+          x.absent_rows = p->dec.absent_rows;
+          x.n_absent = p->dec.n_absent;
+          spttn_dev::launch_mttkrp3_smf(a, x, s);
+        } else if (p->mode == 3)
           spttn_dev::launch_mttkrp_pq(a, 3, s);
         else if (p->mode == 2)
           spttn_dev::launch_mttkrp_pk(a, 3, s);
@@ -839,7 +914,8 @@ int spttn_execute_stage(spttn_plan* p, int stage, void* stream) {
         spttn_dev::launch_ttmc4(a, s);
         break;
     }
-    if (stage != 0 && p->kind != SPTTN_NEST_TTTP3) spttn_dev::launch_fixup(p->dec, a.t, p->out, s);
+    if (stage != 0 && p->kind != SPTTN_NEST_TTTP3 && !(p->kind == SPTTN_NEST_MTTKRP3 && p->mode == 4))
+      spttn_dev::launch_fixup(p->dec, a.t, p->out, s);
   });
 }
 

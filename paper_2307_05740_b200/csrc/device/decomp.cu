@@ -596,6 +596,8 @@ void free_decomp(Decomp& d) {
   dfree(d.pv);
   dfree(d.slice_grp);
   dfree(d.slice_seg);
+  dfree(d.cta_grp);
+  dfree(d.hdr2);
   d = Decomp{};
 }
 

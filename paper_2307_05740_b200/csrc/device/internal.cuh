@@ -95,6 +95,10 @@ struct Decomp {
   double* pv = nullptr;            // interleaved leaf values
   int32_t* slice_grp = nullptr;    // [n0+1] first group of each slice
   int32_t* slice_seg = nullptr;    // [n0+1]   segment offset of each slice
+  // CTA-range kernels (k_mttkrp3_smf): slice-aligned group range per CTA
+  int64_t n_cta = 0;
+  int32_t* cta_grp = nullptr;      // [n_cta+1]
+  int2* hdr2 = nullptr;            // [n_groups+2] k_mttkrp3_smf headers
 };
 
 // ---- device memory (mem.cu): one stream-ordered pool per device ---------
@@ -149,6 +153,22 @@ void launch_ttmc3_tma(const RootOutArgs& a, const void* mapU, const void* mapV, 
 void launch_mttkrp_seg(const RootOutArgs& a, const int32_t* seg_node1, int order, cudaStream_t s);
 void launch_mttkrp_pk(const RootOutArgs& a, int order, cudaStream_t s);
 void launch_mttkrp_pq(const RootOutArgs& a, int order, cudaStream_t s);
+// MTTKRP-3 with the leaf factor's column halves resident in shared memory
+// (nest_mttkrp_smf.cu): one CTA range of packed 8-slot groups per
+// slice-aligned `cta_grp` entry and column half, no fix-up pass.
+struct SmfArgs {
+  int nq;                   // column halves (R / 16)
+  int n_cta;                // CTAs per half
+  int32_t rows_c;           // leaf-factor rows held in shared memory
+  const int32_t* cta_grp;   // [n_cta + 1] slice-aligned group ranges
+  const int2* hdr2;         // [n_groups + 2] {leaf base, slice * 8 + length}
+  const int32_t* absent_rows;
+  int64_t n_absent;
+};
+size_t mttkrp3_smf_smem(int64_t rows_c);
+// plan time: hdr2 + in-place pre-scaling of grp_node / pk (plan-owned)
+void mttkrp3_smf_prepare(Decomp& d, int R, cudaStream_t s);
+void launch_mttkrp3_smf(const RootOutArgs& a, const SmfArgs& x, cudaStream_t s);
 // MTTKRP-3 with the output on CSF level 1 (mode 1) or 2 (mode 2): atomics.
 void launch_mttkrp3_nonroot(const RootOutArgs& a, int mode, cudaStream_t s);
 void launch_tttp3_leaf(const RootOutArgs& a, const int32_t* leaf_i, const int32_t* leaf_j,

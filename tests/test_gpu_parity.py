@@ -82,6 +82,8 @@ def test_partition_independence(E, name, chunk, monkeypatch):
     csf, factors, z = load_case(m)
     monkeypatch.setenv("SPTTN_CHUNK", chunk)
     monkeypatch.setenv("SPTTN_SEG_LEN", "1" if chunk in ("1", "2") else "3")
+    if name == "mttkrp3_r32":  # the item / fix-up kernel (the default has no items)
+        monkeypatch.setenv("SPTTN_MTTKRP_MODE", "2")
     out, plan, _ = run(E, m["kind"], csf, factors, m["ranks"])
     _, norm = oracle_with_norm(m["kind"], csf, factors, m["ranks"])
     assert_parity(out, z["fused"], norm, f"{name} chunk={chunk}")
@@ -91,7 +93,7 @@ def test_partition_independence(E, name, chunk, monkeypatch):
 
 VARIANTS = [("SPTTN_TTMC3_MODE", m, ["ttmc3_small", "ttmc3_r16"]) for m in ("0", "4", "6", "7", "10", "11")] + \
     [("SPTTN_MTTKRP_MODE", m, ["mttkrp3_small", "mttkrp3_r32", "mttkrp4_small", "mttkrp4_r32"])
-     for m in ("0", "1", "2", "3")] + \
+     for m in ("0", "1", "2", "3", "4")] + \
     [("SPTTN_TTTP_MODE", m, ["tttp3_small", "tttp3_r64"]) for m in ("0", "1")] + \
     [("SPTTN_TTMC4_MODE", m, ["ttmc4_small", "ttmc4_r8"]) for m in ("0", "1", "2", "3")]
 
@@ -413,3 +415,32 @@ def test_device_csf_permute_edge_cases(E):
         for a, b in zip(got.idx + got.ptr, want.idx + want.ptr):
             assert np.array_equal(a, b)
         assert np.array_equal(got.values, want.values)
+
+
+@pytest.mark.parametrize("R", [16, 32])
+@pytest.mark.parametrize("force,skew", [(False, False), (True, True)])
+def test_mttkrp3_shared_factor_kernel(E, R, force, skew, monkeypatch):
+    """k_mttkrp3_smf (factor column blocks resident in shared memory, one
+    launch, no fix-up): slice-aligned CTA ranges, warp-order piece merge,
+    absent root rows zeroed in-kernel. `force` keeps it on a tensor with one
+    heavy slice that the plan would otherwise route to the item kernels."""
+    from paper_2307_05740_b200.tensor import Csf
+    if force:
+        monkeypatch.setenv("SPTTN_SMF_FORCE", "1")
+    rng = np.random.default_rng(R)
+    dims = (700, 300, 500)
+    nnz = 60000
+    coords = np.stack([rng.integers(0, d, nnz) for d in dims], axis=1)
+    coords[:, 0] = coords[:, 0] // 2 * 2  # odd root rows absent
+    if skew:
+        coords[: nnz // 3, 0] = 4
+    vals = rng.uniform(-1, 1, nnz)
+    csf = Csf.from_coo(list(dims), coords, vals)
+    fs = [rng.standard_normal((dims[1], R)), rng.standard_normal((dims[2], R))]
+    out, plan, _ = run(E, 1, csf, fs, (R, 0, 0))
+    assert plan.info()["launches"] == 1, plan.info()
+    want, norm = oracle_with_norm(1, csf, fs, (R, 0, 0))
+    assert_parity(out, want, norm, f"smf R={R} force={force}")
+    assert np.all(out.reshape(dims[0], R)[1::2] == 0.0)
+    plan.execute()
+    assert np.array_equal(plan.read_output(), out)
