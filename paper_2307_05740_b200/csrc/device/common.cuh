@@ -116,6 +116,31 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// Warp-collective forms of the TMA issue helpers : every lane
+// calls them with the same (shuffle-broadcast, hence provably warp-uniform)
+// operands and one elected lane issues, so the operands live in uniform
+// registers — the lane-0-only form made the compiler wrap every bulk copy in
+// a divergent-operand loop (~240 instructions per staged window).
+__device__ __forceinline__ void expect_tx_elect(uint64_t* m, unsigned bytes) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(m));
+  asm volatile(
+      "{\n .reg .pred p;\n elect.sync _|p, 0xffffffff;\n"
+      " @p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n}\n" ::"r"(a),
+      "r"(bytes)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_elect(void* dst, const void* src, unsigned bytes,
+                                               uint64_t* m) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(m));
+  asm volatile(
+      "{\n .reg .pred p;\n elect.sync _|p, 0xffffffff;\n"
+      " @p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n}\n" ::"r"(d),
+      "l"(src), "r"(bytes), "r"(b)
+      : "memory");
+}
+__device__ __forceinline__ int32_t uni(int32_t v) { return __shfl_sync(0xffffffffu, v, 0); }
+
 __device__ __forceinline__ int ldg_i32(const int32_t* p) { return __ldg(p); }
 __device__ __forceinline__ double ldg_f64(const double* p) { return __ldg(p); }
 

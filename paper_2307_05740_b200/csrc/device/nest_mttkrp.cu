@@ -291,8 +291,8 @@ __global__ void __launch_bounds__(kBlock, 3) k_mttkrp_pq(RootOutArgs a) {
   const double* __restrict__ Ftop = a.f[1];
   const int32_t* __restrict__ slice_grp = a.slice_grp;
 
-  const int32_t cbeg = static_cast<int32_t>(w * a.chunk);
-  const int32_t cend = static_cast<int32_t>(min64(cbeg + a.chunk, a.n_groups));
+  const int32_t cbeg = uni(static_cast<int32_t>(w * a.chunk));
+  const int32_t cend = uni(static_cast<int32_t>(min64(cbeg + a.chunk, a.n_groups)));
   int32_t sl = a.item_pos[w];
   int32_t sl_end = slice_grp[sl + 1];
   bool head = slice_grp[sl] < cbeg;
@@ -327,11 +327,11 @@ __global__ void __launch_bounds__(kBlock, 3) k_mttkrp_pq(RootOutArgs a) {
     const int b = wi % 3;
     const unsigned hb = nw * sizeof(int4), nb = nw * kMSlots * sizeof(int32_t);
     fence_proxy_async();
-    mbar_expect_tx(&S.mbar_meta[b], hb + (ORDER == 4 ? 2 : 1) * nb);
-    bulk_g2s(&S.hdr[b][0], a.grp_hdr + g0, hb, &S.mbar_meta[b]);
-    bulk_g2s(&S.node[b][0], a.grp_node + static_cast<int64_t>(g0) * kMSlots, nb, &S.mbar_meta[b]);
+    expect_tx_elect(&S.mbar_meta[b], hb + (ORDER == 4 ? 2 : 1) * nb);
+    bulk_g2s_elect(&S.hdr[b][0], a.grp_hdr + g0, hb, &S.mbar_meta[b]);
+    bulk_g2s_elect(&S.node[b][0], a.grp_node + static_cast<int64_t>(g0) * kMSlots, nb, &S.mbar_meta[b]);
     if (ORDER == 4)
-      bulk_g2s(&S.node1[b][0], a.grp_node1 + static_cast<int64_t>(g0) * kMSlots, nb,
+      bulk_g2s_elect(&S.node1[b][0], a.grp_node1 + static_cast<int64_t>(g0) * kMSlots, nb,
                &S.mbar_meta[b]);
   };
   auto issue_leaves = [&](int32_t wi) {
@@ -339,13 +339,13 @@ __global__ void __launch_bounds__(kBlock, 3) k_mttkrp_pq(RootOutArgs a) {
     const int32_t nw = min(g0 + kMW, cend) - g0;
     const int b = wi % 3, lb = wi & 1;
     mbar_wait(&S.mbar_meta[b], (wi / 3) & 1);
-    const int32_t L0 = S.hdr[b][0].x;
-    const int32_t L1 = S.hdr[b][nw - 1].x + kMSlots * S.hdr[b][nw - 1].y;
+    const int32_t L0 = uni(S.hdr[b][0].x);
+    const int32_t L1 = uni(S.hdr[b][nw - 1].x + kMSlots * S.hdr[b][nw - 1].y);
     const unsigned n = static_cast<unsigned>(L1 - L0);
     fence_proxy_async();
-    mbar_expect_tx(&S.mbar_leaf[lb], n * 12u);
-    bulk_g2s(&S.kk[lb][0], a.pk + L0, n * 4u, &S.mbar_leaf[lb]);
-    bulk_g2s(&S.tv[lb][0], a.pv + L0, n * 8u, &S.mbar_leaf[lb]);
+    expect_tx_elect(&S.mbar_leaf[lb], n * 12u);
+    bulk_g2s_elect(&S.kk[lb][0], a.pk + L0, n * 4u, &S.mbar_leaf[lb]);
+    bulk_g2s_elect(&S.tv[lb][0], a.pv + L0, n * 8u, &S.mbar_leaf[lb]);
   };
 
   const int32_t nwin = (cend - cbeg + kMW - 1) / kMW;
@@ -353,17 +353,17 @@ __global__ void __launch_bounds__(kBlock, 3) k_mttkrp_pq(RootOutArgs a) {
     for (int b = 0; b < 3; ++b) mbar_init(&S.mbar_meta[b], 1);
     for (int b = 0; b < 2; ++b) mbar_init(&S.mbar_leaf[b], 1);
     mbar_init_fence();
+  }
+  __syncwarp();
+  if (nwin > 0) {  // warp-collective issue (elected lane), uniform operands
     issue_meta(0);
     if (nwin > 1) issue_meta(1);
     issue_leaves(0);
   }
-  __syncwarp();
   for (int32_t win = 0; win < nwin; ++win) {
     const int mb = win % 3, lbf = win & 1;
-    if (lane == 0) {
-      if (win + 1 < nwin) issue_leaves(win + 1);
-      if (win + 2 < nwin) issue_meta(win + 2);
-    }
+    if (win + 1 < nwin) issue_leaves(win + 1);
+    if (win + 2 < nwin) issue_meta(win + 2);
     mbar_wait(&S.mbar_meta[mb], (win / 3) & 1);
     mbar_wait(&S.mbar_leaf[lbf], (win / 2) & 1);
     const int32_t g0 = cbeg + win * kMW;
