@@ -638,8 +638,22 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
       p->out_count = D.dims[p->kind == SPTTN_NEST_MTTKRP3_J ? 1 : 2] * R;
       dev_malloc(reinterpret_cast<void**>(&p->out), std::max<int64_t>(1, p->out_count) * 8, s);
       p->vec = (R % 4 == 0) && facs_aligned32 ? 1 : 0;
+      // mode 4 (default when they fit): column quarters of the gathered
+      // factor and of the output accumulated in shared memory
+      const int nr_mode = p->kind == SPTTN_NEST_MTTKRP3_J ? 1 : 2;
+      const int64_t rows_in = R > 0 ? p->fac_size[1] / R : 0;
+      const int64_t rows_out = D.dims[nr_mode];
+      const bool nr_fits = R % 8 == 0 && facs_aligned16 && D.level_size[0] < (1 << 27) &&
+                           spttn_dev::mttkrp3_nr_smem(rows_in, rows_out) <=
+                               static_cast<size_t>(smem_optin_bytes());
+      p->mode = static_cast<int>(env_int("SPTTN_NONROOT_MODE", nr_fits ? 4 : 0));
+      if (p->mode == 4 && !nr_fits) p->mode = 0;
       spttn_dev::build_segments(D, 1, 4, 1, p->dec, 0, s, false);
-      spttn_dev::build_packed(D, 2, p->dec, s, 4);
+      spttn_dev::build_packed(D, 2, p->dec, s, p->mode == 4 ? 8 : 4);
+      if (p->mode == 4) {
+        spttn_dev::mttkrp3_nr_prepare(p->dec, nr_mode, rows_in, s);
+        p->dec.n_cta = std::max(1, sm_count() / static_cast<int>(R / 8));
+      }
       p->launches = 2;  // memset + kernel
     } else {
       const bool sparse_out = p->kind == SPTTN_NEST_TTTP3;
@@ -850,7 +864,18 @@ int spttn_execute_stage(spttn_plan* p, int stage, void* stream) {
         a.f[0] = p->fac[0];
         a.f[1] = p->fac[1];
         SPTTN_CUDA(cudaMemsetAsync(p->out, 0, std::max<int64_t>(1, p->out_count) * 8, s));
-        spttn_dev::launch_mttkrp3_nonroot(a, p->kind == SPTTN_NEST_MTTKRP3_J ? 1 : 2, s);
+        if (p->mode == 4) {
+          const int nr_mode = p->kind == SPTTN_NEST_MTTKRP3_J ? 1 : 2;
+          spttn_dev::SmfArgs x{};
+          x.nq = static_cast<int>(p->R / 8);
+          x.n_cta = static_cast<int>(p->dec.n_cta);
+          x.rows_c = static_cast<int32_t>(p->fac_size[1] / p->R);
+          x.rows_out = static_cast<int32_t>(p->out_count / p->R);
+          x.hdr2 = p->dec.hdr2;
+          spttn_dev::launch_mttkrp3_nr_smf(a, x, nr_mode, s);
+        } else {
+          spttn_dev::launch_mttkrp3_nonroot(a, p->kind == SPTTN_NEST_MTTKRP3_J ? 1 : 2, s);
+        }
         break;
       case SPTTN_NEST_MTTKRP3:
         a.f[1] = p->fac[0];

@@ -159,7 +159,8 @@ void launch_mttkrp_pq(const RootOutArgs& a, int order, cudaStream_t s);
 struct SmfArgs {
   int nq;                   // column halves (R / 16)
   int n_cta;                // CTAs per half
-  int32_t rows_c;           // leaf-factor rows held in shared memory
+  int32_t rows_c;           // gathered-factor rows held in shared memory
+  int32_t rows_out;         // non-root kernel: output rows accumulated in shared memory
   const int32_t* cta_grp;   // [n_cta + 1] slice-aligned group ranges
   const int2* hdr2;         // [n_groups + 2] {leaf base, slice * 8 + length}
   const int32_t* absent_rows;
@@ -169,6 +170,11 @@ size_t mttkrp3_smf_smem(int64_t rows_c);
 // plan time: hdr2 + in-place pre-scaling of grp_node / pk (plan-owned)
 void mttkrp3_smf_prepare(Decomp& d, int R, cudaStream_t s);
 void launch_mttkrp3_smf(const RootOutArgs& a, const SmfArgs& x, cudaStream_t s);
+// non-root MTTKRP-3 (mode 1 = j, 2 = k) with column quarters of the gathered
+// factor and of the output accumulator in shared memory
+size_t mttkrp3_nr_smem(int64_t rows_in, int64_t rows_out);
+void mttkrp3_nr_prepare(Decomp& d, int mode, int64_t rows_in, cudaStream_t s);
+void launch_mttkrp3_nr_smf(const RootOutArgs& a, const SmfArgs& x, int mode, cudaStream_t s);
 // MTTKRP-3 with the output on CSF level 1 (mode 1) or 2 (mode 2): atomics.
 void launch_mttkrp3_nonroot(const RootOutArgs& a, int mode, cudaStream_t s);
 void launch_tttp3_leaf(const RootOutArgs& a, const int32_t* leaf_i, const int32_t* leaf_j,

@@ -307,6 +307,181 @@ __global__ void k_smf_prep(const int4* hdr, int32_t ngroups, int2* hdr2, int32_t
   if (e < nleaves) pk[e] *= kHalf * 8;
 }
 
+
+// ---- MTTKRP-3 for the non-root output modes, shared-memory form ----------
+//
+// The other two CP-ALS products on the same (i,j,k) CSF (nest_mttkrp.cu
+// k_mttkrp3_nonroot has the reference nests): mode j  B[j] += (sum_k t C[k])
+// * A[i]; mode k  C[k] += (A[i] * B[j]) * t. The output row is not owned by
+// a root slice, so contributions are accumulated — here into a per-CTA copy
+// of the output's column quarter in shared memory (fp64 shared atomics),
+// together with the gathered factor's column quarter (C for mode j, B for
+// mode k), both rows * 64 bytes (64 KB each at the BASELINE shape). Each CTA
+// then adds its accumulator into the zeroed global output with fp64 RED
+// (rows_out * 8 per CTA instead of one global atomic per contribution:
+// 2.4 M instead of 20-32 M). A[i] quarter rows come from L2 once per slice
+// change. Summation order varies with atomic arrival (within tolerance).
+__global__ void __launch_bounds__(kSmfWarps * 32, 1) k_mttkrp3_nr_smf(RootOutArgs a, SmfArgs x,
+                                                                     int mode) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr int NT = kSmfWarps * 32;
+  const int tid = threadIdx.x;
+  const int wid = uni(tid >> 5);
+  const int lane = tid & 31;
+  const int slot = lane >> 2;  // 8 slots, 4 lanes per 64-byte row
+  const int cp = lane & 3;     // columns 2cp, 2cp+1 of the quarter
+  const int q = blockIdx.x % x.nq;
+  const int cta = blockIdx.x / x.nq;
+  const int R = a.R;
+  const int col = 8 * q + 2 * cp;
+  const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const unsigned cs = sbase + 16u * cp;
+  const int32_t rows_in = x.rows_c, rows_out = x.rows_out;
+  double* acc_sm = reinterpret_cast<double*>(smem + static_cast<int64_t>(rows_in) * 64);
+  StageS* stages = reinterpret_cast<StageS*>(smem + static_cast<int64_t>(rows_in + rows_out) * 64);
+  StageS& S = stages[wid];
+
+  // 1. gathered factor quarter -> shared memory; accumulator quarter = 0
+  {
+    const double* F = a.f[1];  // C (mode j) or B (mode k)
+    for (int32_t e = tid; e < rows_in * 4; e += NT) {
+      const double* src = F + static_cast<int64_t>(e >> 2) * R + 8 * q + 2 * (e & 3);
+      cp_async16_cg(smem + static_cast<int64_t>(e) * 16, src, 16);
+    }
+    cp_async_commit();
+    for (int32_t e = tid; e < rows_out * 4; e += NT)
+      reinterpret_cast<double2*>(acc_sm)[e] = make_double2(0, 0);
+  }
+
+  // 2. even group ranges (outputs are not slice-owned)
+  const int64_t G = a.n_groups;
+  const int32_t G0 = static_cast<int32_t>(G * cta / x.n_cta);
+  const int32_t G1 = static_cast<int32_t>(G * (cta + 1) / x.n_cta);
+  const int32_t cbeg =
+      uni(G0 + static_cast<int32_t>((static_cast<int64_t>(G1 - G0) * wid) / kSmfWarps));
+  const int32_t cend =
+      uni(G0 + static_cast<int32_t>((static_cast<int64_t>(G1 - G0) * (wid + 1)) / kSmfWarps));
+
+  auto issue_meta = [&](int32_t wi) {
+    const int32_t g0 = cbeg + wi * kSW;
+    const int32_t nw = min(g0 + kSW, cend) - g0;
+    const int b = wi % 3;
+    const unsigned hb = ((static_cast<unsigned>(nw + (g0 & 1)) * 8u) + 15u) & ~15u;
+    const unsigned nb = nw * kSSlots * sizeof(int32_t);
+    fence_proxy_async();
+    expect_tx_elect(&S.mbar_meta[b], hb + nb);
+    bulk_g2s_elect(&S.hdr[b][0], x.hdr2 + (g0 & ~1), hb, &S.mbar_meta[b]);
+    bulk_g2s_elect(&S.node[b][0], a.grp_node + static_cast<int64_t>(g0) * kSSlots, nb,
+                   &S.mbar_meta[b]);
+  };
+  auto issue_leaves = [&](int32_t wi) {
+    const int32_t g0 = cbeg + wi * kSW;
+    const int32_t nw = min(g0 + kSW, cend) - g0;
+    const int b = wi % 3, lb = wi & 1;
+    mbar_wait(&S.mbar_meta[b], (wi / 3) & 1);
+    const int o = g0 & 1;
+    const int32_t L0 = uni(S.hdr[b][o].x);
+    const int32_t L1 =
+        uni(S.hdr[b][o + nw - 1].x + kSSlots * (S.hdr[b][o + nw - 1].y & 7));
+    const unsigned n = static_cast<unsigned>(L1 - L0);
+    fence_proxy_async();
+    expect_tx_elect(&S.mbar_leaf[lb], n * 12u);
+    bulk_g2s_elect(&S.kk[lb][0], a.pk + L0, n * 4u, &S.mbar_leaf[lb]);
+    bulk_g2s_elect(&S.tv[lb][0], a.pv + L0, n * 8u, &S.mbar_leaf[lb]);
+  };
+  const int32_t nwin = (cend - cbeg + kSW - 1) / kSW;
+  if (nwin > 0) {
+    if (lane == 0) {
+      for (int b = 0; b < 3; ++b) mbar_init(&S.mbar_meta[b], 1);
+      for (int b = 0; b < 2; ++b) mbar_init(&S.mbar_leaf[b], 1);
+      mbar_init_fence();
+    }
+    __syncwarp();
+    issue_meta(0);
+    if (nwin > 1) issue_meta(1);
+    issue_leaves(0);
+  }
+  cp_async_wait<0>();
+  __syncthreads();  // factor quarter resident, accumulator zeroed
+
+  const double* __restrict__ Aq = a.f[0] + col;
+  int32_t cur = -1;
+  double2 ar = make_double2(0, 0);
+  auto add2 = [&](unsigned off, double vx, double vy) {  // shared fp64 atomics
+    double* p = reinterpret_cast<double*>(smem + (off - sbase));
+    atomicAdd(p, vx);
+    atomicAdd(p + 1, vy);
+  };
+  for (int32_t win = 0; win < nwin; ++win) {
+    const int mb = win % 3, lbf = win & 1;
+    if (win + 1 < nwin) issue_leaves(win + 1);
+    if (win + 2 < nwin) issue_meta(win + 2);
+    mbar_wait(&S.mbar_meta[mb], (win / 3) & 1);
+    mbar_wait(&S.mbar_leaf[lbf], (win / 2) & 1);
+    const int32_t g0 = cbeg + win * kSW;
+    const int ng = min(g0 + kSW, cend) - g0;
+    const int o = g0 & 1;
+    const int32_t L0 = S.hdr[mb][o].x;
+    for (int gi = 0; gi < ng; ++gi) {
+      const int2 hh = S.hdr[mb][o + gi];
+      const int32_t sl = hh.y >> 3;
+      if (sl != cur) {  // warp-uniform: A[i] once per root slice
+        cur = sl;
+        ar = ld128(Aq + static_cast<int64_t>(__ldg(a.t.idx[0] + sl)) * R);
+      }
+      const int n = hh.y & 7;  // warp-uniform
+      const int lb = hh.x - L0 + slot;
+      const unsigned nodeoff = static_cast<unsigned>(S.node[mb][gi * kSSlots + slot]);
+      if (mode == 1) {  // B[j] += (sum_k t C[k]) * A[i]
+        double2 X = make_double2(0, 0);
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          if (it < n) {
+            const unsigned kof = static_cast<unsigned>(S.kk[lbf][lb + it * kSSlots]);
+            const double t = S.tv[lbf][lb + it * kSSlots];
+            const double2 c = lds128(cs + kof);
+            X.x = fma(t, c.x, X.x);
+            X.y = fma(t, c.y, X.y);
+          }
+        }
+        add2(cs + nodeoff, X.x * ar.x, X.y * ar.y);
+      } else {  // C[k] += (A[i] * B[j]) * t
+        const double2 b = lds128(cs + nodeoff);
+        const double2 W = make_double2(ar.x * b.x, ar.y * b.y);
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          if (it < n) {
+            const unsigned kof = static_cast<unsigned>(S.kk[lbf][lb + it * kSSlots]);
+            const double t = S.tv[lbf][lb + it * kSSlots];
+            add2(cs + kof, W.x * t, W.y * t);
+          }
+        }
+      }
+    }
+    __syncwarp();  // this window's stage buffers are free
+  }
+
+  // 3. accumulator quarter -> global output (fp64 RED, zero entries skipped)
+  __syncthreads();
+  for (int32_t e = tid; e < rows_out * 8; e += NT) {
+    const double v = acc_sm[e];
+    if (v != 0.0) atomicAdd(a.out + static_cast<int64_t>(e >> 3) * R + 8 * q + (e & 7), v);
+  }
+}
+
+// plan time (non-root kernel): shared-memory byte offsets — the gathered
+// factor's rows from 0, the accumulator's rows from rows_in * 64
+__global__ void k_nr_prep(const int4* hdr, int32_t ngroups, int2* hdr2, int32_t* gnode,
+                          int32_t* pk, int64_t nleaves, int node_base, int leaf_base) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e < ngroups) {
+    const int4 hh = hdr[e];
+    hdr2[e] = make_int2(hh.x, hh.w * 8 + hh.y);
+  }
+  if (e < static_cast<int64_t>(ngroups) * kSSlots) gnode[e] = node_base + gnode[e] * 64;
+  if (e < nleaves) pk[e] = leaf_base + pk[e] * 64;
+}
+
 }  // namespace
 
 size_t mttkrp3_smf_smem(int64_t rows_c) {
@@ -331,6 +506,37 @@ void launch_mttkrp3_smf(const RootOutArgs& a, const SmfArgs& x, cudaStream_t s) 
   SPTTN_CUDA(cudaFuncSetAttribute(k_mttkrp3_smf, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(sm)));
   k_mttkrp3_smf<<<blocks, kSmfWarps * 32, sm, s>>>(a, x);
+  SPTTN_CUDA(cudaGetLastError());
+}
+
+}  // namespace spttn_dev
+
+namespace spttn_dev {
+
+size_t mttkrp3_nr_smem(int64_t rows_in, int64_t rows_out) {
+  return static_cast<size_t>(rows_in + rows_out) * 64 + kSmfWarps * sizeof(StageS);
+}
+
+void mttkrp3_nr_prepare(Decomp& d, int mode, int64_t rows_in, cudaStream_t s) {
+  dmalloc(&d.hdr2, (d.n_groups + 2) * sizeof(int2), s);
+  SPTTN_CUDA(cudaMemsetAsync(d.hdr2, 0, (d.n_groups + 2) * sizeof(int2), s));
+  const int64_t n = std::max<int64_t>(d.n_groups * kSSlots, d.n_packed_leaves);
+  const int acc0 = static_cast<int>(rows_in * 64);
+  if (n > 0) {
+    k_nr_prep<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
+        d.grp_hdr, static_cast<int32_t>(d.n_groups), d.hdr2, d.grp_node, d.pk, d.n_packed_leaves,
+        mode == 1 ? acc0 : 0, mode == 1 ? 0 : acc0);
+    SPTTN_CUDA(cudaGetLastError());
+  }
+}
+
+void launch_mttkrp3_nr_smf(const RootOutArgs& a, const SmfArgs& x, int mode, cudaStream_t s) {
+  const unsigned blocks = static_cast<unsigned>(x.nq * x.n_cta);
+  if (blocks == 0 || a.n_groups == 0) return;
+  const size_t sm = mttkrp3_nr_smem(x.rows_c, x.rows_out);
+  SPTTN_CUDA(cudaFuncSetAttribute(k_mttkrp3_nr_smf, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(sm)));
+  k_mttkrp3_nr_smf<<<blocks, kSmfWarps * 32, sm, s>>>(a, x, mode);
   SPTTN_CUDA(cudaGetLastError());
 }
 

@@ -95,7 +95,9 @@ VARIANTS = [("SPTTN_TTMC3_MODE", m, ["ttmc3_small", "ttmc3_r16"]) for m in ("0",
     [("SPTTN_MTTKRP_MODE", m, ["mttkrp3_small", "mttkrp3_r32", "mttkrp4_small", "mttkrp4_r32"])
      for m in ("0", "1", "2", "3", "4")] + \
     [("SPTTN_TTTP_MODE", m, ["tttp3_small", "tttp3_r64"]) for m in ("0", "1")] + \
-    [("SPTTN_TTMC4_MODE", m, ["ttmc4_small", "ttmc4_r8"]) for m in ("0", "1", "2", "3")]
+    [("SPTTN_TTMC4_MODE", m, ["ttmc4_small", "ttmc4_r8"]) for m in ("0", "1", "2", "3")] + \
+    [("SPTTN_NONROOT_MODE", m, ["mttkrp3j_small", "mttkrp3j_r32", "mttkrp3k_small", "mttkrp3k_r32"])
+     for m in ("0", "4")]
 
 
 @pytest.mark.parametrize("env,mode,names", VARIANTS, ids=[f"{v[0]}={v[1]}" for v in VARIANTS])
@@ -111,7 +113,8 @@ def test_kernel_variants_agree(E, env, mode, names, monkeypatch):
         _, norm = oracle_with_norm(m["kind"], csf, factors, m["ranks"])
         assert_parity(out, z["fused"], norm, f"{name} {env}={mode}")
     key = {"SPTTN_TTMC3_MODE": "ttmc3", "SPTTN_MTTKRP_MODE": "mttkrp4",
-           "SPTTN_TTTP_MODE": "tttp3", "SPTTN_TTMC4_MODE": "ttmc4"}[env]
+           "SPTTN_TTTP_MODE": "tttp3", "SPTTN_TTMC4_MODE": "ttmc4",
+           "SPTTN_NONROOT_MODE": "mttkrp3_k"}[env]
     w = make_workload(key, scale=2e-3)
     c = w.cfg
     out, _, _ = run(E, c.kind, w.csf, w.factors, c.ranks, E.FLAG_RESIDUAL if c.residual else 0)
