@@ -37,6 +37,7 @@ struct spttn_plan {
   int batch = 4;  // TTTP leaves per group step
   int32_t* leaf_i = nullptr;  // TTTP leaf kernel: per-leaf root / level-1 coordinates
   int32_t* leaf_j = nullptr;
+  spttn_dev::TttpKb kb;  // TTTP mode 2: C-bucketed leaf layout
   spttn_dev::Decomp dec;
   spttn_dev::GenericState gen;
   spg_program* prog = nullptr;  // host copy (GENERIC)
@@ -345,6 +346,7 @@ int spttn_plan_destroy(spttn_plan* p) {
     spttn_dev::dfree(p->d_dense);
     spttn_dev::dfree(p->leaf_i);
     spttn_dev::dfree(p->leaf_j);
+    spttn_dev::free_tttp_buckets(p->kb);
     spttn_dev::free_decomp(p->dec);
     spttn_dev::generic_free(p->gen);
     delete p->prog;
@@ -776,11 +778,26 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
         if (chunk <= 0) chunk = std::clamp<int64_t>((nnz + groups - 1) / groups, 16, 4096);
         if (sparse_out) {
           // 1 = leaf-parallel kernel over expanded (i, j) coordinates (default)
+          // 1 = leaf-parallel (default), 2 = C-bucketed (tttp_buckets.cu:
+          // 3.42 vs 3.52 ms at the BASELINE shape, but a radix sort of the
+          // leaves at plan time)
           p->mode = static_cast<int>(env_int("SPTTN_TTTP_MODE", 1));
+          if (p->mode == 2 && !facs_aligned16) p->mode = 1;  // 16-byte cp.async of C rows
           p->batch = static_cast<int>(env_int("SPTTN_TTTP_BATCH", 4));
         }
-        if (sparse_out && p->mode == 1)
+        if (sparse_out && (p->mode == 1 || p->mode == 2)) {
           spttn_dev::build_leaf_coords(D, &p->leaf_i, &p->leaf_j, s);
+          if (p->mode == 2) {
+            if (spttn_dev::build_tttp_buckets(D, static_cast<int>(R), sms, p->leaf_i, p->leaf_j,
+                                              p->kb, s)) {
+              spttn_dev::dfree(p->leaf_i, s);  // the bucketed streams carry i, j
+              spttn_dev::dfree(p->leaf_j, s);
+              p->leaf_i = p->leaf_j = nullptr;
+            } else {
+              p->mode = 1;
+            }
+          }
+        }
         else
           spttn_dev::build_leaf_items(D, chunk, p->dec, sparse_out ? 0 : tile, s);
       }
@@ -916,7 +933,9 @@ int spttn_execute_stage(spttn_plan* p, int stage, void* stream) {
         a.f[0] = p->fac[0];
         a.f[1] = p->fac[1];
         a.f[2] = p->fac[2];
-        if (p->mode == 1)
+        if (p->mode == 2)
+          spttn_dev::launch_tttp3_kb(a, p->kb, s);
+        else if (p->mode == 1)
           spttn_dev::launch_tttp3_leaf(a, p->leaf_i, p->leaf_j, p->batch, s);
         else
           spttn_dev::launch_tttp3(a, s);

@@ -49,6 +49,16 @@ __device__ __forceinline__ double4 ld256_if(const double* p, bool pred) {
   return v;
 }
 
+__device__ __forceinline__ double2 ld128_if(const double* p, bool pred) {
+  double2 v;
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.b32 q, %3, 0;\n mov.b64 %0, 0;\n mov.b64 %1, 0;\n"
+      " @q ld.global.nc.v2.f64 {%0,%1}, [%2];\n}\n"
+      : "=d"(v.x), "=d"(v.y)
+      : "l"(p), "r"(static_cast<int>(pred)));
+  return v;
+}
+
 __device__ __forceinline__ double2 ld128(const double* p) {
   double2 v;
   asm volatile("ld.global.nc.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));

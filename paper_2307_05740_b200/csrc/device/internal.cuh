@@ -179,6 +179,27 @@ void launch_mttkrp3_nr_smf(const RootOutArgs& a, const SmfArgs& x, int mode, cud
 void launch_mttkrp3_nonroot(const RootOutArgs& a, int mode, cudaStream_t s);
 void launch_tttp3_leaf(const RootOutArgs& a, const int32_t* leaf_i, const int32_t* leaf_j,
                        int batch, cudaStream_t s);
+// TTTP-3 bucketed by C row ranges (nest_tttp.cu k_tttp3_kb): leaves grouped
+// by k-bucket (stable), each bucket padded to a multiple of 4 leaves.
+struct TttpKb {
+  int nkey = 0;                 // (i range, k bucket) pairs = n_i_ranges * nb
+  int nb = 0, ppb = 0, kb = 0;  // k buckets, CTAs per pair, C rows per bucket
+  int32_t rows_c = 0;
+  int64_t* bstart = nullptr;    // [nkey+1] padded starts of the (i range, k bucket) pairs
+  int32_t *li = nullptr, *lj = nullptr, *lk = nullptr, *lp = nullptr;  // i, j, k - k0, CSF position
+  double* lv = nullptr;
+};
+struct TttpKbArgs {
+  const int64_t* bstart;
+  int nb, ppb, kb;
+  int32_t rows_c;
+  const int32_t *li, *lj, *lk, *lp;
+  const double* lv;
+};
+bool build_tttp_buckets(const DevCsf& csf, int R, int sms, const int32_t* leaf_i,
+                        const int32_t* leaf_j, TttpKb& kbl, cudaStream_t s);
+void free_tttp_buckets(TttpKb& kbl);
+void launch_tttp3_kb(const RootOutArgs& a, const TttpKb& kbl, cudaStream_t s);
 // Per-leaf root / level-1 coordinates of an order-3 CSF (TTTP leaf kernel).
 void build_leaf_coords(const DevCsf& csf, int32_t** leaf_i, int32_t** leaf_j, cudaStream_t s);
 

@@ -18,36 +18,13 @@
 // butterfly): 2U-1 shuffles for U leaves instead of U*log2(G), after which
 // lane (G/U)*q holds leaf q's sum and writes it.
 #include "internal.cuh"
+#include "tttp_reduce.cuh"
 
 namespace spttn_dev {
 
 namespace {
 
 constexpr int kBlock = 256;
-
-template <int G, int U>
-__device__ __forceinline__ double transpose_reduce(double (&v)[U], int lane_in_group, int* leaf) {
-  // halving exchanges: after them each lane holds one leaf's partial sum
-  int q = 0;
-  int o = G / 2;
-#pragma unroll
-  for (int n = U; n > 1; n >>= 1, o >>= 1) {
-    const int half = n / 2;
-    const bool hi = (lane_in_group & o) != 0;
-#pragma unroll
-    for (int i = 0; i < half; ++i) {
-      const double send = hi ? v[i] : v[i + half];
-      const double keep = hi ? v[i + half] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-    }
-    q = (q << 1) | (hi ? 1 : 0);
-  }
-  double s = v[0];
-#pragma unroll
-  for (; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  *leaf = q;
-  return s;
-}
 
 template <int G, int U, bool VEC>
 __global__ void __launch_bounds__(kBlock) k_tttp3_leaf(RootOutArgs a, const int32_t* leaf_i,
@@ -108,6 +85,7 @@ __global__ void __launch_bounds__(kBlock) k_tttp3_leaf(RootOutArgs a, const int3
     }
   }
 }
+
 
 template <int G, int U>
 void launch_g(const RootOutArgs& a, const int32_t* li, const int32_t* lj, cudaStream_t s,

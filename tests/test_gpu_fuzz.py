@@ -16,7 +16,7 @@ VARIANT_ENV = {1: ("SPTTN_MTTKRP_MODE", ["0", "1", "2", "3", "4"]),
                4: ("SPTTN_MTTKRP_MODE", ["0", "1", "2", "3"]),
                2: ("SPTTN_TTMC3_MODE", ["0", "4", "6", "7", "10"]),
                5: ("SPTTN_TTMC4_MODE", ["0", "1", "2", "3"]),
-               3: ("SPTTN_TTTP_MODE", ["0", "1"])}
+               3: ("SPTTN_TTTP_MODE", ["0", "1", "2"])}
 
 
 @pytest.fixture(scope="module")

@@ -94,7 +94,7 @@ def test_partition_independence(E, name, chunk, monkeypatch):
 VARIANTS = [("SPTTN_TTMC3_MODE", m, ["ttmc3_small", "ttmc3_r16"]) for m in ("0", "4", "6", "7", "10", "11")] + \
     [("SPTTN_MTTKRP_MODE", m, ["mttkrp3_small", "mttkrp3_r32", "mttkrp4_small", "mttkrp4_r32"])
      for m in ("0", "1", "2", "3", "4")] + \
-    [("SPTTN_TTTP_MODE", m, ["tttp3_small", "tttp3_r64"]) for m in ("0", "1")] + \
+    [("SPTTN_TTTP_MODE", m, ["tttp3_small", "tttp3_r64"]) for m in ("0", "1", "2")] + \
     [("SPTTN_TTMC4_MODE", m, ["ttmc4_small", "ttmc4_r8"]) for m in ("0", "1", "2", "3")] + \
     [("SPTTN_NONROOT_MODE", m, ["mttkrp3j_small", "mttkrp3j_r32", "mttkrp3k_small", "mttkrp3k_r32"])
      for m in ("0", "4")]
@@ -447,3 +447,27 @@ def test_mttkrp3_shared_factor_kernel(E, R, force, skew, monkeypatch):
     assert np.all(out.reshape(dims[0], R)[1::2] == 0.0)
     plan.execute()
     assert np.array_equal(plan.read_output(), out)
+
+
+def test_tttp_bucketed_layout_skew_and_residual(E, monkeypatch):
+    """TTTP mode 2 (leaves grouped by (i range, C-row bucket), 4-padded
+    runs, C rows in shared memory): a k-skewed pattern forced through it and
+    the residual flag, against the oracle; re-execution bit-identical."""
+    from paper_2307_05740_b200.tensor import Csf
+    monkeypatch.setenv("SPTTN_TTTP_MODE", "2")
+    monkeypatch.setenv("SPTTN_TTTP_KB_FORCE", "1")
+    rng = np.random.default_rng(7)
+    dims = (300, 200, 3000)
+    nnz = 50000
+    coords = np.stack([rng.integers(0, d, nnz) for d in dims], axis=1)
+    coords[: nnz // 4, 2] = 17  # one hot C row
+    vals = rng.uniform(-1, 1, nnz)
+    csf = Csf.from_coo(list(dims), coords, vals)
+    R = 64
+    fs = [rng.standard_normal((d, R)) * 0.35 for d in dims]
+    for flags, residual in ((0, False), (E.FLAG_RESIDUAL, True)):
+        out, plan, _ = run(E, 3, csf, fs, (R, 0, 0), flags)
+        want, norm = oracle_with_norm(3, csf, fs, (R, 0, 0), residual=residual)
+        assert_parity(out, want, norm, f"tttp bucketed residual={residual}")
+        plan.execute()
+        assert np.array_equal(plan.read_output(), out)
