@@ -1073,7 +1073,10 @@ __global__ void __launch_bounds__(kBlock, 2) k_ttmc4pq(RootOutArgs a) {
           // BLK: 64-byte rows, 16-byte chunk c stored at c ^ ((row >> 1) & 1)
           *reinterpret_cast<double2*>(BLK ? &S.vs[0][0] + gs * 8 + 2 * (gc ^ ((gs >> 1) & 1))
                                           : &S.vs[gs][2 * gc]) = vg;
-          *reinterpret_cast<double2*>(&S.ws[gs][2 * gc]) = wg;
+          // BLK: W rows swizzled like V (64-byte rows; the padded 80-byte rows
+          // of the other path made these stores 2-way bank conflicts)
+          *reinterpret_cast<double2*>(BLK ? &S.ws[0][0] + gs * 8 + 2 * (gc ^ ((gs >> 1) & 1))
+                                          : &S.ws[gs][2 * gc]) = wg;
           __syncwarp();
           const int32_t eA = hh.x - L0 + it * kPackSlots + q, eB = eA + 4;
           const double vA = S.tv[lbf][eA], vB = S.tv[lbf][eB];
@@ -1088,8 +1091,9 @@ __global__ void __launch_bounds__(kBlock, 2) k_ttmc4pq(RootOutArgs a) {
             const double2 b0 = *reinterpret_cast<const double2*>(vsf + (q + 4) * 8 + 2 * ((2 * sb) ^ sw));
             const double2 b1 =
                 *reinterpret_cast<const double2*>(vsf + (q + 4) * 8 + 2 * ((2 * sb + 1) ^ sw));
-            const double2 wa = *reinterpret_cast<const double2*>(&S.ws[q][2 * tb]);
-            const double2 wb = *reinterpret_cast<const double2*>(&S.ws[q + 4][2 * tb]);
+            const double* wsf = &S.ws[0][0];
+            const double2 wa = *reinterpret_cast<const double2*>(wsf + q * 8 + 2 * (tb ^ sw));
+            const double2 wb = *reinterpret_cast<const double2*>(wsf + (q + 4) * 8 + 2 * (tb ^ sw));
             __syncwarp();  // row tiles are rewritten by the next iteration
             const double va[4] = {a0.x, a0.y, a1.x, a1.y}, vb[4] = {b0.x, b0.y, b1.x, b1.y};
             const double xa[2] = {vA * wa.x, vA * wa.y}, xb[2] = {vB * wb.x, vB * wb.y};
