@@ -300,6 +300,10 @@ __global__ void __launch_bounds__(kBlock, 3) k_mttkrp_pq(RootOutArgs a) {
   int32_t nx_end = sl + 2 <= t.nlev[0] ? __ldg(slice_grp + sl + 2) : 0;
   int32_t nx_row = sl + 1 < t.nlev[0] ? __ldg(t.idx[0] + sl + 1) : 0;
   bool pending = false;
+  // order 4: the B[j] row stays in registers while consecutive groups give
+  // the lane's slot segments of the same (i,j) fiber (predicated-off load)
+  int32_t prev_j = -1;
+  double4 brow = make_double4(0, 0, 0, 0);
   double4 acc = make_double4(0, 0, 0, 0);
   const bool colok = c < R;
 
@@ -385,7 +389,15 @@ __global__ void __launch_bounds__(kBlock, 3) k_mttkrp_pq(RootOutArgs a) {
       }
       const double4 ur = rowq(Funit, u, true);
       double4 tr = make_double4(0, 0, 0, 0);
-      if (ORDER == 4) tr = rowq(Ftop, j, true);
+      if (ORDER == 4) {
+        const bool fresh = j != prev_j;
+        const double4 ld = VEC ? ld256_if(Ftop + static_cast<int64_t>(j) * R + c, fresh && colok)
+                               : (fresh ? row4<false>(Ftop + static_cast<int64_t>(j) * R, c, R)
+                                        : brow);
+        brow = fresh ? ld : brow;
+        prev_j = j;
+        tr = brow;
+      }
       double4 rr[4];
 #pragma unroll
       for (int it = 0; it < 4; ++it) rr[it] = rowq(Fleaf, kk[it], it < n);
