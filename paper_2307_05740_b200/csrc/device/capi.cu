@@ -44,6 +44,7 @@ struct spttn_plan {
   const double** d_dense = nullptr;
   int64_t launches = 0;
   int64_t last_madds = -1;
+  int fac_align = 8;  // factor alignment the plan's kernels were chosen for
   void* arena = nullptr;                // GENERIC: one allocation for all plan state
   std::vector<int64_t> last_counters;   // GENERIC: madds, resets, log cursor, overflow
   alignas(64) unsigned char tmap[2][128];  // TTMc-3 mode 11: U / V gather4 tensor maps
@@ -618,6 +619,7 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
       facs_aligned32 &= aligned(p->fac[f], 32);
       facs_aligned16 &= aligned(p->fac[f], 16);
     }
+    p->fac_align = facs_aligned32 ? 32 : facs_aligned16 ? 16 : 8;
 
     if (p->kind == SPTTN_NEST_GENERIC) {
       p->out_count = p->prog->out_size;
@@ -824,6 +826,12 @@ int spttn_plan_set_factors(spttn_plan* p, const double* const* factors, int32_t 
     if (!p) fail(SPTTN_EINVAL, "null plan");
     if (on_device && p->own_fac) fail(SPTTN_EINVAL, "plan owns its factor copies; pass host arrays");
     if (!on_device && !p->own_fac) fail(SPTTN_EINVAL, "plan uses device factors; pass device arrays");
+    if (on_device) {  // vector / cp.async kernels were picked for the plan's alignment
+      for (int f = 0; f < p->nf; ++f)
+        if (factors[f] && !aligned(factors[f], p->fac_align))
+          fail(SPTTN_EINVAL, "device factor less aligned than at plan creation (" +
+                                 std::to_string(p->fac_align) + " bytes); create a new plan");
+    }
     copy_factors(p, factors, on_device != 0, as_stream(stream));
     if (p->kind == SPTTN_NEST_GENERIC && on_device) {
       const double* hp[16] = {nullptr};

@@ -471,3 +471,24 @@ def test_tttp_bucketed_layout_skew_and_residual(E, monkeypatch):
         assert_parity(out, want, norm, f"tttp bucketed residual={residual}")
         plan.execute()
         assert np.array_equal(plan.read_output(), out)
+
+
+def test_set_factors_rejects_less_aligned_device_factors(E):
+    """Kernels are chosen for the factor alignment seen at plan creation
+    (256/128-bit gathers, 16-byte cp.async of factor columns); refreshing
+    device factors with a less aligned pointer is an EINVAL, not a fault."""
+    import torch
+    m = [c for c in CASES if c["name"] == "mttkrp3_r32"][0]
+    csf, factors, _ = load_case(m)
+    dev = E.DeviceCsf(csf)
+    tf = [torch.from_numpy(np.ascontiguousarray(f)).cuda() for f in factors]
+    plan = E.Plan(E.NEST_MTTKRP3, dev, [t.data_ptr() for t in tf], ranks=(32,),
+                  on_device=True, factor_sizes=[t.numel() for t in tf])
+    buf = torch.zeros(tf[0].numel() + 4, dtype=torch.float64, device="cuda")
+    view = buf[1:1 + tf[0].numel()]
+    with pytest.raises(ValueError):
+        plan.set_factors([view.data_ptr(), tf[1].data_ptr()], on_device=True)
+    plan.set_factors([t.data_ptr() for t in tf], on_device=True)
+    plan.execute()
+    want, norm = oracle_with_norm(1, csf, factors, (32, 0, 0))
+    assert_parity(plan.read_output(), want, norm, "after rejected refresh")
