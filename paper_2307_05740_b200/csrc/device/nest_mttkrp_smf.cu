@@ -329,13 +329,13 @@ __global__ void __launch_bounds__(kSmfWarps * 32, 1) k_mttkrp3_nr_smf(RootOutArg
   const int wid = uni(tid >> 5);
   const int lane = tid & 31;
   const int slot = lane >> 2;  // 8 slots, 4 lanes per 64-byte row
-  const int cp = lane & 3;     // columns 2cp, 2cp+1 of the quarter
+  const int cp = lane & 3;     // columns cp, cp+4 of the quarter (see add2)
   const int q = blockIdx.x % x.nq;
   const int cta = blockIdx.x / x.nq;
   const int R = a.R;
-  const int col = 8 * q + 2 * cp;
+  const int col = 8 * q + cp;
   const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  const unsigned cs = sbase + 16u * cp;
+  const unsigned cs = sbase + 8u * cp;
   const int32_t rows_in = x.rows_c, rows_out = x.rows_out;
   double* acc_sm = reinterpret_cast<double*>(smem + static_cast<int64_t>(rows_in) * 64);
   StageS* stages = reinterpret_cast<StageS*>(smem + static_cast<int64_t>(rows_in + rows_out) * 64);
@@ -407,10 +407,19 @@ __global__ void __launch_bounds__(kSmfWarps * 32, 1) k_mttkrp3_nr_smf(RootOutArg
   const double* __restrict__ Aq = a.f[0] + col;
   int32_t cur = -1;
   double2 ar = make_double2(0, 0);
-  auto add2 = [&](unsigned off, double vx, double vy) {  // shared fp64 atomics
+  // shared fp64 atomics (CAS loops) on columns cp and cp+4 of a 64-byte row:
+  // the row's half picked first alternates with bit 1 of the row index, so
+  // the 8 slots' rows of one instruction spread over 4 bank groups (2-way)
+  // instead of 2 (4-way, with columns 2cp, 2cp+1)
+  auto add2 = [&](unsigned off, double vx, double vy) {
     double* p = reinterpret_cast<double*>(smem + (off - sbase));
-    atomicAdd(p, vx);
-    atomicAdd(p + 1, vy);
+    const bool h = ((off - sbase) >> 7) & 1;  // (row >> 1) & 1
+    atomicAdd(p + (h ? 4 : 0), h ? vy : vx);
+    atomicAdd(p + (h ? 0 : 4), h ? vx : vy);
+  };
+  auto lds2 = [&](unsigned off) {  // columns cp, cp+4
+    const double* p = reinterpret_cast<const double*>(smem + (off - sbase));
+    return make_double2(p[0], p[4]);
   };
   for (int32_t win = 0; win < nwin; ++win) {
     const int mb = win % 3, lbf = win & 1;
@@ -427,7 +436,8 @@ __global__ void __launch_bounds__(kSmfWarps * 32, 1) k_mttkrp3_nr_smf(RootOutArg
       const int32_t sl = hh.y >> 3;
       if (sl != cur) {  // warp-uniform: A[i] once per root slice
         cur = sl;
-        ar = ld128(Aq + static_cast<int64_t>(__ldg(a.t.idx[0] + sl)) * R);
+        const double* arow = Aq + static_cast<int64_t>(__ldg(a.t.idx[0] + sl)) * R;
+        ar = make_double2(__ldg(arow), __ldg(arow + 4));
       }
       const int n = hh.y & 7;  // warp-uniform
       const int lb = hh.x - L0 + slot;
@@ -439,14 +449,14 @@ __global__ void __launch_bounds__(kSmfWarps * 32, 1) k_mttkrp3_nr_smf(RootOutArg
           if (it < n) {
             const unsigned kof = static_cast<unsigned>(S.kk[lbf][lb + it * kSSlots]);
             const double t = S.tv[lbf][lb + it * kSSlots];
-            const double2 c = lds128(cs + kof);
+            const double2 c = lds2(cs + kof);
             X.x = fma(t, c.x, X.x);
             X.y = fma(t, c.y, X.y);
           }
         }
         add2(cs + nodeoff, X.x * ar.x, X.y * ar.y);
       } else {  // C[k] += (A[i] * B[j]) * t
-        const double2 b = lds128(cs + nodeoff);
+        const double2 b = lds2(cs + nodeoff);
         const double2 W = make_double2(ar.x * b.x, ar.y * b.y);
 #pragma unroll
         for (int it = 0; it < 4; ++it) {
