@@ -695,10 +695,16 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
         int64_t chunk = env_int("SPTTN_CHUNK", 0);
         if (chunk <= 0) chunk = std::clamp<int64_t>((units + warps - 1) / warps, 8, 1024);
         if (p->kind == SPTTN_NEST_TTMC4)
-          // 3 = packed, TMA-staged, row-contiguous gathers, 4x2 (s,t) blocks per
-          // lane (default); 2 = same with a full s row per lane; 1 = packed
-          p->mode = static_cast<int>(env_int("SPTTN_TTMC4_MODE", 3));
-        if (p->kind == SPTTN_NEST_TTMC4 && p->mode >= 1 && p->mode <= 3) {
+          // 4 = 3 with the V / W row gathers by cp.async one leaf step ahead
+          // (default when S = T = 8, R <= 8, 16-byte aligned factors); 3 =
+          // packed, TMA-staged, row-contiguous gathers, 4x2 (s,t) blocks per
+          // lane; 2 = same with a full s row per lane; 1 = packed
+          p->mode = static_cast<int>(env_int(
+              "SPTTN_TTMC4_MODE", (R <= 8 && S == 8 && p->T == 8 && facs_aligned16) ? 4 : 3));
+        if (p->kind == SPTTN_NEST_TTMC4 && p->mode == 4 &&
+            !(R <= 8 && S == 8 && p->T == 8 && facs_aligned16))
+          p->mode = 3;
+        if (p->kind == SPTTN_NEST_TTMC4 && p->mode >= 1 && p->mode <= 4) {
           // (i,j) pieces of <= 4 leaves, length-sorted groups of 8, with each
           // leaf's level-2 (k) coordinate packed next to its level-3 (l) one
           spttn_dev::build_segments(D, 1, std::clamp(seg_len, 1, 4), chunk, p->dec, tile, s,

@@ -1267,6 +1267,213 @@ __global__ void __launch_bounds__(kBlock) k_ttmc4(RootOutArgs a) {
   if (pending) flush(head ? 0 : 1);
 }
 
+
+// TTMc-4 packed + TMA-staged, asynchronous row gathers (mode 4, default for
+// R, S, T <= 8 with S = T = 8 and 16-byte aligned factors). k_ttmc4pq's
+// mapping and math, but the V and W rows of a leaf step are copied into the
+// row tiles by cp.async (16 bytes per lane, the same row-contiguous lanes)
+// one step ahead — within a group, across groups and across staged windows —
+// into double-buffered tiles. ncu on k_ttmc4pq: the hottest instructions
+// were the tile stores waiting on their gathers (long-scoreboard 30 % at
+// 12.8 warps per SM); here the gather of step s+1 is in flight while step s
+// is computed, with no extra registers.
+struct StageT4a {
+  alignas(16) double vs[2][kPackSlots * 8];  // V rows (64 bytes, swizzled), double-buffered
+  alignas(16) double ws[2][kPackSlots * 8];  // W rows
+  alignas(16) int4 hdr[3][kGW];
+  alignas(16) int32_t node[3][kGW * kPackSlots];
+  alignas(16) int32_t ll[2][kGWLeaves];
+  alignas(16) int32_t kk[2][kGWLeaves];
+  alignas(16) double tv[2][kGWLeaves];
+  uint64_t mbar_meta[3];
+  uint64_t mbar_leaf[2];
+};
+constexpr size_t kT4aSmem = sizeof(StageT4a) * (kBlock / 32);
+
+__global__ void __launch_bounds__(kBlock, 2) k_ttmc4pa(RootOutArgs a) {
+  grid_launch_dependents();
+  extern __shared__ __align__(16) unsigned char t4a_smem[];
+  const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
+  if (w >= a.n_items) return;  // warp-uniform
+  StageT4a& S = reinterpret_cast<StageT4a*>(t4a_smem)[threadIdx.x / 32];
+  const int lane = threadIdx.x & 31;
+  const int q = lane & 3;   // fragment role: segment (K) index
+  const int h = lane >> 2;  //   and r / t index
+  const int gs = lane >> 2, gc = lane & 3;  // gather role: row slot, 16-byte chunk
+  const int R = a.R;
+  const CsfView& t = a.t;
+  const double* __restrict__ U = a.f[1];
+  const double* __restrict__ V = a.f[2];
+  const double* __restrict__ W = a.f[3];
+  const int32_t* __restrict__ slice_grp = a.slice_grp;
+  const int64_t tile = static_cast<int64_t>(R) * 64;
+  const int st_off = gs * 8 + 2 * (gc ^ ((gs >> 1) & 1));  // swizzled chunk of this lane
+
+  const int32_t cbeg = uni(static_cast<int32_t>(w * a.chunk));
+  const int32_t cend = uni(static_cast<int32_t>(min64(cbeg + a.chunk, a.n_groups)));
+  int32_t sl = a.item_pos[w];
+  int32_t sl_end = slice_grp[sl + 1];
+  bool head = slice_grp[sl] < cbeg;
+  int32_t row = t.idx[0][sl];
+  int32_t nx_end = sl + 2 <= t.nlev[0] ? __ldg(slice_grp + sl + 2) : 0;
+  int32_t nx_row = sl + 1 < t.nlev[0] ? __ldg(t.idx[0] + sl + 1) : 0;
+  bool pending = false;
+  double acc[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) acc[e] = 0.0;
+
+  auto flush = [&](int dslot) {
+    double* dst = dslot < 0 ? a.out + static_cast<int64_t>(row) * tile
+                            : a.part + (w * 2 + dslot) * tile;
+#pragma unroll
+    for (int nb = 0; nb < 8; ++nb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = 2 * q + e;
+        const int ss = 4 * (c & 1) + (nb >> 1);
+        const int tt = 2 * (c >> 1) + (nb & 1);
+        if (h < R) dst[(h * 8 + ss) * 8 + tt] = acc[2 * nb + e];
+      }
+#pragma unroll
+    for (int e = 0; e < 16; ++e) acc[e] = 0.0;
+  };
+  auto issue_meta = [&](int32_t wi) {
+    const int32_t g0 = cbeg + wi * kGW;
+    const int32_t nw = min(g0 + kGW, cend) - g0;
+    const int b = wi % 3;
+    const unsigned hb = nw * sizeof(int4), nb = nw * kPackSlots * sizeof(int32_t);
+    fence_proxy_async();
+    expect_tx_elect(&S.mbar_meta[b], hb + nb);
+    bulk_g2s_elect(&S.hdr[b][0], a.grp_hdr + g0, hb, &S.mbar_meta[b]);
+    bulk_g2s_elect(&S.node[b][0], a.grp_node + static_cast<int64_t>(g0) * kPackSlots, nb, &S.mbar_meta[b]);
+  };
+  auto issue_leaves = [&](int32_t wi) {
+    const int32_t g0 = cbeg + wi * kGW;
+    const int32_t nw = min(g0 + kGW, cend) - g0;
+    const int b = wi % 3, lb = wi & 1;
+    mbar_wait(&S.mbar_meta[b], (wi / 3) & 1);
+    const int32_t L0 = uni(S.hdr[b][0].x);
+    const int32_t L1 = uni(S.hdr[b][nw - 1].x + kPackSlots * S.hdr[b][nw - 1].y);
+    const unsigned n = static_cast<unsigned>(L1 - L0);
+    fence_proxy_async();
+    expect_tx_elect(&S.mbar_leaf[lb], n * 16u);
+    bulk_g2s_elect(&S.ll[lb][0], a.pk + L0, n * 4u, &S.mbar_leaf[lb]);
+    bulk_g2s_elect(&S.kk[lb][0], a.pk2 + L0, n * 4u, &S.mbar_leaf[lb]);
+    bulk_g2s_elect(&S.tv[lb][0], a.pv + L0, n * 8u, &S.mbar_leaf[lb]);
+  };
+  // cp.async of one leaf step's V and W rows (slot gs, chunk gc) into tile buf
+  auto issue_rows = [&](int buf, int lbuf, int32_t e) {
+    cp_async16_ca(&S.vs[buf][st_off], V + static_cast<int64_t>(S.kk[lbuf][e]) * 8 + 2 * gc);
+    cp_async16_ca(&S.ws[buf][st_off], W + static_cast<int64_t>(S.ll[lbuf][e]) * 8 + 2 * gc);
+    cp_async_commit();
+  };
+
+  const int32_t nwin = (cend - cbeg + kGW - 1) / kGW;
+  if (lane == 0) {
+    for (int b = 0; b < 3; ++b) mbar_init(&S.mbar_meta[b], 1);
+    for (int b = 0; b < 2; ++b) mbar_init(&S.mbar_leaf[b], 1);
+    mbar_init_fence();
+  }
+  __syncwarp();
+  if (nwin > 0) {
+    issue_meta(0);
+    if (nwin > 1) issue_meta(1);
+    issue_leaves(0);
+    mbar_wait(&S.mbar_meta[0], 0);
+    mbar_wait(&S.mbar_leaf[0], 0);
+    issue_rows(0, 0, gs);  // first step of the item (window 0 starts at its L0)
+  }
+  int buf = 0;  // tile of the current step
+  for (int32_t win = 0; win < nwin; ++win) {
+    const int mb = win % 3, lbf = win & 1;
+    if (win + 1 < nwin) issue_leaves(win + 1);
+    if (win + 2 < nwin) issue_meta(win + 2);
+    mbar_wait(&S.mbar_meta[mb], (win / 3) & 1);
+    mbar_wait(&S.mbar_leaf[lbf], (win / 2) & 1);
+    const int32_t g0 = cbeg + win * kGW;
+    const int32_t ge = min(g0 + kGW, cend);
+    const int32_t L0 = S.hdr[mb][0].x;
+    for (int32_t g = g0; g < ge; ++g) {
+      const int4 hh = S.hdr[mb][g - g0];
+      const int n = hh.y;  // warp-uniform leaves per segment
+      const int32_t jA = S.node[mb][(g - g0) * kPackSlots + q];
+      const int32_t jB = S.node[mb][(g - g0) * kPackSlots + 4 + q];
+      const double uA = h < R ? __ldg(U + static_cast<int64_t>(jA) * R + h) : 0.0;
+      const double uB = h < R ? __ldg(U + static_cast<int64_t>(jB) * R + h) : 0.0;
+      double YA[8], YB[8];
+#pragma unroll
+      for (int s = 0; s < 8; ++s) YA[s] = YB[s] = 0.0;
+#pragma unroll
+      for (int it = 0; it < 4; ++it) {
+        if (it < n) {  // warp-uniform
+          // prefetch the next leaf step (this group, the next group of the
+          // window, or the first group of the next window)
+          bool more = true;
+          if (it + 1 < n) {
+            issue_rows(buf ^ 1, lbf, hh.x - L0 + (it + 1) * kPackSlots + gs);
+          } else if (g + 1 < ge) {
+            issue_rows(buf ^ 1, lbf, S.hdr[mb][g + 1 - g0].x - L0 + gs);
+          } else if (win + 1 < nwin) {
+            const int nm = (win + 1) % 3, nl = (win + 1) & 1;
+            mbar_wait(&S.mbar_meta[nm], ((win + 1) / 3) & 1);
+            mbar_wait(&S.mbar_leaf[nl], ((win + 1) / 2) & 1);
+            issue_rows(buf ^ 1, nl, gs);  // the next window's first group starts at its L0
+          } else {
+            more = false;
+          }
+          if (more) cp_async_wait<1>(); else cp_async_wait<0>();
+          __syncwarp();
+          const int32_t eA = hh.x - L0 + it * kPackSlots + q, eB = eA + 4;
+          const double vA = S.tv[lbf][eA], vB = S.tv[lbf][eB];
+          // lane (q, h) owns Y[s = 4sb + i][t = 2tb + j] (i < 4, j < 2)
+          const int sb = h & 1, tb = h >> 1;
+          const int sw = (q >> 1) & 1;
+          const double* vsf = S.vs[buf];
+          const double* wsf = S.ws[buf];
+          const double2 a0 = *reinterpret_cast<const double2*>(vsf + q * 8 + 2 * ((2 * sb) ^ sw));
+          const double2 a1 = *reinterpret_cast<const double2*>(vsf + q * 8 + 2 * ((2 * sb + 1) ^ sw));
+          const double2 b0 = *reinterpret_cast<const double2*>(vsf + (q + 4) * 8 + 2 * ((2 * sb) ^ sw));
+          const double2 b1 =
+              *reinterpret_cast<const double2*>(vsf + (q + 4) * 8 + 2 * ((2 * sb + 1) ^ sw));
+          const double2 wa = *reinterpret_cast<const double2*>(wsf + q * 8 + 2 * (tb ^ sw));
+          const double2 wb = *reinterpret_cast<const double2*>(wsf + (q + 4) * 8 + 2 * (tb ^ sw));
+          __syncwarp();  // this tile is refilled by the step after next
+          buf ^= 1;
+          const double va[4] = {a0.x, a0.y, a1.x, a1.y}, vb[4] = {b0.x, b0.y, b1.x, b1.y};
+          const double xa[2] = {vA * wa.x, vA * wa.y}, xb[2] = {vB * wb.x, vB * wb.y};
+#pragma unroll
+          for (int i2 = 0; i2 < 4; ++i2)
+#pragma unroll
+            for (int j2 = 0; j2 < 2; ++j2) {
+              YA[2 * i2 + j2] = fma(va[i2], xa[j2], YA[2 * i2 + j2]);  // Y[s,t] += V[k,s] * X[t]
+              YB[2 * i2 + j2] = fma(vb[i2], xb[j2], YB[2 * i2 + j2]);
+            }
+        }
+      }
+      // Out_i[r, s, t] += U[j, r] * Y[s, t] for both K-chunks
+#pragma unroll
+      for (int s = 0; s < 8; ++s) dmma_8x8x4(acc[2 * s], acc[2 * s + 1], uA, YA[s]);
+#pragma unroll
+      for (int s = 0; s < 8; ++s) dmma_8x8x4(acc[2 * s], acc[2 * s + 1], uB, YB[s]);
+      pending = true;
+      if (g + 1 == sl_end) {
+        flush(head ? 0 : -1);
+        pending = false;
+        head = false;
+        if (g + 1 < cend) {
+          ++sl;
+          sl_end = nx_end;
+          row = nx_row;
+          nx_end = sl + 2 <= t.nlev[0] ? __ldg(slice_grp + sl + 2) : 0;
+          nx_row = sl + 1 < t.nlev[0] ? __ldg(t.idx[0] + sl + 1) : 0;
+        }
+      }
+    }
+    __syncwarp();  // stage buffers of this window are free after this point
+  }
+  if (pending) flush(head ? 0 : 1);
+}
+
 }  // namespace
 
 void launch_ttmc3(const RootOutArgs& a, cudaStream_t s) {
@@ -1345,7 +1552,11 @@ void launch_ttmc4(const RootOutArgs& a, cudaStream_t s) {
   const int64_t blocks = (a.n_items * 32 + kBlock - 1) / kBlock;
   if (blocks == 0) return;
   const int mode = a.flags >> 8;
-  if (mode == 2 || mode == 3) {
+  if (mode == 4) {  // async row gathers (the plan checked S = T = 8, R <= 8, alignment)
+    SPTTN_CUDA(cudaFuncSetAttribute(k_ttmc4pa, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kT4aSmem)));
+    k_ttmc4pa<<<static_cast<unsigned>(blocks), kBlock, kT4aSmem, s>>>(a);
+  } else if (mode == 2 || mode == 3) {
     const bool vv = a.vec & 2, vw = a.vec & 4;
     const unsigned b = static_cast<unsigned>(blocks);
     if (mode == 3) {  // 4 x 2 (s, t) blocks per lane

@@ -15,7 +15,7 @@ RANKS = [1, 2, 3, 4, 5, 7, 8, 12, 16, 17, 24, 31, 32, 33, 48, 64, 100, 128]
 VARIANT_ENV = {1: ("SPTTN_MTTKRP_MODE", ["0", "1", "2", "3", "4"]),
                4: ("SPTTN_MTTKRP_MODE", ["0", "1", "2", "3"]),
                2: ("SPTTN_TTMC3_MODE", ["0", "4", "6", "7", "10"]),
-               5: ("SPTTN_TTMC4_MODE", ["0", "1", "2", "3"]),
+               5: ("SPTTN_TTMC4_MODE", ["0", "1", "2", "3", "4"]),
                3: ("SPTTN_TTTP_MODE", ["0", "1", "2"])}
 
 

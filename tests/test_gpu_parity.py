@@ -95,7 +95,7 @@ VARIANTS = [("SPTTN_TTMC3_MODE", m, ["ttmc3_small", "ttmc3_r16"]) for m in ("0",
     [("SPTTN_MTTKRP_MODE", m, ["mttkrp3_small", "mttkrp3_r32", "mttkrp4_small", "mttkrp4_r32"])
      for m in ("0", "1", "2", "3", "4")] + \
     [("SPTTN_TTTP_MODE", m, ["tttp3_small", "tttp3_r64"]) for m in ("0", "1", "2")] + \
-    [("SPTTN_TTMC4_MODE", m, ["ttmc4_small", "ttmc4_r8"]) for m in ("0", "1", "2", "3")] + \
+    [("SPTTN_TTMC4_MODE", m, ["ttmc4_small", "ttmc4_r8"]) for m in ("0", "1", "2", "3", "4")] + \
     [("SPTTN_NONROOT_MODE", m, ["mttkrp3j_small", "mttkrp3j_r32", "mttkrp3k_small", "mttkrp3k_r32"])
      for m in ("0", "4")]
 
