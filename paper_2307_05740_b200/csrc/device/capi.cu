@@ -724,8 +724,14 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
           spttn_dev::build_segments(D, 1, seg_len, chunk, p->dec, tile, s, false);
           spttn_dev::build_packed(D, 2, p->dec, s);
           int64_t gchunk = env_int("SPTTN_GCHUNK", 0);
-          if (gchunk <= 0)
-            gchunk = std::clamp<int64_t>((p->dec.n_groups + warps - 1) / warps, 4, 512);
+          if (gchunk <= 0) {
+            // mode 10: one item per resident warp (a single wave; 2.6 waves of
+            // half-size items measured 278 vs 269 us per step at the BASELINE
+            // shape — fewer split slices for the fix-up, no tail wave)
+            const int64_t wv = p->mode == 10 ? static_cast<int64_t>(sms) * spttn_dev::ttmc3pq_warps_per_sm()
+                                             : warps;
+            gchunk = std::clamp<int64_t>((p->dec.n_groups + wv - 1) / wv, 4, 512);
+          }
           spttn_dev::finish_unit_items(D, p->dec, p->dec.slice_grp, p->dec.n_groups, gchunk, tile, s);
         } else {
           spttn_dev::build_segments(D, 1, seg_len, chunk, p->dec, tile, s);

@@ -143,6 +143,7 @@ void launch_mttkrp3(const RootOutArgs& a, cudaStream_t s);
 void launch_mttkrp4(const RootOutArgs& a, cudaStream_t s);
 void launch_tttp3(const RootOutArgs& a, cudaStream_t s);
 void launch_ttmc3(const RootOutArgs& a, cudaStream_t s);
+int ttmc3pq_warps_per_sm();
 void launch_ttmc4(const RootOutArgs& a, cudaStream_t s);
 // TTMc-3 with TMA gather4 row loads (nest_ttmc3_tma.cu): needs R = S = 16.
 bool ttmc3_tma_supported(int R, int S);

@@ -1476,6 +1476,18 @@ __global__ void __launch_bounds__(kBlock, 2) k_ttmc4pa(RootOutArgs a) {
 
 }  // namespace
 
+// resident warps per SM of the TTMc-3 default kernel (plan-time item sizing:
+// one item per resident warp, a single wave)
+int ttmc3pq_warps_per_sm() {
+  int blocks = 0;
+  if (cudaFuncSetAttribute(k_ttmc3pq<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(kPqSmem)) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_ttmc3pq<true, true>, kBlock,
+                                                    kPqSmem) != cudaSuccess)
+    blocks = 3;
+  return std::max(1, blocks) * (kBlock / 32);
+}
+
 void launch_ttmc3(const RootOutArgs& a, cudaStream_t s) {
   const int64_t blocks = (a.n_items * 32 + kBlock - 1) / kBlock;
   if (blocks == 0) return;
