@@ -119,7 +119,9 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
                       spttn_plan** out);
 int spttn_plan_destroy(spttn_plan* plan);
 
-/* Replaces the factor values (same shapes), e.g. between ALS sweeps. */
+/* Replaces the factor values (same shapes), e.g. between ALS sweeps. Device
+ * factors (on_device) must be at least as aligned as those the plan was
+ * created with (the kernel variant depends on it): SPTTN_EINVAL otherwise. */
 int spttn_plan_set_factors(spttn_plan* plan, const double* const* factors, int32_t on_device,
                            void* stream);
 
