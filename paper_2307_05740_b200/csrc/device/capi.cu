@@ -732,7 +732,11 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
                                              : warps;
             gchunk = std::clamp<int64_t>((p->dec.n_groups + wv - 1) / wv, 4, 512);
           }
-          spttn_dev::finish_unit_items(D, p->dec, p->dec.slice_grp, p->dec.n_groups, gchunk, tile, s);
+          // k_ttmc3pq reads variable item ranges cut at equal work (leaf steps
+          // + a per-group overhead, decomp.cu k_group_work): 256 -> 249 us
+          const bool balanced = p->mode == 10 && env_int("SPTTN_ITEM_BALANCE", 1) != 0;
+          spttn_dev::finish_unit_items(D, p->dec, p->dec.slice_grp, p->dec.n_groups, gchunk, tile, s,
+                                       balanced);
         } else {
           spttn_dev::build_segments(D, 1, seg_len, chunk, p->dec, tile, s);
         }
@@ -895,6 +899,7 @@ int spttn_execute_stage(spttn_plan* p, int stage, void* stream) {
     a.pv = p->dec.pv;
     a.slice_grp = p->dec.slice_grp;
     a.n_groups = p->dec.n_groups;
+    a.item_unit = p->dec.item_unit;
     if (stage != 1) switch (p->kind) {
       case SPTTN_NEST_MTTKRP3_J:
       case SPTTN_NEST_MTTKRP3_K:

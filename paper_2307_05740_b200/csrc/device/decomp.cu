@@ -145,18 +145,28 @@ __global__ void k_slice_seg(CsfView t, int unit_level, const int32_t* off, int32
 }
 
 __global__ void k_seg_items(const int32_t* slice_seg, int32_t n0, int64_t chunk, int64_t n_items,
-                            int32_t* item_pos) {
+                            const int32_t* item_unit, int32_t* item_pos) {
   const int64_t w = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (w >= n_items) return;
-  item_pos[w] = parent_of(slice_seg, n0, static_cast<int32_t>(w * chunk));
+  const int32_t u0 = item_unit ? item_unit[w] : static_cast<int32_t>(w * chunk);
+  item_pos[w] = parent_of(slice_seg, n0, u0);
 }
 
-__global__ void k_seg_splits(CsfView t, const int32_t* slice_seg, int64_t chunk, int32_t* node,
+// item holding unit u: fixed chunks, or the last item starting at or before u
+__device__ __forceinline__ int64_t item_of(int64_t u, int64_t chunk, const int32_t* item_unit,
+                                           int64_t n_items) {
+  if (!item_unit) return u / chunk;
+  return parent_of(item_unit, static_cast<int32_t>(n_items), static_cast<int32_t>(u));
+}
+
+__global__ void k_seg_splits(CsfView t, const int32_t* slice_seg, int64_t chunk,
+                             const int32_t* item_unit, int64_t n_items, int32_t* node,
                              int32_t* first, int32_t* last, int32_t* count,
                              unsigned char* present) {
   const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= t.nlev[0]) return;
-  const int64_t f = slice_seg[s] / chunk, g = (static_cast<int64_t>(slice_seg[s + 1]) - 1) / chunk;
+  const int64_t f = item_of(slice_seg[s], chunk, item_unit, n_items);
+  const int64_t g = item_of(static_cast<int64_t>(slice_seg[s + 1]) - 1, chunk, item_unit, n_items);
   if (f != g) {
     const int32_t slot = atomicAdd(count, 1);
     node[slot] = s;
@@ -164,6 +174,37 @@ __global__ void k_seg_splits(CsfView t, const int32_t* slice_seg, int64_t chunk,
     last[slot] = static_cast<int32_t>(g);
   }
   present[t.idx[0][s]] = 1;
+}
+
+// per-group work of a packed group: its leaf steps plus the group overhead
+// (header / slot loads, U gather, fragment transposition, 8 DMMA) in
+// leaf-step units. Measured on the TTMc-3 BASELINE shape (kernel us):
+// overhead 2: 295, 6: 259, 9: 252, 12: 249, 16: 249, 24: 251, equal group
+// counts (infinite overhead): 256.
+constexpr int kGroupOverhead = 12;
+__global__ void k_group_work(const int4* hdr, int64_t n, int32_t* work) {
+  const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (g < n) work[g] = hdr[g].y + kGroupOverhead;
+}
+
+// item t starts at the first group whose inclusive work prefix exceeds
+// t * total / n_items (strictly increasing: one group never holds a whole
+// item's share at the sizes this is used for; clamped anyway)
+__global__ void k_work_bounds(const int32_t* cum, int64_t n, int64_t n_items, int32_t* item_unit) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t > n_items) return;
+  if (t == 0) { item_unit[0] = 0; return; }
+  if (t == n_items) { item_unit[t] = static_cast<int32_t>(n); return; }
+  const int64_t total = cum[n - 1];
+  const int64_t target = total * t / n_items;
+  int64_t lo = 0, hi = n;  // first g with cum[g] > target
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (cum[mid] > target) hi = mid; else lo = mid + 1;
+  }
+  lo = lo < t ? t : lo;                       // >= one group per earlier item
+  lo = lo > n - (n_items - t) ? n - (n_items - t) : lo;
+  item_unit[t] = static_cast<int32_t>(lo);
 }
 
 unsigned blocks_for(int64_t n, int b) { return static_cast<unsigned>((n + b - 1) / b); }
@@ -213,9 +254,9 @@ void find_splits_and_absent(const DevCsf& csf, Decomp& d, const int32_t* slice_u
   dmalloc(&d.absent_rows, csf.dims[0] * sizeof(int32_t), s);
   if (n0 > 0) {
     if (segments)
-      k_seg_splits<<<blocks_for(n0, 256), 256, 0, s>>>(t, slice_units, d.chunk, d.split_node,
-                                                       d.split_first, d.split_last, counts,
-                                                       present);
+      k_seg_splits<<<blocks_for(n0, 256), 256, 0, s>>>(t, slice_units, d.chunk, d.item_unit,
+                                                       d.n_items, d.split_node, d.split_first,
+                                                       d.split_last, counts, present);
     else
       k_leaf_splits<<<blocks_for(n0, 256), 256, 0, s>>>(t, d.chunk, d.split_node, d.split_first,
                                                         d.split_last, counts, present);
@@ -321,15 +362,33 @@ void build_segments(const DevCsf& csf, int unit_level, int seg_len, int64_t chun
 }
 
 void finish_unit_items(const DevCsf& csf, Decomp& d, const int32_t* slice_units, int64_t n_units,
-                       int64_t chunk, int64_t tile, cudaStream_t s) {
+                       int64_t chunk, int64_t tile, cudaStream_t s, bool work_groups) {
   const int32_t n0 = static_cast<int32_t>(csf.level_size[0]);
   d.chunk = chunk;
   d.tile = tile;
   d.n_items = (n_units + chunk - 1) / chunk;
+  if (work_groups && d.n_items > 1) {
+    // cumulative work per packed group (leaf steps + per-group overhead),
+    // then item t starts at the first group whose prefix reaches t/n of it
+    int32_t* cum = nullptr;
+    dmalloc(&cum, n_units * sizeof(int32_t), s);
+    k_group_work<<<blocks_for(n_units, 256), 256, 0, s>>>(d.grp_hdr, n_units, cum);
+    size_t bytes = 0;
+    SPTTN_CUDA(cub::DeviceScan::InclusiveSum(nullptr, bytes, cum, cum, static_cast<int>(n_units), s));
+    void* tmp = nullptr;
+    dmalloc(&tmp, std::max<size_t>(1, bytes), s);
+    SPTTN_CUDA(cub::DeviceScan::InclusiveSum(tmp, bytes, cum, cum, static_cast<int>(n_units), s));
+    dfree(tmp, s);
+    dmalloc(&d.item_unit, (d.n_items + 1) * sizeof(int32_t), s);
+    k_work_bounds<<<blocks_for(d.n_items + 1, 256), 256, 0, s>>>(cum, n_units, d.n_items,
+                                                                 d.item_unit);
+    SPTTN_CUDA(cudaGetLastError());
+    dfree(cum, s);
+  }
   dmalloc(&d.item_pos, std::max<int64_t>(1, d.n_items) * sizeof(int32_t), s);
   if (d.n_items > 0) {
     k_seg_items<<<blocks_for(d.n_items, 256), 256, 0, s>>>(slice_units, n0, chunk, d.n_items,
-                                                          d.item_pos);
+                                                          d.item_unit, d.item_pos);
     SPTTN_CUDA(cudaGetLastError());
   }
   dmalloc(&d.part, std::max<int64_t>(1, d.n_items * 2 * tile) * sizeof(double), s);
@@ -597,6 +656,7 @@ void free_decomp(Decomp& d) {
   dfree(d.slice_grp);
   dfree(d.slice_seg);
   dfree(d.cta_grp);
+  dfree(d.item_unit);
   dfree(d.hdr2);
   d = Decomp{};
 }

@@ -95,6 +95,9 @@ struct Decomp {
   double* pv = nullptr;            // interleaved leaf values
   int32_t* slice_grp = nullptr;    // [n0+1] first group of each slice
   int32_t* slice_seg = nullptr;    // [n0+1]   segment offset of each slice
+  // variable items (finish_unit_items with unit_work): item t = units
+  // [item_unit[t], item_unit[t+1]), cut at equal cumulative work
+  int32_t* item_unit = nullptr;    // [n_items+1] or nullptr (fixed `chunk` items)
   // CTA-range kernels (k_mttkrp3_smf): slice-aligned group range per CTA
   int64_t n_cta = 0;
   int32_t* cta_grp = nullptr;      // [n_cta+1]
@@ -137,6 +140,7 @@ struct RootOutArgs {
   const double* pv;
   const int32_t* slice_grp;
   int64_t n_groups;
+  const int32_t* item_unit;  // variable item boundaries (TTMc-3 default kernel) or nullptr
 };
 
 void launch_mttkrp3(const RootOutArgs& a, cudaStream_t s);
@@ -233,8 +237,11 @@ void expand_coords(const DevCsf& csf, int level, const int32_t* coords, int32_t*
                    cudaStream_t s);
 // Items of `chunk` consecutive units (segments or packed groups) given the
 // first unit of every root slice; partial tiles, split slices, absent rows.
+// work_groups (packed groups only): items cut at equal cumulative work
+// (leaf steps + a per-group constant) instead of equal group counts; the
+// kernel must then read its range from d.item_unit.
 void finish_unit_items(const DevCsf& csf, Decomp& d, const int32_t* slice_units, int64_t n_units,
-                       int64_t chunk, int64_t tile, cudaStream_t s);
+                       int64_t chunk, int64_t tile, cudaStream_t s, bool work_groups = false);
 // Length-sorted packed groups of 8 segments (pack.cu); leaf_level = CSF level
 // of the streamed coordinates.
 constexpr int kPackSlots = 8;  // TTMc-3 groups (128-byte rows)
