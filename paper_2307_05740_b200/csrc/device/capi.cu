@@ -718,7 +718,12 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
           int64_t gchunk = env_int("SPTTN_GCHUNK", 0);
           if (gchunk <= 0)
             gchunk = std::clamp<int64_t>((p->dec.n_groups + w16 - 1) / w16, 4, 1024);
-          spttn_dev::finish_unit_items(D, p->dec, p->dec.slice_grp, p->dec.n_groups, gchunk, tile, s);
+          // mode 4: items cut at equal work, leaf steps + 3 per group
+          // (BASELINE shape, kernel us: equal group counts 448; overhead 2:
+          // 408, 3: 404, 4: 409, 6: 416)
+          const int ovh4 = p->mode == 4 ? static_cast<int>(env_int("SPTTN_GROUP_OVERHEAD", 3)) : 0;
+          spttn_dev::finish_unit_items(D, p->dec, p->dec.slice_grp, p->dec.n_groups, gchunk, tile, s,
+                                       ovh4);
         } else if (p->kind == SPTTN_NEST_TTMC3 && (p->mode == 6 || p->mode == 7 || p->mode == 10 || p->mode == 11)) {
           // packed length-sorted groups of 8 segments (pack.cu)
           spttn_dev::build_segments(D, 1, seg_len, chunk, p->dec, tile, s, false);
@@ -734,9 +739,9 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
           }
           // k_ttmc3pq reads variable item ranges cut at equal work (leaf steps
           // + a per-group overhead, decomp.cu k_group_work): 256 -> 249 us
-          const bool balanced = p->mode == 10 && env_int("SPTTN_ITEM_BALANCE", 1) != 0;
+          const int ovh = p->mode == 10 ? static_cast<int>(env_int("SPTTN_GROUP_OVERHEAD", 12)) : 0;
           spttn_dev::finish_unit_items(D, p->dec, p->dec.slice_grp, p->dec.n_groups, gchunk, tile, s,
-                                       balanced);
+                                       ovh);
         } else {
           spttn_dev::build_segments(D, 1, seg_len, chunk, p->dec, tile, s);
         }
@@ -784,7 +789,10 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
           if (gchunk <= 0)
             gchunk = std::clamp<int64_t>((p->dec.n_groups + w24 - 1) / w24, 4,
                                          p->mode == 3 ? 64 : 1024);
-          spttn_dev::finish_unit_items(D, p->dec, p->dec.slice_grp, p->dec.n_groups, gchunk, tile, s);
+          // equal group counts by default (work-cut items: within 1 %)
+          const int ovhm = p->mode == 3 ? static_cast<int>(env_int("SPTTN_GROUP_OVERHEAD", 0)) : 0;
+          spttn_dev::finish_unit_items(D, p->dec, p->dec.slice_grp, p->dec.n_groups, gchunk, tile, s,
+                                       ovhm);
         } else if (p->mode != 4) {
           spttn_dev::build_segments(D, unit_level, seg_len, chunk, p->dec, tile, s);
         }

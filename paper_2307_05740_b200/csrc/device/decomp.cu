@@ -181,10 +181,10 @@ __global__ void k_seg_splits(CsfView t, const int32_t* slice_seg, int64_t chunk,
 // leaf-step units. Measured on the TTMc-3 BASELINE shape (kernel us):
 // overhead 2: 295, 6: 259, 9: 252, 12: 249, 16: 249, 24: 251, equal group
 // counts (infinite overhead): 256.
-constexpr int kGroupOverhead = 12;
-__global__ void k_group_work(const int4* hdr, int64_t n, int32_t* work) {
+
+__global__ void k_group_work(const int4* hdr, int64_t n, int overhead, int32_t* work) {
   const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (g < n) work[g] = hdr[g].y + kGroupOverhead;
+  if (g < n) work[g] = hdr[g].y + overhead;
 }
 
 // item t starts at the first group whose inclusive work prefix exceeds
@@ -362,17 +362,17 @@ void build_segments(const DevCsf& csf, int unit_level, int seg_len, int64_t chun
 }
 
 void finish_unit_items(const DevCsf& csf, Decomp& d, const int32_t* slice_units, int64_t n_units,
-                       int64_t chunk, int64_t tile, cudaStream_t s, bool work_groups) {
+                       int64_t chunk, int64_t tile, cudaStream_t s, int group_overhead) {
   const int32_t n0 = static_cast<int32_t>(csf.level_size[0]);
   d.chunk = chunk;
   d.tile = tile;
   d.n_items = (n_units + chunk - 1) / chunk;
-  if (work_groups && d.n_items > 1) {
+  if (group_overhead > 0 && d.n_items > 1) {
     // cumulative work per packed group (leaf steps + per-group overhead),
     // then item t starts at the first group whose prefix reaches t/n of it
     int32_t* cum = nullptr;
     dmalloc(&cum, n_units * sizeof(int32_t), s);
-    k_group_work<<<blocks_for(n_units, 256), 256, 0, s>>>(d.grp_hdr, n_units, cum);
+    k_group_work<<<blocks_for(n_units, 256), 256, 0, s>>>(d.grp_hdr, n_units, group_overhead, cum);
     size_t bytes = 0;
     SPTTN_CUDA(cub::DeviceScan::InclusiveSum(nullptr, bytes, cum, cum, static_cast<int>(n_units), s));
     void* tmp = nullptr;

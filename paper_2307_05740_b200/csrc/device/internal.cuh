@@ -237,11 +237,11 @@ void expand_coords(const DevCsf& csf, int level, const int32_t* coords, int32_t*
                    cudaStream_t s);
 // Items of `chunk` consecutive units (segments or packed groups) given the
 // first unit of every root slice; partial tiles, split slices, absent rows.
-// work_groups (packed groups only): items cut at equal cumulative work
-// (leaf steps + a per-group constant) instead of equal group counts; the
-// kernel must then read its range from d.item_unit.
+// group_overhead > 0 (packed groups only): items cut at equal cumulative
+// work (leaf steps + group_overhead per group) instead of equal group
+// counts; the kernel must then read its range from d.item_unit.
 void finish_unit_items(const DevCsf& csf, Decomp& d, const int32_t* slice_units, int64_t n_units,
-                       int64_t chunk, int64_t tile, cudaStream_t s, bool work_groups = false);
+                       int64_t chunk, int64_t tile, cudaStream_t s, int group_overhead = 0);
 // Length-sorted packed groups of 8 segments (pack.cu); leaf_level = CSF level
 // of the streamed coordinates.
 constexpr int kPackSlots = 8;  // TTMc-3 groups (128-byte rows)

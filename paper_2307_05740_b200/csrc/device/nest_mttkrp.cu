@@ -291,8 +291,10 @@ __global__ void __launch_bounds__(kBlock, 3) k_mttkrp_pq(RootOutArgs a) {
   const double* __restrict__ Ftop = a.f[1];
   const int32_t* __restrict__ slice_grp = a.slice_grp;
 
-  const int32_t cbeg = uni(static_cast<int32_t>(w * a.chunk));
-  const int32_t cend = uni(static_cast<int32_t>(min64(cbeg + a.chunk, a.n_groups)));
+  const int32_t cbeg =
+      uni(a.item_unit ? __ldg(a.item_unit + w) : static_cast<int32_t>(w * a.chunk));
+  const int32_t cend = uni(a.item_unit ? __ldg(a.item_unit + w + 1)
+                                       : static_cast<int32_t>(min64(cbeg + a.chunk, a.n_groups)));
   int32_t sl = a.item_pos[w];
   int32_t sl_end = slice_grp[sl + 1];
   bool head = slice_grp[sl] < cbeg;

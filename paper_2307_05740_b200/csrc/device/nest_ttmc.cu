@@ -1311,8 +1311,10 @@ __global__ void __launch_bounds__(kBlock, 2) k_ttmc4pa(RootOutArgs a) {
   const int64_t tile = static_cast<int64_t>(R) * 64;
   const int st_off = gs * 8 + 2 * (gc ^ ((gs >> 1) & 1));  // swizzled chunk of this lane
 
-  const int32_t cbeg = uni(static_cast<int32_t>(w * a.chunk));
-  const int32_t cend = uni(static_cast<int32_t>(min64(cbeg + a.chunk, a.n_groups)));
+  const int32_t cbeg =
+      uni(a.item_unit ? __ldg(a.item_unit + w) : static_cast<int32_t>(w * a.chunk));
+  const int32_t cend = uni(a.item_unit ? __ldg(a.item_unit + w + 1)
+                                       : static_cast<int32_t>(min64(cbeg + a.chunk, a.n_groups)));
   int32_t sl = a.item_pos[w];
   int32_t sl_end = slice_grp[sl + 1];
   bool head = slice_grp[sl] < cbeg;
