@@ -100,3 +100,11 @@ build/tests/generic_scale: tests/cpp/generic_scale.cpp $(LIB)/libspttn_b200_host
 	@mkdir -p $(dir $@)
 	$(CXX) $(HOSTFLAGS) -I$(REF)/tests $< -L$(LIB) -lspttn_b200_host -lspttn_b200 \
 	  -Wl,-rpath,'$$ORIGIN/../../$(LIB)' -o $@
+
+# Microbenchmark probes behind the DESIGN.md measurements (not part of `all`;
+# binaries are git-ignored): make probes
+PROBES := $(patsubst tools/%.cu,tools/%,$(wildcard tools/*_probe.cu))
+probes: $(PROBES)
+tools/%_probe: tools/%_probe.cu
+	$(NVCC) $(ARCH) -O3 -lineinfo -std=c++17 $< -o $@ -lcuda
+.PHONY: probes

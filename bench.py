@@ -63,6 +63,8 @@ def parse():
                     help="target CPU time of a bounded reference sample")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true",
+                    help="skip the per-config parity check against the C oracle")
     ap.add_argument("--shard", action="store_true",
                     help="N>1: split ONE tensor's root slices over the ranks (strong "
                          "scaling) instead of one independent tensor per rank (weak)")
@@ -208,6 +210,38 @@ def device_time_config(P, w, steps, warmup, stream, flush, ev):
     w_ms = [a.elapsed_time(b) for a, b in whole]
     return {"main_ms": statistics.mean(m), "epi_ms": statistics.mean(e),
             "main_ms_min": min(m), "step_ms": statistics.mean(w_ms)}, plan, dev, tfac
+
+
+def parity_check(P, w, plan, stream):
+    """Checker, outside every timed region: the output of the plan just timed
+    against the plain-C oracle (test infrastructure, pinned to the reference
+    by tests/test_oracle.py) on the same full-size inputs. Bar: |gpu - cpu|
+    <= 1e-10 * sum|contributions| per entry, entries without contributions
+    exactly 0, a second execute bit-identical (owner-computes kernels)."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_bindings as OB
+    c = w.cfg
+    t0 = time.perf_counter()
+    plan.execute(stream)
+    got = plan.read_output(stream)
+    plan.execute(stream)
+    again = plan.read_output(stream)
+    want = OB.oracle_nest(c.kind, w.csf, w.factors, c.ranks, residual=c.residual)
+    norm = OB.oracle_abs_nest(c.kind, w.csf, w.factors, c.ranks, residual=c.residual)
+    err = np.abs(got - want)
+    nz = norm > 0
+    rel = float((err[nz] / norm[nz]).max()) if nz.any() else 0.0
+    atomic = c.kind in (P.NEST_MTTKRP3_J, P.NEST_MTTKRP3_K)
+    return {"checker": "oracle/spttn_oracle.c (pinned to the reference executor)",
+            "entries": int(got.size), "max_normalised_err": rel, "tol": 1e-10,
+            "outside_tol": int((err > 1e-10 * norm).sum()),
+            "zero_entries": int((~nz).sum()),
+            "nonzero_where_zero": int((got[~nz] != 0.0).sum()),
+            "rerun_bit_identical": bool(np.array_equal(got, again)),
+            "rerun_required_bit_identical": not atomic,
+            "ok": bool(rel <= 1e-10 and not (got[~nz] != 0.0).any() and
+                       (atomic or np.array_equal(got, again))),
+            "seconds": time.perf_counter() - t0}
 
 
 def e2e_config(P, w, steps, stream):
@@ -464,6 +498,8 @@ def main():
              "epilogue_ms": st["epi_ms"], "launches_per_step": info["launches"],
              "items": info["items"], "split_slices": info["split_slices"],
              "region_s": region, "roofline": roof}
+        if not args.no_parity:
+            r["parity"] = parity_check(P, w, plan, stream)
         plan.close()
         dev.close()
         del tfac
@@ -505,6 +541,7 @@ def main():
         "roofline": h["roofline"], "gpu_launches": h["launches_per_step"] * args.steps,
         "clocks": head_clocks, "e2e": h.get("e2e"), "cpu_baseline": h.get("cpu_baseline"),
         "fp64_peaks": fp64,
+        "parity": {k: v.get("parity", {}).get("ok") for k, v in results.items()},
         "configs": {k: v for k, v in results.items()},
     }
     if rank == 0:

@@ -184,6 +184,9 @@ int spttn_device_info(int64_t* out, int n);
  * context creation; SPTTN_LAZY_INIT=1 skips that). SPTTN_ECUDA without a
  * device. */
 int spttn_init(void);
+/* Waits for all work on `stream` (NULL = the whole device); used by the
+ * drop-in's phase tracing (SPTTN_SHIM_TRACE=2). */
+int spttn_synchronize(void* stream);
 /* Build identification string (arch, nvcc version). */
 const char* spttn_build_info(void);
 /* Device memory of CSF layouts and plans comes from a per-device

@@ -69,7 +69,7 @@ ENGINE_SYMBOLS = [
     "spttn_plan_set_factors", "spttn_execute", "spttn_execute_stage", "spttn_output_count", "spttn_output_device",
     "spttn_read_output", "spttn_plan_info", "spttn_generic_resets", "spttn_generic_log_bytes",
     "spttn_generic_read_log", "spttn_unfactorized", "spttn_device_info", "spttn_build_info",
-    "spttn_release_cached", "spttn_init", "spttn_csf_from_coo", "spttn_csf_download",
+    "spttn_release_cached", "spttn_init", "spttn_synchronize", "spttn_csf_from_coo", "spttn_csf_download",
     "spttn_csf_dim", "spttn_csf_permute",
 ]
 
@@ -116,6 +116,7 @@ def engine() -> C.CDLL:
         lib.spttn_generic_read_log.argtypes = [P, C.c_void_p, c_i64, P]
         lib.spttn_unfactorized.argtypes = [C.POINTER(UnfactDesc), P, c_dbl_p, c_i64, P]
         lib.spttn_device_info.argtypes = [c_i64_p, C.c_int]
+        lib.spttn_synchronize.argtypes = [P]
         lib.spttn_csf_from_coo.argtypes = [C.c_int, c_i64_p, c_i64, c_i64_p, c_dbl_p, P,
                                            C.POINTER(P)]
         lib.spttn_csf_download.argtypes = [P, C.POINTER(c_i64_p), C.POINTER(c_i64_p), c_dbl_p, P]

@@ -179,6 +179,13 @@ int spttn_init(void) {
   });
 }
 
+int spttn_synchronize(void* stream) {
+  return guarded([&] {
+    if (stream) SPTTN_CUDA(cudaStreamSynchronize(as_stream(stream)));
+    else SPTTN_CUDA(cudaDeviceSynchronize());
+  });
+}
+
 int spttn_device_info(int64_t* out, int n) {
   return guarded([&] {
     int dev = 0;

@@ -182,29 +182,41 @@ __global__ void k_seg_splits(CsfView t, const int32_t* slice_seg, int64_t chunk,
 // overhead 2: 295, 6: 259, 9: 252, 12: 249, 16: 249, 24: 251, equal group
 // counts (infinite overhead): 256.
 
-__global__ void k_group_work(const int4* hdr, int64_t n, int overhead, int32_t* work) {
+__global__ void k_group_work(const int4* hdr, int64_t n, int overhead, int64_t* work) {
   const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (g < n) work[g] = hdr[g].y + overhead;
+  if (g < n) work[g] = static_cast<int64_t>(hdr[g].y) + overhead;
 }
 
-// item t starts at the first group whose inclusive work prefix exceeds
-// t * total / n_items (strictly increasing: one group never holds a whole
-// item's share at the sizes this is used for; clamped anyway)
-__global__ void k_work_bounds(const int32_t* cum, int64_t n, int64_t n_items, int32_t* item_unit) {
+// raw bound of item t: the first group whose inclusive work prefix (int64:
+// total work reaches ~1.6 x nnz) exceeds t * total / n_items, stored as
+// raw(t) - t for the max-scan that makes the bounds strictly increasing
+__global__ void k_work_raw(const int64_t* cum, int64_t n, int64_t n_items, int32_t* raw_minus_t) {
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t > n_items) return;
-  if (t == 0) { item_unit[0] = 0; return; }
-  if (t == n_items) { item_unit[t] = static_cast<int32_t>(n); return; }
+  if (t >= n_items) return;
+  if (t == 0) { raw_minus_t[0] = 0; return; }
   const int64_t total = cum[n - 1];
-  const int64_t target = total * t / n_items;
+  // total * t / n_items without overflowing int64
+  const int64_t target = static_cast<int64_t>(
+      (static_cast<__int128>(total) * t) / n_items);
   int64_t lo = 0, hi = n;  // first g with cum[g] > target
   while (lo < hi) {
     const int64_t mid = (lo + hi) >> 1;
     if (cum[mid] > target) hi = mid; else lo = mid + 1;
   }
-  lo = lo < t ? t : lo;                       // >= one group per earlier item
-  lo = lo > n - (n_items - t) ? n - (n_items - t) : lo;
-  item_unit[t] = static_cast<int32_t>(lo);
+  raw_minus_t[t] = static_cast<int32_t>(lo - t);
+}
+
+// item_unit[t] = t + max_{s<=t}(raw(s) - s), capped at n - (n_items - t):
+// both sequences rise by >= 1 per item, so every item holds >= 1 group even
+// when one heavy group spans several items' shares of the work
+__global__ void k_work_bounds(const int32_t* scanned, int64_t n, int64_t n_items,
+                              int32_t* item_unit) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t > n_items) return;
+  if (t == n_items) { item_unit[t] = static_cast<int32_t>(n); return; }
+  int64_t b = static_cast<int64_t>(scanned[t]) + t;
+  const int64_t cap = n - (n_items - t);
+  item_unit[t] = static_cast<int32_t>(b < cap ? b : cap);
 }
 
 unsigned blocks_for(int64_t n, int b) { return static_cast<unsigned>((n + b - 1) / b); }
@@ -370,19 +382,31 @@ void finish_unit_items(const DevCsf& csf, Decomp& d, const int32_t* slice_units,
   if (group_overhead > 0 && d.n_items > 1) {
     // cumulative work per packed group (leaf steps + per-group overhead),
     // then item t starts at the first group whose prefix reaches t/n of it
-    int32_t* cum = nullptr;
-    dmalloc(&cum, n_units * sizeof(int32_t), s);
+    int64_t* cum = nullptr;
+    dmalloc(&cum, n_units * sizeof(int64_t), s);
     k_group_work<<<blocks_for(n_units, 256), 256, 0, s>>>(d.grp_hdr, n_units, group_overhead, cum);
     size_t bytes = 0;
-    SPTTN_CUDA(cub::DeviceScan::InclusiveSum(nullptr, bytes, cum, cum, static_cast<int>(n_units), s));
+    SPTTN_CUDA(cub::DeviceScan::InclusiveSum(nullptr, bytes, cum, cum, n_units, s));
     void* tmp = nullptr;
     dmalloc(&tmp, std::max<size_t>(1, bytes), s);
-    SPTTN_CUDA(cub::DeviceScan::InclusiveSum(tmp, bytes, cum, cum, static_cast<int>(n_units), s));
+    SPTTN_CUDA(cub::DeviceScan::InclusiveSum(tmp, bytes, cum, cum, n_units, s));
+    dfree(tmp, s);
+    int32_t* raw = nullptr;
+    dmalloc(&raw, d.n_items * sizeof(int32_t), s);
+    k_work_raw<<<blocks_for(d.n_items, 256), 256, 0, s>>>(cum, n_units, d.n_items, raw);
+    SPTTN_CUDA(cudaGetLastError());
+    bytes = 0;
+    SPTTN_CUDA(cub::DeviceScan::InclusiveScan(nullptr, bytes, raw, raw, MaxI32{},
+                                              static_cast<int>(d.n_items), s));
+    dmalloc(&tmp, std::max<size_t>(1, bytes), s);
+    SPTTN_CUDA(cub::DeviceScan::InclusiveScan(tmp, bytes, raw, raw, MaxI32{},
+                                              static_cast<int>(d.n_items), s));
     dfree(tmp, s);
     dmalloc(&d.item_unit, (d.n_items + 1) * sizeof(int32_t), s);
-    k_work_bounds<<<blocks_for(d.n_items + 1, 256), 256, 0, s>>>(cum, n_units, d.n_items,
+    k_work_bounds<<<blocks_for(d.n_items + 1, 256), 256, 0, s>>>(raw, n_units, d.n_items,
                                                                  d.item_unit);
     SPTTN_CUDA(cudaGetLastError());
+    dfree(raw, s);
     dfree(cum, s);
   }
   dmalloc(&d.item_pos, std::max<int64_t>(1, d.n_items) * sizeof(int32_t), s);

@@ -298,7 +298,7 @@ uint64_t fingerprint(const CsfTensor& csf) {
 // fingerprint) so re-planning the same tensor (every order of a study, every
 // sweep of a solver) does not re-upload it; the most recent kCsfKeep stay
 // resident after their plans are gone.
-std::shared_ptr<DeviceCsfHandle> upload_csf(const CsfTensor& csf) {
+std::shared_ptr<DeviceCsfHandle> upload_csf(const CsfTensor& csf, uint64_t fp) {
   constexpr int64_t kCacheMaxNnz = int64_t{1} << 20;
   constexpr size_t kCsfKeep = 4;
   if (csf.nnz() > kCacheMaxNnz) return upload_csf_uncached(csf);
@@ -310,7 +310,6 @@ std::shared_ptr<DeviceCsfHandle> upload_csf(const CsfTensor& csf) {
   static std::mutex mu;
   // most recent last; intentionally leaked: no device frees at process exit
   static std::vector<Entry>& cache = *new std::vector<Entry>;
-  const uint64_t fp = fingerprint(csf);
   std::lock_guard<std::mutex> lock(mu);
   for (size_t e = 0; e < cache.size(); ++e)
     if (cache[e].key == &csf && cache[e].fp == fp) {
@@ -330,7 +329,7 @@ std::shared_ptr<DeviceCsfHandle> upload_csf(const CsfTensor& csf) {
 
 // The device tensor re-rooted to `order` (spttn_csf_permute), cached like
 // the uploads: (tensor, fingerprint, order) -> handle, the last kCsfKeep kept.
-std::shared_ptr<DeviceCsfHandle> rerooted_csf(const CsfTensor& csf,
+std::shared_ptr<DeviceCsfHandle> rerooted_csf(const CsfTensor& csf, uint64_t fp_all,
                                               const std::shared_ptr<DeviceCsfHandle>& base,
                                               const std::vector<int>& order) {
   constexpr size_t kCsfKeep = 4;
@@ -343,7 +342,7 @@ std::shared_ptr<DeviceCsfHandle> rerooted_csf(const CsfTensor& csf,
   static std::mutex mu;
   static std::vector<Entry>& cache = *new std::vector<Entry>;  // leaked: no frees at exit
   const bool small = csf.nnz() <= (int64_t{1} << 20);
-  const uint64_t fp = small ? fingerprint(csf) : 0;
+  const uint64_t fp = small ? fp_all : 0;
   std::lock_guard<std::mutex> lock(mu);
   if (small)
     for (const auto& e : cache)
@@ -398,6 +397,10 @@ class ExecPlanImpl {
   std::unique_ptr<spg_program> prog;  // GENERIC only
   PinnedMatch pinned;
   std::shared_ptr<DeviceCsfHandle> csf;
+  // content fingerprint of *inputs.sparse when the device copy was made: the
+  // reference reads the sparse tensor at every execute (executor.cpp:92,
+  // :495), so execute() rebinds the device side when it has changed
+  uint64_t csf_fp = 0;
   spttn_plan* plan = nullptr;
   std::vector<int> factor_inputs;  // spec inputs in device factor order
 
@@ -705,14 +708,17 @@ void run_observer(ExecPlanImpl& P) {
 
 namespace {
 // Development aid (SPTTN_SHIM_TRACE=1): per-phase wall time of prepare /
-// execute, printed at exit.
+// execute, printed at exit; =2 also drains the device after every phase so
+// asynchronous work is charged to the phase that issued it.
 struct ShimTrace {
   bool on = false;
+  bool sync = false;
   double t[8] = {0};
   int64_t n[8] = {0};
   ShimTrace() {
     const char* e = std::getenv("SPTTN_SHIM_TRACE");
-    on = e && *e == '1';
+    on = e && (*e == '1' || *e == '2');
+    sync = e && *e == '2';
   }
   ~ShimTrace() {
     if (!on) return;
@@ -724,11 +730,88 @@ struct ShimTrace {
   }
   void add(int k, Clock::time_point a) {
     if (!on) return;
+    if (sync) spttn_synchronize(nullptr);
     t[k] += std::chrono::duration<double>(Clock::now() - a).count();
     ++n[k];
   }
 } g_trace;
 }  // namespace
+
+// The device half of prepare(): device CSF (cached / re-rooted), kernel
+// choice and plan creation. Re-run by execute() when the caller's sparse
+// tensor changed since (the plan otherwise holds a device snapshot of it).
+void bind_device(ExecPlanImpl& P) {
+  Clock::time_point tc;
+  spttn_plan_desc desc{};
+  desc.buffer_limit_bytes = P.opts.buffer_limit_bytes;
+  tc = Clock::now();
+  P.csf_fp = fingerprint(*P.inputs.sparse);
+  P.csf = upload_csf(*P.inputs.sparse, P.csf_fp);
+  g_trace.add(1, tc);
+  tc = Clock::now();
+  P.pinned = match_pinned(P.spec, P.path, P.spec.sparse_input().indices);
+  const std::shared_ptr<DeviceCsfHandle> base_csf = P.csf;  // the interpreter walks this one
+  // A dense output on a non-root mode m: re-root the tensor on the device
+  // (level order m, then the rest) so the nest becomes a root-output pinned
+  // nest — owner computes, deterministic. Preferred over the atomic
+  // non-root MTTKRP kernels unless SPTTN_NONROOT=atomics.
+  if (P.opts.observer == nullptr && !P.spec.output_sparse && !P.spec.output().indices.empty() &&
+      (P.pinned.kind == 0 || P.pinned.kind == SPTTN_NEST_MTTKRP3_J ||
+       P.pinned.kind == SPTTN_NEST_MTTKRP3_K)) {
+    const auto& sp = P.spec.sparse_input().indices;
+    const auto it = std::find(sp.begin(), sp.end(), P.spec.output().indices[0]);
+    const char* pref = std::getenv("SPTTN_NONROOT");
+    const bool atomics = pref && std::string(pref) == "atomics" && P.pinned.kind != 0;
+    if (it != sp.end() && it != sp.begin() && !atomics) {
+      const int m = static_cast<int>(it - sp.begin());
+      std::vector<int> rr{sp[m]};
+      std::vector<int> order_lv{m};
+      for (int l = 0; l < static_cast<int>(sp.size()); ++l)
+        if (l != m) {
+          rr.push_back(sp[l]);
+          order_lv.push_back(l);
+        }
+      PinnedMatch m2 = match_pinned(P.spec, P.path, rr);
+      if (m2.kind >= SPTTN_NEST_MTTKRP3 && m2.kind <= SPTTN_NEST_TTMC4 &&
+          m2.kind != SPTTN_NEST_TTTP3) {
+        P.pinned = m2;
+        P.csf = rerooted_csf(*P.inputs.sparse, P.csf_fp, P.csf, order_lv);
+      }
+    }
+  }
+  int rc = SPTTN_EUNSUPPORTED;
+  if (P.pinned.kind != 0 && P.opts.observer == nullptr) {
+    desc.kind = P.pinned.kind;
+    for (int k = 0; k < 3; ++k) desc.rank[k] = P.pinned.rank[k];
+    P.factor_inputs = P.pinned.factor_inputs;
+    desc.num_factors = static_cast<int32_t>(P.factor_inputs.size());
+    for (size_t f = 0; f < P.factor_inputs.size(); ++f) {
+      const DenseTensor* t = P.inputs.dense[P.factor_inputs[f] - 1];
+      desc.factors[f] = t->values.data();
+      desc.factor_size[f] = static_cast<int64_t>(t->values.size());
+    }
+    rc = spttn_plan_create(&desc, P.csf->h, nullptr, &P.plan);
+    if (rc != SPTTN_OK && rc != SPTTN_EUNSUPPORTED) throw_status(rc, "prepare");
+  }
+  if (rc != SPTTN_OK) {  // any other admissible order: device forest interpreter
+    P.pinned = PinnedMatch{};
+    P.csf = base_csf;
+    desc = spttn_plan_desc{};
+    desc.kind = SPTTN_NEST_GENERIC;
+    desc.buffer_limit_bytes = P.opts.buffer_limit_bytes;
+    P.factor_inputs.clear();
+    for (int f = 1; f < P.spec.num_inputs(); ++f) P.factor_inputs.push_back(f);
+    desc.num_factors = static_cast<int32_t>(P.factor_inputs.size());
+    for (size_t f = 0; f < P.factor_inputs.size(); ++f) {
+      desc.factors[f] = P.inputs.dense[f]->values.data();
+      desc.factor_size[f] = static_cast<int64_t>(P.inputs.dense[f]->values.size());
+    }
+    desc.program = P.prog.get();
+    desc.program_bytes = sizeof(spg_program);
+    check(spttn_plan_create(&desc, P.csf->h, nullptr, &P.plan), "prepare");
+  }
+  g_trace.add(2, tc);
+}
 
 ExecPlan prepare(const KernelSpec& spec, const ContractionPath& path, const LoopOrder& order,
                  const ExecInputs& inputs, const ExecOptions& opts) {
@@ -750,74 +833,7 @@ ExecPlan prepare(const KernelSpec& spec, const ContractionPath& path, const Loop
   P.flops = forest_flops(spec, path, P.forest, *inputs.sparse);
   g_trace.add(0, tc);
 
-  tc = Clock::now();
-  P.csf = upload_csf(*inputs.sparse);
-  g_trace.add(1, tc);
-  tc = Clock::now();
-  spttn_plan_desc desc{};
-  desc.buffer_limit_bytes = opts.buffer_limit_bytes;
-  P.pinned = match_pinned(spec, path, spec.sparse_input().indices);
-  const std::shared_ptr<DeviceCsfHandle> base_csf = P.csf;  // the interpreter walks this one
-  // A dense output on a non-root mode m: re-root the tensor on the device
-  // (level order m, then the rest) so the nest becomes a root-output pinned
-  // nest — owner computes, deterministic. Preferred over the atomic
-  // non-root MTTKRP kernels unless SPTTN_NONROOT=atomics.
-  if (opts.observer == nullptr && !spec.output_sparse && !spec.output().indices.empty() &&
-      (P.pinned.kind == 0 || P.pinned.kind == SPTTN_NEST_MTTKRP3_J ||
-       P.pinned.kind == SPTTN_NEST_MTTKRP3_K)) {
-    const auto& sp = spec.sparse_input().indices;
-    const auto it = std::find(sp.begin(), sp.end(), spec.output().indices[0]);
-    const char* pref = std::getenv("SPTTN_NONROOT");
-    const bool atomics = pref && std::string(pref) == "atomics" && P.pinned.kind != 0;
-    if (it != sp.end() && it != sp.begin() && !atomics) {
-      const int m = static_cast<int>(it - sp.begin());
-      std::vector<int> rr{sp[m]};
-      std::vector<int> order_lv{m};
-      for (int l = 0; l < static_cast<int>(sp.size()); ++l)
-        if (l != m) {
-          rr.push_back(sp[l]);
-          order_lv.push_back(l);
-        }
-      PinnedMatch m2 = match_pinned(spec, path, rr);
-      if (m2.kind >= SPTTN_NEST_MTTKRP3 && m2.kind <= SPTTN_NEST_TTMC4 &&
-          m2.kind != SPTTN_NEST_TTTP3) {
-        P.pinned = m2;
-        P.csf = rerooted_csf(*inputs.sparse, P.csf, order_lv);
-      }
-    }
-  }
-  int rc = SPTTN_EUNSUPPORTED;
-  if (P.pinned.kind != 0 && opts.observer == nullptr) {
-    desc.kind = P.pinned.kind;
-    for (int k = 0; k < 3; ++k) desc.rank[k] = P.pinned.rank[k];
-    P.factor_inputs = P.pinned.factor_inputs;
-    desc.num_factors = static_cast<int32_t>(P.factor_inputs.size());
-    for (size_t f = 0; f < P.factor_inputs.size(); ++f) {
-      const DenseTensor* t = inputs.dense[P.factor_inputs[f] - 1];
-      desc.factors[f] = t->values.data();
-      desc.factor_size[f] = static_cast<int64_t>(t->values.size());
-    }
-    rc = spttn_plan_create(&desc, P.csf->h, nullptr, &P.plan);
-    if (rc != SPTTN_OK && rc != SPTTN_EUNSUPPORTED) throw_status(rc, "prepare");
-  }
-  if (rc != SPTTN_OK) {  // any other admissible order: device forest interpreter
-    P.pinned = PinnedMatch{};
-    P.csf = base_csf;
-    desc = spttn_plan_desc{};
-    desc.kind = SPTTN_NEST_GENERIC;
-    desc.buffer_limit_bytes = opts.buffer_limit_bytes;
-    P.factor_inputs.clear();
-    for (int f = 1; f < spec.num_inputs(); ++f) P.factor_inputs.push_back(f);
-    desc.num_factors = static_cast<int32_t>(P.factor_inputs.size());
-    for (size_t f = 0; f < P.factor_inputs.size(); ++f) {
-      desc.factors[f] = inputs.dense[f]->values.data();
-      desc.factor_size[f] = static_cast<int64_t>(inputs.dense[f]->values.size());
-    }
-    desc.program = P.prog.get();
-    desc.program_bytes = sizeof(spg_program);
-    check(spttn_plan_create(&desc, P.csf->h, nullptr, &P.plan), "prepare");
-  }
-  g_trace.add(2, tc);
+  bind_device(P);
   ExecPlan plan;
   plan.impl = std::move(impl);
   return plan;
@@ -826,6 +842,12 @@ ExecPlan prepare(const KernelSpec& spec, const ContractionPath& path, const Loop
 ExecResult execute(ExecPlan& plan) {
   const auto start = Clock::now();
   ExecPlanImpl& P = *plan.impl;
+  if (fingerprint(*P.inputs.sparse) != P.csf_fp) {  // sparse tensor changed since prepare
+    if (P.plan) spttn_plan_destroy(P.plan);
+    P.plan = nullptr;
+    P.csf.reset();
+    bind_device(P);
+  }
   // The reference plan reads the caller's dense tensors at execute time
   // (executor.cpp:373-387): refresh the device copies.
   std::vector<const double*> f(P.factor_inputs.size());
@@ -964,7 +986,7 @@ ExecResult execute_unfactorized(const KernelSpec& spec, const ExecInputs& inputs
     count = 1;
     for (int id : oi) count *= spec.dim(id);
   }
-  auto dev = upload_csf(csf);
+  auto dev = upload_csf(csf, fingerprint(csf));
   std::vector<double> out(static_cast<size_t>(count));
   check(spttn_unfactorized(&d, dev->h, out.data(), count, nullptr), "execute_unfactorized");
   ExecResult res;

@@ -5,6 +5,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 
 #include "fixtures.hpp"
 #include "spttn/executor.hpp"
@@ -14,6 +15,7 @@ using namespace spttn::testing;
 
 int main(int argc, char** argv) {
   const int limit = argc > 1 ? std::atoi(argv[1]) : 200;
+  const char* only = argc > 2 ? argv[2] : nullptr;  // run one fixture
   struct F {
     const char* name;
     KernelSpec spec;
@@ -23,6 +25,7 @@ int main(int argc, char** argv) {
             {"TTTP-3", tttp3(4, 4, 3, 2), 0.2}, {"TTMc-4", ttmc4(3, 2, 2, 2), 0.15},
             {"TTTc-4", tttc4(3, 2), 0.15}};
   for (auto& f : fs) {
+    if (only && std::string(only) != f.name) continue;
     Tensors t = make_tensors(f.spec, random_coo(f.spec, f.density, 101));
     auto in = t.inputs();
     ExecResult oracle = execute_unfactorized(f.spec, in);

@@ -70,10 +70,24 @@ def _case(seed):
         env["SPTTN_CHUNK"] = str(int(rng.choice([1, 2, 3, 8])))
         env["SPTTN_GCHUNK"] = str(int(rng.choice([1, 2, 4])))
     residual = kind == 3 and rng.random() < 0.5
+    # work-cut items (decomp.cu finish_unit_items): the per-group overhead of
+    # the modes that read variable item bounds, incl. overhead 1 with tiny
+    # GCHUNK, where one heavy group spans several items' shares (separate
+    # stream: the original draws above stay unchanged)
+    r2 = np.random.default_rng(5000 + seed)
+    item_mode = {1: ("SPTTN_MTTKRP_MODE", "3"), 4: ("SPTTN_MTTKRP_MODE", "3"),
+                 2: ("SPTTN_TTMC3_MODE", "10"), 5: ("SPTTN_TTMC4_MODE", "4")}
+    if kind in item_mode and (env.get(item_mode[kind][0], item_mode[kind][1]) == item_mode[kind][1]
+                              or seed >= 160):
+        env[item_mode[kind][0]] = item_mode[kind][1]
+        env["SPTTN_GROUP_OVERHEAD"] = str(int(r2.choice([0, 1, 3, 12])))
+        if seed >= 160 or r2.random() < 0.5:
+            env["SPTTN_GCHUNK"] = str(int(r2.choice([1, 2, 4])))
+            env["SPTTN_CHUNK"] = str(int(r2.choice([1, 2, 3])))
     return kind, dims, coords, vals, fs, ranks, env, residual
 
 
-@pytest.mark.parametrize("seed", range(160))
+@pytest.mark.parametrize("seed", range(220))
 def test_random_case_matches_oracle(E, seed, monkeypatch):
     from paper_2307_05740_b200.tensor import Csf
     kind, dims, coords, vals, fs, ranks, env, residual = _case(seed)

@@ -3,7 +3,7 @@
 // Each warp repeatedly gathers random rows of a ROWS x 16-double table;
 // WIDTH = bytes per lane per load (8, 16, 32); rows are 128 B, so
 // 128/WIDTH lanes share a row and 32*WIDTH/128 rows are read per instruction.
-// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o gp tools/gather_probe.cu
+// Build: make probes (-> tools/gather_probe)
 #include <cstdio>
 #include <cuda_runtime.h>
 
