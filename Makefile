@@ -108,3 +108,17 @@ probes: $(PROBES)
 tools/%_probe: tools/%_probe.cu
 	$(NVCC) $(ARCH) -O3 -lineinfo -std=c++17 $< -o $@ -lcuda
 .PHONY: probes
+
+# Drop-in pinned to the reference executor in one process: the reference side
+# is compiled with -Dspttn=spttn_ref and linked with oracle/_ref/libspttn_ref.a
+# (oracle/Makefile), the drop-in side with libspttn_b200_host.so.
+REF_LIB := oracle/_ref/libspttn_ref.a
+ifneq ($(HAVE_HOST),)
+host: build/tests/ref_pin
+endif
+build/tests/ref_side.o: tests/cpp/ref_side.cpp tests/cpp/ref_side.hpp
+	@mkdir -p $(dir $@)
+	$(CXX) -std=c++20 -O2 -fPIC -Dspttn=spttn_ref -I$(REF)/include -I$(REF)/tests -c $< -o $@
+build/tests/ref_pin: tests/cpp/ref_pin.cpp build/tests/ref_side.o $(LIB)/libspttn_b200_host.so oracle
+	$(CXX) $(HOSTFLAGS) -I$(REF)/tests -Itests/cpp $< build/tests/ref_side.o $(REF_LIB) \
+	  -L$(LIB) -lspttn_b200_host -lspttn_b200 -Wl,-rpath,'$$ORIGIN/../../$(LIB)' -o $@

@@ -59,14 +59,16 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--configs", default="all", help="comma list or 'all'")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0,
-                    help="target CPU time of a bounded reference sample")
+    ap.add_argument("--cpu-seconds", type=float, default=3.0,
+                    help="target CPU time of one bounded reference sample")
+    ap.add_argument("--dump-workload", default=None, help=argparse.SUPPRESS)
+    ap.add_argument("--out", default=None, help=argparse.SUPPRESS)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true",
                     help="skip the per-config parity check against the C oracle")
     ap.add_argument("--shard", action="store_true",
-                    help="N>1: split ONE tensor's root slices over the ranks (strong "
+                    help="N>1: split ONE tensor's fibers over the ranks (strong "
                          "scaling) instead of one independent tensor per rank (weak)")
     return ap.parse_args()
 
@@ -369,6 +371,19 @@ def cpu_sample(w, seconds, threads):
     return sub, stride
 
 
+def _geomean_ratios(results):
+    """Geometric means over the BASELINE configs of this arm's value / e2e
+    against the reference on all host threads (same run, same box)."""
+    out = {}
+    for k in ("value_ratio", "e2e_ratio"):
+        xs = [r["vs_reference"][k] for key, r in results.items()
+              if key in BASELINE_KEYS and r.get("vs_reference", {}).get(k)]
+        if xs:
+            out[k] = float(np.exp(np.mean(np.log(xs))))
+            out["configs"] = len(xs)
+    return out or None
+
+
 def cpu_reference(w, seconds, threads, repeats=1, sample=None):
     sub, stride = sample if sample is not None else cpu_sample(w, seconds, threads)
     path = ref_args(w)[2]
@@ -379,37 +394,89 @@ def cpu_reference(w, seconds, threads, repeats=1, sample=None):
                       f"on the pinned nest {path}", "seconds": secs}
 
 
-def run_reference_impl(args, rank, world):
-    """--impl reference: the reference CPU executor on all host threads."""
+BASELINE_KEYS = ["mttkrp3", "ttmc3", "tttp3", "mttkrp4", "ttmc4"]
+
+
+def dump_workload(key, out_dir):
+    """--dump-workload (run in a child process): generate one workload with
+    the repo's generator and store its arrays, so the reference arm's own
+    process maps only the reference build (oracle/_ref)."""
     from paper_2307_05740_b200.configs import make_workload
+    w = make_workload(key)
+    arrs = {"dims": np.asarray(w.dims, np.int64), "values": w.csf.values}
+    for l, a in enumerate(w.csf.idx):
+        arrs[f"idx{l}"] = a
+    for l, a in enumerate(w.csf.ptr):
+        arrs[f"ptr{l}"] = a
+    for f, a in enumerate(w.factors):
+        arrs[f"factor{f}"] = a
+    np.savez(Path(out_dir) / f"{key}.npz", **arrs)
+
+
+def load_workload_via_child(key):
+    """The workload generated in a child process (dump_workload) and loaded
+    here from .npz: no repo native library enters this process."""
+    from paper_2307_05740_b200.configs import CONFIGS, Workload
+    from paper_2307_05740_b200.tensor import Csf
+    with tempfile.TemporaryDirectory(prefix="spttn_ref_in_") as d:
+        subprocess.run([sys.executable, str(Path(__file__).resolve()), "--dump-workload", key,
+                        "--out", d], check=True)
+        z = np.load(Path(d) / f"{key}.npz")
+        dims = [int(x) for x in z["dims"]]
+        order = len(dims)
+        csf = Csf(dims, [z[f"idx{l}"] for l in range(order)],
+                  [z[f"ptr{l}"] for l in range(order - 1)], z["values"],
+                  list(CONFIGS[key].mode_names))
+        nf = len([k for k in z.files if k.startswith("factor")])
+        factors = [z[f"factor{f}"] for f in range(nf)]
+    return Workload(CONFIGS[key], csf, factors, tuple(dims), csf.nnz)
+
+
+def run_reference_impl(args, rank, world):
+    """--impl reference: the reference CPU executor (oracle/_ref, compiled
+    from /root/reference) on all host threads, one plan per thread over
+    nnz-balanced root-slice partitions, on a bounded sample of each BASELINE
+    config; the headline fields are TTMc-3 (configs[1]), the rest under
+    "configs". Inputs come from a child process (load_workload_via_child)."""
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    w = make_workload(HEADLINE)
-    # one bounded sample, sized so all warmup + timed steps take ~cpu_seconds
-    sample = cpu_sample(w, args.cpu_seconds / max(1, args.steps + args.warmup), threads)
-    vals = []
-    res = None
-    for step in range(args.warmup + args.steps):
-        res = cpu_reference(w, 0, threads, sample=sample)
-        if step >= args.warmup:
-            vals.append(res["value"])
-    v = statistics.median(vals)
+    per_step = 2 * args.cpu_seconds / max(1, args.steps + args.warmup)
+    results = {}
+    for key in BASELINE_KEYS:
+        w = load_workload_via_child(key)
+        sample = cpu_sample(w, per_step, threads)
+        vals = []
+        res = None
+        for step in range(args.warmup + args.steps):
+            res = cpu_reference(w, 0, threads, sample=sample)
+            if step >= args.warmup:
+                vals.append(res["value"])
+        results[key] = {"value": statistics.median(vals), "unit": "nnz/s",
+                        "ms_per_step": res["seconds"] * 1e3, "sample": res["sample"]}
+        print(f"[bench-ref] {key}: {results[key]['value']:.3e} nnz/s", file=sys.stderr, flush=True)
+    h = results[HEADLINE]
+    v = h["value"]
     line = {"impl": "reference", "metric": METRIC,
             "value": v, "unit": "nnz/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": res["seconds"] * 1e3,
+            "warmup": args.warmup, "ms_per_step": h["ms_per_step"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": WORKLOAD,
-                                            "threads": threads},
+                                            "l2": "n/a (host CPU)",
+                                            "parallelism": f"{threads} host threads"},
             "cpu_baseline": {"value": v, "unit": "nnz/s", "cores": threads, "kind": "reference",
-                             "sample": res["sample"]},
+                             "sample": h["sample"]},
             "e2e": {"value": v, "unit": "nnz/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+                    "d2h_bytes_per_step": 0},
+            "configs": results}
     print(json.dumps(line), flush=True)
 
 
 def main():
     args = parse()
+    if args.dump_workload:
+        dump_workload(args.dump_workload, args.out)
+        return
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -436,13 +503,14 @@ def main():
     for key in keys:
         strong = args.shard and world > 1
         if strong and key.startswith("mttkrp3_"):
-            continue  # non-root outputs: root-slice shards would need an output all-reduce
+            continue  # non-root outputs: fiber shards would need an output all-reduce
         w = make_workload(key, seed_offset=0 if strong else rank)
         job_nnz = w.csf.nnz if strong else w.csf.nnz * world
-        if strong:  # this rank's nnz-balanced root range (no data-path collective)
+        if strong:  # this rank's nnz-balanced fiber range (split root slices are
+            # partial rows, summed by distributed.reduce_split_rows after the step)
             from paper_2307_05740_b200 import distributed as D
-            r0, r1 = D.partition_roots(w.csf, world)[rank]
-            w.csf = D.shard_csf(w.csf, r0, r1)
+            f0, f1 = D.partition_fibers(w.csf, world)[rank]
+            w.csf = D.shard_csf_fibers(w.csf, f0, f1)
         ev = []
         if world > 1:
             dist.barrier()
@@ -515,7 +583,16 @@ def main():
                         "d2h_bytes_per_step": e["d2h_bytes_per_step"], "ms_per_step": secs * 1e3,
                         "breakdown_ms": e["breakdown_ms"]}
         if rank == 0 and world == 1 and not args.no_cpu:
-            r["cpu_baseline"] = cpu_reference(w, args.cpu_seconds, 1)
+            r["cpu_baseline"] = cpu_reference(w, args.cpu_seconds, 1, repeats=3)
+            # the reference arm's setting (all host threads) on a bounded
+            # sample, for per-config ratios (the driver computes the headline)
+            threads = os.cpu_count() or 1
+            mt = cpu_reference(w, args.cpu_seconds / 2, threads, repeats=3)
+            r["reference_threads"] = {"value": mt["value"], "cores": threads,
+                                      "sample": mt["sample"]}
+            r["vs_reference"] = {"value_ratio": r["value"] / mt["value"],
+                                 "e2e_ratio": (r["e2e"]["value"] / mt["value"]) if "e2e" in r
+                                 else None}
             if key == HEADLINE:
                 r["csf_build"] = csf_build_config(P, w, stream)
         if key == HEADLINE:
@@ -535,13 +612,14 @@ def main():
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD,
                    "l2": "256 MB L2 flush write between timed steps",
-                   "parallelism": (f"root-slice shards x{world} of one tensor"
+                   "parallelism": (f"fiber shards x{world} of one tensor"
                                    if (args.shard and world > 1) else
                                    f"weak x{world} (independent tensor per rank)")},
         "roofline": h["roofline"], "gpu_launches": h["launches_per_step"] * args.steps,
         "clocks": head_clocks, "e2e": h.get("e2e"), "cpu_baseline": h.get("cpu_baseline"),
         "fp64_peaks": fp64,
         "parity": {k: v.get("parity", {}).get("ok") for k, v in results.items()},
+        "vs_reference_geomean": _geomean_ratios(results),
         "configs": {k: v for k, v in results.items()},
     }
     if rank == 0:

@@ -142,7 +142,11 @@ int spttn_read_output(spttn_plan* plan, double* host_out, int64_t count, void* s
  * [2] split root slices, [3] absent root rows, [4] device scratch bytes,
  * [5] nest kind actually run, [6] segments (DMMA kernels),
  * [7] multiply-adds counted by the device interpreter on the last execute
- *     (GENERIC only; fast kernels report -1: use flops_estimate).       */
+ *     (GENERIC only; fast kernels report -1: use flops_estimate),
+ * [8] GENERIC decomposition: 0 sequential walk, 1 root slices written
+ *     directly, 2 root ranges into per-worker outputs summed in worker
+ *     order, 3 level-1 fibers (JIT only); -1 for the fused kernels,
+ * [9] GENERIC: 1 when the forest runs as an NVRTC-compiled kernel.       */
 int spttn_plan_info(const spttn_plan* plan, int64_t* out, int n);
 
 /* GENERIC only: per-buffer reset counts of the last execute (as counted on

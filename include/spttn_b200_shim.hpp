@@ -14,6 +14,10 @@
 // device forest interpreter).
 int spttn_b200_plan_device_kind(const spttn::ExecPlan& plan);
 
+// spttn_plan_info (include/spttn_b200.h) of the device plan behind `plan`:
+// launches, work items, ..., [8] interpreter decomposition, [9] JIT flag.
+int spttn_b200_plan_info(const spttn::ExecPlan& plan, int64_t* out, int n);
+
 // CooTensor::normalize + build_csf (proj/src/tensor.cpp:24-94) on the GPU:
 // the same CsfTensor (duplicates summed in input order), ~1000x faster than
 // the host build at 1e7 nonzeros. Throws std::invalid_argument like the

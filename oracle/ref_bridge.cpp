@@ -436,12 +436,17 @@ int ref_execute_threads(const char* kernel, const char* dims, const char* path, 
     }
     double best = 1e300;
     for (int r = 0; r < std::max(1, repeats); ++r) {
+      // timed: the reference executor on every thread (each execute
+      // allocates and zeroes its own output, as spttn::execute does)
       const auto t0 = std::chrono::steady_clock::now();
       std::vector<std::thread> th;
       for (int t = 0; t < nthreads; ++t)
         th.emplace_back([&, t] { parts[t].res = execute(*parts[t].plan); });
       for (auto& x : th) x.join();
-      // merge: dense outputs are root-row disjoint -> sum; sparse -> place.
+      const double s =
+          std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      best = std::min(best, s);
+      // untimed: merge (dense outputs are root-row disjoint -> sum; sparse -> place)
       if (spec.output_sparse) {
         for (auto& pt : parts)
           std::memcpy(out + pt.leaf_begin, pt.res.sparse_out_values.data(),
@@ -454,9 +459,6 @@ int ref_execute_threads(const char* kernel, const char* dims, const char* path, 
           for (int64_t q = 0; q < out_count; ++q) out[q] += v[q];
         }
       }
-      const double s =
-          std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-      best = std::min(best, s);
     }
     *best_seconds = best;
     return 0;

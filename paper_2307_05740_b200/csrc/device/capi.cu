@@ -133,6 +133,18 @@ int smem_optin_bytes() {
 }
 
 void copy_factors(spttn_plan* p, const double* const* src, bool on_device, cudaStream_t s) {
+  auto& g = p->gen;
+  if (g.parcel && !on_device) {  // small GENERIC plan: one upload from the pinned parcel
+    SPTTN_CUDA(cudaEventSynchronize(g.up_done));  // the previous upload has left the parcel
+    for (int f = 0; f < p->nf; ++f)
+      if (p->fac_size[f] > 0) std::memcpy(g.parcel + g.fac_off[f], src[f], p->fac_size[f] * 8);
+    if (g.up_end > g.up_fac)
+      SPTTN_CUDA(cudaMemcpyAsync(static_cast<unsigned char*>(p->arena) + g.up_fac,
+                                 g.parcel + g.up_fac, g.up_end - g.up_fac,
+                                 cudaMemcpyHostToDevice, s));
+    SPTTN_CUDA(cudaEventRecord(g.up_done, s));
+    return;
+  }
   for (int f = 0; f < p->nf; ++f) {
     if (on_device) {
       p->fac[f] = const_cast<double*>(src[f]);
@@ -342,6 +354,8 @@ int spttn_plan_destroy(spttn_plan* p) {
     if (!p) return;
     cudaDeviceSynchronize();  // as cudaFree would: no kernel may still use it
     if (p->arena) {  // GENERIC: everything lives in the arena
+      if (p->gen.up_done) cudaEventDestroy(p->gen.up_done);
+      spttn_dev::pinned_free(p->gen.parcel, p->gen.parcel_bytes);
       spttn_dev::dfree(p->arena);
       spttn_dev::free_decomp(p->dec);
       delete p->prog;
@@ -576,13 +590,65 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
           }
         }
       }
+      // Small working sets run shared-memory resident (generic.cu
+      // k_generic_sm): root slices to up to 8 walkers where mode 1 applies.
+      // Only where the walk is sequential anyway or its root slices fit the
+      // 8 walkers: wider plans keep the global interpreter's parallelism.
+      const bool sm_par_ok = g.par_mode == 0 || (g.par_mode == 1 && D.level_size[0] <= 8);
+      if (!G.observe && env_int("SPTTN_GENERIC_SM", 1) != 0 && !want_jit && sm_par_ok) {
+        const int smw = g.par_mode == 1 ? static_cast<int>(std::min<int64_t>(g.workers, 8)) : 1;
+        spttn_dev::GenericState t{};
+        if (spttn_dev::generic_sm_layout(G, D, smw, smem_optin_bytes(), t) ||
+            (smw > 1 && spttn_dev::generic_sm_layout(G, D, 1, smem_optin_bytes(), t))) {
+          g.sm = true;
+          g.sm_workers = t.sm_workers;
+          g.sm_bytes = t.sm_bytes;
+          std::memcpy(g.sm_off, t.sm_off, sizeof(g.sm_off));
+          std::memcpy(g.dense_size, t.dense_size, sizeof(g.dense_size));
+          g.par_mode = g.sm_workers > 1 ? 1 : 0;
+          g.workers = 1;  // no global replicas
+          g.priv = g.tail = false;
+        }
+      }
+      if (g.sm) {
+        // device arena [prog | boff | factors][out | counters] mirrored by a
+        // pinned host parcel: program + offsets uploaded here, factors by
+        // one copy per set_factors, out + counters read back by one copy
+        g.up_prog = al(sizeof(spg_program));
+        size_t up = g.up_prog + al((nb + 1) * sizeof(int64_t));
+        g.up_fac = up;
+        for (int f = 0; f < p->nf; ++f) {
+          g.fac_off[f] = up;
+          if (!on_dev) up += al(p->fac_size[f] * 8);
+        }
+        g.up_end = up;
+        g.down_cnt = up + al(std::max<int64_t>(1, G.out_size) * 8);
+        g.down_end = g.down_cnt + al((nb + 5) * sizeof(int64_t));
+        g.parcel_bytes = g.down_end;
+        dev_malloc(&p->arena, g.parcel_bytes, s);
+        g.parcel = static_cast<unsigned char*>(spttn_dev::pinned_alloc(g.parcel_bytes));
+        unsigned char* dev = static_cast<unsigned char*>(p->arena);
+        g.d_prog = reinterpret_cast<spg_program*>(dev);
+        g.buffer_off = reinterpret_cast<int64_t*>(dev + g.up_prog);
+        if (!on_dev)
+          for (int f = 0; f < p->nf; ++f) p->fac[f] = reinterpret_cast<double*>(dev + g.fac_off[f]);
+        p->out = reinterpret_cast<double*>(dev + g.up_end);
+        g.counters = reinterpret_cast<int64_t*>(dev + g.down_cnt);
+        g.total_buffer_elems = off[nb];
+        g.in_arena = true;
+        std::memcpy(g.parcel, &G, sizeof(spg_program));
+        std::memcpy(g.parcel + g.up_prog, off.data(), off.size() * sizeof(int64_t));
+        SPTTN_CUDA(cudaMemcpyAsync(dev, g.parcel, g.up_fac, cudaMemcpyHostToDevice, s));
+        SPTTN_CUDA(cudaEventCreateWithFlags(&g.up_done, cudaEventDisableTiming));
+        SPTTN_CUDA(cudaEventRecord(g.up_done, s));
+      } else {
       const int64_t reps = g.workers;
       const size_t n_cnt = (nb + 5) * sizeof(int64_t);  // + slice counter (mode 1)
       const size_t n_buf = static_cast<size_t>(std::max<int64_t>(1, off[nb]) * reps) * 8;
       const size_t n_out = static_cast<size_t>(std::max<int64_t>(1, G.out_size)) * 8;
       const size_t n_priv =
           g.priv ? static_cast<size_t>(std::max<int64_t>(1, G.out_size) * reps) * 8 : 0;
-      const bool lookup = G.need_leaf_lookup && nnz > 0;
+      const bool lookup = G.need_leaf_lookup && nnz > 0 && !g.sm;
       size_t total = n_cnt + n_buf + n_out + n_priv;  // contiguous, 8-byte aligned
       total = al(total) + al(sizeof(spg_program)) + al((nb + 1) * sizeof(int64_t)) +
               al(16 * sizeof(double*));
@@ -617,6 +683,7 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
       SPTTN_CUDA(cudaMemcpyAsync(g.d_prog, &G, sizeof(spg_program), cudaMemcpyHostToDevice, s));
       SPTTN_CUDA(cudaMemcpyAsync(g.buffer_off, off.data(), off.size() * sizeof(int64_t),
                                  cudaMemcpyHostToDevice, s));
+      }
     }
     spttn_dev::plan_trace("plan: setup", s);
     copy_factors(p, desc->factors, on_dev, s);
@@ -632,13 +699,15 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
       p->out_count = p->prog->out_size;
       const double* hp[16] = {nullptr};
       for (int f = 0; f < p->nf; ++f) hp[f + 1] = p->fac[f];
-      SPTTN_CUDA(cudaMemcpyAsync(p->d_dense, hp, sizeof(hp), cudaMemcpyHostToDevice, s));
-      if (p->gen.n_leaf_keys > 0) {
+      for (int f = 0; f < 16; ++f) p->gen.dense_dev[f] = hp[f];
+      if (!p->gen.sm)
+        SPTTN_CUDA(cudaMemcpyAsync(p->d_dense, hp, sizeof(hp), cudaMemcpyHostToDevice, s));
+      if (p->gen.n_leaf_keys > 0 && !p->gen.sm) {
         k_leaf_keys<<<static_cast<unsigned>((nnz + 255) / 256), 256, 0, s>>>(
             D.view(), p->gen.d_prog, p->gen.leaf_keys, p->gen.leaf_pos);
         SPTTN_CUDA(cudaGetLastError());
       }
-      p->launches = 2 + (p->gen.priv ? 1 : 0) + (p->gen.tail ? p->gen.n_tail_bufs + 1 : 0);
+      p->launches = p->gen.sm ? 1 : 2 + (p->gen.priv ? 1 : 0) + (p->gen.tail ? p->gen.n_tail_bufs + 1 : 0);
       const int64_t jit_env2 = env_int("SPTTN_GENERIC_JIT", -1);
       if (!p->prog->observe && spttn_dev::jit_available() &&
           (jit_env2 == 1 || (jit_env2 < 0 && nnz >= (int64_t{1} << 16))))
@@ -867,6 +936,7 @@ int spttn_plan_set_factors(spttn_plan* p, const double* const* factors, int32_t 
     if (p->kind == SPTTN_NEST_GENERIC && on_device) {
       const double* hp[16] = {nullptr};
       for (int f = 0; f < p->nf; ++f) hp[f + 1] = p->fac[f];
+      for (int f = 0; f < 16; ++f) p->gen.dense_dev[f] = hp[f];
       SPTTN_CUDA(cudaMemcpyAsync(p->d_dense, hp, sizeof(hp), cudaMemcpyHostToDevice,
                                  as_stream(stream)));
     }
@@ -1011,6 +1081,19 @@ int spttn_read_output(spttn_plan* p, double* host_out, int64_t count, void* stre
     if (!p || (!host_out && count)) fail(SPTTN_EINVAL, "null argument");
     if (count != p->out_count) fail(SPTTN_EINVAL, "output count mismatch");
     cudaStream_t s = as_stream(stream);
+    auto& g = p->gen;
+    if (g.parcel) {  // small GENERIC plan: [out | counters] in one pinned copy
+      unsigned char* dev = static_cast<unsigned char*>(p->arena);
+      SPTTN_CUDA(cudaMemcpyAsync(g.parcel + g.up_end, dev + g.up_end, g.down_end - g.up_end,
+                                 cudaMemcpyDeviceToHost, s));
+      SPTTN_CUDA(cudaStreamSynchronize(s));
+      if (count) std::memcpy(host_out, g.parcel + g.up_end, count * sizeof(double));
+      p->last_counters.resize(p->prog->num_buffers + 4);
+      std::memcpy(p->last_counters.data(), g.parcel + g.down_cnt,
+                  p->last_counters.size() * sizeof(int64_t));
+      p->last_madds = p->last_counters[0];
+      return;
+    }
     if (count)
       SPTTN_CUDA(cudaMemcpyAsync(host_out, p->out, count * sizeof(double), cudaMemcpyDeviceToHost, s));
     if (p->kind == SPTTN_NEST_GENERIC) {  // counters travel with the output
@@ -1027,10 +1110,13 @@ int spttn_read_output(spttn_plan* p, double* host_out, int64_t count, void* stre
 int spttn_plan_info(const spttn_plan* p, int64_t* out, int n) {
   return guarded([&] {
     if (!p) fail(SPTTN_EINVAL, "null plan");
-    const int64_t v[8] = {p->launches,   p->dec.n_items, p->dec.n_split, p->dec.n_absent,
-                          p->dec.n_items * 2 * p->dec.tile * 8,
-                          p->kind,        p->dec.n_seg,   p->kind == SPTTN_NEST_GENERIC ? p->last_madds : -1};
-    for (int i = 0; i < n && i < 8; ++i) out[i] = v[i];
+    const bool gen = p->kind == SPTTN_NEST_GENERIC;
+    const int64_t v[10] = {p->launches,   p->dec.n_items, p->dec.n_split, p->dec.n_absent,
+                           p->dec.n_items * 2 * p->dec.tile * 8,
+                           p->kind,        p->dec.n_seg,   gen ? p->last_madds : -1,
+                           gen ? p->gen.par_mode : -1,
+                           gen ? (p->gen.jit_kernel != nullptr ? 1 : 0) : -1};
+    for (int i = 0; i < n && i < 10; ++i) out[i] = v[i];
   });
 }
 

@@ -71,7 +71,7 @@ struct Interp {
           if (leaf_keys[mid] < key) lo = mid + 1; else hi = mid;
         }
         // off-pattern coordinates only produce exact zeros (executor.cpp:400)
-        if (lo < nkeys && leaf_keys[lo] == key) out[leaf_pos[lo]] += v;
+        if (lo < nkeys && leaf_keys[lo] == key) out[leaf_pos ? leaf_pos[lo] : lo] += v;
       } else {
         out[pos[t.order - 1]] += v;
       }
@@ -283,6 +283,184 @@ __global__ void k_generic_reduce(const double* priv, int64_t workers, int64_t ou
   out[e] = sum;
 }
 
+// ---- small plans: the whole working set in shared memory -------------------
+//
+// The global-memory interpreter above is latency bound on tiny tensors (the
+// regime of the reference's acceptance criterion 6: every admissible order of
+// 10-100-nonzero fixtures): each buffer / output update is a store followed by
+// a load of the same word, i.e. an L2 round trip per multiply-add. When the
+// program, the CSF, the dense inputs, the intermediate buffers and the output
+// together fit one CTA's shared memory, the CTA stages them there (all
+// threads, coalesced), walks the forest out of shared memory, and writes the
+// output and counters back once. Same walk, same arithmetic (no FMA
+// contraction in this file): results stay bit-identical to the reference.
+// Root slices go to up to 8 walkers (thread 0 of each warp) only where the
+// global interpreter's mode 1 would (disjoint outputs, no root resets).
+
+enum SmSlot {
+  kSmProg = 0, kSmBoff, kSmDenseTab, kSmBufs, kSmOut, kSmCnt, kSmVals, kSmKeys,
+  kSmIdx = 8,                       // + level
+  kSmPtr = 8 + SPG_MAX_LEVELS,      // + level
+  kSmDense = 8 + 2 * SPG_MAX_LEVELS,  // + dense slot (1..)
+  kSmSlots = kSmDense + SPG_MAX_DENSE
+};
+static_assert(kSmSlots <= 48, "GenericState::sm_off capacity");
+
+struct SmArgs {
+  const spg_program* P;
+  const int64_t* boff;
+  CsfView t;
+  const double* dense[SPG_MAX_DENSE];
+  int64_t dense_size[SPG_MAX_DENSE];
+  double* out;
+  int64_t* counters;
+  int64_t buf_elems;
+  int32_t off[48];
+  int32_t workers;
+};
+
+bool generic_sm_layout_impl(const spg_program& G, const DevCsf& csf, int workers, int64_t limit,
+                            GenericState& g) {
+  int64_t cur = 0;
+  auto take = [&](int slot, int64_t bytes) {
+    g.sm_off[slot] = static_cast<int32_t>(cur);
+    cur += (bytes + 15) & ~int64_t{15};
+  };
+  const int nb = G.num_buffers;
+  int64_t buf_elems = 0;
+  for (int b = 0; b < nb; ++b) buf_elems += G.buffer_size[b];
+  take(kSmProg, sizeof(spg_program));
+  take(kSmBoff, (nb + 1) * 8);
+  take(kSmDenseTab, SPG_MAX_DENSE * 8);
+  take(kSmBufs, std::max<int64_t>(1, buf_elems) * workers * 8);
+  take(kSmOut, std::max<int64_t>(1, G.out_size) * 8);
+  take(kSmCnt, (nb + 4) * 8);
+  const int d = csf.order;
+  const int64_t nnz = d > 0 ? csf.level_size[d - 1] : 0;
+  take(kSmVals, std::max<int64_t>(1, nnz) * 8);
+  take(kSmKeys, G.need_leaf_lookup ? std::max<int64_t>(1, nnz) * 8 : 0);
+  for (int l = 0; l < d; ++l) {
+    take(kSmIdx + l, std::max<int64_t>(1, csf.level_size[l]) * 4);
+    if (l + 1 < d) take(kSmPtr + l, (csf.level_size[l] + 1) * 4);
+  }
+  for (int f = 1; f <= G.num_dense && f < SPG_MAX_DENSE; ++f) take(kSmDense + f, G.dense_size[f] * 8);
+  if (cur > limit) return false;
+  g.sm_bytes = cur;
+  g.sm_workers = workers;
+  for (int f = 0; f < SPG_MAX_DENSE; ++f) g.dense_size[f] = (f >= 1 && f <= G.num_dense) ? G.dense_size[f] : 0;
+  return true;
+}
+
+__device__ __forceinline__ void sm_copy(void* dst, const void* src, int64_t bytes) {
+  // 8-byte words; every staged array is 8-byte sized except the int32 CSF
+  // arrays, which are copied as int32
+  const double* s = static_cast<const double*>(src);
+  double* o = static_cast<double*>(dst);
+  for (int64_t w = threadIdx.x; w < bytes / 8; w += blockDim.x) o[w] = s[w];
+}
+
+__device__ __forceinline__ void sm_copy32(int32_t* dst, const int32_t* src, int64_t n) {
+  for (int64_t w = threadIdx.x; w < n; w += blockDim.x) dst[w] = src[w];
+}
+
+__global__ void __launch_bounds__(256) k_generic_sm(SmArgs a) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const spg_program* P = reinterpret_cast<const spg_program*>(sm + a.off[kSmProg]);
+  {
+    const int4* src = reinterpret_cast<const int4*>(a.P);
+    int4* dst = reinterpret_cast<int4*>(sm + a.off[kSmProg]);
+    for (int w = threadIdx.x; w < static_cast<int>(sizeof(spg_program) / sizeof(int4)); w += blockDim.x)
+      dst[w] = src[w];
+  }
+  const int d = a.t.order;
+  CsfView t{};
+  t.order = d;
+  for (int l = 0; l < d; ++l) {
+    t.nlev[l] = a.t.nlev[l];
+    int32_t* idx = reinterpret_cast<int32_t*>(sm + a.off[kSmIdx + l]);
+    sm_copy32(idx, a.t.idx[l], a.t.nlev[l]);
+    t.idx[l] = idx;
+    if (l + 1 < d) {
+      int32_t* ptr = reinterpret_cast<int32_t*>(sm + a.off[kSmPtr + l]);
+      sm_copy32(ptr, a.t.ptr[l], a.t.nlev[l] + 1);
+      t.ptr[l] = ptr;
+    }
+  }
+  const int64_t nnz = d > 0 ? a.t.nlev[d - 1] : 0;
+  double* vals = reinterpret_cast<double*>(sm + a.off[kSmVals]);
+  sm_copy(vals, a.t.vals, nnz * 8);
+  t.vals = vals;
+  const double** tab = reinterpret_cast<const double**>(sm + a.off[kSmDenseTab]);
+  for (int f = 1; f < SPG_MAX_DENSE; ++f) {
+    if (a.dense_size[f] <= 0) continue;
+    double* dst = reinterpret_cast<double*>(sm + a.off[kSmDense + f]);
+    sm_copy(dst, a.dense[f], a.dense_size[f] * 8);
+  }
+  if (threadIdx.x < SPG_MAX_DENSE)
+    tab[threadIdx.x] = a.dense_size[threadIdx.x] > 0
+                           ? reinterpret_cast<const double*>(sm + a.off[kSmDense + threadIdx.x])
+                           : nullptr;
+  __syncthreads();  // program staged: sizes below come from it
+  const int nb = P->num_buffers;
+  int64_t* boff = reinterpret_cast<int64_t*>(sm + a.off[kSmBoff]);
+  sm_copy(boff, a.boff, (nb + 1) * 8);
+  double* bufs = reinterpret_cast<double*>(sm + a.off[kSmBufs]);
+  for (int64_t w = threadIdx.x; w < a.buf_elems * a.workers; w += blockDim.x) bufs[w] = 0.0;
+  double* out = reinterpret_cast<double*>(sm + a.off[kSmOut]);
+  for (int64_t w = threadIdx.x; w < P->out_size; w += blockDim.x) out[w] = 0.0;
+  int64_t* cnt = reinterpret_cast<int64_t*>(sm + a.off[kSmCnt]);
+  for (int w = threadIdx.x; w < nb + 4; w += blockDim.x) cnt[w] = 0;
+  int64_t* keys = P->need_leaf_lookup ? reinterpret_cast<int64_t*>(sm + a.off[kSmKeys]) : nullptr;
+  __syncthreads();  // CSF staged: leaf keys (sorted by construction) from it
+  if (keys)
+    for (int64_t leaf = threadIdx.x; leaf < nnz; leaf += blockDim.x) {
+      int64_t node = leaf, key = 0;
+      for (int l = d - 1; l >= 0; --l) {
+        key += static_cast<int64_t>(t.idx[l][node]) * P->mode_key_stride[l];
+        if (l > 0) {
+          int64_t lo = 0, hi = t.nlev[l - 1];
+          while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (t.ptr[l - 1][mid] <= node) lo = mid; else hi = mid;
+          }
+          node = lo;
+        }
+      }
+      keys[leaf] = key;
+    }
+  __syncthreads();
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0 && w < a.workers) {
+    Interp I{};
+    I.P = P;
+    I.t = t;
+    I.dense = tab;
+    I.out = out;
+    I.bufs = bufs + w * a.buf_elems;
+    I.boff = boff;
+    I.counters = cnt;
+    I.log = nullptr;
+    I.log_cap = 0;
+    I.leaf_keys = keys;
+    I.leaf_pos = nullptr;
+    I.nkeys = keys ? nnz : 0;
+    for (int k = 0; k < SPG_MAX_IDX; ++k) I.ival[k] = 0;
+    for (int k = 0; k < SPG_MAX_LEVELS; ++k) I.pos[k] = 0;
+    I.madds = 0;
+    if (a.workers == 1) {
+      for (int ri = 0; ri < P->num_roots; ++ri) walk(I, P, P->roots[ri], -1, -1);
+    } else {  // disjoint root slices, fixed round-robin assignment
+      const int64_t n0 = t.nlev[0];
+      for (int64_t sl = w; sl < n0; sl += a.workers) walk(I, P, P->roots[0], sl, sl + 1);
+    }
+    atomicAdd(reinterpret_cast<unsigned long long*>(&cnt[0]),
+              static_cast<unsigned long long>(I.madds));
+  }
+  __syncthreads();
+  for (int64_t e = threadIdx.x; e < P->out_size; e += blockDim.x) a.out[e] = out[e];
+  for (int k = threadIdx.x; k < nb + 4; k += blockDim.x) a.counters[k] = cnt[k];
+}
+
 // ---- unfactorized ---------------------------------------------------------
 
 struct Unf {
@@ -434,8 +612,41 @@ __global__ void k_unf_sparse(Unf u, const int32_t* leaf_parent /* unused */) {
 
 }  // namespace
 
+bool generic_sm_layout(const spg_program& G, const DevCsf& csf, int workers, int64_t limit,
+                       GenericState& g) {
+  return generic_sm_layout_impl(G, csf, workers, limit, g);
+}
+
 void generic_execute(const spg_program& prog, const DevCsf& csf, const double* const* dense,
                      double* out, GenericState& g, cudaStream_t s) {
+  if (g.sm) {
+    // every input is staged by the kernel and the output / counters are
+    // written in full: no memset, one launch
+    SmArgs a{};
+    a.P = g.d_prog;
+    a.boff = g.buffer_off;
+    a.t = csf.view();
+    for (int f = 0; f < SPG_MAX_DENSE; ++f) {
+      a.dense[f] = g.dense_dev[f];
+      a.dense_size[f] = a.dense[f] ? g.dense_size[f] : 0;
+    }
+    a.out = out;
+    a.counters = g.counters;
+    a.buf_elems = g.total_buffer_elems;
+    for (int k = 0; k < 48; ++k) a.off[k] = g.sm_off[k];
+    a.workers = g.sm_workers;
+    static int configured = -1;
+    int dev = 0;
+    SPTTN_CUDA(cudaGetDevice(&dev));
+    if (configured != dev) {  // opt in to the large dynamic shared memory once per device
+      SPTTN_CUDA(cudaFuncSetAttribute(k_generic_sm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      227 * 1024));
+      configured = dev;
+    }
+    k_generic_sm<<<1, 256, static_cast<size_t>(g.sm_bytes), s>>>(a);
+    SPTTN_CUDA(cudaGetLastError());
+    return;
+  }
   // counters, buffers and output are contiguous in the plan arena
   SPTTN_CUDA(cudaMemsetAsync(g.counters, 0, g.zero_bytes, s));
   Interp I{};

@@ -113,6 +113,11 @@ inline void dmalloc(T** p, size_t bytes, cudaStream_t s) {
 // Frees in stream order on `s`; owners free with s = 0 after synchronising.
 void dfree(void* p, cudaStream_t s = 0);
 void release_cached();
+// Page-locked host staging blocks (size classes over cudaHostAlloc slabs), so
+// a small plan's uploads / downloads are single DMA copies without a
+// pageable bounce; blocks are recycled, never returned to the driver.
+void* pinned_alloc(size_t bytes);
+void pinned_free(void* p, size_t bytes);
 
 // ---- kernel launchers (nest_*.cu) --------------------------------------
 struct RootOutArgs {
@@ -287,7 +292,27 @@ struct GenericState {
   bool tail = false;
   int n_tail_bufs = 0;
   int64_t tail_off[16] = {}, tail_len[16] = {};
+  // small plans (generic.cu k_generic_sm): the whole working set — program,
+  // CSF, dense inputs, buffers, output, counters — staged into one CTA's
+  // shared memory; `sm_workers` threads (one per warp) walk root slices
+  bool sm = false;
+  int sm_workers = 1;
+  int64_t sm_bytes = 0;
+  int32_t sm_off[48] = {};  // byte offsets, see generic.cu SmSlot
+  int64_t dense_size[SPG_MAX_DENSE] = {};
+  const double* dense_dev[SPG_MAX_DENSE] = {};  // device factor pointers, slot 1..
+  // sm plans: pinned host parcel mirroring the device arena
+  // [prog | boff | factors][out | counters]; the factor block is uploaded by
+  // one copy per set_factors, [out | counters] downloaded by one copy
+  unsigned char* parcel = nullptr;
+  size_t parcel_bytes = 0, up_prog = 0, up_fac = 0, up_end = 0, down_cnt = 0, down_end = 0;
+  size_t fac_off[8] = {};
+  cudaEvent_t up_done = nullptr;  // last factor upload from the parcel
 };
+// Shared-memory footprint / layout of a small GENERIC plan; returns false when
+// it does not fit `limit` bytes (generic.cu).
+bool generic_sm_layout(const spg_program& G, const DevCsf& csf, int workers, int64_t limit,
+                       GenericState& g);
 // Which JIT parallel decompositions a forest admits (jit.cu).
 struct JitSplit {
   bool ok = false;           // root 0 is the CSF level-0 loop, accumulators are safe

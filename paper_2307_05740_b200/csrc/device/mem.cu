@@ -9,6 +9,8 @@
 // spttn_release_cached() trims the pools back to the driver.
 #include <mutex>
 #include <string>
+#include <vector>
+#include <algorithm>
 
 #include "internal.cuh"
 #include "../../../include/spttn_b200.h"
@@ -58,6 +60,47 @@ void dmalloc_raw(void** p, size_t bytes, cudaStream_t s) {
 
 void dfree(void* p, cudaStream_t s) {
   if (p) cudaFreeAsync(p, s);
+}
+
+namespace {
+std::mutex g_pin_mu;
+std::vector<void*> g_pin_free[40];
+unsigned char* g_pin_cur = nullptr;
+size_t g_pin_left = 0;
+
+int pin_class(size_t bytes) {
+  int c = 8;  // 256 B minimum
+  while ((size_t{1} << c) < bytes) ++c;
+  return c;
+}
+}  // namespace
+
+void* pinned_alloc(size_t bytes) {
+  const int c = pin_class(bytes);
+  const size_t sz = size_t{1} << c;
+  std::lock_guard<std::mutex> lock(g_pin_mu);
+  if (!g_pin_free[c].empty()) {
+    void* p = g_pin_free[c].back();
+    g_pin_free[c].pop_back();
+    return p;
+  }
+  if (g_pin_left < sz) {
+    const size_t slab = std::max<size_t>(sz, size_t{8} << 20);
+    void* p = nullptr;
+    SPTTN_CUDA(cudaHostAlloc(&p, slab, cudaHostAllocPortable));
+    g_pin_cur = static_cast<unsigned char*>(p);  // the old slab's tail is dropped
+    g_pin_left = slab;
+  }
+  void* p = g_pin_cur;
+  g_pin_cur += sz;
+  g_pin_left -= sz;
+  return p;
+}
+
+void pinned_free(void* p, size_t bytes) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lock(g_pin_mu);
+  g_pin_free[pin_class(bytes)].push_back(p);
 }
 
 void release_cached() {

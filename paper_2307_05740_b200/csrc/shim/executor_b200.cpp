@@ -896,6 +896,10 @@ int spttn_b200_plan_device_kind(const spttn::ExecPlan& plan) {
   return plan.impl->pinned.kind != 0 ? plan.impl->pinned.kind : SPTTN_NEST_GENERIC;
 }
 
+int spttn_b200_plan_info(const spttn::ExecPlan& plan, int64_t* out, int n) {
+  return spttn_plan_info(plan.impl->plan, out, n);
+}
+
 spttn::CsfTensor spttn_b200_build_csf(const spttn::CooTensor& coo,
                                       const std::vector<std::string>& mode_order) {
   const int d = static_cast<int>(coo.order());

@@ -215,11 +215,27 @@ class Plan:
     def output_ptr(self) -> int:
         return int(N.engine().spttn_output_device(self.handle) or 0)
 
+    def output_tensor(self):
+        """The plan's device output as a torch CUDA tensor (zero-copy view via
+        __cuda_array_interface__; valid while the plan lives), e.g. for NCCL
+        collectives on it (distributed.py)."""
+        import torch
+
+        class _View:
+            def __init__(self, ptr, n):
+                self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8",
+                                                 "data": (ptr, False), "version": 3,
+                                                 "strides": None}
+        n = self.output_count
+        if n == 0:
+            return torch.zeros(0, dtype=torch.float64, device="cuda")
+        return torch.as_tensor(_View(self.output_ptr, n), device="cuda")
+
     def info(self) -> dict:
-        out = (C.c_int64 * 8)()
-        _check(N.engine().spttn_plan_info(self.handle, out, 8))
+        out = (C.c_int64 * 10)()
+        _check(N.engine().spttn_plan_info(self.handle, out, 10))
         keys = ["launches", "items", "split_slices", "absent_rows", "scratch_bytes", "kind",
-                "segments", "device_madds"]
+                "segments", "device_madds", "generic_mode", "generic_jit"]
         return dict(zip(keys, list(out)))
 
     def set_factors(self, factors, stream=None, on_device=False):
