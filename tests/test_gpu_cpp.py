@@ -3,6 +3,12 @@
 * build/tests/test_executor_b200 — the reference executor test cases
   (proj/tests/test_executor.cpp) restated against the device executor, plus
   device-routing checks;
+* build/tests/ref_pin — every device route (dedicated kernels, forest
+  interpreter, NVRTC-compiled forests, device execute_unfactorized) against
+  the reference executor itself (spttn_ref::, compiled from /root/reference
+  and linked into the same binary): every admissible order of the
+  acceptance fixtures (TTTc-4 sampled in --quick), sampled TTTc-6 orders,
+  BASELINE-rank fixtures; bit-identical where the route claims it;
 * build/tests/acceptance_b200 — the reference's acceptance harness
   (proj/tests/acceptance.cpp, compiled from /root/reference) linked against
   the device executor instead of proj/src/executor.cpp.
@@ -19,10 +25,10 @@ ROOT = Path(__file__).resolve().parents[1]
 BIN = ROOT / "build" / "tests"
 
 
-def run(name, timeout):
+def run(name, timeout, *args):
     exe = BIN / name
     assert exe.exists(), f"{exe} not built (built from /root/reference headers by build())"
-    return subprocess.run([str(exe)], capture_output=True, text=True, timeout=timeout)
+    return subprocess.run([str(exe), *args], capture_output=True, text=True, timeout=timeout)
 
 
 def test_reference_executor_cases_on_device():
@@ -30,6 +36,14 @@ def test_reference_executor_cases_on_device():
     print(r.stdout)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
     assert "0 failures" in r.stdout
+
+
+def test_every_device_route_pinned_to_the_reference_executor():
+    r = run("ref_pin", 1500, "--quick")
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert "REF PIN OK" in r.stdout
+    assert "failures 0" in r.stdout
 
 
 @pytest.mark.skipif(not os.environ.get("SPTTN_RUN_ACCEPTANCE"),
