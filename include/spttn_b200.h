@@ -60,6 +60,15 @@ typedef struct {
  * (SoA int32 fiber pointers / coordinates, 256-B aligned fp64 values).
  * Fails with SPTTN_EINVAL on malformed trees or coordinates beyond int32. */
 int spttn_csf_create(const spttn_csf_host* host, void* stream, spttn_csf** out);
+/* As spttn_csf_create, but the leaf values are uploaded on a side stream
+ * while the call returns after the (validated) structure: plan creation,
+ * whose decomposition needs only idx / ptr, overlaps the values' transfer
+ * (every consumer of the values waits for it on its own stream). The caller
+ * must keep host->values unchanged and allocated until the first plan
+ * created on the CSF has finished spttn_plan_create (or any execute /
+ * download on it has completed); with page-locked host->values the transfer
+ * is a true background DMA. */
+int spttn_csf_create_async(const spttn_csf_host* host, void* stream, spttn_csf** out);
 int spttn_csf_destroy(spttn_csf* csf);
 /* Builds the device CSF from COO on the GPU (replaces CooTensor::normalize +
  * build_csf, proj/src/tensor.cpp:24-94): coords are nnz x order int64,

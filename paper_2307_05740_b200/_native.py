@@ -64,7 +64,7 @@ class UnfactDesc(C.Structure):
 
 # exported C-ABI symbols (include/spttn_b200.h), checked by the CPU tests
 ENGINE_SYMBOLS = [
-    "spttn_last_error", "spttn_csf_create", "spttn_csf_destroy", "spttn_csf_level_size",
+    "spttn_last_error", "spttn_csf_create", "spttn_csf_create_async", "spttn_csf_destroy", "spttn_csf_level_size",
     "spttn_csf_device_bytes", "spttn_plan_create", "spttn_plan_destroy",
     "spttn_plan_set_factors", "spttn_execute", "spttn_execute_stage", "spttn_output_count", "spttn_output_device",
     "spttn_read_output", "spttn_plan_info", "spttn_generic_resets", "spttn_generic_log_bytes",
@@ -94,6 +94,7 @@ def engine() -> C.CDLL:
         lib.spttn_last_error.restype = C.c_char_p
         lib.spttn_build_info.restype = C.c_char_p
         lib.spttn_csf_create.argtypes = [C.POINTER(CsfHost), P, C.POINTER(P)]
+        lib.spttn_csf_create_async.argtypes = [C.POINTER(CsfHost), P, C.POINTER(P)]
         lib.spttn_csf_destroy.argtypes = [P]
         lib.spttn_csf_level_size.argtypes = [P, C.c_int]
         lib.spttn_csf_level_size.restype = c_i64

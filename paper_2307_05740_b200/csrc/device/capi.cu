@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -255,7 +256,32 @@ int64_t spttn_csf_dim(const spttn_csf* c, int l) {
   return (c && l >= 0 && l < c->d.order) ? c->d.dims[l] : -1;
 }
 
+namespace {
+// side stream per device for the asynchronous leaf-value upload
+cudaStream_t values_stream() {
+  static std::mutex mu;
+  static cudaStream_t st[64] = {};
+  int dev = 0;
+  SPTTN_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev < 0 || dev >= 64) throw spttn_dev::Status(SPTTN_ECUDA, "device ordinal out of range");
+  if (!st[dev]) SPTTN_CUDA(cudaStreamCreateWithFlags(&st[dev], cudaStreamNonBlocking));
+  return st[dev];
+}
+
+int csf_create(const spttn_csf_host* h, void* stream, spttn_csf** out, bool async_values);
+}  // namespace
+
 int spttn_csf_create(const spttn_csf_host* h, void* stream, spttn_csf** out) {
+  return csf_create(h, stream, out, false);
+}
+
+int spttn_csf_create_async(const spttn_csf_host* h, void* stream, spttn_csf** out) {
+  return csf_create(h, stream, out, true);
+}
+
+namespace {
+int csf_create(const spttn_csf_host* h, void* stream, spttn_csf** out, bool async_values) {
   return guarded([&] {
     if (!h || !out) fail(SPTTN_EINVAL, "spttn_csf_create: null argument");
     *out = nullptr;
@@ -306,9 +332,25 @@ int spttn_csf_create(const spttn_csf_host* h, void* stream, spttn_csf** out) {
       const int64_t nnz = h->level_size[d - 1];
       dev_malloc(reinterpret_cast<void**>(&D.vals), std::max<int64_t>(1, nnz) * sizeof(double), s);
       D.bytes += nnz * sizeof(double);
-      if (nnz > 0)
+      if (async_values) {
+        // the values go up on a side stream while the caller builds plans
+        // (whose structure work needs only idx / ptr); consumers of D.vals
+        // wait on D.vals_ready (DevCsf::wait_values)
+        cudaStream_t vs = values_stream();
+        cudaEvent_t alloc_done = nullptr;
+        SPTTN_CUDA(cudaEventCreateWithFlags(&alloc_done, cudaEventDisableTiming));
+        SPTTN_CUDA(cudaEventRecord(alloc_done, s));
+        SPTTN_CUDA(cudaStreamWaitEvent(vs, alloc_done, 0));
+        SPTTN_CUDA(cudaEventDestroy(alloc_done));
+        if (nnz > 0)
+          SPTTN_CUDA(cudaMemcpyAsync(D.vals, h->values, nnz * sizeof(double),
+                                     cudaMemcpyHostToDevice, vs));
+        SPTTN_CUDA(cudaEventCreateWithFlags(&D.vals_ready, cudaEventDisableTiming));
+        SPTTN_CUDA(cudaEventRecord(D.vals_ready, vs));
+      } else if (nnz > 0) {
         SPTTN_CUDA(cudaMemcpyAsync(D.vals, h->values, nnz * sizeof(double),
                                    cudaMemcpyHostToDevice, s));
+      }
       int herr = 0;
       SPTTN_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, s));
       SPTTN_CUDA(cudaStreamSynchronize(s));
@@ -329,6 +371,7 @@ int spttn_csf_create(const spttn_csf_host* h, void* stream, spttn_csf** out) {
     *out = c.release();
   });
 }
+}  // namespace
 
 int spttn_csf_destroy(spttn_csf* c) {
   return guarded([&] {
@@ -339,6 +382,7 @@ int spttn_csf_destroy(spttn_csf* c) {
       spttn_dev::dfree(c->d.ptr[l]);
     }
     spttn_dev::dfree(c->d.vals);
+    if (c->d.vals_ready) cudaEventDestroy(c->d.vals_ready);
     delete c;
   });
 }
@@ -951,6 +995,7 @@ int spttn_execute_stage(spttn_plan* p, int stage, void* stream) {
     if (stage < -1 || stage > 1) fail(SPTTN_EINVAL, "stage must be -1, 0 or 1");
     cudaStream_t s = as_stream(stream);
     const auto& D = p->csf->d;
+    D.wait_values(s);
     if (p->kind == SPTTN_NEST_GENERIC) {
       if (stage != 1) {
         if (p->gen.jit_kernel)
@@ -1156,6 +1201,7 @@ int spttn_unfactorized(const spttn_unfact_desc* desc, spttn_csf* csf, double* ho
   const int rc = guarded([&] {
     if (!desc || !csf) fail(SPTTN_EINVAL, "null argument");
     cudaStream_t s = as_stream(stream);
+    csf->d.wait_values(s);
     if (desc->num_factors < 0 || desc->num_factors > 8) fail(SPTTN_EINVAL, "bad factor count");
     const double* dptr[8] = {nullptr};
     for (int f = 0; f < desc->num_factors; ++f) {

@@ -265,6 +265,7 @@ void csf_from_coo(DevCsf& D, int d, const int64_t* dims, int64_t nnz, const int6
 }
 
 void csf_permute(const DevCsf& src, const int* order, DevCsf& D, cudaStream_t s) {
+  src.wait_values(s);
   const int d = src.order;
   const int64_t nnz = src.level_size[d - 1];
   // every leaf's coordinate at every level (parents broadcast downwards)
@@ -298,6 +299,7 @@ void csf_permute(const DevCsf& src, const int* order, DevCsf& D, cudaStream_t s)
 
 void csf_download(const DevCsf& D, int64_t* const* idx, int64_t* const* ptr, double* values,
                   cudaStream_t s) {
+  D.wait_values(s);
   int64_t maxn = 1;
   for (int l = 0; l < D.order; ++l) maxn = std::max(maxn, D.level_size[l] + 1);
   int64_t* wide = scratch<int64_t>(maxn, s);

@@ -32,6 +32,13 @@ struct DevCsf {
   int32_t* ptr[kMaxOrder] = {nullptr};
   double* vals = nullptr;
   int64_t bytes = 0;
+  // spttn_csf_create_async: the leaf values arrive on a side stream; every
+  // consumer of `vals` orders itself after this event (wait_values)
+  cudaEvent_t vals_ready = nullptr;
+
+  void wait_values(cudaStream_t s) const {
+    if (vals_ready) cudaStreamWaitEvent(s, vals_ready, 0);
+  }
 
   CsfView view() const {
     CsfView v{};

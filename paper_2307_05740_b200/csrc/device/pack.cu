@@ -219,6 +219,7 @@ void build_packed(const DevCsf& csf, int leaf_level, Decomp& d, cudaStream_t s, 
     SPTTN_CUDA(cudaMemsetAsync(d.pk2, 0, nl * sizeof(int32_t), s));
   }
   const CsfView t = csf.view();
+  csf.wait_values(s);  // the structure work above overlaps an async values upload
   k_fill_groups<<<nblk(nseg, 256), 256, 0, s>>>(ids2, runstart, gid, leaf_off, d.seg_begin,
                                                 d.seg_node, d.seg_node1, t.idx[leaf_level],
                                                 leaf_coord2, t.vals, nseg, slots, d.grp_hdr,

@@ -159,6 +159,7 @@ __global__ void k_kb_fill(const uint32_t* skeys, const int32_t* perm, int64_t nn
 
 bool build_tttp_buckets(const DevCsf& csf, int R, int sms, const int32_t* leaf_i,
                         const int32_t* leaf_j, TttpKb& kbl, cudaStream_t s) {
+  csf.wait_values(s);
   const int64_t nnz = csf.level_size[2];
   const int64_t rows_c = csf.dims[2];
   const int G = group_lanes_for(R);

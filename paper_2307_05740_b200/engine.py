@@ -76,9 +76,11 @@ def release_cached() -> None:
 
 
 class DeviceCsf:
-    """spttn_csf_create: copies a host Csf and builds the int32 device layout."""
+    """spttn_csf_create: copies a host Csf and builds the int32 device layout.
+    async_values=True: spttn_csf_create_async (values uploaded in the
+    background; keep csf.values alive until a plan on it has been created)."""
 
-    def __init__(self, csf: Csf, stream=None):
+    def __init__(self, csf: Csf, stream=None, async_values: bool = False):
         lib = N.engine()
         self.csf = csf
         d = csf.order
@@ -90,9 +92,10 @@ class DeviceCsf:
         vals = np.ascontiguousarray(csf.values, np.float64)
         host = N.CsfHost(d, self._dims, self._sizes, idx_p, ptr_p, vals.ctypes.data_as(N.c_dbl_p))
         h = C.c_void_p()
-        _check(lib.spttn_csf_create(C.byref(host), _stream_ptr(stream), C.byref(h)))
+        fn = lib.spttn_csf_create_async if async_values else lib.spttn_csf_create
+        _check(fn(C.byref(host), _stream_ptr(stream), C.byref(h)))
         self.handle = h
-        self._keep = None
+        self._keep = [vals] if async_values else None
 
     @classmethod
     def from_coo(cls, dims, coords: np.ndarray, values: np.ndarray, stream=None) -> "DeviceCsf":

@@ -492,3 +492,24 @@ def test_set_factors_rejects_less_aligned_device_factors(E):
     plan.execute()
     want, norm = oracle_with_norm(1, csf, factors, (32, 0, 0))
     assert_parity(plan.read_output(), want, norm, "after rejected refresh")
+
+
+@pytest.mark.parametrize("key", ["mttkrp3", "ttmc3", "tttp3", "mttkrp4", "ttmc4"])
+def test_async_value_upload(E, key):
+    """spttn_csf_create_async: values arrive on a side stream while the plan
+    is built; every consumer orders itself after them (plan packing, execute,
+    download) — same results as the synchronous upload, bit for bit."""
+    import torch
+    from paper_2307_05740_b200.configs import make_workload
+    w = make_workload(key, scale=2e-3)
+    c = w.cfg
+    flags = E.FLAG_RESIDUAL if c.residual else 0
+    s = torch.cuda.Stream()
+    dev = E.DeviceCsf(w.csf, stream=s, async_values=True)
+    plan = E.Plan(c.kind, dev, w.factors, ranks=c.ranks, flags=flags, stream=s)
+    plan.execute(s)
+    got = plan.read_output(s)
+    back = dev.download(s)
+    assert np.array_equal(back.values, w.csf.values)
+    ref, _, _ = run(E, c.kind, w.csf, w.factors, c.ranks, flags)
+    assert np.array_equal(got, ref)
