@@ -39,6 +39,9 @@ struct spttn_plan {
   int32_t* leaf_i = nullptr;  // TTTP leaf kernel: per-leaf root / level-1 coordinates
   int32_t* leaf_j = nullptr;
   spttn_dev::TttpKb kb;  // TTTP mode 2: C-bucketed leaf layout
+  int4* pieces = nullptr;  // TTTP mode 3: slice pieces {i, leaf lo, leaf hi}
+  int64_t n_pieces = 0;
+  int2* leaf_jk = nullptr;  // TTTP mode 3: per-leaf {j, k}
   spttn_dev::Decomp dec;
   spttn_dev::GenericState gen;
   spg_program* prog = nullptr;  // host copy (GENERIC)
@@ -412,6 +415,8 @@ int spttn_plan_destroy(spttn_plan* p) {
     spttn_dev::dfree(p->d_dense);
     spttn_dev::dfree(p->leaf_i);
     spttn_dev::dfree(p->leaf_j);
+    spttn_dev::dfree(p->pieces);
+    spttn_dev::dfree(p->leaf_jk);
     spttn_dev::free_tttp_buckets(p->kb);
     spttn_dev::free_decomp(p->dec);
     spttn_dev::generic_free(p->gen);
@@ -927,11 +932,20 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
           // 1 = leaf-parallel (default), 2 = C-bucketed (tttp_buckets.cu:
           // 3.42 vs 3.52 ms at the BASELINE shape, but a radix sort of the
           // leaves at plan time)
-          p->mode = static_cast<int>(env_int("SPTTN_TTTP_MODE", 1));
+          // 3 = slice pieces (A[i] once per piece; default)
+          p->mode = static_cast<int>(env_int("SPTTN_TTTP_MODE", 3));
           if (p->mode == 2 && !facs_aligned16) p->mode = 1;  // 16-byte cp.async of C rows
           p->batch = static_cast<int>(env_int("SPTTN_TTTP_BATCH", 4));
         }
-        if (sparse_out && (p->mode == 1 || p->mode == 2)) {
+        if (sparse_out && p->mode == 3) {
+          spttn_dev::build_leaf_coords(D, &p->leaf_i, &p->leaf_j, s);
+          spttn_dev::pack_leaf_jk(D, p->leaf_j, &p->leaf_jk, s);
+          spttn_dev::dfree(p->leaf_i, s);  // pieces carry i, leaf_jk carries j and k
+          spttn_dev::dfree(p->leaf_j, s);
+          p->leaf_i = p->leaf_j = nullptr;
+          const int P = static_cast<int>(env_int("SPTTN_TTTP_PIECE", 64));
+          p->n_pieces = spttn_dev::build_tttp_pieces(D, std::max(1, P), &p->pieces, s);
+        } else if (sparse_out && (p->mode == 1 || p->mode == 2)) {
           spttn_dev::build_leaf_coords(D, &p->leaf_i, &p->leaf_j, s);
           if (p->mode == 2) {
             if (spttn_dev::build_tttp_buckets(D, static_cast<int>(R), sms, p->leaf_i, p->leaf_j,
@@ -1088,7 +1102,9 @@ int spttn_execute_stage(spttn_plan* p, int stage, void* stream) {
         a.f[0] = p->fac[0];
         a.f[1] = p->fac[1];
         a.f[2] = p->fac[2];
-        if (p->mode == 2)
+        if (p->mode == 3)
+          spttn_dev::launch_tttp3_pieces(a, p->pieces, p->n_pieces, p->leaf_jk, p->batch, s);
+        else if (p->mode == 2)
           spttn_dev::launch_tttp3_kb(a, p->kb, s);
         else if (p->mode == 1)
           spttn_dev::launch_tttp3_leaf(a, p->leaf_i, p->leaf_j, p->batch, s);

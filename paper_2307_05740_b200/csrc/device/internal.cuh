@@ -158,6 +158,12 @@ struct RootOutArgs {
 void launch_mttkrp3(const RootOutArgs& a, cudaStream_t s);
 void launch_mttkrp4(const RootOutArgs& a, cudaStream_t s);
 void launch_tttp3(const RootOutArgs& a, cudaStream_t s);
+// TTTP-3 slice pieces (nest_tttp.cu): {i, leaf lo, leaf hi} per piece of <= P
+// leaves of one root slice; A[i] gathered once per piece.
+int64_t build_tttp_pieces(const DevCsf& D, int P, int4** pieces, cudaStream_t s);
+void pack_leaf_jk(const DevCsf& D, const int32_t* leaf_j, int2** jk, cudaStream_t s);
+void launch_tttp3_pieces(const RootOutArgs& a, const int4* pieces, int64_t n_pieces,
+                         const int2* leaf_jk, int batch, cudaStream_t s);
 void launch_ttmc3(const RootOutArgs& a, cudaStream_t s);
 int ttmc3pq_warps_per_sm();
 void launch_ttmc4(const RootOutArgs& a, cudaStream_t s);
