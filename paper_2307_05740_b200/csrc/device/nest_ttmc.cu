@@ -20,6 +20,8 @@
 // segment) and on the column pair/index h = L/4 of the fragments. Rows and
 // columns are interleaved (r = 2h+mt, s = 2(2q+e)+nt for TTMc-3) so every
 // factor-row gather is one 16-byte load per lane, 8 lanes per 128-byte row.
+#include <cstdlib>
+
 #include "internal.cuh"
 
 namespace spttn_dev {
@@ -1290,12 +1292,13 @@ struct StageT4a {
   uint64_t mbar_meta[3];
   uint64_t mbar_leaf[2];
 };
-constexpr size_t kT4aSmem = sizeof(StageT4a) * (kBlock / 32);
+constexpr size_t t4a_smem_bytes(int nb) { return sizeof(StageT4a) * (nb / 32); }
 
-__global__ void __launch_bounds__(kBlock, 2) k_ttmc4pa(RootOutArgs a) {
+template <int NB, int MB>
+__global__ void __launch_bounds__(NB, MB) k_ttmc4pa(RootOutArgs a) {
   grid_launch_dependents();
   extern __shared__ __align__(16) unsigned char t4a_smem[];
-  const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
+  const int64_t w = (static_cast<int64_t>(blockIdx.x) * NB + threadIdx.x) / 32;
   if (w >= a.n_items) return;  // warp-uniform
   StageT4a& S = reinterpret_cast<StageT4a*>(t4a_smem)[threadIdx.x / 32];
   const int lane = threadIdx.x & 31;
@@ -1569,9 +1572,14 @@ void launch_ttmc4(const RootOutArgs& a, cudaStream_t s) {
   if (blocks == 0) return;
   const int mode = a.flags >> 8;
   if (mode == 4) {  // async row gathers (the plan checked S = T = 8, R <= 8, alignment)
-    SPTTN_CUDA(cudaFuncSetAttribute(k_ttmc4pa, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(kT4aSmem)));
-    k_ttmc4pa<<<static_cast<unsigned>(blocks), kBlock, kT4aSmem, s>>>(a);
+    // 384 threads x 1 block per SM: up to 168 registers (163 used, no spill);
+    // 256 x 2 capped them at 128 and spilled 32 B per group at the same speed
+    // (404 vs 407 us at the BASELINE shape)
+    constexpr int nb = 384;
+    const size_t sm = t4a_smem_bytes(nb);
+    SPTTN_CUDA(cudaFuncSetAttribute(k_ttmc4pa<nb, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(sm)));
+    k_ttmc4pa<nb, 1><<<static_cast<unsigned>((a.n_items * 32 + nb - 1) / nb), nb, sm, s>>>(a);
   } else if (mode == 2 || mode == 3) {
     const bool vv = a.vec & 2, vw = a.vec & 4;
     const unsigned b = static_cast<unsigned>(blocks);
