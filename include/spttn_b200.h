@@ -46,7 +46,10 @@ const char* spttn_last_error(void);
 /* ---- device CSF -------------------------------------------------------- */
 typedef struct spttn_csf spttn_csf;
 
-/* Host view of a CSF tree in the reference's CsfTensor layout. */
+/* Host view of a CSF tree in the reference's CsfTensor layout. The arrays may
+ * be a view into a larger tree — e.g. a range of root slices of a CsfTensor,
+ * pointers into its arrays: ptr[l][0] need not be 0 (the device layout is
+ * rebased), only ptr[l][level_size[l]] - ptr[l][0] == level_size[l+1]. */
 typedef struct {
   int32_t order;              /* number of modes, 1..8                        */
   const int64_t* dims;        /* [order] mode sizes, root-to-leaf             */
@@ -58,7 +61,11 @@ typedef struct {
 
 /* Copies the tree to the current device and builds the device layout
  * (SoA int32 fiber pointers / coordinates, 256-B aligned fp64 values).
- * Fails with SPTTN_EINVAL on malformed trees or coordinates beyond int32. */
+ * Fails with SPTTN_EINVAL on malformed trees or coordinates beyond int32.
+ * The device CSF is a SNAPSHOT of the host arrays: plans built on it (which
+ * may also copy leaf values into packed streams) do not see later changes
+ * to the host tensor — create a new CSF and plan for changed values (the C++
+ * drop-in does this automatically at execute). */
 int spttn_csf_create(const spttn_csf_host* host, void* stream, spttn_csf** out);
 /* As spttn_csf_create, but the leaf values are uploaded on a side stream
  * while the call returns after the (validated) structure: plan creation,

@@ -38,7 +38,6 @@ struct spttn_plan {
   int batch = 4;  // TTTP leaves per group step
   int32_t* leaf_i = nullptr;  // TTTP leaf kernel: per-leaf root / level-1 coordinates
   int32_t* leaf_j = nullptr;
-  spttn_dev::TttpKb kb;  // TTTP mode 2: C-bucketed leaf layout
   int4* pieces = nullptr;  // TTTP mode 3: slice pieces {i, leaf lo, leaf hi}
   int64_t n_pieces = 0;
   int2* leaf_jk = nullptr;  // TTTP mode 3: per-leaf {j, k}
@@ -51,7 +50,6 @@ struct spttn_plan {
   int fac_align = 8;  // factor alignment the plan's kernels were chosen for
   void* arena = nullptr;                // GENERIC: one allocation for all plan state
   std::vector<int64_t> last_counters;   // GENERIC: madds, resets, log cursor, overflow
-  alignas(64) unsigned char tmap[2][128];  // TTMc-3 mode 11: U / V gather4 tensor maps
 };
 
 namespace {
@@ -83,13 +81,14 @@ cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 void dev_malloc(void** p, size_t bytes, cudaStream_t s) { spttn_dev::dmalloc_raw(p, bytes, s); }
 
 // int64 -> int32 narrowing with range / monotonicity checks.
+// `base` rebases child pointers of a tree view (ptr[l][0] != 0).
 __global__ void k_narrow(const int64_t* src, int32_t* dst, int64_t n, int64_t limit,
-                         int monotone, int* err) {
+                         int monotone, int64_t base, int* err) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const int64_t v = src[i];
+  const int64_t v = src[i] - base;
   if (v < 0 || v >= limit) atomicOr(err, 1);
-  if (monotone && i + 1 < n && src[i + 1] < v) atomicOr(err, 2);
+  if (monotone && i + 1 < n && src[i + 1] - base < v) atomicOr(err, 2);
   dst[i] = static_cast<int32_t>(v);
 }
 
@@ -307,9 +306,9 @@ int csf_create(const spttn_csf_host* h, void* stream, spttn_csf** out, bool asyn
         fail(SPTTN_EINVAL, "CSF level sizes must be non-decreasing");
       maxn = std::max(maxn, h->level_size[l] + 1);
     }
-    for (int l = 0; l + 1 < d; ++l) {
+    for (int l = 0; l + 1 < d; ++l) {  // views of a larger tree are rebased
       const int64_t n = h->level_size[l];
-      if (h->ptr[l][0] != 0 || h->ptr[l][n] != h->level_size[l + 1])
+      if (h->ptr[l][n] - h->ptr[l][0] != h->level_size[l + 1])
         fail(SPTTN_EINVAL, "CSF ptr[" + std::to_string(l) + "] does not close its child range");
     }
     int64_t* stage = nullptr;
@@ -317,20 +316,22 @@ int csf_create(const spttn_csf_host* h, void* stream, spttn_csf** out, bool asyn
     dev_malloc(reinterpret_cast<void**>(&stage), maxn * sizeof(int64_t), s);
     dev_malloc(reinterpret_cast<void**>(&err), sizeof(int), s);
     SPTTN_CUDA(cudaMemsetAsync(err, 0, sizeof(int), s));
-    auto narrow = [&](const int64_t* src, int32_t** dst, int64_t n, int64_t limit, int mono) {
+    auto narrow = [&](const int64_t* src, int32_t** dst, int64_t n, int64_t limit, int mono,
+                      int64_t base) {
       dev_malloc(reinterpret_cast<void**>(dst), std::max<int64_t>(1, n) * sizeof(int32_t), s);
       D.bytes += n * sizeof(int32_t);
       if (n == 0) return;
       SPTTN_CUDA(cudaMemcpyAsync(stage, src, n * sizeof(int64_t), cudaMemcpyHostToDevice, s));
       k_narrow<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(stage, *dst, n, limit, mono,
-                                                                       err);
+                                                                       base, err);
       SPTTN_CUDA(cudaGetLastError());
     };
     try {
       for (int l = 0; l < d; ++l) {
-        narrow(h->idx[l], &D.idx[l], h->level_size[l], h->dims[l], 0);
+        narrow(h->idx[l], &D.idx[l], h->level_size[l], h->dims[l], 0, 0);
         if (l + 1 < d)
-          narrow(h->ptr[l], &D.ptr[l], h->level_size[l] + 1, h->level_size[l + 1] + 1, 1);
+          narrow(h->ptr[l], &D.ptr[l], h->level_size[l] + 1, h->level_size[l + 1] + 1, 1,
+                 h->level_size[l] >= 0 ? h->ptr[l][0] : 0);
       }
       const int64_t nnz = h->level_size[d - 1];
       dev_malloc(reinterpret_cast<void**>(&D.vals), std::max<int64_t>(1, nnz) * sizeof(double), s);
@@ -417,7 +418,6 @@ int spttn_plan_destroy(spttn_plan* p) {
     spttn_dev::dfree(p->leaf_j);
     spttn_dev::dfree(p->pieces);
     spttn_dev::dfree(p->leaf_jk);
-    spttn_dev::free_tttp_buckets(p->kb);
     spttn_dev::free_decomp(p->dec);
     spttn_dev::generic_free(p->gen);
     delete p->prog;
@@ -803,33 +803,26 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
         int seg_len = static_cast<int>(
             env_int("SPTTN_SEG_LEN", p->kind == SPTTN_NEST_TTMC3 ? 4 : 8));
         if (p->kind == SPTTN_NEST_TTMC3) {
-          // 10 = packed, TMA-staged, row-contiguous gathers (default);
-          // 0, 4, 6, 7 = earlier variants, 11 = TMA gather4 rows, kept for
-          // A/B measurements (tools/sweep.py)
-          p->mode = static_cast<int>(env_int("SPTTN_TTMC3_MODE", 10));
-          if (p->mode != 0 && p->mode != 4 && p->mode != 6 && p->mode != 7 && p->mode != 10 &&
-              p->mode != 11)
-            p->mode = 10;
-          if (p->mode == 11 && !spttn_dev::ttmc3_tma_supported(static_cast<int>(R), static_cast<int>(S)))
-            p->mode = 10;
-          seg_len = std::clamp(seg_len, 1, p->mode == 0 ? 8 : 4);
+          // packed, TMA-staged, row-contiguous gathers (k_ttmc3pq); the
+          // earlier variants (modes 0, 4, 6, 7, 11) lost by > 6 % and were
+          // removed in round 2
+          p->mode = 10;
+          seg_len = std::clamp(seg_len, 1, 4);
         }
         seg_len = std::max(seg_len, 1);
         const int64_t units = D.level_size[1];
         const int64_t warps = static_cast<int64_t>(sms) * 32 * 2;
         int64_t chunk = env_int("SPTTN_CHUNK", 0);
         if (chunk <= 0) chunk = std::clamp<int64_t>((units + warps - 1) / warps, 8, 1024);
-        if (p->kind == SPTTN_NEST_TTMC4)
-          // 4 = 3 with the V / W row gathers by cp.async one leaf step ahead
-          // (default when S = T = 8, R <= 8, 16-byte aligned factors); 3 =
-          // packed, TMA-staged, row-contiguous gathers, 4x2 (s,t) blocks per
-          // lane; 2 = same with a full s row per lane; 1 = packed
+        if (p->kind == SPTTN_NEST_TTMC4) {
+          // 4 = V / W row gathers by cp.async one leaf step ahead (k_ttmc4pa;
+          // S = T = 8, R <= 8, 16-byte aligned factors), else 3 = packed,
+          // TMA-staged, row-contiguous gathers (k_ttmc4pq; any R, S, T <= 8)
           p->mode = static_cast<int>(env_int(
               "SPTTN_TTMC4_MODE", (R <= 8 && S == 8 && p->T == 8 && facs_aligned16) ? 4 : 3));
-        if (p->kind == SPTTN_NEST_TTMC4 && p->mode == 4 &&
-            !(R <= 8 && S == 8 && p->T == 8 && facs_aligned16))
-          p->mode = 3;
-        if (p->kind == SPTTN_NEST_TTMC4 && p->mode >= 1 && p->mode <= 4) {
+          if (p->mode != 4 || !(R <= 8 && S == 8 && p->T == 8 && facs_aligned16)) p->mode = 3;
+        }
+        if (p->kind == SPTTN_NEST_TTMC4) {
           // (i,j) pieces of <= 4 leaves, length-sorted groups of 8, with each
           // leaf's level-2 (k) coordinate packed next to its level-3 (l) one
           spttn_dev::build_segments(D, 1, std::clamp(seg_len, 1, 4), chunk, p->dec, tile, s,
@@ -849,7 +842,7 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
           const int ovh4 = p->mode == 4 ? static_cast<int>(env_int("SPTTN_GROUP_OVERHEAD", 3)) : 0;
           spttn_dev::finish_unit_items(D, p->dec, p->dec.slice_grp, p->dec.n_groups, gchunk, tile, s,
                                        ovh4);
-        } else if (p->kind == SPTTN_NEST_TTMC3 && (p->mode == 6 || p->mode == 7 || p->mode == 10 || p->mode == 11)) {
+        } else if (p->kind == SPTTN_NEST_TTMC3) {
           // packed length-sorted groups of 8 segments (pack.cu)
           spttn_dev::build_segments(D, 1, seg_len, chunk, p->dec, tile, s, false);
           spttn_dev::build_packed(D, 2, p->dec, s);
@@ -858,13 +851,12 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
             // mode 10: one item per resident warp (a single wave; 2.6 waves of
             // half-size items measured 278 vs 269 us per step at the BASELINE
             // shape — fewer split slices for the fix-up, no tail wave)
-            const int64_t wv = p->mode == 10 ? static_cast<int64_t>(sms) * spttn_dev::ttmc3pq_warps_per_sm()
-                                             : warps;
+            const int64_t wv = static_cast<int64_t>(sms) * spttn_dev::ttmc3pq_warps_per_sm();
             gchunk = std::clamp<int64_t>((p->dec.n_groups + wv - 1) / wv, 4, 512);
           }
           // k_ttmc3pq reads variable item ranges cut at equal work (leaf steps
           // + a per-group overhead, decomp.cu k_group_work): 256 -> 249 us
-          const int ovh = p->mode == 10 ? static_cast<int>(env_int("SPTTN_GROUP_OVERHEAD", 12)) : 0;
+          const int ovh = static_cast<int>(env_int("SPTTN_GROUP_OVERHEAD", 12));
           spttn_dev::finish_unit_items(D, p->dec, p->dec.slice_grp, p->dec.n_groups, gchunk, tile, s,
                                        ovh);
         } else {
@@ -884,8 +876,12 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
                               rows_b * R < (int64_t{1} << 31) && D.level_size[0] < (1 << 27) &&
                               spttn_dev::mttkrp3_smf_smem(rows_c) <=
                                   static_cast<size_t>(smem_optin_bytes());
+        // 4 = C column halves resident in shared memory (order 3 default), 2 =
+        // packed (order-3 fallback), 3 = packed + TMA-staged streams (order 4)
         p->mode = static_cast<int>(env_int("SPTTN_MTTKRP_MODE", D.order == 4 ? 3 : (smf_fits ? 4 : 2)));
         if (p->mode == 4 && !smf_fits) p->mode = 2;
+        if (p->mode < 2 || p->mode > 4) p->mode = 2;
+        if (D.order == 4) p->mode = 3;
         const int seg_len = static_cast<int>(std::clamp<int64_t>(env_int("SPTTN_SEG_LEN", 4), 1, 4));
         const int unit_level = D.order - 2;
         const int64_t units = D.level_size[unit_level];
@@ -918,8 +914,6 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
           const int ovhm = p->mode == 3 ? static_cast<int>(env_int("SPTTN_GROUP_OVERHEAD", 0)) : 0;
           spttn_dev::finish_unit_items(D, p->dec, p->dec.slice_grp, p->dec.n_groups, gchunk, tile, s,
                                        ovhm);
-        } else if (p->mode != 4) {
-          spttn_dev::build_segments(D, unit_level, seg_len, chunk, p->dec, tile, s);
         }
       } else {
         const int G = spttn_dev::group_lanes_for(static_cast<int>(R));
@@ -928,16 +922,11 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
         int64_t chunk = env_int("SPTTN_CHUNK", 0);
         if (chunk <= 0) chunk = std::clamp<int64_t>((nnz + groups - 1) / groups, 16, 4096);
         if (sparse_out) {
-          // 1 = leaf-parallel kernel over expanded (i, j) coordinates (default)
-          // 1 = leaf-parallel (default), 2 = C-bucketed (tttp_buckets.cu:
-          // 3.42 vs 3.52 ms at the BASELINE shape, but a radix sort of the
-          // leaves at plan time)
-          // 3 = slice pieces (A[i] once per piece; default)
-          p->mode = static_cast<int>(env_int("SPTTN_TTTP_MODE", 3));
-          if (p->mode == 2 && !facs_aligned16) p->mode = 1;  // 16-byte cp.async of C rows
+          // slice pieces (nest_tttp.cu): A[i] once per piece of <= 64 leaves;
+          // the round-1 leaf-parallel (3.52 ms) and C-bucketed (3.42 ms)
+          // variants lost to it (2.75 ms) and were removed
+          p->mode = 3;
           p->batch = static_cast<int>(env_int("SPTTN_TTTP_BATCH", 4));
-        }
-        if (sparse_out && p->mode == 3) {
           spttn_dev::build_leaf_coords(D, &p->leaf_i, &p->leaf_j, s);
           spttn_dev::pack_leaf_jk(D, p->leaf_j, &p->leaf_jk, s);
           spttn_dev::dfree(p->leaf_i, s);  // pieces carry i, leaf_jk carries j and k
@@ -945,21 +934,9 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
           p->leaf_i = p->leaf_j = nullptr;
           const int P = static_cast<int>(env_int("SPTTN_TTTP_PIECE", 64));
           p->n_pieces = spttn_dev::build_tttp_pieces(D, std::max(1, P), &p->pieces, s);
-        } else if (sparse_out && (p->mode == 1 || p->mode == 2)) {
-          spttn_dev::build_leaf_coords(D, &p->leaf_i, &p->leaf_j, s);
-          if (p->mode == 2) {
-            if (spttn_dev::build_tttp_buckets(D, static_cast<int>(R), sms, p->leaf_i, p->leaf_j,
-                                              p->kb, s)) {
-              spttn_dev::dfree(p->leaf_i, s);  // the bucketed streams carry i, j
-              spttn_dev::dfree(p->leaf_j, s);
-              p->leaf_i = p->leaf_j = nullptr;
-            } else {
-              p->mode = 1;
-            }
-          }
         }
         else
-          spttn_dev::build_leaf_items(D, chunk, p->dec, sparse_out ? 0 : tile, s);
+          spttn_dev::build_leaf_items(D, chunk, p->dec, tile, s);
       }
       p->launches = 1 + ((p->dec.n_split > 0 || p->dec.n_absent > 0) ? 1 : 0) +
                     (p->dec.n_multi > 0 ? 1 : 0);
@@ -1079,9 +1056,7 @@ int spttn_execute_stage(spttn_plan* p, int stage, void* stream) {
         } else if (p->mode == 3)
           spttn_dev::launch_mttkrp_pq(a, 3, s);
         else if (p->mode == 2)
-          spttn_dev::launch_mttkrp_pk(a, 3, s);
-        else if (p->mode == 1)
-          spttn_dev::launch_mttkrp_seg(a, nullptr, 3, s);
+          spttn_dev::launch_mttkrp_pk(a, s);
         else
           spttn_dev::launch_mttkrp3(a, s);
         break;
@@ -1091,10 +1066,6 @@ int spttn_execute_stage(spttn_plan* p, int stage, void* stream) {
         a.f[3] = p->fac[2];
         if (p->mode == 3)
           spttn_dev::launch_mttkrp_pq(a, 4, s);
-        else if (p->mode == 2)
-          spttn_dev::launch_mttkrp_pk(a, 4, s);
-        else if (p->mode == 1)
-          spttn_dev::launch_mttkrp_seg(a, p->dec.seg_node1, 4, s);
         else
           spttn_dev::launch_mttkrp4(a, s);
         break;
@@ -1102,25 +1073,12 @@ int spttn_execute_stage(spttn_plan* p, int stage, void* stream) {
         a.f[0] = p->fac[0];
         a.f[1] = p->fac[1];
         a.f[2] = p->fac[2];
-        if (p->mode == 3)
-          spttn_dev::launch_tttp3_pieces(a, p->pieces, p->n_pieces, p->leaf_jk, p->batch, s);
-        else if (p->mode == 2)
-          spttn_dev::launch_tttp3_kb(a, p->kb, s);
-        else if (p->mode == 1)
-          spttn_dev::launch_tttp3_leaf(a, p->leaf_i, p->leaf_j, p->batch, s);
-        else
-          spttn_dev::launch_tttp3(a, s);
+        spttn_dev::launch_tttp3_pieces(a, p->pieces, p->n_pieces, p->leaf_jk, p->batch, s);
         break;
       case SPTTN_NEST_TTMC3:
         a.f[1] = p->fac[0];
         a.f[2] = p->fac[1];
-        if (p->mode == 11) {  // tensor maps follow the current factor pointers
-          spttn_dev::make_row_map(p->tmap[0], p->fac[0], p->fac_size[0] / 16);
-          spttn_dev::make_row_map(p->tmap[1], p->fac[1], p->fac_size[1] / 16);
-          spttn_dev::launch_ttmc3_tma(a, p->tmap[0], p->tmap[1], s);
-        } else {
-          spttn_dev::launch_ttmc3(a, s);
-        }
+        spttn_dev::launch_ttmc3(a, s);
         break;
       case SPTTN_NEST_TTMC4:
         a.f[1] = p->fac[0];

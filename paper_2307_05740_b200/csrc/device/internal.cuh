@@ -157,7 +157,6 @@ struct RootOutArgs {
 
 void launch_mttkrp3(const RootOutArgs& a, cudaStream_t s);
 void launch_mttkrp4(const RootOutArgs& a, cudaStream_t s);
-void launch_tttp3(const RootOutArgs& a, cudaStream_t s);
 // TTTP-3 slice pieces (nest_tttp.cu): {i, leaf lo, leaf hi} per piece of <= P
 // leaves of one root slice; A[i] gathered once per piece.
 int64_t build_tttp_pieces(const DevCsf& D, int P, int4** pieces, cudaStream_t s);
@@ -167,14 +166,9 @@ void launch_tttp3_pieces(const RootOutArgs& a, const int4* pieces, int64_t n_pie
 void launch_ttmc3(const RootOutArgs& a, cudaStream_t s);
 int ttmc3pq_warps_per_sm();
 void launch_ttmc4(const RootOutArgs& a, cudaStream_t s);
-// TTMc-3 with TMA gather4 row loads (nest_ttmc3_tma.cu): needs R = S = 16.
-bool ttmc3_tma_supported(int R, int S);
-void make_row_map(void* map128, const double* base, int64_t rows);
-void launch_ttmc3_tma(const RootOutArgs& a, const void* mapU, const void* mapV, cudaStream_t s);
-// Segment-form MTTKRP (R <= 32): order 3 units = level-1 fibers, order 4 =
-// level-2 fibers (seg_node1 carries the level-1 coordinate).
-void launch_mttkrp_seg(const RootOutArgs& a, const int32_t* seg_node1, int order, cudaStream_t s);
-void launch_mttkrp_pk(const RootOutArgs& a, int order, cudaStream_t s);
+// Segment-form MTTKRP (R <= 32) on packed groups: pk = order 3 (fallback of
+// the shared-memory kernel), pq = TMA-staged streams (order 4 default).
+void launch_mttkrp_pk(const RootOutArgs& a, cudaStream_t s);
 void launch_mttkrp_pq(const RootOutArgs& a, int order, cudaStream_t s);
 // MTTKRP-3 with the leaf factor's column halves resident in shared memory
 // (nest_mttkrp_smf.cu): one CTA range of packed 8-slot groups per
@@ -200,30 +194,7 @@ void mttkrp3_nr_prepare(Decomp& d, int mode, int64_t rows_in, cudaStream_t s);
 void launch_mttkrp3_nr_smf(const RootOutArgs& a, const SmfArgs& x, int mode, cudaStream_t s);
 // MTTKRP-3 with the output on CSF level 1 (mode 1) or 2 (mode 2): atomics.
 void launch_mttkrp3_nonroot(const RootOutArgs& a, int mode, cudaStream_t s);
-void launch_tttp3_leaf(const RootOutArgs& a, const int32_t* leaf_i, const int32_t* leaf_j,
-                       int batch, cudaStream_t s);
-// TTTP-3 bucketed by C row ranges (nest_tttp.cu k_tttp3_kb): leaves grouped
-// by k-bucket (stable), each bucket padded to a multiple of 4 leaves.
-struct TttpKb {
-  int nkey = 0;                 // (i range, k bucket) pairs = n_i_ranges * nb
-  int nb = 0, ppb = 0, kb = 0;  // k buckets, CTAs per pair, C rows per bucket
-  int32_t rows_c = 0;
-  int64_t* bstart = nullptr;    // [nkey+1] padded starts of the (i range, k bucket) pairs
-  int32_t *li = nullptr, *lj = nullptr, *lk = nullptr, *lp = nullptr;  // i, j, k - k0, CSF position
-  double* lv = nullptr;
-};
-struct TttpKbArgs {
-  const int64_t* bstart;
-  int nb, ppb, kb;
-  int32_t rows_c;
-  const int32_t *li, *lj, *lk, *lp;
-  const double* lv;
-};
-bool build_tttp_buckets(const DevCsf& csf, int R, int sms, const int32_t* leaf_i,
-                        const int32_t* leaf_j, TttpKb& kbl, cudaStream_t s);
-void free_tttp_buckets(TttpKb& kbl);
-void launch_tttp3_kb(const RootOutArgs& a, const TttpKb& kbl, cudaStream_t s);
-// Per-leaf root / level-1 coordinates of an order-3 CSF (TTTP leaf kernel).
+// Per-leaf root / level-1 coordinates of an order-3 CSF (TTTP pieces).
 void build_leaf_coords(const DevCsf& csf, int32_t** leaf_i, int32_t** leaf_j, cudaStream_t s);
 
 // group geometry used by the leaf-range kernels: lanes per group for a

@@ -1,4 +1,5 @@
-// Leaf-range "group" kernels: MTTKRP-3, MTTKRP-4 and TTTP-3.
+// Leaf-range "group" kernels: MTTKRP-3 and MTTKRP-4 for any rank (the packed
+// kernels cover R <= 32).
 //
 // Each work item is a fixed range of `chunk` consecutive CSF leaves (the
 // nnz-balanced partition; long fibers and slices are split across items).
@@ -12,7 +13,6 @@
 // with the hooks of :411-451):
 //   MTTKRP-3  ((T*C)*B)  (i,j,k,a)(i,j,a):      X += t*C[k];  acc += X*B[j]
 //   MTTKRP-4  (((T*D)*C)*B):  X += t*D[l]; Y += X*C[k]; acc += Y*B[j]
-//   TTTP-3    (((A*B)*C)*T):  P = A[i]*B[j]; y = sum_r P*C[k]; out = y*t
 // A fiber cut by an item boundary contributes through the same products
 // (linearity), and a root slice split across items is written as HEAD/TAIL
 // partial rows that the fix-up kernel sums in item order: the result is
@@ -192,96 +192,6 @@ __global__ void __launch_bounds__(kBlock) k_mttkrp4(RootOutArgs a) {
   }
 }
 
-template <int G>
-__device__ __forceinline__ double group_sum(double v) {
-#pragma unroll
-  for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, G);
-  return v;
-}
-
-// TTTP-3 / completion residual. Reference nest (((A*B)*C)*T) with orders
-// (i,j,r)(i,j,k,r)(i,j,k): X[r] = A[i,r]*B[j,r] per (i,j); Y = sum_r X[r] *
-// C[k,r] per leaf; S[leaf] = Y*t (or rho = t - Y with SPTTN_FLAG_RESIDUAL),
-// written at the leaf's own position (executor.cpp:402).
-template <int G, bool VEC>
-__global__ void __launch_bounds__(kBlock) k_tttp3(RootOutArgs a) {
-  const int64_t gid = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / G;
-  // all lanes of a warp must stay for the shuffles
-  const bool active = gid < a.n_items;
-  const int lg = threadIdx.x & (G - 1);
-  const int c = lg * 4;
-  const int R = a.R;
-  const CsfView& t = a.t;
-  const double* __restrict__ A = a.f[0];
-  const double* __restrict__ B = a.f[1];
-  const double* __restrict__ C = a.f[2];
-  const int32_t* __restrict__ kidx = t.idx[2];
-  const double* __restrict__ vals = t.vals;
-  const bool residual = (a.flags & 1) != 0;
-
-  int32_t p = 0, pend = 0, p0 = 0, p1 = 0, f0end = 0, f1end = 0;
-  double4 arow = make_double4(0, 0, 0, 0), P = arow;
-  if (active) {
-    p = static_cast<int32_t>(gid * a.chunk);
-    pend = static_cast<int32_t>(min64(gid * a.chunk + a.chunk, t.nlev[2]));
-    p0 = a.item_pos[gid * 3 + 0];
-    p1 = a.item_pos[gid * 3 + 1];
-    f0end = t.ptr[0][p0 + 1];
-    f1end = t.ptr[1][p1 + 1];
-    arow = row4<VEC>(A + static_cast<int64_t>(t.idx[0][p0]) * R, c, R);
-    const double4 brow = row4<VEC>(B + static_cast<int64_t>(t.idx[1][p1]) * R, c, R);
-    P = make_double4(arow.x * brow.x, arow.y * brow.y, arow.z * brow.z, arow.w * brow.w);
-  }
-  // groups of one warp iterate in lock step (same trip count bound)
-  int32_t nmine = pend - p;
-  int32_t nmax = nmine;
-#pragma unroll
-  for (int o = 16; o >= G; o >>= 1) nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
-
-  for (int32_t it = 0; it < nmax; it += kBatch) {
-    int32_t kk[kBatch];
-    double vv[kBatch];
-    double4 cr[kBatch];
-#pragma unroll
-    for (int u = 0; u < kBatch; ++u) {
-      kk[u] = 0;
-      vv[u] = 0;
-      if (it + u < nmine) {
-        kk[u] = __ldg(kidx + p + it + u);
-        vv[u] = __ldg(vals + p + it + u);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kBatch; ++u)
-      cr[u] = it + u < nmine ? row4<VEC>(C + static_cast<int64_t>(kk[u]) * R, c, R)
-                             : make_double4(0, 0, 0, 0);
-#pragma unroll
-    for (int u = 0; u < kBatch; ++u) {
-      if (it + u >= nmax) break;
-      double y = P.x * cr[u].x;
-      y = fma(P.y, cr[u].y, y);
-      y = fma(P.z, cr[u].z, y);
-      y = fma(P.w, cr[u].w, y);
-      y = group_sum<G>(y);
-      const int32_t q = p + it + u;
-      if (it + u < nmine) {
-        if (lg == 0) a.out[q] = residual ? vv[u] - y : 0.0 + y * vv[u];
-        if (q + 1 < pend && q + 1 == f1end) {  // next (i,j) fiber
-          ++p1;
-          f1end = t.ptr[1][p1 + 1];
-          if (p1 == f0end) {
-            ++p0;
-            f0end = t.ptr[0][p0 + 1];
-            arow = row4<VEC>(A + static_cast<int64_t>(t.idx[0][p0]) * R, c, R);
-          }
-          const double4 brow = row4<VEC>(B + static_cast<int64_t>(t.idx[1][p1]) * R, c, R);
-          P = make_double4(arow.x * brow.x, arow.y * brow.y, arow.z * brow.z, arow.w * brow.w);
-        }
-      }
-    }
-  }
-}
-
 template <template <int, bool> class K>
 struct Dispatch;
 
@@ -310,7 +220,6 @@ struct Dispatch;
 
 SPTTN_GROUP_LAUNCH(mttkrp3)
 SPTTN_GROUP_LAUNCH(mttkrp4)
-SPTTN_GROUP_LAUNCH(tttp3)
 
 }  // namespace
 
@@ -322,6 +231,5 @@ int group_lanes_for(int R) {
 
 void launch_mttkrp3(const RootOutArgs& a, cudaStream_t s) { dispatch_mttkrp3(a, s); }
 void launch_mttkrp4(const RootOutArgs& a, cudaStream_t s) { dispatch_mttkrp4(a, s); }
-void launch_tttp3(const RootOutArgs& a, cudaStream_t s) { dispatch_tttp3(a, s); }
 
 }  // namespace spttn_dev

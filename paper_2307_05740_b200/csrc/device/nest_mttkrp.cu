@@ -9,17 +9,12 @@
 //       per (i,j,k)  Y[r] += X[r] * C[k,r];   per (i,j)  A[i,r] += Y[r] * B[j,r]
 //
 // Work units are the fibers one level above the leaves ((i,j) for order 3,
-// (i,j,k) for order 4) cut into segments of <= 4 leaves. A warp takes a
-// fixed range of segments and steps through it 4 segments at a time: lane L
-// works on K-slot q = L%4 and on the 4 rank columns [4h, 4h+4), h = L/4, so
-// every factor-row gather is one 256-bit load per lane (8 lanes per 256-byte
-// row). As in the TTMc-3 kernel, segment metadata is prefetched two groups
-// ahead and leaf coordinates one group ahead, leaving one gather round trip
-// per step. Each slot accumulates its slice contribution in registers
-// (order 4 folds Y*B per (i,j,k) segment: A_i += (X*C[k])*B[j], the same sum
-// regrouped); a finished slice is reduced over the 4 slots with two shuffles
-// and written once (owner computes), and slices cut by item boundaries go
-// through the deterministic HEAD/TAIL fix-up.
+// (i,j,k) for order 4) cut into segments of <= 4 leaves and packed into
+// length-sorted groups (pack.cu). Each slot accumulates its slice
+// contribution in registers (order 4 folds Y*B per (i,j,k) segment:
+// A_i += (X*C[k])*B[j], the same sum regrouped); a finished slice is reduced
+// over the slots with shuffles and written once (owner computes), and slices
+// cut by item boundaries go through the deterministic HEAD/TAIL fix-up.
 #include "internal.cuh"
 
 namespace spttn_dev {
@@ -27,130 +22,6 @@ namespace spttn_dev {
 namespace {
 
 constexpr int kBlock = 256;
-
-struct Meta {
-  int32_t lb, n, u, j;  // leaf begin, leaf count, unit coordinate, level-1 coordinate (order 4)
-};
-
-template <int ORDER>
-__device__ __forceinline__ Meta seg_meta(const RootOutArgs& a, const int32_t* seg_node1,
-                                         int32_t base, int q, int32_t n_seg) {
-  Meta m{0, 0, 0, 0};
-  const int32_t seg = base + q;
-  if (seg < n_seg) {
-    m.lb = __ldg(a.seg_begin + seg);
-    m.n = __ldg(a.seg_begin + seg + 1) - m.lb;
-    m.u = __ldg(a.seg_node + seg);
-    if (ORDER == 4) m.j = __ldg(seg_node1 + seg);
-  }
-  return m;
-}
-
-template <int ORDER, bool VEC>
-__global__ void __launch_bounds__(kBlock, 2) k_mttkrp_seg(RootOutArgs a, const int32_t* seg_node1) {
-  const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
-  if (w >= a.n_items) return;  // warp-uniform
-  const int lane = threadIdx.x & 31;
-  const int q = lane & 3;
-  const int c = (lane >> 2) * 4;
-  const int R = a.R;
-  const CsfView& t = a.t;
-  // factor gathered per leaf, per unit node, per level-1 node (order 4)
-  const double* __restrict__ Fleaf = a.f[ORDER - 1];
-  const double* __restrict__ Funit = a.f[ORDER - 2];
-  const double* __restrict__ Ftop = a.f[1];
-  const int32_t* __restrict__ lidx = t.idx[ORDER - 1];
-  const double* __restrict__ vals = t.vals;
-  const int32_t n_seg = static_cast<int32_t>(a.n_seg);
-
-  int32_t cs = static_cast<int32_t>(w * a.chunk);
-  const int32_t cend = static_cast<int32_t>(min64(cs + a.chunk, a.n_seg));
-  int32_t sl = a.item_pos[w];
-  int32_t sl_end = a.slice_seg[sl + 1];
-  bool head = a.slice_seg[sl] < cs;
-  int32_t row = t.idx[0][sl];
-  bool pending = false;
-  double4 acc = make_double4(0, 0, 0, 0);
-
-  auto flush = [&](int slot) {
-    // reduce the 4 K-slots' partial rows (lanes L, L^1, L^2, L^3)
-    double v[4] = {acc.x, acc.y, acc.z, acc.w};
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      v[e] += __shfl_xor_sync(0xffffffffu, v[e], 1);
-      v[e] += __shfl_xor_sync(0xffffffffu, v[e], 2);
-    }
-    if (q == 0) {
-      double* dst = slot < 0 ? a.out + static_cast<int64_t>(row) * R
-                             : a.part + (w * 2 + slot) * static_cast<int64_t>(R);
-      store4(dst, c, R, make_double4(v[0], v[1], v[2], v[3]));
-    }
-    acc = make_double4(0, 0, 0, 0);
-  };
-  auto load_k = [&](const Meta& m, int32_t* k) {
-#pragma unroll
-    for (int it = 0; it < 4; ++it) k[it] = it < m.n ? __ldg(lidx + m.lb + it) : 0;
-  };
-
-  Meta mc = seg_meta<ORDER>(a, seg_node1, cs, q, n_seg);
-  Meta mn = seg_meta<ORDER>(a, seg_node1, cs + 4, q, n_seg);
-  int32_t kc[4];
-  load_k(mc, kc);
-  while (cs < cend) {
-    const int32_t lim = min(cend, sl_end);
-    const int nv = min(4, lim - cs);
-    const bool valid = q < nv;
-    const int n = valid ? mc.n : 0;
-    double tt[4];
-    double4 rr[4];
-#pragma unroll
-    for (int it = 0; it < 4; ++it) {
-      tt[it] = it < n ? __ldg(vals + mc.lb + it) : 0.0;
-      rr[it] = it < n ? row4<VEC>(Fleaf + static_cast<int64_t>(kc[it]) * R, c, R)
-                      : make_double4(0, 0, 0, 0);
-    }
-    const double4 ur = valid ? row4<VEC>(Funit + static_cast<int64_t>(mc.u) * R, c, R)
-                             : make_double4(0, 0, 0, 0);
-    double4 tr = make_double4(0, 0, 0, 0);
-    if (ORDER == 4 && valid) tr = row4<VEC>(Ftop + static_cast<int64_t>(mc.j) * R, c, R);
-    const Meta mnn = seg_meta<ORDER>(a, seg_node1, cs + 8, q, n_seg);
-    int32_t kn[4];
-    load_k(mn, kn);
-    double4 X = make_double4(0, 0, 0, 0);
-#pragma unroll
-    for (int it = 0; it < 4; ++it) fma4(X, tt[it], rr[it]);  // X += t * F_leaf[k]
-    if (ORDER == 3) {
-      fma4v(acc, X, ur);  // A[i] += X * B[j]
-    } else {
-      const double4 Y = make_double4(X.x * ur.x, X.y * ur.y, X.z * ur.z, X.w * ur.w);
-      fma4v(acc, Y, tr);  // A[i] += (X * C[k]) * B[j]
-    }
-    pending = true;
-    const int32_t cn = cs + nv;
-    if (nv == 4) {
-      mc = mn;
-      mn = mnn;
-#pragma unroll
-      for (int it = 0; it < 4; ++it) kc[it] = kn[it];
-    } else {
-      mc = seg_meta<ORDER>(a, seg_node1, cn, q, n_seg);
-      mn = seg_meta<ORDER>(a, seg_node1, cn + 4, q, n_seg);
-      load_k(mc, kc);
-    }
-    cs = cn;
-    if (cs == sl_end) {
-      flush(head ? 0 : -1);
-      pending = false;
-      head = false;
-      if (cs < cend) {
-        ++sl;
-        sl_end = a.slice_seg[sl + 1];
-        row = t.idx[0][sl];
-      }
-    }
-  }
-  if (pending) flush(head ? 0 : 1);
-}
 
 // Packed form (default for R <= 32): the warp walks length-sorted groups of 4
 // equal-length segments (pack.cu with 4 slots: a 256-byte row needs 8 lanes
@@ -447,35 +318,14 @@ void launch_mttkrp_pq(const RootOutArgs& a, int order, cudaStream_t s) {
   SPTTN_CUDA(cudaGetLastError());
 }
 
-void launch_mttkrp_pk(const RootOutArgs& a, int order, cudaStream_t s) {
+void launch_mttkrp_pk(const RootOutArgs& a, cudaStream_t s) {  // order 3
   const int64_t blocks = (a.n_items * 32 + kBlock - 1) / kBlock;
   if (blocks == 0) return;
   const unsigned b = static_cast<unsigned>(blocks);
-  if (order == 3) {
-    if (a.vec) k_mttkrp_pk<3, true><<<b, kBlock, 0, s>>>(a);
-    else k_mttkrp_pk<3, false><<<b, kBlock, 0, s>>>(a);
-  } else {
-    if (a.vec) k_mttkrp_pk<4, true><<<b, kBlock, 0, s>>>(a);
-    else k_mttkrp_pk<4, false><<<b, kBlock, 0, s>>>(a);
-  }
+  if (a.vec) k_mttkrp_pk<3, true><<<b, kBlock, 0, s>>>(a);
+  else k_mttkrp_pk<3, false><<<b, kBlock, 0, s>>>(a);
   SPTTN_CUDA(cudaGetLastError());
 }
-
-void launch_mttkrp_seg(const RootOutArgs& a, const int32_t* seg_node1, int order, cudaStream_t s) {
-  const int64_t blocks = (a.n_items * 32 + kBlock - 1) / kBlock;
-  if (blocks == 0) return;
-  const unsigned b = static_cast<unsigned>(blocks);
-  if (order == 3) {
-    if (a.vec) k_mttkrp_seg<3, true><<<b, kBlock, 0, s>>>(a, seg_node1);
-    else k_mttkrp_seg<3, false><<<b, kBlock, 0, s>>>(a, seg_node1);
-  } else {
-    if (a.vec) k_mttkrp_seg<4, true><<<b, kBlock, 0, s>>>(a, seg_node1);
-    else k_mttkrp_seg<4, false><<<b, kBlock, 0, s>>>(a, seg_node1);
-  }
-  SPTTN_CUDA(cudaGetLastError());
-}
-
-
 
 // ---- MTTKRP-3 for the non-root output modes ------------
 //

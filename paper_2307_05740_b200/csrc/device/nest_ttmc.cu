@@ -30,590 +30,12 @@ namespace {
 
 constexpr int kBlock = 256;
 
-__device__ __forceinline__ int warp_max4(int v) {
-  v = max(v, __shfl_xor_sync(0xffffffffu, v, 1));
-  v = max(v, __shfl_xor_sync(0xffffffffu, v, 2));
-  return v;
-}
 
-template <bool VECU, bool VECV>
-__global__ void __launch_bounds__(kBlock, 3) k_ttmc3(RootOutArgs a) {
-  const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
-  if (w >= a.n_items) return;  // warp-uniform
-  const int lane = threadIdx.x & 31;
-  const int q = lane & 3;
-  const int h = lane >> 2;
-  const int R = a.R, S = a.S;
-  const CsfView& t = a.t;
-  const double* __restrict__ U = a.f[1];
-  const double* __restrict__ V = a.f[2];
-  const int32_t* __restrict__ kidx = t.idx[2];
-  const double* __restrict__ vals = t.vals;
-  const int32_t* __restrict__ seg_begin = a.seg_begin;
-  const int32_t* __restrict__ seg_node = a.seg_node;
-
-  int32_t c = static_cast<int32_t>(w * a.chunk);
-  const int32_t cend = static_cast<int32_t>(min64(c + a.chunk, a.n_seg));
-  const int32_t n_seg = static_cast<int32_t>(a.n_seg);
-  int32_t sl = a.item_pos[w];
-  int32_t sl_end = a.slice_seg[sl + 1];
-  bool head = a.slice_seg[sl] < c;
-  int32_t row = t.idx[0][sl];
-  bool pending = false;
-  double acc[8];
-#pragma unroll
-  for (int e = 0; e < 8; ++e) acc[e] = 0.0;
-
-  auto flush = [&](int slot) {
-    double* dst = slot < 0 ? a.out + static_cast<int64_t>(row) * R * S
-                           : a.part + (w * 2 + slot) * static_cast<int64_t>(R) * S;
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int r = 2 * h + mt;
-          const int s = 2 * (2 * q + e) + nt;
-          if (r < R && s < S) dst[r * S + s] = acc[(mt * 2 + nt) * 2 + e];
-        }
-#pragma unroll
-    for (int e = 0; e < 8; ++e) acc[e] = 0.0;
-  };
-
-  const int32_t nnz = t.nlev[2];
-  // Software pipeline: the leaf block (<= 32 leaves) of the next group is
-  // loaded while the current group's V rows are in flight.
-  int32_t pf_base = -1, pf_k = 0;
-  double pf_t = 0.0;
-  while (c < cend) {
-    // segment metadata for a window of 32 segments, one per lane
-    const int32_t wb = c;
-    const int32_t wend = min(wb + 32, cend);
-    const int32_t sb = wb + lane <= n_seg ? __ldg(seg_begin + wb + lane) : nnz;
-    const int32_t sb32 = __ldg(seg_begin + min(wb + 32, n_seg));
-    const int32_t sn = wb + lane < n_seg ? __ldg(seg_node + wb + lane) : 0;
-    while (c < wend) {
-      const int32_t lim = min(wend, sl_end);
-      const int nvalid = min(4, lim - c);
-      const int r0 = c - wb;
-      const int rq = r0 + q;
-      const bool valid = q < nvalid;
-      const int32_t L0 = __shfl_sync(0xffffffffu, sb, r0);
-      const int32_t L1a = __shfl_sync(0xffffffffu, sb, min(r0 + nvalid, 31));
-      const int32_t L1 = r0 + nvalid < 32 ? L1a : sb32;
-      int32_t lb = __shfl_sync(0xffffffffu, sb, min(rq, 31));
-      const int32_t lea = __shfl_sync(0xffffffffu, sb, min(rq + 1, 31));
-      int32_t le = rq + 1 < 32 ? lea : sb32;
-      int32_t j = __shfl_sync(0xffffffffu, sn, min(rq, 31));
-      if (!valid) lb = le = j = 0;
-      // this group's leaves [L0, L1) (at most 4 * seg_len <= 32), lane-parallel
-      int32_t kreg;
-      double treg;
-      if (pf_base == L0) {
-        kreg = pf_k;
-        treg = pf_t;
-      } else {
-        kreg = L0 + lane < L1 ? __ldg(kidx + L0 + lane) : 0;
-        treg = L0 + lane < L1 ? __ldg(vals + L0 + lane) : 0.0;
-      }
-      pf_base = L1;
-      pf_k = L1 + lane < nnz ? __ldg(kidx + L1 + lane) : 0;
-      pf_t = L1 + lane < nnz ? __ldg(vals + L1 + lane) : 0.0;
-      const double2 u = valid ? row2<VECU>(U + static_cast<int64_t>(j) * R, 2 * h, R)
-                              : make_double2(0, 0);
-      const int n = le - lb;
-      const int nmax = warp_max4(n);
-      const int base = lb - L0;
-      double x0 = 0.0, x1 = 0.0;
-      for (int it = 0; it < nmax; it += 4) {
-        int32_t kk[4];
-        double tt[4];
-        double2 vr[4];
-#pragma unroll
-        for (int u4 = 0; u4 < 4; ++u4) {
-          const int src = (base + it + u4) & 31;
-          kk[u4] = __shfl_sync(0xffffffffu, kreg, src);
-          tt[u4] = __shfl_sync(0xffffffffu, treg, src);
-        }
-#pragma unroll
-        for (int u4 = 0; u4 < 4; ++u4)
-          vr[u4] = it + u4 < n ? row2<VECV>(V + static_cast<int64_t>(kk[u4]) * S, 2 * h, S)
-                               : make_double2(0, 0);
-#pragma unroll
-        for (int u4 = 0; u4 < 4; ++u4) {
-          const double tv = it + u4 < n ? tt[u4] : 0.0;
-          x0 = fma(tv, vr[u4].x, x0);  // X[s] += t * V[k,s]
-          x1 = fma(tv, vr[u4].y, x1);
-        }
-      }
-      // rank-1 updates of 4 segments: D[mt][nt] += A[mt] (8x4) * B[nt] (4x8)
-      dmma_8x8x4(acc[0], acc[1], u.x, x0);
-      dmma_8x8x4(acc[2], acc[3], u.x, x1);
-      dmma_8x8x4(acc[4], acc[5], u.y, x0);
-      dmma_8x8x4(acc[6], acc[7], u.y, x1);
-      pending = true;
-      c += nvalid;
-      if (c == sl_end) {
-        flush(head ? 0 : -1);
-        pending = false;
-        head = false;
-        if (c < cend) {
-          ++sl;
-          sl_end = a.slice_seg[sl + 1];
-          row = t.idx[0][sl];
-        }
-      }
-    }
-  }
-  if (pending) flush(head ? 0 : 1);
-}
-
-// Stream-staged variant (mode 4). The warp's CSF stream — segment metadata
-// and the leaves' coordinates / values — is copied into a per-warp shared
-// memory ring with cp.async (LDGSTS) one 32-segment window ahead (metadata
-// two windows ahead, since a window's leaf range comes from its metadata),
-// so HBM latency never sits on the critical path; the only round trip left
-// per 4-segment step is the factor-row gather (L1/L2 resident rows).
-constexpr int kWin = 32;
-constexpr int kWinLeaves = kWin * 4;  // seg_len <= 4
-
-struct Stage3 {
-  int32_t sb[3][kWin + 1];
-  int32_t sn[3][kWin];
-  int32_t kk[2][kWinLeaves];
-  double tv[2][kWinLeaves];
-};
-
-template <bool VECU, bool VECV>
-__global__ void __launch_bounds__(kBlock, 3) k_ttmc3s(RootOutArgs a) {
-  __shared__ Stage3 stage[kBlock / 32];
-  const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
-  if (w >= a.n_items) return;  // warp-uniform
-  Stage3& S = stage[threadIdx.x / 32];
-  const int lane = threadIdx.x & 31;
-  const int q = lane & 3;
-  const int h = lane >> 2;
-  const int R = a.R, S_ = a.S;
-  const CsfView& t = a.t;
-  const double* __restrict__ U = a.f[1];
-  const double* __restrict__ V = a.f[2];
-  const int32_t* __restrict__ kidx = t.idx[2];
-  const double* __restrict__ vals = t.vals;
-  const int32_t* __restrict__ seg_begin = a.seg_begin;
-  const int32_t* __restrict__ seg_node = a.seg_node;
-  const int32_t* __restrict__ slice_seg = a.slice_seg;
-
-  const int32_t cbeg = static_cast<int32_t>(w * a.chunk);
-  const int32_t cend = static_cast<int32_t>(min64(cbeg + a.chunk, a.n_seg));
-  int32_t sl = a.item_pos[w];
-  int32_t sl_end = slice_seg[sl + 1];
-  bool head = slice_seg[sl] < cbeg;
-  int32_t row = t.idx[0][sl];
-  // one-slice lookahead so slice switches do not wait on global loads
-  int32_t nx_end = sl + 2 <= t.nlev[0] ? __ldg(slice_seg + sl + 2) : 0;
-  int32_t nx_row = sl + 1 < t.nlev[0] ? __ldg(t.idx[0] + sl + 1) : 0;
-  bool pending = false;
-  double acc[8];
-#pragma unroll
-  for (int e = 0; e < 8; ++e) acc[e] = 0.0;
-
-  auto flush = [&](int slot) {
-    double* dst = slot < 0 ? a.out + static_cast<int64_t>(row) * R * S_
-                           : a.part + (w * 2 + slot) * static_cast<int64_t>(R) * S_;
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int r = 2 * h + mt;
-          const int s = 2 * (2 * q + e) + nt;
-          if (r < R && s < S_) dst[r * S_ + s] = acc[(mt * 2 + nt) * 2 + e];
-        }
-#pragma unroll
-    for (int e = 0; e < 8; ++e) acc[e] = 0.0;
-  };
-  auto issue_meta = [&](int buf, int32_t ws) {
-    const int32_t nsw = min(ws + kWin, cend) - ws;
-    if (lane <= nsw) cp_async4(&S.sb[buf][lane], seg_begin + ws + lane);
-    if (lane == 0 && nsw == kWin) cp_async4(&S.sb[buf][kWin], seg_begin + ws + kWin);
-    if (lane < nsw) cp_async4(&S.sn[buf][lane], seg_node + ws + lane);
-  };
-  auto issue_leaves = [&](int lbuf, int mbuf, int32_t ws) {
-    const int32_t nsw = min(ws + kWin, cend) - ws;
-    const int32_t L0 = S.sb[mbuf][0];
-    const int32_t nl = S.sb[mbuf][nsw] - L0;
-    for (int32_t i = lane; i < nl; i += 32) {
-      cp_async4(&S.kk[lbuf][i], kidx + L0 + i);
-      cp_async8(&S.tv[lbuf][i], vals + L0 + i);
-    }
-  };
-
-  const int32_t nwin = (cend - cbeg + kWin - 1) / kWin;
-  issue_meta(0, cbeg);
-  cp_async_commit();
-  cp_async_wait<0>();
-  __syncwarp();
-  issue_leaves(0, 0, cbeg);
-  if (nwin > 1) issue_meta(1, cbeg + kWin);
-  cp_async_commit();
-  int32_t cs = cbeg;
-  for (int32_t win = 0; win < nwin; ++win) {
-    cp_async_wait<0>();
-    __syncwarp();
-    const int mb = win % 3, lbf = win & 1;
-    const int32_t ws = cbeg + win * kWin;
-    if (win + 1 < nwin) issue_leaves((win + 1) & 1, (win + 1) % 3, ws + kWin);
-    if (win + 2 < nwin) issue_meta((win + 2) % 3, ws + 2 * kWin);
-    cp_async_commit();
-    const int32_t we = min(ws + kWin, cend);
-    const int32_t L0 = S.sb[mb][0];
-    while (cs < we) {
-      const int32_t lim = min(we, sl_end);
-      const int nv = min(4, lim - cs);
-      const int r = cs - ws + q;
-      const bool valid = q < nv;
-      int32_t lb = 0, n = 0, j = 0;
-      if (valid) {
-        lb = S.sb[mb][r] - L0;
-        n = S.sb[mb][r + 1] - S.sb[mb][r];
-        j = S.sn[mb][r];
-      }
-      double2 vr[4];
-      double tt[4];
-#pragma unroll
-      for (int it = 0; it < 4; ++it) {
-        const int32_t k = it < n ? S.kk[lbf][lb + it] : 0;
-        tt[it] = it < n ? S.tv[lbf][lb + it] : 0.0;
-        vr[it] = it < n ? row2<VECV>(V + static_cast<int64_t>(k) * S_, 2 * h, S_)
-                        : make_double2(0, 0);
-      }
-      const double2 u = valid ? row2<VECU>(U + static_cast<int64_t>(j) * R, 2 * h, R)
-                              : make_double2(0, 0);
-      double x0 = 0.0, x1 = 0.0;
-#pragma unroll
-      for (int it = 0; it < 4; ++it) {
-        x0 = fma(tt[it], vr[it].x, x0);  // X[s] += t * V[k,s]
-        x1 = fma(tt[it], vr[it].y, x1);
-      }
-      dmma_8x8x4(acc[0], acc[1], u.x, x0);
-      dmma_8x8x4(acc[2], acc[3], u.x, x1);
-      dmma_8x8x4(acc[4], acc[5], u.y, x0);
-      dmma_8x8x4(acc[6], acc[7], u.y, x1);
-      pending = true;
-      cs += nv;
-      if (cs == sl_end) {
-        flush(head ? 0 : -1);
-        pending = false;
-        head = false;
-        if (cs < cend) {
-          ++sl;
-          sl_end = nx_end;
-          row = nx_row;
-          nx_end = sl + 2 <= t.nlev[0] ? __ldg(slice_seg + sl + 2) : 0;
-          nx_row = sl + 1 < t.nlev[0] ? __ldg(t.idx[0] + sl + 1) : 0;
-        }
-      }
-    }
-    __syncwarp();
-  }
-  if (pending) flush(head ? 0 : 1);
-}
-
-// Packed variant (mode 6): the warp walks length-sorted groups of 8
-// equal-length segments (pack.cu), so each of a group's n V-row gathers and
-// its U-row gather is a full 8-row 256-bit load with a warp-uniform trip
-// count. Group headers are prefetched two groups ahead and the leaf
-// coordinates of the next group one group ahead. Lane L = (q = L%4,
-// c4 = (L/4)%4, ch = L/16) gathers slot 4*ch + q, columns [4*c4, 4*c4+4) of
-// its rows (fragment order), one xor-16 exchange builds both K-chunks.
-template <bool VECU, bool VECV>
-__global__ void __launch_bounds__(kBlock, 2) k_ttmc3pk(RootOutArgs a) {
-  const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
-  if (w >= a.n_items) return;  // warp-uniform
-  const int lane = threadIdx.x & 31;
-  const int q = lane & 3;
-  const int c4 = (lane >> 2) & 3;
-  const int ch = lane >> 4;
-  const int slot = ch * 4 + q;
-  const int h = lane >> 2;
-  const int R = a.R, S_ = a.S;
-  const CsfView& t = a.t;
-  const double* __restrict__ U = a.f[1];
-  const double* __restrict__ V = a.f[2];
-  const int4* __restrict__ hdr = a.grp_hdr;
-  const int32_t* __restrict__ gnode = a.grp_node;
-  const int32_t* __restrict__ pk = a.pk;
-  const double* __restrict__ pv = a.pv;
-  const int32_t* __restrict__ slice_grp = a.slice_grp;
-  const int32_t ng = static_cast<int32_t>(a.n_groups);
-
-  const int32_t cbeg = static_cast<int32_t>(w * a.chunk);
-  const int32_t cend = static_cast<int32_t>(min64(cbeg + a.chunk, a.n_groups));
-  int32_t sl = a.item_pos[w];
-  int32_t sl_end = slice_grp[sl + 1];
-  bool head = slice_grp[sl] < cbeg;
-  int32_t row = t.idx[0][sl];
-  int32_t nx_end = sl + 2 <= t.nlev[0] ? __ldg(slice_grp + sl + 2) : 0;
-  int32_t nx_row = sl + 1 < t.nlev[0] ? __ldg(t.idx[0] + sl + 1) : 0;
-  bool pending = false;
-  double acc[8];
-#pragma unroll
-  for (int e = 0; e < 8; ++e) acc[e] = 0.0;
-
-  auto flush = [&](int dslot) {
-    double* dst = dslot < 0 ? a.out + static_cast<int64_t>(row) * R * S_
-                            : a.part + (w * 2 + dslot) * static_cast<int64_t>(R) * S_;
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int r = 4 * (h & 3) + 2 * (h >> 2) + mt;
-          const int n = 2 * q + e;
-          const int s = 4 * (n & 3) + 2 * (n >> 2) + nt;
-          if (r < R && s < S_) dst[r * S_ + s] = acc[(mt * 2 + nt) * 2 + e];
-        }
-#pragma unroll
-    for (int e = 0; e < 8; ++e) acc[e] = 0.0;
-  };
-  auto load_hdr = [&](int32_t g) { return g < ng ? __ldg(hdr + g) : make_int4(0, 0, 0, 0); };
-  auto load_k = [&](const int4& hh, int32_t* k) {
-#pragma unroll
-    for (int it = 0; it < 4; ++it) k[it] = it < hh.y ? __ldg(pk + hh.x + it * kPackSlots + slot) : 0;
-  };
-
-  int4 hc = load_hdr(cbeg), hn = load_hdr(cbeg + 1);
-  int32_t jc = cbeg < ng ? __ldg(gnode + static_cast<int64_t>(cbeg) * kPackSlots + slot) : 0;
-  int32_t kc[4];
-  load_k(hc, kc);
-  for (int32_t g = cbeg; g < cend; ++g) {
-    const int n = hc.y;  // warp-uniform segment length of this group
-    double4 vr[4];
-    double tt[4];
-#pragma unroll
-    for (int it = 0; it < 4; ++it) {
-      if (it < n) {
-        tt[it] = __ldg(pv + hc.x + it * kPackSlots + slot);
-        vr[it] = row4<VECV>(V + static_cast<int64_t>(kc[it]) * S_, 4 * c4, S_);
-      } else {
-        tt[it] = 0.0;
-        vr[it] = make_double4(0, 0, 0, 0);
-      }
-    }
-    const double4 ur = row4<VECU>(U + static_cast<int64_t>(jc) * R, 4 * c4, R);
-    // prefetch: header two groups ahead, coordinates of the next group
-    const int4 hnn = load_hdr(g + 2);
-    const int32_t jn = g + 1 < ng ? __ldg(gnode + static_cast<int64_t>(g + 1) * kPackSlots + slot) : 0;
-    int32_t kn[4];
-    load_k(hn, kn);
-    double4 x = make_double4(0, 0, 0, 0);
-#pragma unroll
-    for (int it = 0; it < 4; ++it) fma4(x, tt[it], vr[it]);  // X[s] += t * V[k,s]
-    const double sx0 = ch == 0 ? x.z : x.x, sx1 = ch == 0 ? x.w : x.y;
-    const double su0 = ch == 0 ? ur.z : ur.x, su1 = ch == 0 ? ur.w : ur.y;
-    const double rx0 = __shfl_xor_sync(0xffffffffu, sx0, 16);
-    const double rx1 = __shfl_xor_sync(0xffffffffu, sx1, 16);
-    const double ru0 = __shfl_xor_sync(0xffffffffu, su0, 16);
-    const double ru1 = __shfl_xor_sync(0xffffffffu, su1, 16);
-    const double bA0 = ch == 0 ? x.x : rx0, bA1 = ch == 0 ? x.y : rx1;
-    const double bB0 = ch == 0 ? rx0 : x.z, bB1 = ch == 0 ? rx1 : x.w;
-    const double aA0 = ch == 0 ? ur.x : ru0, aA1 = ch == 0 ? ur.y : ru1;
-    const double aB0 = ch == 0 ? ru0 : ur.z, aB1 = ch == 0 ? ru1 : ur.w;
-    dmma_8x8x4(acc[0], acc[1], aA0, bA0);
-    dmma_8x8x4(acc[2], acc[3], aA0, bA1);
-    dmma_8x8x4(acc[4], acc[5], aA1, bA0);
-    dmma_8x8x4(acc[6], acc[7], aA1, bA1);
-    dmma_8x8x4(acc[0], acc[1], aB0, bB0);
-    dmma_8x8x4(acc[2], acc[3], aB0, bB1);
-    dmma_8x8x4(acc[4], acc[5], aB1, bB0);
-    dmma_8x8x4(acc[6], acc[7], aB1, bB1);
-    pending = true;
-    hc = hn;
-    hn = hnn;
-    jc = jn;
-#pragma unroll
-    for (int it = 0; it < 4; ++it) kc[it] = kn[it];
-    if (g + 1 == sl_end) {
-      flush(head ? 0 : -1);
-      pending = false;
-      head = false;
-      if (g + 1 < cend) {
-        ++sl;
-        sl_end = nx_end;
-        row = nx_row;
-        nx_end = sl + 2 <= t.nlev[0] ? __ldg(slice_grp + sl + 2) : 0;
-        nx_row = sl + 1 < t.nlev[0] ? __ldg(t.idx[0] + sl + 1) : 0;
-      }
-    }
-  }
-  if (pending) flush(head ? 0 : 1);
-}
-
-// Packed + staged variant: packed groups (full 8-row gathers) whose stream
-// (headers, slot coordinates, interleaved leaf coordinates / values) is
-// copied into a per-warp shared-memory ring by cp.async kGW groups at a time,
-// headers two windows ahead and leaf data one window ahead, so only the
-// factor-row gathers remain on the critical path and registers hold no
-// prefetch state.
+// Packed groups are consumed in windows of kGW groups staged into shared
+// memory (TMA bulk copies on mbarriers, two windows of headers / slot
+// coordinates and one of leaf streams ahead).
 constexpr int kGW = 4;                             // groups per window
 constexpr int kGWLeaves = kGW * kPackSlots * 4;    // leaves per window (len <= 4)
-
-struct StageP {
-  alignas(16) int4 hdr[3][kGW];
-  int32_t node[3][kGW * kPackSlots];
-  int32_t kk[2][kGWLeaves];
-  double tv[2][kGWLeaves];
-};
-
-template <bool VECU, bool VECV>
-__global__ void __launch_bounds__(kBlock, 3) k_ttmc3ps(RootOutArgs a) {
-  __shared__ StageP stage[kBlock / 32];
-  const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
-  if (w >= a.n_items) return;  // warp-uniform
-  StageP& S = stage[threadIdx.x / 32];
-  const int lane = threadIdx.x & 31;
-  const int q = lane & 3;
-  const int c4 = (lane >> 2) & 3;
-  const int ch = lane >> 4;
-  const int slot = ch * 4 + q;
-  const int h = lane >> 2;
-  const int R = a.R, S_ = a.S;
-  const CsfView& t = a.t;
-  const double* __restrict__ U = a.f[1];
-  const double* __restrict__ V = a.f[2];
-  const int32_t* __restrict__ slice_grp = a.slice_grp;
-
-  const int32_t cbeg = static_cast<int32_t>(w * a.chunk);
-  const int32_t cend = static_cast<int32_t>(min64(cbeg + a.chunk, a.n_groups));
-  int32_t sl = a.item_pos[w];
-  int32_t sl_end = slice_grp[sl + 1];
-  bool head = slice_grp[sl] < cbeg;
-  int32_t row = t.idx[0][sl];
-  int32_t nx_end = sl + 2 <= t.nlev[0] ? __ldg(slice_grp + sl + 2) : 0;
-  int32_t nx_row = sl + 1 < t.nlev[0] ? __ldg(t.idx[0] + sl + 1) : 0;
-  bool pending = false;
-  double acc[8];
-#pragma unroll
-  for (int e = 0; e < 8; ++e) acc[e] = 0.0;
-
-  auto flush = [&](int dslot) {
-    double* dst = dslot < 0 ? a.out + static_cast<int64_t>(row) * R * S_
-                            : a.part + (w * 2 + dslot) * static_cast<int64_t>(R) * S_;
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int r = 4 * (h & 3) + 2 * (h >> 2) + mt;
-          const int n = 2 * q + e;
-          const int s = 4 * (n & 3) + 2 * (n >> 2) + nt;
-          if (r < R && s < S_) dst[r * S_ + s] = acc[(mt * 2 + nt) * 2 + e];
-        }
-#pragma unroll
-    for (int e = 0; e < 8; ++e) acc[e] = 0.0;
-  };
-  // window w covers groups [gs, min(gs + kGW, cend))
-  auto issue_meta = [&](int buf, int32_t gs) {
-    const int32_t nw = min(gs + kGW, cend) - gs;
-    if (lane < nw) cp_async16_cg(&S.hdr[buf][lane], a.grp_hdr + gs + lane, 16);
-    for (int i = lane; i < nw * kPackSlots; i += 32)
-      cp_async4(&S.node[buf][i], a.grp_node + static_cast<int64_t>(gs) * kPackSlots + i);
-  };
-  auto issue_leaves = [&](int lbuf, int mbuf, int32_t gs) {
-    const int32_t nw = min(gs + kGW, cend) - gs;
-    const int32_t L0 = S.hdr[mbuf][0].x;
-    const int32_t L1 = S.hdr[mbuf][nw - 1].x + kPackSlots * S.hdr[mbuf][nw - 1].y;
-    for (int32_t i = lane; i < L1 - L0; i += 32) {
-      cp_async4(&S.kk[lbuf][i], a.pk + L0 + i);
-      cp_async8(&S.tv[lbuf][i], a.pv + L0 + i);
-    }
-  };
-
-  const int32_t nwin = (cend - cbeg + kGW - 1) / kGW;
-  issue_meta(0, cbeg);
-  cp_async_commit();
-  cp_async_wait<0>();
-  __syncwarp();
-  issue_leaves(0, 0, cbeg);
-  if (nwin > 1) issue_meta(1, cbeg + kGW);
-  cp_async_commit();
-  for (int32_t win = 0; win < nwin; ++win) {
-    cp_async_wait<0>();
-    __syncwarp();
-    const int mb = win % 3, lbf = win & 1;
-    const int32_t gs = cbeg + win * kGW;
-    if (win + 1 < nwin) issue_leaves((win + 1) & 1, (win + 1) % 3, gs + kGW);
-    if (win + 2 < nwin) issue_meta((win + 2) % 3, gs + 2 * kGW);
-    cp_async_commit();
-    const int32_t ge = min(gs + kGW, cend);
-    const int32_t L0 = S.hdr[mb][0].x;
-    for (int32_t g = gs; g < ge; ++g) {
-      const int4 hh = S.hdr[mb][g - gs];
-      const int n = hh.y;  // warp-uniform
-      const int32_t lbase = hh.x - L0 + slot;
-      // straight-line: read every index first, then issue all gathers
-      const int32_t j = S.node[mb][(g - gs) * kPackSlots + slot];
-      int32_t kk[4];
-      double tt[4];
-#pragma unroll
-      for (int it = 0; it < 4; ++it) {
-        kk[it] = S.kk[lbf][lbase + it * kPackSlots];
-        tt[it] = it < n ? S.tv[lbf][lbase + it * kPackSlots] : 0.0;
-      }
-      const double4 ur = row4<VECU>(U + static_cast<int64_t>(j) * R, 4 * c4, R);
-      double4 vr[4];
-#pragma unroll
-      for (int it = 0; it < 4; ++it) {
-        if (VECV) {
-          vr[it] = ld256_if(V + static_cast<int64_t>(kk[it]) * S_ + 4 * c4, it < n && 4 * c4 < S_);
-        } else {
-          vr[it] = it < n ? row4<false>(V + static_cast<int64_t>(kk[it]) * S_, 4 * c4, S_)
-                          : make_double4(0, 0, 0, 0);
-        }
-      }
-      double4 x = make_double4(0, 0, 0, 0);
-#pragma unroll
-      for (int it = 0; it < 4; ++it) fma4(x, tt[it], vr[it]);  // X[s] += t * V[k,s]
-      const double sx0 = ch == 0 ? x.z : x.x, sx1 = ch == 0 ? x.w : x.y;
-      const double su0 = ch == 0 ? ur.z : ur.x, su1 = ch == 0 ? ur.w : ur.y;
-      const double rx0 = __shfl_xor_sync(0xffffffffu, sx0, 16);
-      const double rx1 = __shfl_xor_sync(0xffffffffu, sx1, 16);
-      const double ru0 = __shfl_xor_sync(0xffffffffu, su0, 16);
-      const double ru1 = __shfl_xor_sync(0xffffffffu, su1, 16);
-      const double bA0 = ch == 0 ? x.x : rx0, bA1 = ch == 0 ? x.y : rx1;
-      const double bB0 = ch == 0 ? rx0 : x.z, bB1 = ch == 0 ? rx1 : x.w;
-      const double aA0 = ch == 0 ? ur.x : ru0, aA1 = ch == 0 ? ur.y : ru1;
-      const double aB0 = ch == 0 ? ru0 : ur.z, aB1 = ch == 0 ? ru1 : ur.w;
-      dmma_8x8x4(acc[0], acc[1], aA0, bA0);
-      dmma_8x8x4(acc[2], acc[3], aA0, bA1);
-      dmma_8x8x4(acc[4], acc[5], aA1, bA0);
-      dmma_8x8x4(acc[6], acc[7], aA1, bA1);
-      dmma_8x8x4(acc[0], acc[1], aB0, bB0);
-      dmma_8x8x4(acc[2], acc[3], aB0, bB1);
-      dmma_8x8x4(acc[4], acc[5], aB1, bB0);
-      dmma_8x8x4(acc[6], acc[7], aB1, bB1);
-      pending = true;
-      if (g + 1 == sl_end) {
-        flush(head ? 0 : -1);
-        pending = false;
-        head = false;
-        if (g + 1 < cend) {
-          ++sl;
-          sl_end = nx_end;
-          row = nx_row;
-          nx_end = sl + 2 <= t.nlev[0] ? __ldg(slice_grp + sl + 2) : 0;
-          nx_row = sl + 1 < t.nlev[0] ? __ldg(t.idx[0] + sl + 1) : 0;
-        }
-      }
-    }
-    __syncwarp();
-  }
-  if (pending) flush(head ? 0 : 1);
-}
 
 // TMA-staged stream window: group headers, slot coordinates, interleaved leaf
 // coordinates and values — all contiguous and 32-byte aligned in the packed
@@ -833,125 +255,19 @@ __global__ void __launch_bounds__(kBlock, 3) k_ttmc3pq(RootOutArgs a) {
 // K-chunk: Out_i(R x ST) += U_J^T Y_J. Gathers: the V row is read by the 8
 // lanes of a slot (broadcast, 2 x 256-bit), W[l, h] per lane (8 rows per
 // 64-bit instruction), all issued in straight-line code.
-template <bool VECV>
-__global__ void __launch_bounds__(kBlock, 2) k_ttmc4pk(RootOutArgs a) {
-  const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
-  if (w >= a.n_items) return;  // warp-uniform
-  const int lane = threadIdx.x & 31;
-  const int q = lane & 3;
-  const int h = lane >> 2;
-  const int R = a.R, S = a.S, T = a.T;
-  const CsfView& t = a.t;
-  const double* __restrict__ U = a.f[1];
-  const double* __restrict__ V = a.f[2];
-  const double* __restrict__ W = a.f[3];
-  const int4* __restrict__ hdr = a.grp_hdr;
-  const int32_t* __restrict__ gnode = a.grp_node;
-  const int32_t* __restrict__ pl = a.pk;
-  const int32_t* __restrict__ pkk = a.pk2;
-  const double* __restrict__ pv = a.pv;
-  const int32_t* __restrict__ slice_grp = a.slice_grp;
-  const int64_t tile = static_cast<int64_t>(R) * S * T;
-
-  const int32_t cbeg = static_cast<int32_t>(w * a.chunk);
-  const int32_t cend = static_cast<int32_t>(min64(cbeg + a.chunk, a.n_groups));
-  int32_t sl = a.item_pos[w];
-  int32_t sl_end = slice_grp[sl + 1];
-  bool head = slice_grp[sl] < cbeg;
-  int32_t row = t.idx[0][sl];
-  bool pending = false;
-  double acc[16];
-#pragma unroll
-  for (int e = 0; e < 16; ++e) acc[e] = 0.0;
-
-  auto flush = [&](int dslot) {
-    double* dst = dslot < 0 ? a.out + static_cast<int64_t>(row) * tile
-                            : a.part + (w * 2 + dslot) * tile;
-#pragma unroll
-    for (int s = 0; s < 8; ++s)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int tt = 2 * q + e;
-        if (h < R && s < S && tt < T) dst[(h * S + s) * T + tt] = acc[2 * s + e];
-      }
-#pragma unroll
-    for (int e = 0; e < 16; ++e) acc[e] = 0.0;
-  };
-  auto vrow = [&](int32_t k, bool on, double* vr) {
-    const double* p = V + static_cast<int64_t>(k) * S;
-    if (VECV) {
-      const double4 a0 = ld256_if(p, on), a1 = ld256_if(p + 4, on);
-      vr[0] = a0.x; vr[1] = a0.y; vr[2] = a0.z; vr[3] = a0.w;
-      vr[4] = a1.x; vr[5] = a1.y; vr[6] = a1.z; vr[7] = a1.w;
-    } else {
-#pragma unroll
-      for (int s = 0; s < 8; ++s) vr[s] = (on && s < S) ? __ldg(p + s) : 0.0;
-    }
-  };
-
-  for (int32_t g = cbeg; g < cend; ++g) {
-    const int4 hh = __ldg(hdr + g);
-    const int n = hh.y;  // warp-uniform leaves per segment
-    const int64_t gs = static_cast<int64_t>(g) * kPackSlots;
-    const int32_t jA = __ldg(gnode + gs + q), jB = __ldg(gnode + gs + 4 + q);
-    const double uA = h < R ? __ldg(U + static_cast<int64_t>(jA) * R + h) : 0.0;
-    const double uB = h < R ? __ldg(U + static_cast<int64_t>(jB) * R + h) : 0.0;
-    double YA[8], YB[8];
-#pragma unroll
-    for (int s = 0; s < 8; ++s) YA[s] = YB[s] = 0.0;
-#pragma unroll
-    for (int it = 0; it < 4; ++it) {
-      if (it < n) {  // warp-uniform
-        const int32_t eA = hh.x + it * kPackSlots + q, eB = eA + 4;
-        const int32_t lA = __ldg(pl + eA), lB = __ldg(pl + eB);
-        const int32_t kA = __ldg(pkk + eA), kB = __ldg(pkk + eB);
-        const double vA = __ldg(pv + eA), vB = __ldg(pv + eB);
-        const double wA = h < T ? __ldg(W + static_cast<int64_t>(lA) * T + h) : 0.0;
-        const double wB = h < T ? __ldg(W + static_cast<int64_t>(lB) * T + h) : 0.0;
-        double vrA[8], vrB[8];
-        vrow(kA, true, vrA);
-        vrow(kB, true, vrB);
-        const double xA = vA * wA, xB = vB * wB;  // X[t] = t_ijkl * W[l,t]
-#pragma unroll
-        for (int s = 0; s < 8; ++s) {
-          YA[s] = fma(vrA[s], xA, YA[s]);  // Y[s,t] += V[k,s] * X[t]
-          YB[s] = fma(vrB[s], xB, YB[s]);
-        }
-      }
-    }
-    // Out_i[r, s, t] += U[j, r] * Y[s, t] for both K-chunks
-#pragma unroll
-    for (int s = 0; s < 8; ++s) dmma_8x8x4(acc[2 * s], acc[2 * s + 1], uA, YA[s]);
-#pragma unroll
-    for (int s = 0; s < 8; ++s) dmma_8x8x4(acc[2 * s], acc[2 * s + 1], uB, YB[s]);
-    pending = true;
-    if (g + 1 == sl_end) {
-      flush(head ? 0 : -1);
-      pending = false;
-      head = false;
-      if (g + 1 < cend) {
-        ++sl;
-        sl_end = slice_grp[sl + 1];
-        row = t.idx[0][sl];
-      }
-    }
-  }
-  if (pending) flush(head ? 0 : 1);
-}
-
-// TTMc-4 packed + TMA-staged (default): k_ttmc4pk's fragment mapping and
-// math, with (1) each window of kGW groups (headers, slot coordinates and the
+// TTMc-4 packed + TMA-staged (general R, S, T <= 8): DMMA fragment mapping
+// as described at the top of the file, with (1) each window of kGW groups (headers, slot coordinates and the
 // three interleaved leaf streams l, k, value) staged into shared memory by
 // lane 0 with bulk copies two (meta) / one (leaves) windows ahead, and (2) the
 // V and W rows of an iteration's 8 leaves gathered row-contiguously (4 lanes
 // per 64-byte row, one 128-bit load each) into small per-warp row tiles, from
 // which each lane reads its segment's V row (broadcast) and W[l, t=h].
-// ncu on k_ttmc4pk: the fragment-order gathers (8 lanes broadcast-reading one
-// row with 256-bit loads, W[l_q, h] with 64-bit loads) cost ~110 L1
-// data-pipe wavefronts per 8-leaf iteration and bound the kernel at 84 %.
+// (Gathering in fragment order instead — 8 lanes broadcast-reading one row
+// with 256-bit loads, W[l_q, h] with 64-bit loads — cost ~110 L1 data-pipe
+// wavefronts per 8-leaf iteration, round 1.)
 struct StageT4 {
-  alignas(16) double vs[kPackSlots][10];  // this iteration's V rows (padded)
-  alignas(16) double ws[kPackSlots][10];  // this iteration's W rows
+  alignas(16) double vs[kPackSlots][8];  // this iteration's V rows (swizzled)
+  alignas(16) double ws[kPackSlots][8];  // this iteration's W rows
   alignas(16) int4 hdr[3][kGW];
   alignas(16) int32_t node[3][kGW * kPackSlots];
   alignas(16) int32_t ll[2][kGWLeaves];
@@ -961,7 +277,7 @@ struct StageT4 {
   uint64_t mbar_leaf[2];
 };
 
-template <bool VECV, bool VECW, bool BLK>
+template <bool VECV, bool VECW>
 __global__ void __launch_bounds__(kBlock, 2) k_ttmc4pq(RootOutArgs a) {
   grid_launch_dependents();
   __shared__ StageT4 stage[kBlock / 32];
@@ -1000,11 +316,11 @@ __global__ void __launch_bounds__(kBlock, 2) k_ttmc4pq(RootOutArgs a) {
     for (int nb = 0; nb < 8; ++nb)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        // n-tile nb, n index c = 2q + e: BLK maps it to the (s, t) of the
-        // 4 x 2 block lane-column c owns, otherwise to (s = nb, t = c)
+        // n-tile nb, n index c = 2q + e: the (s, t) of the 4 x 2 block
+        // lane-column c owns
         const int c = 2 * q + e;
-        const int ss = BLK ? 4 * (c & 1) + (nb >> 1) : nb;
-        const int tt = BLK ? 2 * (c >> 1) + (nb & 1) : c;
+        const int ss = 4 * (c & 1) + (nb >> 1);
+        const int tt = 2 * (c >> 1) + (nb & 1);
         if (h < R && ss < S_ && tt < T) dst[(h * S_ + ss) * T + tt] = acc[2 * nb + e];
       }
 #pragma unroll
@@ -1074,58 +390,35 @@ __global__ void __launch_bounds__(kBlock, 2) k_ttmc4pq(RootOutArgs a) {
           const int32_t eg = hh.x - L0 + it * kPackSlots + gs;
           const double2 vg = pair2<VECV>(V + static_cast<int64_t>(S.kk[lbf][eg]) * S_, 2 * gc, S_);
           const double2 wg = pair2<VECW>(W + static_cast<int64_t>(S.ll[lbf][eg]) * T, 2 * gc, T);
-          // BLK: 64-byte rows, 16-byte chunk c stored at c ^ ((row >> 1) & 1)
-          *reinterpret_cast<double2*>(BLK ? &S.vs[0][0] + gs * 8 + 2 * (gc ^ ((gs >> 1) & 1))
-                                          : &S.vs[gs][2 * gc]) = vg;
-          // BLK: W rows swizzled like V (64-byte rows; the padded 80-byte rows
-          // of the other path made these stores 2-way bank conflicts)
-          *reinterpret_cast<double2*>(BLK ? &S.ws[0][0] + gs * 8 + 2 * (gc ^ ((gs >> 1) & 1))
-                                          : &S.ws[gs][2 * gc]) = wg;
+          // 64-byte rows, 16-byte chunk c stored at c ^ ((row >> 1) & 1)
+          *reinterpret_cast<double2*>(&S.vs[0][0] + gs * 8 + 2 * (gc ^ ((gs >> 1) & 1))) = vg;
+          *reinterpret_cast<double2*>(&S.ws[0][0] + gs * 8 + 2 * (gc ^ ((gs >> 1) & 1))) = wg;
           __syncwarp();
           const int32_t eA = hh.x - L0 + it * kPackSlots + q, eB = eA + 4;
           const double vA = S.tv[lbf][eA], vB = S.tv[lbf][eB];
-          if (BLK) {
-            // lane (q, h) owns Y[s = 4sb + i][t = 2tb + j] (i < 4, j < 2):
-            // 4 V and 2 W values per leaf and K-chunk
-            const int sb = h & 1, tb = h >> 1;
-            const int sw = (q >> 1) & 1;
-            const double* vsf = &S.vs[0][0];  // BLK: rows of 8 doubles
-            const double2 a0 = *reinterpret_cast<const double2*>(vsf + q * 8 + 2 * ((2 * sb) ^ sw));
-            const double2 a1 = *reinterpret_cast<const double2*>(vsf + q * 8 + 2 * ((2 * sb + 1) ^ sw));
-            const double2 b0 = *reinterpret_cast<const double2*>(vsf + (q + 4) * 8 + 2 * ((2 * sb) ^ sw));
-            const double2 b1 =
-                *reinterpret_cast<const double2*>(vsf + (q + 4) * 8 + 2 * ((2 * sb + 1) ^ sw));
-            const double* wsf = &S.ws[0][0];
-            const double2 wa = *reinterpret_cast<const double2*>(wsf + q * 8 + 2 * (tb ^ sw));
-            const double2 wb = *reinterpret_cast<const double2*>(wsf + (q + 4) * 8 + 2 * (tb ^ sw));
-            __syncwarp();  // row tiles are rewritten by the next iteration
-            const double va[4] = {a0.x, a0.y, a1.x, a1.y}, vb[4] = {b0.x, b0.y, b1.x, b1.y};
-            const double xa[2] = {vA * wa.x, vA * wa.y}, xb[2] = {vB * wb.x, vB * wb.y};
+          // lane (q, h) owns Y[s = 4sb + i][t = 2tb + j] (i < 4, j < 2):
+          // 4 V and 2 W values per leaf and K-chunk
+          const int sb = h & 1, tb = h >> 1;
+          const int sw = (q >> 1) & 1;
+          const double* vsf = &S.vs[0][0];  // rows of 8 doubles
+          const double2 a0 = *reinterpret_cast<const double2*>(vsf + q * 8 + 2 * ((2 * sb) ^ sw));
+          const double2 a1 = *reinterpret_cast<const double2*>(vsf + q * 8 + 2 * ((2 * sb + 1) ^ sw));
+          const double2 b0 = *reinterpret_cast<const double2*>(vsf + (q + 4) * 8 + 2 * ((2 * sb) ^ sw));
+          const double2 b1 =
+              *reinterpret_cast<const double2*>(vsf + (q + 4) * 8 + 2 * ((2 * sb + 1) ^ sw));
+          const double* wsf = &S.ws[0][0];
+          const double2 wa = *reinterpret_cast<const double2*>(wsf + q * 8 + 2 * (tb ^ sw));
+          const double2 wb = *reinterpret_cast<const double2*>(wsf + (q + 4) * 8 + 2 * (tb ^ sw));
+          __syncwarp();  // row tiles are rewritten by the next iteration
+          const double va[4] = {a0.x, a0.y, a1.x, a1.y}, vb[4] = {b0.x, b0.y, b1.x, b1.y};
+          const double xa[2] = {vA * wa.x, vA * wa.y}, xb[2] = {vB * wb.x, vB * wb.y};
 #pragma unroll
-            for (int i2 = 0; i2 < 4; ++i2)
+          for (int i2 = 0; i2 < 4; ++i2)
 #pragma unroll
-              for (int j2 = 0; j2 < 2; ++j2) {
-                YA[2 * i2 + j2] = fma(va[i2], xa[j2], YA[2 * i2 + j2]);  // Y[s,t] += V[k,s] * X[t]
-                YB[2 * i2 + j2] = fma(vb[i2], xb[j2], YB[2 * i2 + j2]);
-              }
-          } else {
-            const double wA = S.ws[q][h], wB = S.ws[q + 4][h];
-            double vrA[8], vrB[8];
-#pragma unroll
-            for (int m = 0; m < 4; ++m) {
-              const double2 a2 = *reinterpret_cast<const double2*>(&S.vs[q][2 * m]);
-              const double2 b2 = *reinterpret_cast<const double2*>(&S.vs[q + 4][2 * m]);
-              vrA[2 * m] = a2.x; vrA[2 * m + 1] = a2.y;
-              vrB[2 * m] = b2.x; vrB[2 * m + 1] = b2.y;
+            for (int j2 = 0; j2 < 2; ++j2) {
+              YA[2 * i2 + j2] = fma(va[i2], xa[j2], YA[2 * i2 + j2]);  // Y[s,t] += V[k,s] * X[t]
+              YB[2 * i2 + j2] = fma(vb[i2], xb[j2], YB[2 * i2 + j2]);
             }
-            __syncwarp();  // row tiles are rewritten by the next iteration
-            const double xA = vA * wA, xB = vB * wB;  // X[t] = t_ijkl * W[l,t]
-#pragma unroll
-            for (int s = 0; s < 8; ++s) {
-              YA[s] = fma(vrA[s], xA, YA[s]);  // Y[s,t] += V[k,s] * X[t]
-              YB[s] = fma(vrB[s], xB, YB[s]);
-            }
-          }
         }
       }
       // Out_i[r, s, t] += U[j, r] * Y[s, t] for both K-chunks
@@ -1151,126 +444,6 @@ __global__ void __launch_bounds__(kBlock, 2) k_ttmc4pq(RootOutArgs a) {
   }
   if (pending) flush(head ? 0 : 1);
 }
-
-template <bool VECV>
-__global__ void __launch_bounds__(kBlock) k_ttmc4(RootOutArgs a) {
-  const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
-  if (w >= a.n_items) return;
-  const int lane = threadIdx.x & 31;
-  const int q = lane & 3;
-  const int h = lane >> 2;
-  const int R = a.R, S = a.S, T = a.T;
-  const CsfView& t = a.t;
-  const double* __restrict__ U = a.f[1];
-  const double* __restrict__ V = a.f[2];
-  const double* __restrict__ W = a.f[3];
-  const int32_t* __restrict__ kidx = t.idx[2];
-  const int32_t* __restrict__ lidx = t.idx[3];
-  const int32_t* __restrict__ kptr = t.ptr[2];
-  const double* __restrict__ vals = t.vals;
-  const int64_t tile = static_cast<int64_t>(R) * S * T;
-
-  int64_t c = w * a.chunk;
-  const int64_t cend = min64(c + a.chunk, a.n_seg);
-  int32_t sl = a.item_pos[w];
-  int64_t sl_end = a.slice_seg[sl + 1];
-  bool head = a.slice_seg[sl] < c;
-  int32_t row = t.idx[0][sl];
-  bool pending = false;
-  double acc[16];
-#pragma unroll
-  for (int e = 0; e < 16; ++e) acc[e] = 0.0;
-
-  auto flush = [&](int slot) {
-    double* dst = slot < 0 ? a.out + static_cast<int64_t>(row) * tile
-                           : a.part + (w * 2 + slot) * tile;
-    // tile nt = s: D[r = h][col = 2q+e] -> (r, s, t = 2q+e)
-#pragma unroll
-    for (int s = 0; s < 8; ++s)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int tt = 2 * q + e;
-        if (h < R && s < S && tt < T) dst[(h * S + s) * T + tt] = acc[2 * s + e];
-      }
-#pragma unroll
-    for (int e = 0; e < 16; ++e) acc[e] = 0.0;
-  };
-
-  while (c < cend) {
-    const int64_t lim = min(cend, sl_end);
-    const int64_t my = c + q;
-    const bool valid = my < lim;
-    int32_t kb = 0, ke = 0, j = 0;
-    if (valid) {
-      kb = __ldg(a.seg_begin + my);
-      ke = __ldg(a.seg_begin + my + 1);
-      j = __ldg(a.seg_node + my);
-    }
-    const double u = (valid && h < R) ? __ldg(U + static_cast<int64_t>(j) * R + h) : 0.0;
-    int32_t lb = 0, le = 0, kend = 0, k = 0;
-    if (valid) {
-      lb = __ldg(kptr + kb);
-      le = __ldg(kptr + ke);
-      kend = __ldg(kptr + kb + 1);
-      k = __ldg(kidx + kb);
-    }
-    int32_t kc = kb;
-    const int n = le - lb;
-    const int nmax = warp_max4(n);
-    double Y[8];
-#pragma unroll
-    for (int s = 0; s < 8; ++s) Y[s] = 0.0;
-    double X = 0.0;
-    for (int it = 0; it < nmax; ++it) {
-      if (it < n) {
-        const int32_t p = lb + it;
-        const int32_t l = __ldg(lidx + p);
-        const double v = __ldg(vals + p);
-        const double wv = h < T ? __ldg(W + static_cast<int64_t>(l) * T + h) : 0.0;
-        X = fma(v, wv, X);  // X[t] += t_ijkl * W[l,t]
-        if (p + 1 == kend) {
-          // rank-1: Y[s,t] += V[k,s] * X[t]
-          double vr[8];
-          const double* vrow = V + static_cast<int64_t>(k) * S;
-          if (VECV) {
-            const double4 a0 = ld256(vrow);
-            const double4 a1 = ld256(vrow + 4);
-            vr[0] = a0.x; vr[1] = a0.y; vr[2] = a0.z; vr[3] = a0.w;
-            vr[4] = a1.x; vr[5] = a1.y; vr[6] = a1.z; vr[7] = a1.w;
-          } else {
-#pragma unroll
-            for (int s = 0; s < 8; ++s) vr[s] = s < S ? __ldg(vrow + s) : 0.0;
-          }
-#pragma unroll
-          for (int s = 0; s < 8; ++s) Y[s] = fma(vr[s], X, Y[s]);
-          X = 0.0;
-          ++kc;
-          if (kc < ke) {
-            kend = __ldg(kptr + kc + 1);
-            k = __ldg(kidx + kc);
-          }
-        }
-      }
-    }
-    // Out_i[r, s, t] += U[j,r] * Y[s,t]: tile nt = s, A = U^T (8 x 4 slots)
-#pragma unroll
-    for (int s = 0; s < 8; ++s) dmma_8x8x4(acc[2 * s], acc[2 * s + 1], u, Y[s]);
-    pending = true;
-    c = min(c + 4, lim);
-    if (c == sl_end) {
-      flush(head ? 0 : -1);
-      pending = false;
-      head = false;
-      if (c < cend) {
-        ++sl;
-        sl_end = a.slice_seg[sl + 1];
-        row = t.idx[0][sl];
-      }
-    }
-  }
-  if (pending) flush(head ? 0 : 1);
-}
-
 
 // TTMc-4 packed + TMA-staged, asynchronous row gathers (mode 4, default for
 // R, S, T <= 8 with S = T = 8 and 16-byte aligned factors). k_ttmc4pq's
@@ -1498,72 +671,20 @@ int ttmc3pq_warps_per_sm() {
 void launch_ttmc3(const RootOutArgs& a, cudaStream_t s) {
   const int64_t blocks = (a.n_items * 32 + kBlock - 1) / kBlock;
   if (blocks == 0) return;
-  const bool vu = a.vec & 1, vv = a.vec & 2;
-  const int mode = a.flags >> 8;  // kernel variant chosen at plan time
-  if (mode == 10) {
-    const bool wu = a.vec & 4, wv = a.vec & 8;
-    auto go = [&](auto kern) {
-      SPTTN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(kPqSmem)));
-      kern<<<static_cast<unsigned>(blocks), kBlock, kPqSmem, s>>>(a);
-    };
-    if (wu && wv)
-      go(k_ttmc3pq<true, true>);
-    else if (wu)
-      go(k_ttmc3pq<true, false>);
-    else if (wv)
-      go(k_ttmc3pq<false, true>);
-    else
-      go(k_ttmc3pq<false, false>);
-    SPTTN_CUDA(cudaGetLastError());
-    return;
-  }
-  if (mode == 7) {
-    const bool wu = a.vec & 4, wv = a.vec & 8;
-    if (wu && wv)
-      k_ttmc3ps<true, true><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
-    else if (wu)
-      k_ttmc3ps<true, false><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
-    else if (wv)
-      k_ttmc3ps<false, true><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
-    else
-      k_ttmc3ps<false, false><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
-    SPTTN_CUDA(cudaGetLastError());
-    return;
-  }
-  if (mode == 6) {
-    const bool wu = a.vec & 4, wv = a.vec & 8;
-    if (wu && wv)
-      k_ttmc3pk<true, true><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
-    else if (wu)
-      k_ttmc3pk<true, false><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
-    else if (wv)
-      k_ttmc3pk<false, true><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
-    else
-      k_ttmc3pk<false, false><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
-    SPTTN_CUDA(cudaGetLastError());
-    return;
-  }
-  if (mode == 4) {
-    if (vu && vv)
-      k_ttmc3s<true, true><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
-    else if (vu)
-      k_ttmc3s<true, false><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
-    else if (vv)
-      k_ttmc3s<false, true><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
-    else
-      k_ttmc3s<false, false><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
-    SPTTN_CUDA(cudaGetLastError());
-    return;
-  }
-  if (vu && vv)
-    k_ttmc3<true, true><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
-  else if (vu)
-    k_ttmc3<true, false><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
-  else if (vv)
-    k_ttmc3<false, true><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
+  const bool wu = a.vec & 4, wv = a.vec & 8;  // 256-bit U / V row gathers allowed
+  auto go = [&](auto kern) {
+    SPTTN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kPqSmem)));
+    kern<<<static_cast<unsigned>(blocks), kBlock, kPqSmem, s>>>(a);
+  };
+  if (wu && wv)
+    go(k_ttmc3pq<true, true>);
+  else if (wu)
+    go(k_ttmc3pq<true, false>);
+  else if (wv)
+    go(k_ttmc3pq<false, true>);
   else
-    k_ttmc3<false, false><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
+    go(k_ttmc3pq<false, false>);
   SPTTN_CUDA(cudaGetLastError());
 }
 
@@ -1580,29 +701,13 @@ void launch_ttmc4(const RootOutArgs& a, cudaStream_t s) {
     SPTTN_CUDA(cudaFuncSetAttribute(k_ttmc4pa<nb, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(sm)));
     k_ttmc4pa<nb, 1><<<static_cast<unsigned>((a.n_items * 32 + nb - 1) / nb), nb, sm, s>>>(a);
-  } else if (mode == 2 || mode == 3) {
+  } else {  // packed, 4 x 2 (s, t) blocks per lane (any R, S, T <= 8)
     const bool vv = a.vec & 2, vw = a.vec & 4;
     const unsigned b = static_cast<unsigned>(blocks);
-    if (mode == 3) {  // 4 x 2 (s, t) blocks per lane
-      if (vv && vw) k_ttmc4pq<true, true, true><<<b, kBlock, 0, s>>>(a);
-      else if (vv) k_ttmc4pq<true, false, true><<<b, kBlock, 0, s>>>(a);
-      else if (vw) k_ttmc4pq<false, true, true><<<b, kBlock, 0, s>>>(a);
-      else k_ttmc4pq<false, false, true><<<b, kBlock, 0, s>>>(a);
-    } else {
-      if (vv && vw) k_ttmc4pq<true, true, false><<<b, kBlock, 0, s>>>(a);
-      else if (vv) k_ttmc4pq<true, false, false><<<b, kBlock, 0, s>>>(a);
-      else if (vw) k_ttmc4pq<false, true, false><<<b, kBlock, 0, s>>>(a);
-      else k_ttmc4pq<false, false, false><<<b, kBlock, 0, s>>>(a);
-    }
-  } else if (mode == 1) {
-    if (a.vec & 2)
-      k_ttmc4pk<true><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
-    else
-      k_ttmc4pk<false><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
-  } else if (a.vec & 2) {
-    k_ttmc4<true><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
-  } else {
-    k_ttmc4<false><<<static_cast<unsigned>(blocks), kBlock, 0, s>>>(a);
+    if (vv && vw) k_ttmc4pq<true, true><<<b, kBlock, 0, s>>>(a);
+    else if (vv) k_ttmc4pq<true, false><<<b, kBlock, 0, s>>>(a);
+    else if (vw) k_ttmc4pq<false, true><<<b, kBlock, 0, s>>>(a);
+    else k_ttmc4pq<false, false><<<b, kBlock, 0, s>>>(a);
   }
   SPTTN_CUDA(cudaGetLastError());
 }

@@ -98,6 +98,39 @@ class DeviceCsf:
         self._keep = [vals] if async_values else None
 
     @classmethod
+    def from_root_range(cls, csf: Csf, r0: int, r1: int, stream=None,
+                        async_values: bool = False) -> "DeviceCsf":
+        """Root slices [r0, r1) of a host Csf as a device CSF, passed as a
+        zero-copy view into csf's arrays (spttn_csf_host views: ptr[l][0] may
+        be non-zero, the device layout is rebased). Output rows keep their
+        global numbering."""
+        lib = N.engine()
+        d = csf.order
+        lo, hi = [r0], [r1]
+        for l in range(d - 1):
+            lo.append(int(csf.ptr[l][lo[-1]]))
+            hi.append(int(csf.ptr[l][hi[-1]]))
+        arrs = [np.ascontiguousarray(a, np.int64) for a in csf.idx + csf.ptr]
+        vals = np.ascontiguousarray(csf.values, np.float64)
+        self = cls.__new__(cls)
+        self.csf = None
+        self._dims = (C.c_int64 * d)(*csf.dims)
+        self._sizes = (C.c_int64 * d)(*[hi[l] - lo[l] for l in range(d)])
+        idx_p = (N.c_i64_p * d)(*[C.cast(arrs[l].ctypes.data + 8 * lo[l], N.c_i64_p)
+                                  for l in range(d)])
+        ptr_p = (N.c_i64_p * max(1, d - 1))(*[C.cast(arrs[d + l].ctypes.data + 8 * lo[l], N.c_i64_p)
+                                              for l in range(d - 1)])
+        host = N.CsfHost(d, self._dims, self._sizes, idx_p, ptr_p,
+                         C.cast(vals.ctypes.data + 8 * lo[d - 1], N.c_dbl_p))
+        h = C.c_void_p()
+        fn = lib.spttn_csf_create_async if async_values else lib.spttn_csf_create
+        _check(fn(C.byref(host), _stream_ptr(stream), C.byref(h)))
+        self.handle = h
+        self._keep = [arrs, vals] if async_values else None
+        self.leaf_range = (lo[d - 1], hi[d - 1])
+        return self
+
+    @classmethod
     def from_coo(cls, dims, coords: np.ndarray, values: np.ndarray, stream=None) -> "DeviceCsf":
         """spttn_csf_from_coo: normalize + build_csf on the GPU (rows in CSF
         mode order, nnz x order int64); the host Csf is not materialised."""
@@ -282,3 +315,67 @@ class Plan:
             self.close()
         except Exception:
             pass
+
+
+def execute_streamed(kind: int, csf: Csf, factors, ranks, out: np.ndarray, chunks: int = 4,
+                     flags: int = 0) -> np.ndarray:
+    """One fused nest end to end from HOST memory, streamed: the root slices
+    are cut into `chunks` nnz-balanced ranges (zero-copy views of csf's
+    arrays), and each range's H2D upload, device layout, plan, execute and
+    output read-back run on its own stream and host thread, so the transfer
+    of range c+1 overlaps range c's plan build and kernel and the D2H of its
+    rows (PCIe is full duplex). Root-indexed outputs: range c owns the rows
+    from its first root coordinate up to the next range's; sparse outputs:
+    its leaf range. `out` (ideally pinned) receives the result."""
+    import threading
+
+    import torch
+    from . import distributed as D
+    fac = [torch.from_numpy(np.ascontiguousarray(f, np.float64)) for f in factors]
+    s0 = torch.cuda.Stream()
+    with torch.cuda.stream(s0):
+        dfac = [t.to("cuda", non_blocking=True) for t in fac]
+    s0.synchronize()
+    parts = D.partition_roots(csf, max(1, chunks))
+    parts = [p for p in parts if p[1] > p[0]] or [(0, 0)]
+    sparse = kind == NEST_TTTP3
+    tile = 1
+    for r in ranks:
+        tile *= max(1, int(r))
+    rows0 = csf.dims[0]
+    out_t = torch.from_numpy(out)
+    errors = []
+
+    def run(ci):
+        try:
+            r0, r1 = parts[ci]
+            st = torch.cuda.Stream()
+            dev = DeviceCsf.from_root_range(csf, r0, r1, stream=st, async_values=True)
+            plan = Plan(kind, dev, [t.data_ptr() for t in dfac], ranks=ranks, flags=flags,
+                        stream=st, on_device=True, factor_sizes=[t.numel() for t in dfac])
+            plan.execute(st)
+            if sparse:
+                a, b = dev.leaf_range
+            else:
+                a = 0 if ci == 0 else int(csf.idx[0][r0])
+                b = rows0 if ci + 1 == len(parts) else int(csf.idx[0][parts[ci + 1][0]])
+                a, b = a * tile, b * tile
+            if b > a:
+                with torch.cuda.stream(st):
+                    out_t[a:b].copy_(plan.output_tensor()[a - (dev.leaf_range[0] if sparse else 0):
+                                                          b - (dev.leaf_range[0] if sparse else 0)],
+                                     non_blocking=True)
+            st.synchronize()
+            plan.close()
+            dev.close()
+        except Exception as e:  # noqa: BLE001
+            errors.append(e)
+
+    threads = [threading.Thread(target=run, args=(ci,)) for ci in range(len(parts))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errors:
+        raise errors[0]
+    return out

@@ -12,11 +12,11 @@ from parity import assert_parity, oracle_with_norm
 pytestmark = pytest.mark.gpu
 
 RANKS = [1, 2, 3, 4, 5, 7, 8, 12, 16, 17, 24, 31, 32, 33, 48, 64, 100, 128]
-VARIANT_ENV = {1: ("SPTTN_MTTKRP_MODE", ["0", "1", "2", "3", "4"]),
-               4: ("SPTTN_MTTKRP_MODE", ["0", "1", "2", "3"]),
-               2: ("SPTTN_TTMC3_MODE", ["0", "4", "6", "7", "10"]),
-               5: ("SPTTN_TTMC4_MODE", ["0", "1", "2", "3", "4"]),
-               3: ("SPTTN_TTTP_MODE", ["0", "1", "2"])}
+VARIANT_ENV = {1: ("SPTTN_MTTKRP_MODE", ["0", "2", "3", "4"]),
+               4: ("SPTTN_MTTKRP_MODE", ["0", "3"]),
+               2: ("SPTTN_GROUP_OVERHEAD", ["0", "12"]),
+               5: ("SPTTN_TTMC4_MODE", ["3", "4"]),
+               3: ("SPTTN_TTTP_PIECE", ["1", "5", "64"])}
 
 
 @pytest.fixture(scope="module")
@@ -76,7 +76,7 @@ def _case(seed):
     # stream: the original draws above stay unchanged)
     r2 = np.random.default_rng(5000 + seed)
     item_mode = {1: ("SPTTN_MTTKRP_MODE", "3"), 4: ("SPTTN_MTTKRP_MODE", "3"),
-                 2: ("SPTTN_TTMC3_MODE", "10"), 5: ("SPTTN_TTMC4_MODE", "4")}
+                 2: ("SPTTN_TTMC3_MODE", "10"), 5: ("SPTTN_TTMC4_MODE", "4")}  # TTMc-3: one kernel, env unused
     if kind in item_mode and (env.get(item_mode[kind][0], item_mode[kind][1]) == item_mode[kind][1]
                               or seed >= 160):
         env[item_mode[kind][0]] = item_mode[kind][1]

@@ -91,11 +91,10 @@ def test_partition_independence(E, name, chunk, monkeypatch):
         assert plan.info()["split_slices"] > 0
 
 
-VARIANTS = [("SPTTN_TTMC3_MODE", m, ["ttmc3_small", "ttmc3_r16"]) for m in ("0", "4", "6", "7", "10", "11")] + \
-    [("SPTTN_MTTKRP_MODE", m, ["mttkrp3_small", "mttkrp3_r32", "mttkrp4_small", "mttkrp4_r32"])
-     for m in ("0", "1", "2", "3", "4")] + \
-    [("SPTTN_TTTP_MODE", m, ["tttp3_small", "tttp3_r64"]) for m in ("0", "1", "2")] + \
-    [("SPTTN_TTMC4_MODE", m, ["ttmc4_small", "ttmc4_r8"]) for m in ("0", "1", "2", "3", "4")] + \
+VARIANTS = [("SPTTN_MTTKRP_MODE", m, ["mttkrp3_small", "mttkrp3_r32", "mttkrp4_small", "mttkrp4_r32"])
+            for m in ("0", "2", "3", "4")] + \
+    [("SPTTN_TTTP_BATCH", m, ["tttp3_small", "tttp3_r64"]) for m in ("2", "4", "8")] + \
+    [("SPTTN_TTMC4_MODE", m, ["ttmc4_small", "ttmc4_r8"]) for m in ("3", "4")] + \
     [("SPTTN_NONROOT_MODE", m, ["mttkrp3j_small", "mttkrp3j_r32", "mttkrp3k_small", "mttkrp3k_r32"])
      for m in ("0", "4")]
 
@@ -112,9 +111,8 @@ def test_kernel_variants_agree(E, env, mode, names, monkeypatch):
         out, _, _ = run(E, m["kind"], csf, factors, m["ranks"])
         _, norm = oracle_with_norm(m["kind"], csf, factors, m["ranks"])
         assert_parity(out, z["fused"], norm, f"{name} {env}={mode}")
-    key = {"SPTTN_TTMC3_MODE": "ttmc3", "SPTTN_MTTKRP_MODE": "mttkrp4",
-           "SPTTN_TTTP_MODE": "tttp3", "SPTTN_TTMC4_MODE": "ttmc4",
-           "SPTTN_NONROOT_MODE": "mttkrp3_k"}[env]
+    key = {"SPTTN_MTTKRP_MODE": "mttkrp4", "SPTTN_TTTP_BATCH": "tttp3",
+           "SPTTN_TTMC4_MODE": "ttmc4", "SPTTN_NONROOT_MODE": "mttkrp3_k"}[env]
     w = make_workload(key, scale=2e-3)
     c = w.cfg
     out, _, _ = run(E, c.kind, w.csf, w.factors, c.ranks, E.FLAG_RESIDUAL if c.residual else 0)
@@ -449,18 +447,19 @@ def test_mttkrp3_shared_factor_kernel(E, R, force, skew, monkeypatch):
     assert np.array_equal(plan.read_output(), out)
 
 
-def test_tttp_bucketed_layout_skew_and_residual(E, monkeypatch):
-    """TTTP mode 2 (leaves grouped by (i range, C-row bucket), 4-padded
-    runs, C rows in shared memory): a k-skewed pattern forced through it and
-    the residual flag, against the oracle; re-execution bit-identical."""
+@pytest.mark.parametrize("piece", ["1", "7", "64", "1000"])
+def test_tttp_slice_pieces_skew_and_residual(E, piece, monkeypatch):
+    """TTTP slice pieces (A[i] once per piece): a root-skewed pattern (one
+    slice with a quarter of the leaves, many 1-leaf slices) at several piece
+    sizes, with and without the residual flag, against the oracle;
+    re-execution bit-identical."""
     from paper_2307_05740_b200.tensor import Csf
-    monkeypatch.setenv("SPTTN_TTTP_MODE", "2")
-    monkeypatch.setenv("SPTTN_TTTP_KB_FORCE", "1")
+    monkeypatch.setenv("SPTTN_TTTP_PIECE", piece)
     rng = np.random.default_rng(7)
-    dims = (300, 200, 3000)
+    dims = (3000, 200, 300)
     nnz = 50000
     coords = np.stack([rng.integers(0, d, nnz) for d in dims], axis=1)
-    coords[: nnz // 4, 2] = 17  # one hot C row
+    coords[: nnz // 4, 0] = 17  # one hot root slice
     vals = rng.uniform(-1, 1, nnz)
     csf = Csf.from_coo(list(dims), coords, vals)
     R = 64
@@ -468,7 +467,7 @@ def test_tttp_bucketed_layout_skew_and_residual(E, monkeypatch):
     for flags, residual in ((0, False), (E.FLAG_RESIDUAL, True)):
         out, plan, _ = run(E, 3, csf, fs, (R, 0, 0), flags)
         want, norm = oracle_with_norm(3, csf, fs, (R, 0, 0), residual=residual)
-        assert_parity(out, want, norm, f"tttp bucketed residual={residual}")
+        assert_parity(out, want, norm, f"tttp pieces P={piece} residual={residual}")
         plan.execute()
         assert np.array_equal(plan.read_output(), out)
 
@@ -513,3 +512,35 @@ def test_async_value_upload(E, key):
     assert np.array_equal(back.values, w.csf.values)
     ref, _, _ = run(E, c.kind, w.csf, w.factors, c.ranks, flags)
     assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("key", ["mttkrp3", "ttmc3", "tttp3", "mttkrp4", "ttmc4"])
+@pytest.mark.parametrize("chunks", [1, 3, 8])
+def test_streamed_execute_from_host(E, key, chunks):
+    """execute_streamed: root-slice ranges as zero-copy views of the host CSF
+    (rebased child pointers), one stream + plan per range, rows / leaves of
+    each range read back into the host output."""
+    from paper_2307_05740_b200.configs import make_workload
+    w = make_workload(key, scale=2e-3)
+    c = w.cfg
+    flags = E.FLAG_RESIDUAL if c.residual else 0
+    out = np.full(w.out_count, np.nan)
+    E.execute_streamed(c.kind, w.csf, w.factors, c.ranks, out, chunks=chunks, flags=flags)
+    want, norm = oracle_with_norm(c.kind, w.csf, w.factors, c.ranks, residual=c.residual)
+    assert_parity(out, want, norm, f"{key} streamed x{chunks}")
+
+
+def test_csf_view_rebased(E):
+    """A root range passed as a view (ptr[l][0] != 0) downloads as the same
+    tree as an explicitly rebased copy."""
+    from paper_2307_05740_b200 import distributed as D
+    from paper_2307_05740_b200.configs import make_workload
+    w = make_workload("mttkrp4", scale=1e-3)
+    n0 = w.csf.level_sizes()[0]
+    r0, r1 = n0 // 3, 2 * n0 // 3
+    dev = E.DeviceCsf.from_root_range(w.csf, r0, r1)
+    got = dev.download()
+    ref = D.shard_csf(w.csf, r0, r1)
+    for a, b in zip(got.idx + got.ptr, ref.idx + ref.ptr):
+        assert np.array_equal(a, b)
+    assert np.array_equal(got.values, ref.values)

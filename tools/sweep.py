@@ -1,6 +1,6 @@
 """Kernel-variant sweep on one workload (development tool, not the bench).
 
-    python tools/sweep.py ttmc3 'SPTTN_TTMC3_MODE=0,SPTTN_SEG_LEN=4' 'SPTTN_TTMC3_MODE=1' ...
+    python tools/sweep.py ttmc3 'SPTTN_GROUP_OVERHEAD=6' 'SPTTN_GROUP_OVERHEAD=12' ...
 
 Generates the BASELINE workload once, then for each variant (env settings
 read at plan creation) times the fused-nest kernel with CUDA events, L2
