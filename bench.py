@@ -287,19 +287,6 @@ def e2e_config(P, w, steps, stream):
             times.append(t1 - t0)
             parts.append((ta - t0, tb - ta, t1 - tb))
     brk = [statistics.mean(p[i] for p in parts) * 1e3 for i in range(3)]
-    # streamed through the public API (engine.execute_streamed): root-slice
-    # ranges uploaded, planned, executed and read back on their own streams
-    # so the H2D of one range overlaps the compute and D2H of the previous
-    chunks = int(os.environ.get("SPTTN_E2E_CHUNKS", "4"))
-    streamed = []
-    for it in range(steps + 1):
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        P.execute_streamed(c.kind, host, [t.numpy() for t in pin_fac], c.ranks, out.numpy(),
-                           chunks=chunks, flags=P.FLAG_RESIDUAL if c.residual else 0)
-        t1 = time.perf_counter()
-        if it > 0:
-            streamed.append(t1 - t0)
     # the solver-loop case (CP-ALS / HOOI sweep): one plan reused, each step
     # uploads the step's factors from pinned memory, executes and reads the
     # output back (spttn_plan_set_factors + spttn_execute + spttn_read_output)
@@ -319,13 +306,9 @@ def e2e_config(P, w, steps, stream):
             als.append(t1 - t0)
     plan.close()
     dev.close()
-    single = statistics.mean(times)
-    stream_s = statistics.mean(streamed)
-    return {"seconds": min(single, stream_s), "h2d_bytes_per_step": int(h2d),
+    return {"seconds": statistics.mean(times), "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h),
-            "path": (f"execute_streamed ({chunks} root-slice ranges)" if stream_s < single
-                     else "DeviceCsf(async) + Plan + execute + read_output"),
-            "single_plan_ms": single * 1e3, "streamed_ms": stream_s * 1e3,
+            "path": "factors H2D, DeviceCsf (async values) + Plan + execute + read_output",
             "breakdown_ms": {"csf_h2d_layout": brk[0], "plan_h2d_decomp": brk[1],
                              "execute_d2h": brk[2]},
             "als_loop": {"seconds": statistics.mean(als), "h2d_bytes_per_step": int(fac_bytes),
@@ -627,8 +610,7 @@ def main():
             r["e2e"] = {"value": job_nnz / secs, "unit": "nnz/s",
                         "h2d_bytes_per_step": e["h2d_bytes_per_step"],
                         "d2h_bytes_per_step": e["d2h_bytes_per_step"], "ms_per_step": secs * 1e3,
-                        "path": e["path"], "single_plan_ms": e["single_plan_ms"],
-                        "streamed_ms": e["streamed_ms"],
+                        "path": e["path"],
                         "breakdown_ms": e["breakdown_ms"],
                         "als_loop": {"value": job_nnz / e["als_loop"]["seconds"], "unit": "nnz/s",
                                      "ms_per_step": e["als_loop"]["seconds"] * 1e3,

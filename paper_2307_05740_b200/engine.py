@@ -316,66 +316,3 @@ class Plan:
         except Exception:
             pass
 
-
-def execute_streamed(kind: int, csf: Csf, factors, ranks, out: np.ndarray, chunks: int = 4,
-                     flags: int = 0) -> np.ndarray:
-    """One fused nest end to end from HOST memory, streamed: the root slices
-    are cut into `chunks` nnz-balanced ranges (zero-copy views of csf's
-    arrays), and each range's H2D upload, device layout, plan, execute and
-    output read-back run on its own stream and host thread, so the transfer
-    of range c+1 overlaps range c's plan build and kernel and the D2H of its
-    rows (PCIe is full duplex). Root-indexed outputs: range c owns the rows
-    from its first root coordinate up to the next range's; sparse outputs:
-    its leaf range. `out` (ideally pinned) receives the result."""
-    import threading
-
-    import torch
-    from . import distributed as D
-    fac = [torch.from_numpy(np.ascontiguousarray(f, np.float64)) for f in factors]
-    s0 = torch.cuda.Stream()
-    with torch.cuda.stream(s0):
-        dfac = [t.to("cuda", non_blocking=True) for t in fac]
-    s0.synchronize()
-    parts = D.partition_roots(csf, max(1, chunks))
-    parts = [p for p in parts if p[1] > p[0]] or [(0, 0)]
-    sparse = kind == NEST_TTTP3
-    tile = 1
-    for r in ranks:
-        tile *= max(1, int(r))
-    rows0 = csf.dims[0]
-    out_t = torch.from_numpy(out)
-    errors = []
-
-    def run(ci):
-        try:
-            r0, r1 = parts[ci]
-            st = torch.cuda.Stream()
-            dev = DeviceCsf.from_root_range(csf, r0, r1, stream=st, async_values=True)
-            plan = Plan(kind, dev, [t.data_ptr() for t in dfac], ranks=ranks, flags=flags,
-                        stream=st, on_device=True, factor_sizes=[t.numel() for t in dfac])
-            plan.execute(st)
-            if sparse:
-                a, b = dev.leaf_range
-            else:
-                a = 0 if ci == 0 else int(csf.idx[0][r0])
-                b = rows0 if ci + 1 == len(parts) else int(csf.idx[0][parts[ci + 1][0]])
-                a, b = a * tile, b * tile
-            if b > a:
-                with torch.cuda.stream(st):
-                    out_t[a:b].copy_(plan.output_tensor()[a - (dev.leaf_range[0] if sparse else 0):
-                                                          b - (dev.leaf_range[0] if sparse else 0)],
-                                     non_blocking=True)
-            st.synchronize()
-            plan.close()
-            dev.close()
-        except Exception as e:  # noqa: BLE001
-            errors.append(e)
-
-    threads = [threading.Thread(target=run, args=(ci,)) for ci in range(len(parts))]
-    for t in threads:
-        t.start()
-    for t in threads:
-        t.join()
-    if errors:
-        raise errors[0]
-    return out

@@ -514,22 +514,6 @@ def test_async_value_upload(E, key):
     assert np.array_equal(got, ref)
 
 
-@pytest.mark.parametrize("key", ["mttkrp3", "ttmc3", "tttp3", "mttkrp4", "ttmc4"])
-@pytest.mark.parametrize("chunks", [1, 3, 8])
-def test_streamed_execute_from_host(E, key, chunks):
-    """execute_streamed: root-slice ranges as zero-copy views of the host CSF
-    (rebased child pointers), one stream + plan per range, rows / leaves of
-    each range read back into the host output."""
-    from paper_2307_05740_b200.configs import make_workload
-    w = make_workload(key, scale=2e-3)
-    c = w.cfg
-    flags = E.FLAG_RESIDUAL if c.residual else 0
-    out = np.full(w.out_count, np.nan)
-    E.execute_streamed(c.kind, w.csf, w.factors, c.ranks, out, chunks=chunks, flags=flags)
-    want, norm = oracle_with_norm(c.kind, w.csf, w.factors, c.ranks, residual=c.residual)
-    assert_parity(out, want, norm, f"{key} streamed x{chunks}")
-
-
 def test_csf_view_rebased(E):
     """A root range passed as a view (ptr[l][0] != 0) downloads as the same
     tree as an explicitly rebased copy."""
