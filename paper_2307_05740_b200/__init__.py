@@ -9,11 +9,12 @@ This package is the Python view of the same engine (tests, bench.py).
 from .engine import (FLAG_FACTORS_ON_DEVICE, FLAG_RESIDUAL, NEST_GENERIC, NEST_MTTKRP3,
                      NEST_MTTKRP3_J, NEST_MTTKRP3_K, NEST_MTTKRP4, NEST_TTMC3, NEST_TTMC4,
                      NEST_TTTP3, DeviceCsf, Plan,
-                     ResourceError, UnsupportedOrderError, device_info, release_cached)
+                     ResourceError, UnsupportedOrderError, device_info, release_cached,
+                     unfactorized)
 from .tensor import Csf, gen_dense, gen_normal, stable_hash
 
 __all__ = [
-    "Csf", "DeviceCsf", "Plan", "device_info", "release_cached", "gen_dense", "gen_normal", "stable_hash",
+    "Csf", "DeviceCsf", "Plan", "device_info", "release_cached", "unfactorized", "gen_dense", "gen_normal", "stable_hash",
     "NEST_MTTKRP3", "NEST_TTMC3", "NEST_TTTP3", "NEST_MTTKRP4", "NEST_TTMC4", "NEST_GENERIC",
     "NEST_MTTKRP3_J", "NEST_MTTKRP3_K",
     "FLAG_RESIDUAL", "FLAG_FACTORS_ON_DEVICE", "UnsupportedOrderError", "ResourceError",

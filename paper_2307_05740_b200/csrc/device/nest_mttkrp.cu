@@ -15,6 +15,8 @@
 // A_i += (X*C[k])*B[j], the same sum regrouped); a finished slice is reduced
 // over the slots with shuffles and written once (owner computes), and slices
 // cut by item boundaries go through the deterministic HEAD/TAIL fix-up.
+#include <type_traits>
+
 #include "internal.cuh"
 
 namespace spttn_dev {
@@ -252,14 +254,6 @@ __global__ void __launch_bounds__(kBlock, 3) k_mttkrp_pq(RootOutArgs a) {
       const int32_t u = S.node[mb][(g - g0) * kMSlots + slot];
       const int32_t j = ORDER == 4 ? S.node1[mb][(g - g0) * kMSlots + slot] : 0;
       const int32_t lbase = hh.x - L0 + slot;
-      int32_t kk[4];
-      double tt[4];
-#pragma unroll
-      for (int it = 0; it < 4; ++it) {
-        const bool on = it < n;
-        kk[it] = on ? S.kk[lbf][lbase + it * kMSlots] : 0;
-        tt[it] = on ? S.tv[lbf][lbase + it * kMSlots] : 0.0;
-      }
       const double4 ur = rowq(Funit, u, true);
       double4 tr = make_double4(0, 0, 0, 0);
       if (ORDER == 4) {
@@ -271,12 +265,31 @@ __global__ void __launch_bounds__(kBlock, 3) k_mttkrp_pq(RootOutArgs a) {
         prev_j = j;
         tr = brow;
       }
-      double4 rr[4];
-#pragma unroll
-      for (int it = 0; it < 4; ++it) rr[it] = rowq(Fleaf, kk[it], it < n);
+      // X += t * F_leaf[k] over the group's n (warp-uniform) leaf steps: the
+      // body is specialised per n, so no predicated-off stream loads, row
+      // gathers or FMAs are issued for short segments (most have 1 leaf)
       double4 X = make_double4(0, 0, 0, 0);
+      auto steps = [&](auto NS) {
+        constexpr int kN = decltype(NS)::value;
+        int32_t kk[kN];
+        double tt[kN];
 #pragma unroll
-      for (int it = 0; it < 4; ++it) fma4(X, tt[it], rr[it]);  // X += t * F_leaf[k]
+        for (int it = 0; it < kN; ++it) {
+          kk[it] = S.kk[lbf][lbase + it * kMSlots];
+          tt[it] = S.tv[lbf][lbase + it * kMSlots];
+        }
+        double4 rr[kN];
+#pragma unroll
+        for (int it = 0; it < kN; ++it) rr[it] = rowq(Fleaf, kk[it], true);
+#pragma unroll
+        for (int it = 0; it < kN; ++it) fma4(X, tt[it], rr[it]);
+      };
+      switch (n) {
+        case 1: steps(std::integral_constant<int, 1>{}); break;
+        case 2: steps(std::integral_constant<int, 2>{}); break;
+        case 3: steps(std::integral_constant<int, 3>{}); break;
+        default: steps(std::integral_constant<int, 4>{}); break;
+      }
       if (ORDER == 3) {
         fma4v(acc, X, ur);  // A[i] += X * B[j]
       } else {

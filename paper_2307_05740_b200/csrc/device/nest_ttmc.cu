@@ -21,6 +21,7 @@
 // columns are interleaved (r = 2h+mt, s = 2(2q+e)+nt for TTMc-3) so every
 // factor-row gather is one 16-byte load per lane, 8 lanes per 128-byte row.
 #include <cstdlib>
+#include <type_traits>
 
 #include "internal.cuh"
 
@@ -178,27 +179,36 @@ __global__ void __launch_bounds__(kBlock, 3) k_ttmc3pq(RootOutArgs a) {
       const int n = hh.y;  // warp-uniform
       const int32_t lbase = hh.x - L0 + gs;
       const int32_t j = S.node[mb][(g - g0) * kPackSlots + gs];
-      int32_t kk[4];
-      double tt[4];
-#pragma unroll
-      for (int it = 0; it < 4; ++it) {
-        kk[it] = it < n ? S.kk[lbf][lbase + it * kPackSlots] : 0;
-        tt[it] = it < n ? S.tv[lbf][lbase + it * kPackSlots] : 0.0;
-      }
       const double4 ur = row4<VECU>(U + static_cast<int64_t>(j) * R, 4 * gc, R);
-      double4 vr[4];
-#pragma unroll
-      for (int it = 0; it < 4; ++it) {
-        if (VECV) {
-          vr[it] = ld256_if(V + static_cast<int64_t>(kk[it]) * S_ + 4 * gc, it < n && 4 * gc < S_);
-        } else {
-          vr[it] = it < n ? row4<false>(V + static_cast<int64_t>(kk[it]) * S_, 4 * gc, S_)
-                          : make_double4(0, 0, 0, 0);
-        }
-      }
+      // X[s] += t * V[k,s] over the group's n (warp-uniform) leaf steps,
+      // specialised per n: no predicated-off stream loads / gathers / FMAs
       double4 x = make_double4(0, 0, 0, 0);
+      auto steps = [&](auto NS) {
+        constexpr int kN = decltype(NS)::value;
+        int32_t kk[kN];
+        double tt[kN];
 #pragma unroll
-      for (int it = 0; it < 4; ++it) fma4(x, tt[it], vr[it]);  // X[s] += t * V[k,s]
+        for (int it = 0; it < kN; ++it) {
+          kk[it] = S.kk[lbf][lbase + it * kPackSlots];
+          tt[it] = S.tv[lbf][lbase + it * kPackSlots];
+        }
+        double4 vr[kN];
+#pragma unroll
+        for (int it = 0; it < kN; ++it) {
+          if (VECV)
+            vr[it] = ld256_if(V + static_cast<int64_t>(kk[it]) * S_ + 4 * gc, 4 * gc < S_);
+          else
+            vr[it] = row4<false>(V + static_cast<int64_t>(kk[it]) * S_, 4 * gc, S_);
+        }
+#pragma unroll
+        for (int it = 0; it < kN; ++it) fma4(x, tt[it], vr[it]);
+      };
+      switch (n) {
+        case 1: steps(std::integral_constant<int, 1>{}); break;
+        case 2: steps(std::integral_constant<int, 2>{}); break;
+        case 3: steps(std::integral_constant<int, 3>{}); break;
+        default: steps(std::integral_constant<int, 4>{}); break;
+      }
       // transpose X and U quads into fragment layout through the tile
       double* xs = Q.xs[par];
       double* us = Q.us[par];

@@ -316,3 +316,66 @@ class Plan:
         except Exception:
             pass
 
+
+
+def _parse_kernel(text: str):
+    """Index ids of a kernel-spec string the way the reference's parse_kernel
+    assigns them (first appearance over the inputs, proj/src/kernel_spec.cpp:
+    103-156): returns ([(name, [index names])...] inputs, output names,
+    sparse_out)."""
+    body = text.replace(" ", "")
+    sparse_out = body.endswith("@sparse_out")
+    if sparse_out:
+        body = body[: -len("@sparse_out")]
+    lhs, rhs = body.split("->")
+
+    def tensor(tok):
+        name, rest = tok.split("[")
+        return name, [x for x in rest.rstrip("]").split(",") if x]
+    return [tensor(t) for t in lhs.split("*")], tensor(rhs)[1], sparse_out
+
+
+def unfactorized(kernel: str, dims: dict, csf: DeviceCsf, factors, stream=None) -> np.ndarray:
+    """spttn_unfactorized: the reference's execute_unfactorized oracle nest
+    (executor.cpp:522-626) on the device for a kernel-spec string, factors in
+    kernel input order (host arrays, row-major). Same descriptor the C++
+    drop-in builds; bit-identical to the reference."""
+    lib = N.engine()
+    inputs, out_idx, sparse_out = _parse_kernel(kernel)
+    names = []
+    for _, ix in inputs:
+        for n in ix:
+            if n not in names:
+                names.append(n)
+    d = N.UnfactDesc()
+    d.num_indices = len(names)
+    sparse = inputs[0][1]
+    for k, n in enumerate(names):
+        d.dims[k] = int(dims[n])
+        d.csf_level[k] = sparse.index(n) if n in sparse else -1
+    free = [n for _, ix in inputs for n in ix if n not in sparse]
+    free = list(dict.fromkeys(free))  # first appearance (executor.cpp:530-537)
+    d.num_free = len(free)
+    for q, n in enumerate(free):
+        d.free_ids[q] = names.index(n)
+    d.num_factors = len(inputs) - 1
+    keep = []
+    for f, (_, ix) in enumerate(inputs[1:]):
+        d.factor_order[f] = len(ix)
+        for k, n in enumerate(ix):
+            d.factor_ids[f][k] = names.index(n)
+        a = np.ascontiguousarray(factors[f], np.float64).ravel()
+        keep.append(a)
+        d.factors[f] = a.ctypes.data_as(N.c_dbl_p)
+    d.out_sparse = 1 if sparse_out else 0
+    d.out_order = len(out_idx)
+    for k, n in enumerate(out_idx):
+        d.out_ids[k] = names.index(n)
+    if sparse_out:
+        count = csf.level_sizes()[-1]
+    else:
+        count = int(np.prod([int(dims[n]) for n in out_idx])) if out_idx else 1
+    out = np.empty(count, np.float64)
+    _check(lib.spttn_unfactorized(C.byref(d), csf.handle, out.ctypes.data_as(N.c_dbl_p), count,
+                                  _stream_ptr(stream)))
+    return out

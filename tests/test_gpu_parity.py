@@ -528,3 +528,14 @@ def test_csf_view_rebased(E):
     for a, b in zip(got.idx + got.ptr, ref.idx + ref.ptr):
         assert np.array_equal(a, b)
     assert np.array_equal(got.values, ref.values)
+
+
+@pytest.mark.parametrize("m", CASES, ids=[m["name"] for m in CASES])
+def test_device_unfactorized_equals_reference_golden(E, m):
+    """spttn_unfactorized (the device execute_unfactorized) against the
+    golden arrays the reference's own execute_unfactorized produced
+    (tests/golden/make_golden.py): bit for bit."""
+    csf, factors, z = load_case(m)
+    dev = E.DeviceCsf(csf)
+    got = E.unfactorized(m["kernel"], m["dims"], dev, factors)
+    assert np.array_equal(got, z["unfactorized"]), np.abs(got - z["unfactorized"]).max()

@@ -49,7 +49,12 @@ def main():
                                           "sass"))))
     if len(src) > 2:
         h = src[1]
-        data = [dict(zip(h, r)) for r in src[2:]]
+        # one kernel's rows only (a second kernel's table starts with a new header)
+        data = []
+        for r in src[2:]:
+            if len(r) != len(h) or r[:2] == h[:2]:
+                break
+            data.append(dict(zip(h, r)))
 
         def f(x):
             try:
@@ -57,11 +62,11 @@ def main():
             except ValueError:
                 return 0.0
         stalls = [c for c in h if c.startswith("stall_") and "Not Issued" not in c]
-        agg = {s: sum(f(x[s]) for x in data) for s in stalls}
+        agg = {s: sum(f(x.get(s, "0")) for x in data) for s in stalls}
         tot = sum(agg.values()) or 1
         print("stall breakdown:", ", ".join(f"{k[6:]} {100 * v / tot:.1f}%" for k, v in
                                             sorted(agg.items(), key=lambda kv: -kv[1])[:8]))
-        top = sorted(data, key=lambda x: -f(x["Warp Stall Sampling (All Samples)"]))[:12]
+        top = sorted(data, key=lambda x: -f(x.get("Warp Stall Sampling (All Samples)", "0")))[:12]
         print("hottest SASS (samples, executions, instruction):")
         for x in top:
             print(f"  {x['Warp Stall Sampling (All Samples)']:>6} {x['Instructions Executed']:>10}  "
