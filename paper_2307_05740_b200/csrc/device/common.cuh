@@ -38,6 +38,16 @@ __device__ __forceinline__ double4 ld256(const double* p) {
 // Predicated 256-bit load without a branch: the load is issued (or not) in
 // straight-line code, so several gathers stay in flight together; inactive
 // lanes / iterations read as zero.
+// Predicated 256-bit load into existing registers: when pred is false the
+// destination keeps its value (no zero fill, no select) — row reuse.
+__device__ __forceinline__ void ld256_keep(double4& v, const double* p, bool pred) {
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.b32 q, %5, 0;\n"
+      " @q ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];\n}\n"
+      : "+d"(v.x), "+d"(v.y), "+d"(v.z), "+d"(v.w)
+      : "l"(p), "r"(static_cast<int>(pred)));
+}
+
 __device__ __forceinline__ double4 ld256_if(const double* p, bool pred) {
   double4 v;
   asm volatile(

@@ -147,7 +147,9 @@ struct StageM {
   uint64_t mbar_leaf[2];
 };
 
-template <int ORDER, bool VEC>
+// RC = compile-time rank (32 at the BASELINE shapes: full 256-byte rows over
+// 8 lanes, constant row strides, no column predicates) or 0 = a.R at run time
+template <int ORDER, bool VEC, int RC = 0>
 __global__ void __launch_bounds__(kBlock, 3) k_mttkrp_pq(RootOutArgs a) {
   grid_launch_dependents();
   __shared__ StageM stage[kBlock / 32];
@@ -157,7 +159,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_mttkrp_pq(RootOutArgs a) {
   const int lane = threadIdx.x & 31;
   const int slot = lane >> 3;
   const int c = (lane & 7) * 4;
-  const int R = a.R;
+  const int R = RC > 0 ? RC : a.R;
   const CsfView& t = a.t;
   const double* __restrict__ Fleaf = a.f[ORDER - 1];
   const double* __restrict__ Funit = a.f[ORDER - 2];
@@ -180,7 +182,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_mttkrp_pq(RootOutArgs a) {
   int32_t prev_j = -1;
   double4 brow = make_double4(0, 0, 0, 0);
   double4 acc = make_double4(0, 0, 0, 0);
-  const bool colok = c < R;
+  const bool colok = RC > 0 ? true : c < R;
 
   auto flush = [&](int dslot) {
     double v[4] = {acc.x, acc.y, acc.z, acc.w};
@@ -197,6 +199,8 @@ __global__ void __launch_bounds__(kBlock, 3) k_mttkrp_pq(RootOutArgs a) {
     acc = make_double4(0, 0, 0, 0);
   };
   auto rowq = [&](const double* base, int32_t r, bool pred) {
+    // full rows (RC > 0): every lane's quad is in range, no zero-fill / predicate
+    if (VEC && RC > 0) return ld256(base + static_cast<int64_t>(r) * R + c);
     if (VEC) return ld256_if(base + static_cast<int64_t>(r) * R + c, pred && colok);
     return pred ? row4<false>(base + static_cast<int64_t>(r) * R, c, R) : make_double4(0, 0, 0, 0);
   };
@@ -258,10 +262,11 @@ __global__ void __launch_bounds__(kBlock, 3) k_mttkrp_pq(RootOutArgs a) {
       double4 tr = make_double4(0, 0, 0, 0);
       if (ORDER == 4) {
         const bool fresh = j != prev_j;
-        const double4 ld = VEC ? ld256_if(Ftop + static_cast<int64_t>(j) * R + c, fresh && colok)
-                               : (fresh ? row4<false>(Ftop + static_cast<int64_t>(j) * R, c, R)
-                                        : brow);
-        brow = fresh ? ld : brow;
+        if (VEC) {  // reload only for a new fiber; otherwise the registers keep B[j]
+          ld256_keep(brow, Ftop + static_cast<int64_t>(j) * R + c, fresh && colok);
+        } else if (fresh) {
+          brow = row4<false>(Ftop + static_cast<int64_t>(j) * R, c, R);
+        }
         prev_j = j;
         tr = brow;
       }
@@ -281,8 +286,10 @@ __global__ void __launch_bounds__(kBlock, 3) k_mttkrp_pq(RootOutArgs a) {
         double4 rr[kN];
 #pragma unroll
         for (int it = 0; it < kN; ++it) rr[it] = rowq(Fleaf, kk[it], true);
+        // first step as a product (= fma with a zero addend, bit for bit)
+        X = make_double4(tt[0] * rr[0].x, tt[0] * rr[0].y, tt[0] * rr[0].z, tt[0] * rr[0].w);
 #pragma unroll
-        for (int it = 0; it < kN; ++it) fma4(X, tt[it], rr[it]);
+        for (int it = 1; it < kN; ++it) fma4(X, tt[it], rr[it]);
       };
       switch (n) {
         case 1: steps(std::integral_constant<int, 1>{}); break;
@@ -325,7 +332,8 @@ void launch_mttkrp_pq(const RootOutArgs& a, int order, cudaStream_t s) {
     if (a.vec) k_mttkrp_pq<3, true><<<b, kBlock, 0, s>>>(a);
     else k_mttkrp_pq<3, false><<<b, kBlock, 0, s>>>(a);
   } else {
-    if (a.vec) k_mttkrp_pq<4, true><<<b, kBlock, 0, s>>>(a);
+    if (a.vec && a.R == 32) k_mttkrp_pq<4, true, 32><<<b, kBlock, 0, s>>>(a);
+    else if (a.vec) k_mttkrp_pq<4, true><<<b, kBlock, 0, s>>>(a);
     else k_mttkrp_pq<4, false><<<b, kBlock, 0, s>>>(a);
   }
   SPTTN_CUDA(cudaGetLastError());
