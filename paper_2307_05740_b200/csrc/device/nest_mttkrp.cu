@@ -15,6 +15,7 @@
 // A_i += (X*C[k])*B[j], the same sum regrouped); a finished slice is reduced
 // over the slots with shuffles and written once (owner computes), and slices
 // cut by item boundaries go through the deterministic HEAD/TAIL fix-up.
+#include <cstdlib>
 #include <type_traits>
 
 #include "internal.cuh"
