@@ -101,9 +101,10 @@ int main(int argc, char** argv) {
       {"TTTP-3 R64", "tttp3", {40, 30, 20, 64}, 0.1, 9},
       {"TTMc-4 R8", "ttmc4", {16, 8, 8, 8}, 0.05, 10},
       {"TTTc-4 N20 (JIT)", "tttc4", {20, 2}, 0.45, 11},
+      {"TTTc-6 N7 (JIT)", "tttc6", {7, 2}, 0.6, 12},
   };
   // orders per fixture: 0 = all; >0 = a seeded sample of that many
-  const std::vector<int64_t> sample = {0, 0, 0, 0, quick ? 20000 : 0, 3000, 48, 96, 60, 60, 6};
+  const std::vector<int64_t> sample = {0, 0, 0, 0, quick ? 20000 : 0, 3000, 48, 96, 60, 60, 6, 4};
   refpin::ref_register(fx);
   int total_fail = 0;
   const auto t_start = std::chrono::steady_clock::now();
