@@ -165,6 +165,13 @@ int spttn_read_output(spttn_plan* plan, double* host_out, int64_t count, void* s
  * [9] GENERIC: 1 when the forest runs as an NVRTC-compiled kernel.       */
 int spttn_plan_info(const spttn_plan* plan, int64_t* out, int n);
 
+/* Diagnostics (kernel tuning): with SPTTN_ITEM_CLOCKS=1 set at plan
+ * creation, the packed TTMc-3 kernels record per work item {start ns, end
+ * ns, SM id} (%globaltimer, %smid) on every execute; this copies the last
+ * execute's records (3 * items int64) to host memory. EINVAL when the plan
+ * records none.                                                           */
+int spttn_plan_item_clocks(const spttn_plan* plan, int64_t* host_out, int64_t n);
+
 /* GENERIC only: per-buffer reset counts of the last execute (as counted on
  * the device, ExecStats::buffer_resets) and the observer log (buffer id +
  * buffer contents after each reset, in execution order) when the program

@@ -70,7 +70,7 @@ ENGINE_SYMBOLS = [
     "spttn_read_output", "spttn_plan_info", "spttn_generic_resets", "spttn_generic_log_bytes",
     "spttn_generic_read_log", "spttn_unfactorized", "spttn_device_info", "spttn_build_info",
     "spttn_release_cached", "spttn_init", "spttn_synchronize", "spttn_csf_from_coo", "spttn_csf_download",
-    "spttn_csf_dim", "spttn_csf_permute",
+    "spttn_csf_dim", "spttn_csf_permute", "spttn_plan_item_clocks",
 ]
 
 _engine = None
@@ -111,6 +111,7 @@ def engine() -> C.CDLL:
         lib.spttn_output_device.restype = C.c_void_p
         lib.spttn_read_output.argtypes = [P, c_dbl_p, c_i64, P]
         lib.spttn_plan_info.argtypes = [P, c_i64_p, C.c_int]
+        lib.spttn_plan_item_clocks.argtypes = [P, c_i64_p, c_i64]
         lib.spttn_generic_resets.argtypes = [P, c_i64_p, C.c_int]
         lib.spttn_generic_log_bytes.argtypes = [P]
         lib.spttn_generic_log_bytes.restype = c_i64

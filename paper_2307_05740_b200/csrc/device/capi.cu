@@ -50,6 +50,7 @@ struct spttn_plan {
   int fac_align = 8;  // factor alignment the plan's kernels were chosen for
   void* arena = nullptr;                // GENERIC: one allocation for all plan state
   std::vector<int64_t> last_counters;   // GENERIC: madds, resets, log cursor, overflow
+  long long* item_clk = nullptr;        // diagnostics: per item {start, end, smid}
 };
 
 namespace {
@@ -413,6 +414,7 @@ int spttn_plan_destroy(spttn_plan* p) {
     if (p->own_fac)
       for (int f = 0; f < p->nf; ++f) spttn_dev::dfree(p->fac[f]);
     spttn_dev::dfree(p->out);
+    spttn_dev::dfree(p->item_clk);
     spttn_dev::dfree(p->d_dense);
     spttn_dev::dfree(p->leaf_i);
     spttn_dev::dfree(p->leaf_j);
@@ -804,8 +806,8 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
             env_int("SPTTN_SEG_LEN", p->kind == SPTTN_NEST_TTMC3 ? 4 : 8));
         if (p->kind == SPTTN_NEST_TTMC3) {
           // packed, TMA-staged, row-contiguous gathers (k_ttmc3pq); the
-          // earlier variants (modes 0, 4, 6, 7, 11) lost by > 6 % and were
-          // removed in round 2
+          // earlier variants (modes 0, 4, 6, 7, 11) and the shuffle-transposed
+          // kernel lost by > 6 % and were removed in round 2
           p->mode = 10;
           seg_len = std::clamp(seg_len, 1, 4);
         }
@@ -855,10 +857,17 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
             gchunk = std::clamp<int64_t>((p->dec.n_groups + wv - 1) / wv, 4, 512);
           }
           // k_ttmc3pq reads variable item ranges cut at equal work (leaf steps
-          // + a per-group overhead, decomp.cu k_group_work): 256 -> 249 us
-          const int ovh = static_cast<int>(env_int("SPTTN_GROUP_OVERHEAD", 12));
+          // + a per-group overhead, decomp.cu k_group_work). Measured on the
+          // BASELINE shape with the step-specialised kernel (per-item
+          // %globaltimer records, tools/item_balance.py): overhead 1 / 2 / 3 /
+          // 4 / 6 / 12 / 24 -> 259 / 241 / 228 / 224 / 230 / 241 / 248 us;
+          // busy efficiency 0.85 at 12, 0.92 at 4
+          const int ovh = static_cast<int>(env_int("SPTTN_GROUP_OVERHEAD", 4));
           spttn_dev::finish_unit_items(D, p->dec, p->dec.slice_grp, p->dec.n_groups, gchunk, tile, s,
                                        ovh);
+          if (env_int("SPTTN_ITEM_CLOCKS", 0) == 1)
+            dev_malloc(reinterpret_cast<void**>(&p->item_clk),
+                       std::max<int64_t>(1, 3 * p->dec.n_items) * sizeof(long long), s);
         } else {
           spttn_dev::build_segments(D, 1, seg_len, chunk, p->dec, tile, s);
         }
@@ -1008,6 +1017,7 @@ int spttn_execute_stage(spttn_plan* p, int stage, void* stream) {
     a.out = p->out;
     a.part = p->dec.part;
     a.flags = ((p->flags & SPTTN_FLAG_RESIDUAL) ? 1 : 0) | (p->mode << 8);
+    a.clk = p->item_clk;
     a.seg_begin = p->dec.seg_begin;
     a.seg_node = p->dec.seg_node;
     a.slice_seg = p->dec.slice_seg;
@@ -1136,6 +1146,15 @@ int spttn_plan_info(const spttn_plan* p, int64_t* out, int n) {
                            gen ? p->gen.par_mode : -1,
                            gen ? (p->gen.jit_kernel != nullptr ? 1 : 0) : -1};
     for (int i = 0; i < n && i < 10; ++i) out[i] = v[i];
+  });
+}
+
+int spttn_plan_item_clocks(const spttn_plan* p, int64_t* host_out, int64_t n) {
+  return guarded([&] {
+    if (!p || !p->item_clk) fail(SPTTN_EINVAL, "plan records no item clocks (SPTTN_ITEM_CLOCKS=1)");
+    const int64_t m = std::min<int64_t>(n, 3 * p->dec.n_items);
+    SPTTN_CUDA(cudaDeviceSynchronize());
+    SPTTN_CUDA(cudaMemcpy(host_out, p->item_clk, m * sizeof(int64_t), cudaMemcpyDeviceToHost));
   });
 }
 

@@ -164,6 +164,17 @@ __device__ __forceinline__ void bulk_g2s_elect(void* dst, const void* src, unsig
       "l"(src), "r"(bytes), "r"(b)
       : "memory");
 }
+__device__ __forceinline__ long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return static_cast<long long>(t);
+}
+__device__ __forceinline__ int smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return static_cast<int>(r);
+}
+
 __device__ __forceinline__ int32_t uni(int32_t v) { return __shfl_sync(0xffffffffu, v, 0); }
 
 __device__ __forceinline__ int ldg_i32(const int32_t* p) { return __ldg(p); }

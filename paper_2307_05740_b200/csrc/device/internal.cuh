@@ -153,6 +153,7 @@ struct RootOutArgs {
   const int32_t* slice_grp;
   int64_t n_groups;
   const int32_t* item_unit;  // variable item boundaries (TTMc-3 default kernel) or nullptr
+  long long* clk;            // per item {start ns, end ns, smid} (diagnostics) or nullptr
 };
 
 void launch_mttkrp3(const RootOutArgs& a, cudaStream_t s);

@@ -80,6 +80,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_ttmc3pq(RootOutArgs a) {
   StageQ* tiles = reinterpret_cast<StageQ*>(pq_smem + sizeof(StageT) * (kBlock / 32));
   const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
   if (w >= a.n_items) return;  // warp-uniform
+  if (a.clk && (threadIdx.x & 31) == 0) a.clk[3 * w] = globaltimer_ns();
   StageT& S = stage[threadIdx.x / 32];
   StageQ& Q = tiles[threadIdx.x / 32];
   const int lane = threadIdx.x & 31;
@@ -253,6 +254,10 @@ __global__ void __launch_bounds__(kBlock, 3) k_ttmc3pq(RootOutArgs a) {
     __syncwarp();  // stage buffers of this window are free after this point
   }
   if (pending) flush(head ? 0 : 1);
+  if (a.clk && lane == 0) {
+    a.clk[3 * w + 1] = globaltimer_ns();
+    a.clk[3 * w + 2] = smid();
+  }
 }
 
 // TTMc-4, packed form (default). Units are (i,j) fiber pieces of <= 4 LEAVES

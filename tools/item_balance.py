@@ -1,0 +1,51 @@
+"""Load balance of the packed TTMc-3 kernel (development tool):
+    python tools/item_balance.py [env settings...]
+Runs the BASELINE ttmc3 plan with SPTTN_ITEM_CLOCKS=1 and prints the spread
+of per-item and per-SM busy times from the kernel's %globaltimer records."""
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import paper_2307_05740_b200 as P  # noqa: E402
+from paper_2307_05740_b200.configs import make_workload  # noqa: E402
+
+
+def main():
+    os.environ["SPTTN_ITEM_CLOCKS"] = "1"
+    w = make_workload("ttmc3", scale=float(os.environ.get("SWEEP_SCALE", "1")))
+    c = w.cfg
+    s = torch.cuda.Stream()
+    dev = P.DeviceCsf(w.csf, stream=s)
+    tf = [torch.from_numpy(np.ascontiguousarray(f)).cuda() for f in w.factors]
+    for v in sys.argv[1:] or [""]:
+        env = dict(kv.split("=") for kv in v.split(",") if kv)
+        os.environ.update(env)
+        plan = P.Plan(c.kind, dev, [t.data_ptr() for t in tf], ranks=c.ranks, stream=s,
+                      on_device=True, factor_sizes=[t.numel() for t in tf])
+        for _ in range(3):
+            plan.execute(s)
+        torch.cuda.synchronize()
+        k = plan.item_clocks()
+        t0 = k[:, 0].min()
+        st, en, sm = (k[:, 0] - t0) / 1e3, (k[:, 1] - t0) / 1e3, k[:, 2]
+        d = en - st
+        span = en.max()
+        sm_end = np.array([en[sm == i].max() for i in np.unique(sm)])
+        sm_busy = np.array([d[sm == i].sum() for i in np.unique(sm)])
+        q = lambda a: " ".join(f"{x:7.1f}" for x in np.percentile(a, [0, 10, 50, 90, 100]))
+        print(f"[{v}] items {len(d)} span {span:.1f} us; item us p0/10/50/90/100: {q(d)}")
+        print(f"   start p0..100: {q(st)}   SM last end: {q(sm_end)}   SM busy sum/24: {q(sm_busy / 24)}")
+        print(f"   efficiency sum(d)/(span*items) = {d.sum() / (span * len(d)):.3f}")
+        order = np.argsort(d)
+        print("   longest items (idx, us):", [(int(i), round(float(d[i]), 1)) for i in order[-6:]])
+        plan.close()
+        for kk in env:
+            os.environ.pop(kk)
+
+
+if __name__ == "__main__":
+    main()
