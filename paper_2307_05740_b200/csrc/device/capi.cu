@@ -806,8 +806,8 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
             env_int("SPTTN_SEG_LEN", p->kind == SPTTN_NEST_TTMC3 ? 4 : 8));
         if (p->kind == SPTTN_NEST_TTMC3) {
           // packed, TMA-staged, row-contiguous gathers (k_ttmc3pq); the
-          // earlier variants (modes 0, 4, 6, 7, 11) and the shuffle-transposed
-          // kernel lost by > 6 % and were removed in round 2
+          // earlier variants (modes 0, 4, 6, 7, 11), the shuffle-transposed
+          // and the cp.async-fed kernels lost and were removed
           p->mode = 10;
           seg_len = std::clamp(seg_len, 1, 4);
         }

@@ -24,13 +24,14 @@ enum {
   SHFL = 16,      // SHFL.IDX 32-bit, arbitrary source lane
   S128_ST = 17,   // STS.128 row order (then one LDS.128 back)
   S64_ROW = 18,   // LDS.64 row order (2 rows)
+  CPA16_ROW = 20, // cp.async 16 B (LDGSTS.128), 8 consecutive lanes per row, 4 rows, into smem
 };
 
 template <int PAT>
 __global__ void k_probe(const double* __restrict__ table, int rows, int iters, double* out) {
   extern __shared__ double sh[];
   const int lane = threadIdx.x & 31;
-  constexpr bool SMEM = PAT >= 10;
+  constexpr bool SMEM = PAT >= 10 && PAT < 20;
   if (SMEM) {
     for (int i = threadIdx.x; i < rows * 16; i += blockDim.x) sh[i] = table[i];
     __syncthreads();
@@ -38,7 +39,7 @@ __global__ void k_probe(const double* __restrict__ table, int rows, int iters, d
   int slot, col;
   switch (PAT) {
     case G256_ROW: slot = lane >> 2; col = 4 * (lane & 3); break;
-    case G128_ROW: case S128_ROW: case S128_ST: slot = lane >> 3; col = 2 * (lane & 7); break;
+    case G128_ROW: case S128_ROW: case S128_ST: case CPA16_ROW: slot = lane >> 3; col = 2 * (lane & 7); break;
     case G128_FRAG: case S128_FRAG: slot = lane & 3; col = 2 * (lane >> 2); break;
     case G64_FRAG: case S64_FRAG: slot = lane & 3; col = lane >> 2; break;
     case G64_ROW: case S64_ROW: slot = lane >> 4; col = lane & 15; break;
@@ -50,7 +51,7 @@ __global__ void k_probe(const double* __restrict__ table, int rows, int iters, d
   unsigned x = 12345u + blockIdx.x * 977u + (threadIdx.x >> 5) * 131u + slot * 7u;
   double acc = 0;
   constexpr int U = 8;
-  double* wsh = sh + (threadIdx.x >> 5) * 64;  // per-warp scratch for S128_ST (smem table unused)
+  double* wsh = sh + (threadIdx.x >> 5) * 128;  // per-warp scratch (S128_ST, CPA16_ROW)
   for (int it = 0; it < iters; it += U) {
     double v[U];
 #pragma unroll
@@ -77,6 +78,17 @@ __global__ void k_probe(const double* __restrict__ table, int rows, int iters, d
       } else if (PAT == SHFL) {
         v[u] = __int_as_float(__shfl_sync(0xffffffffu, __float_as_int(static_cast<float>(acc)) + u,
                                           (x >> 3) & 31));
+      } else if (PAT == CPA16_ROW) {
+        const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(wsh + 2 * lane + 64 * (u & 1)));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(p) : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        if (u & 1) {
+          asm volatile("cp.async.wait_group 0;" ::: "memory");
+          __syncwarp();
+          v[u] = wsh[2 * lane] + wsh[2 * lane + 64];
+        } else {
+          v[u] = 0;
+        }
       } else {  // S128_ST
         *reinterpret_cast<double2*>(wsh + 2 * (lane & 31)) = make_double2(acc, u);
         __syncwarp();
@@ -94,7 +106,8 @@ __global__ void k_probe(const double* __restrict__ table, int rows, int iters, d
 template <int PAT>
 void run(const char* name, const double* table, int rows, double* out, int sms) {
   const int iters = 4096, threads = 256, blocks = sms * 4;
-  const size_t smem = PAT >= 10 ? static_cast<size_t>(rows) * 16 * sizeof(double) : 0;
+  const size_t smem = PAT >= 20 ? 8 * 128 * sizeof(double)
+                     : PAT >= 10 ? static_cast<size_t>(rows) * 16 * sizeof(double) : 0;
   if (smem) cudaFuncSetAttribute(k_probe<PAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
@@ -126,6 +139,7 @@ int main() {
     run<G64_FRAG>("g64frag", table, rows, out, sms);
     run<G64_ROW>("g64row", table, rows, out, sms);
   }
+  run<CPA16_ROW>("cpa16row", table, 20000, out, sms);
   const int srows = 256;
   run<S128_ROW>("s128row", table, srows, out, sms);
   run<S128_FRAG>("s128frag", table, srows, out, sms);
