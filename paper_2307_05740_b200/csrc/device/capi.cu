@@ -919,8 +919,10 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
           if (gchunk <= 0)
             gchunk = std::clamp<int64_t>((p->dec.n_groups + w24 - 1) / w24, 4,
                                          p->mode == 3 ? 64 : 1024);
-          // equal group counts by default (work-cut items: within 1 %)
-          const int ovhm = p->mode == 3 ? static_cast<int>(env_int("SPTTN_GROUP_OVERHEAD", 0)) : 0;
+          // order 4: items cut at equal work, leaf steps + 4 per group (BASELINE
+          // MTTKRP-4 kernel us: equal group counts 644, overhead 1: 637, 2: 631,
+          // 4: 625, 8: 631)
+          const int ovhm = p->mode == 3 ? static_cast<int>(env_int("SPTTN_GROUP_OVERHEAD", 4)) : 0;
           spttn_dev::finish_unit_items(D, p->dec, p->dec.slice_grp, p->dec.n_groups, gchunk, tile, s,
                                        ovhm);
         }
