@@ -539,3 +539,23 @@ def test_device_unfactorized_equals_reference_golden(E, m):
     dev = E.DeviceCsf(csf)
     got = E.unfactorized(m["kernel"], m["dims"], dev, factors)
     assert np.array_equal(got, z["unfactorized"]), np.abs(got - z["unfactorized"]).max()
+
+
+def test_item_clock_diagnostics(E, monkeypatch):
+    """SPTTN_ITEM_CLOCKS=1 (tuning aid): the packed TTMc-3 kernel records one
+    {start, end, SM} per work item; the plan without it reports EINVAL."""
+    from paper_2307_05740_b200.configs import make_workload
+    w = make_workload("ttmc3", scale=2e-3)
+    monkeypatch.setenv("SPTTN_ITEM_CLOCKS", "1")
+    monkeypatch.setenv("SPTTN_GCHUNK", "4")
+    out, plan, dev = run(E, w.cfg.kind, w.csf, w.factors, w.cfg.ranks)
+    k = plan.item_clocks()
+    assert k.shape == (plan.info()["items"], 3) and k.shape[0] > 1
+    assert np.all(k[:, 1] >= k[:, 0]) and np.all(k[:, 0] > 0)
+    assert np.all((k[:, 2] >= 0) & (k[:, 2] < 1024))
+    monkeypatch.delenv("SPTTN_ITEM_CLOCKS")
+    plain = E.Plan(w.cfg.kind, dev, w.factors, ranks=w.cfg.ranks)
+    plain.execute()
+    assert np.array_equal(plain.read_output(), out)  # the records do not change results
+    with pytest.raises(Exception):
+        plain.item_clocks()
