@@ -166,9 +166,10 @@ int spttn_read_output(spttn_plan* plan, double* host_out, int64_t count, void* s
 int spttn_plan_info(const spttn_plan* plan, int64_t* out, int n);
 
 /* Diagnostics (kernel tuning): with SPTTN_ITEM_CLOCKS=1 set at plan
- * creation, the packed TTMc-3 kernels record per work item {start ns, end
- * ns, SM id} (%globaltimer, %smid) on every execute; this copies the last
- * execute's records (3 * items int64) to host memory. EINVAL when the plan
+ * creation, the packed TTMc-3 kernel (its diagnostics instantiation)
+ * records per work item {start ns, end ns, SM id, groups, leaf steps, tile
+ * flushes} (%globaltimer, %smid) on every execute; this copies the last
+ * execute's records (6 * items int64) to host memory. EINVAL when the plan
  * records none.                                                           */
 int spttn_plan_item_clocks(const spttn_plan* plan, int64_t* host_out, int64_t n);
 

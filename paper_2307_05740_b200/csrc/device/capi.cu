@@ -867,7 +867,7 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
                                        ovh);
           if (env_int("SPTTN_ITEM_CLOCKS", 0) == 1)
             dev_malloc(reinterpret_cast<void**>(&p->item_clk),
-                       std::max<int64_t>(1, 3 * p->dec.n_items) * sizeof(long long), s);
+                       std::max<int64_t>(1, 6 * p->dec.n_items) * sizeof(long long), s);
         } else {
           spttn_dev::build_segments(D, 1, seg_len, chunk, p->dec, tile, s);
         }
@@ -1154,7 +1154,7 @@ int spttn_plan_info(const spttn_plan* p, int64_t* out, int n) {
 int spttn_plan_item_clocks(const spttn_plan* p, int64_t* host_out, int64_t n) {
   return guarded([&] {
     if (!p || !p->item_clk) fail(SPTTN_EINVAL, "plan records no item clocks (SPTTN_ITEM_CLOCKS=1)");
-    const int64_t m = std::min<int64_t>(n, 3 * p->dec.n_items);
+    const int64_t m = std::min<int64_t>(n, 6 * p->dec.n_items);
     SPTTN_CUDA(cudaDeviceSynchronize());
     SPTTN_CUDA(cudaMemcpy(host_out, p->item_clk, m * sizeof(int64_t), cudaMemcpyDeviceToHost));
   });

@@ -72,7 +72,9 @@ struct StageQ {
 
 constexpr size_t kPqSmem = (sizeof(StageT) + sizeof(StageQ)) * (kBlock / 32);
 
-template <bool VECU, bool VECV>
+// CLK (diagnostics build, SPTTN_ITEM_CLOCKS=1): per item {start ns, end ns,
+// SM, groups, leaf steps, tile flushes} for fitting the item work model
+template <bool VECU, bool VECV, bool CLK = false>
 __global__ void __launch_bounds__(kBlock, 3) k_ttmc3pq(RootOutArgs a) {
   grid_launch_dependents();
   extern __shared__ __align__(16) unsigned char pq_smem[];  // kPqSmem bytes
@@ -80,7 +82,8 @@ __global__ void __launch_bounds__(kBlock, 3) k_ttmc3pq(RootOutArgs a) {
   StageQ* tiles = reinterpret_cast<StageQ*>(pq_smem + sizeof(StageT) * (kBlock / 32));
   const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
   if (w >= a.n_items) return;  // warp-uniform
-  if (a.clk && (threadIdx.x & 31) == 0) a.clk[3 * w] = globaltimer_ns();
+  if (CLK && (threadIdx.x & 31) == 0) a.clk[6 * w] = globaltimer_ns();
+  int dbg_steps = 0, dbg_flush = 0;
   StageT& S = stage[threadIdx.x / 32];
   StageQ& Q = tiles[threadIdx.x / 32];
   const int lane = threadIdx.x & 31;
@@ -178,6 +181,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_ttmc3pq(RootOutArgs a) {
     for (int32_t g = g0; g < ge; ++g) {
       const int4 hh = S.hdr[mb][g - g0];
       const int n = hh.y;  // warp-uniform
+      if (CLK) dbg_steps += n;
       const int32_t lbase = hh.x - L0 + gs;
       const int32_t j = S.node[mb][(g - g0) * kPackSlots + gs];
       const double4 ur = row4<VECU>(U + static_cast<int64_t>(j) * R, 4 * gc, R);
@@ -238,6 +242,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_ttmc3pq(RootOutArgs a) {
             dmma_8x8x4(acc[(mt * 2 + nt) * 2], acc[(mt * 2 + nt) * 2 + 1], af[kc][mt], bf[kc][nt]);
       par ^= 1;
       pending = true;
+      if (CLK) ++dbg_flush;
       if (g + 1 == sl_end) {
         flush(head ? 0 : -1);
         pending = false;
@@ -253,10 +258,14 @@ __global__ void __launch_bounds__(kBlock, 3) k_ttmc3pq(RootOutArgs a) {
     }
     __syncwarp();  // stage buffers of this window are free after this point
   }
+  if (CLK && pending) ++dbg_flush;
   if (pending) flush(head ? 0 : 1);
-  if (a.clk && lane == 0) {
-    a.clk[3 * w + 1] = globaltimer_ns();
-    a.clk[3 * w + 2] = smid();
+  if (CLK && lane == 0) {
+    a.clk[6 * w + 1] = globaltimer_ns();
+    a.clk[6 * w + 2] = smid();
+    a.clk[6 * w + 3] = cend - cbeg;
+    a.clk[6 * w + 4] = dbg_steps;
+    a.clk[6 * w + 5] = dbg_flush;
   }
 }
 
@@ -692,7 +701,9 @@ void launch_ttmc3(const RootOutArgs& a, cudaStream_t s) {
                                     static_cast<int>(kPqSmem)));
     kern<<<static_cast<unsigned>(blocks), kBlock, kPqSmem, s>>>(a);
   };
-  if (wu && wv)
+  if (wu && wv && a.clk)
+    go(k_ttmc3pq<true, true, true>);
+  else if (wu && wv)
     go(k_ttmc3pq<true, true>);
   else if (wu)
     go(k_ttmc3pq<true, false>);

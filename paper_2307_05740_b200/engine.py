@@ -275,12 +275,13 @@ class Plan:
         return dict(zip(keys, list(out)))
 
     def item_clocks(self) -> np.ndarray:
-        """Diagnostics: per work item [start ns, end ns, SM id] of the last
-        execute (plans created with SPTTN_ITEM_CLOCKS=1; packed TTMc-3)."""
+        """Diagnostics: per work item [start ns, end ns, SM id, groups, leaf
+        steps, tile flushes] of the last execute (plans created with
+        SPTTN_ITEM_CLOCKS=1; packed TTMc-3)."""
         n = self.info()["items"]
-        out = np.zeros(3 * n, np.int64)
+        out = np.zeros(6 * n, np.int64)
         _check(N.engine().spttn_plan_item_clocks(self.handle, out.ctypes.data_as(N.c_i64_p), out.size))
-        return out.reshape(n, 3)
+        return out.reshape(n, 6)
 
     def set_factors(self, factors, stream=None, on_device=False):
         arrs = []

@@ -550,9 +550,10 @@ def test_item_clock_diagnostics(E, monkeypatch):
     monkeypatch.setenv("SPTTN_GCHUNK", "4")
     out, plan, dev = run(E, w.cfg.kind, w.csf, w.factors, w.cfg.ranks)
     k = plan.item_clocks()
-    assert k.shape == (plan.info()["items"], 3) and k.shape[0] > 1
+    assert k.shape == (plan.info()["items"], 6) and k.shape[0] > 1
     assert np.all(k[:, 1] >= k[:, 0]) and np.all(k[:, 0] > 0)
     assert np.all((k[:, 2] >= 0) & (k[:, 2] < 1024))
+    assert np.all(k[:, 3] >= 1) and np.all(k[:, 4] >= k[:, 3]) and np.all(k[:, 5] >= 1)
     monkeypatch.delenv("SPTTN_ITEM_CLOCKS")
     plain = E.Plan(w.cfg.kind, dev, w.factors, ranks=w.cfg.ranks)
     plain.execute()
