@@ -865,9 +865,11 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
           const int ovh = static_cast<int>(env_int("SPTTN_GROUP_OVERHEAD", 4));
           spttn_dev::finish_unit_items(D, p->dec, p->dec.slice_grp, p->dec.n_groups, gchunk, tile, s,
                                        ovh);
-          if (env_int("SPTTN_ITEM_CLOCKS", 0) == 1)
-            dev_malloc(reinterpret_cast<void**>(&p->item_clk),
-                       std::max<int64_t>(1, 6 * p->dec.n_items) * sizeof(long long), s);
+          if (env_int("SPTTN_ITEM_CLOCKS", 0) == 1) {  // recorded by the 256-bit-gather kernel only
+            const int64_t cb = std::max<int64_t>(1, 6 * p->dec.n_items) * sizeof(long long);
+            dev_malloc(reinterpret_cast<void**>(&p->item_clk), cb, s);
+            SPTTN_CUDA(cudaMemsetAsync(p->item_clk, 0, cb, s));
+          }
         } else {
           spttn_dev::build_segments(D, 1, seg_len, chunk, p->dec, tile, s);
         }
