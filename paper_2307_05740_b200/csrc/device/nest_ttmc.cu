@@ -242,8 +242,8 @@ __global__ void __launch_bounds__(kBlock, 3) k_ttmc3pq(RootOutArgs a) {
             dmma_8x8x4(acc[(mt * 2 + nt) * 2], acc[(mt * 2 + nt) * 2 + 1], af[kc][mt], bf[kc][nt]);
       par ^= 1;
       pending = true;
-      if (CLK) ++dbg_flush;
       if (g + 1 == sl_end) {
+        if (CLK) ++dbg_flush;
         flush(head ? 0 : -1);
         pending = false;
         head = false;
