@@ -565,10 +565,13 @@ __global__ void __launch_bounds__(NB, MB) k_ttmc4pa(RootOutArgs a) {
     bulk_g2s_elect(&S.kk[lb][0], a.pk2 + L0, n * 4u, &S.mbar_leaf[lb]);
     bulk_g2s_elect(&S.tv[lb][0], a.pv + L0, n * 8u, &S.mbar_leaf[lb]);
   };
-  // cp.async of one leaf step's V and W rows (slot gs, chunk gc) into tile buf
+  // cp.async of one leaf step's V and W rows (slot gs, chunk gc) into tile
+  // buf — .cg (L2 -> shared, no L1 allocation: LDGSTS.BYPASS): 391 vs 408 us
+  // for the L1-allocating .ca at the BASELINE shape (fewer L1 wavefronts per
+  // copy; the 128 KB V / W are L2-resident)
   auto issue_rows = [&](int buf, int lbuf, int32_t e) {
-    cp_async16_ca(&S.vs[buf][st_off], V + static_cast<int64_t>(S.kk[lbuf][e]) * 8 + 2 * gc);
-    cp_async16_ca(&S.ws[buf][st_off], W + static_cast<int64_t>(S.ll[lbuf][e]) * 8 + 2 * gc);
+    cp_async16_cg(&S.vs[buf][st_off], V + static_cast<int64_t>(S.kk[lbuf][e]) * 8 + 2 * gc, 16);
+    cp_async16_cg(&S.ws[buf][st_off], W + static_cast<int64_t>(S.ll[lbuf][e]) * 8 + 2 * gc, 16);
     cp_async_commit();
   };
 
