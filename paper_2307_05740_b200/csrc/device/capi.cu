@@ -834,16 +834,27 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
           spttn_dev::expand_coords(D, 2, D.idx[2], leaf_k, s);
           spttn_dev::build_packed(D, 3, p->dec, s, spttn_dev::kPackSlots, leaf_k);
           spttn_dev::dfree(leaf_k, s);
-          const int64_t w16 = static_cast<int64_t>(sms) * 16 * 2;
+          // mode 4: one item per resident warp of k_ttmc4pa (a single wave of
+          // 12-warp CTAs; BASELINE shape: 1773 items 338 us, 2 waves 346 us,
+          // the earlier 2.66 waves 391 us — the last partial wave idled a
+          // third of the SMs); mode 3: two items per 32 warps per SM
+          const int64_t wv4 = p->mode == 4
+                                  ? static_cast<int64_t>(sms) * spttn_dev::ttmc4pa_warps_per_sm()
+                                  : static_cast<int64_t>(sms) * 16 * 2;
           int64_t gchunk = env_int("SPTTN_GCHUNK", 0);
           if (gchunk <= 0)
-            gchunk = std::clamp<int64_t>((p->dec.n_groups + w16 - 1) / w16, 4, 1024);
+            gchunk = std::clamp<int64_t>((p->dec.n_groups + wv4 - 1) / wv4, 4, 1024);
           // mode 4: items cut at equal work, leaf steps + 3 per group
           // (BASELINE shape, kernel us: equal group counts 448; overhead 2:
           // 408, 3: 404, 4: 409, 6: 416)
           const int ovh4 = p->mode == 4 ? static_cast<int>(env_int("SPTTN_GROUP_OVERHEAD", 3)) : 0;
           spttn_dev::finish_unit_items(D, p->dec, p->dec.slice_grp, p->dec.n_groups, gchunk, tile, s,
                                        ovh4);
+          if (p->mode == 4 && env_int("SPTTN_ITEM_CLOCKS", 0) == 1) {
+            const int64_t cb = std::max<int64_t>(1, 6 * p->dec.n_items) * sizeof(long long);
+            dev_malloc(reinterpret_cast<void**>(&p->item_clk), cb, s);
+            SPTTN_CUDA(cudaMemsetAsync(p->item_clk, 0, cb, s));
+          }
         } else if (p->kind == SPTTN_NEST_TTMC3) {
           // packed length-sorted groups of 8 segments (pack.cu)
           spttn_dev::build_segments(D, 1, seg_len, chunk, p->dec, tile, s, false);

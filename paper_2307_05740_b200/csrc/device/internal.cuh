@@ -166,6 +166,7 @@ void launch_tttp3_pieces(const RootOutArgs& a, const int4* pieces, int64_t n_pie
                          const int2* leaf_jk, int batch, cudaStream_t s);
 void launch_ttmc3(const RootOutArgs& a, cudaStream_t s);
 int ttmc3pq_warps_per_sm();
+int ttmc4pa_warps_per_sm();
 void launch_ttmc4(const RootOutArgs& a, cudaStream_t s);
 // Segment-form MTTKRP (R <= 32) on packed groups: pk = order 3 (fallback of
 // the shared-memory kernel), pq = TMA-staged streams (order 4 default).

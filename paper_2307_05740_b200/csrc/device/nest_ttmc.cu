@@ -490,13 +490,17 @@ struct StageT4a {
   uint64_t mbar_leaf[2];
 };
 constexpr size_t t4a_smem_bytes(int nb) { return sizeof(StageT4a) * (nb / 32); }
+// TTMc-4 default kernel: 384 threads x 1 CTA per SM (up to 168 registers)
+constexpr int kT4Block = 384;
 
-template <int NB, int MB>
+template <int NB, int MB, bool CLK = false>
 __global__ void __launch_bounds__(NB, MB) k_ttmc4pa(RootOutArgs a) {
   grid_launch_dependents();
   extern __shared__ __align__(16) unsigned char t4a_smem[];
   const int64_t w = (static_cast<int64_t>(blockIdx.x) * NB + threadIdx.x) / 32;
   if (w >= a.n_items) return;  // warp-uniform
+  if (CLK && (threadIdx.x & 31) == 0) a.clk[6 * w] = globaltimer_ns();
+  int dbg_steps = 0, dbg_flush = 0;
   StageT4a& S = reinterpret_cast<StageT4a*>(t4a_smem)[threadIdx.x / 32];
   const int lane = threadIdx.x & 31;
   const int q = lane & 3;   // fragment role: segment (K) index
@@ -603,6 +607,7 @@ __global__ void __launch_bounds__(NB, MB) k_ttmc4pa(RootOutArgs a) {
     for (int32_t g = g0; g < ge; ++g) {
       const int4 hh = S.hdr[mb][g - g0];
       const int n = hh.y;  // warp-uniform leaves per segment
+      if (CLK) dbg_steps += n;
       const int32_t jA = S.node[mb][(g - g0) * kPackSlots + q];
       const int32_t jB = S.node[mb][(g - g0) * kPackSlots + 4 + q];
       const double uA = h < R ? __ldg(U + static_cast<int64_t>(jA) * R + h) : 0.0;
@@ -664,6 +669,7 @@ __global__ void __launch_bounds__(NB, MB) k_ttmc4pa(RootOutArgs a) {
       for (int s = 0; s < 8; ++s) dmma_8x8x4(acc[2 * s], acc[2 * s + 1], uB, YB[s]);
       pending = true;
       if (g + 1 == sl_end) {
+        if (CLK) ++dbg_flush;
         flush(head ? 0 : -1);
         pending = false;
         head = false;
@@ -678,7 +684,15 @@ __global__ void __launch_bounds__(NB, MB) k_ttmc4pa(RootOutArgs a) {
     }
     __syncwarp();  // stage buffers of this window are free after this point
   }
+  if (CLK && pending) ++dbg_flush;
   if (pending) flush(head ? 0 : 1);
+  if (CLK && lane == 0) {
+    a.clk[6 * w + 1] = globaltimer_ns();
+    a.clk[6 * w + 2] = smid();
+    a.clk[6 * w + 3] = cend - cbeg;
+    a.clk[6 * w + 4] = dbg_steps;
+    a.clk[6 * w + 5] = dbg_flush;
+  }
 }
 
 }  // namespace
@@ -693,6 +707,20 @@ int ttmc3pq_warps_per_sm() {
                                                     kPqSmem) != cudaSuccess)
     blocks = 3;
   return std::max(1, blocks) * (kBlock / 32);
+}
+
+// resident warps per SM of the TTMc-4 default kernel (plan-time item sizing:
+// one item per resident warp — items past a whole wave of 384-thread CTAs
+// left 1/3 of the SMs idle for the last third of the kernel)
+int ttmc4pa_warps_per_sm() {
+  int blocks = 0;
+  const size_t sm = t4a_smem_bytes(kT4Block);
+  if (cudaFuncSetAttribute(k_ttmc4pa<kT4Block, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(sm)) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_ttmc4pa<kT4Block, 1>, kT4Block, sm) !=
+          cudaSuccess)
+    blocks = 1;
+  return std::max(1, blocks) * (kT4Block / 32);
 }
 
 void launch_ttmc3(const RootOutArgs& a, cudaStream_t s) {
@@ -725,11 +753,16 @@ void launch_ttmc4(const RootOutArgs& a, cudaStream_t s) {
     // 384 threads x 1 block per SM: up to 168 registers (163 used, no spill);
     // 256 x 2 capped them at 128 and spilled 32 B per group at the same speed
     // (404 vs 407 us at the BASELINE shape)
-    constexpr int nb = 384;
-    const size_t sm = t4a_smem_bytes(nb);
-    SPTTN_CUDA(cudaFuncSetAttribute(k_ttmc4pa<nb, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(sm)));
-    k_ttmc4pa<nb, 1><<<static_cast<unsigned>((a.n_items * 32 + nb - 1) / nb), nb, sm, s>>>(a);
+    auto go4 = [&](auto kern, int nb) {
+      const size_t sm = t4a_smem_bytes(nb);
+      SPTTN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(sm)));
+      kern<<<static_cast<unsigned>((a.n_items * 32 + nb - 1) / nb), nb, sm, s>>>(a);
+    };
+    if (a.clk)  // diagnostics instantiation (SPTTN_ITEM_CLOCKS=1)
+      go4(k_ttmc4pa<kT4Block, 1, true>, kT4Block);
+    else
+      go4(k_ttmc4pa<kT4Block, 1>, kT4Block);
   } else {  // packed, 4 x 2 (s, t) blocks per lane (any R, S, T <= 8)
     const bool vv = a.vec & 2, vw = a.vec & 4;
     const unsigned b = static_cast<unsigned>(blocks);

@@ -1,4 +1,5 @@
-"""Load balance of the packed TTMc-3 kernel (development tool):
+"""Load balance of the packed TTMc-3 / TTMc-4 kernels (development tool;
+BALANCE_KEY=ttmc4 for TTMc-4):
     python tools/item_balance.py [env settings...]
 Runs the BASELINE ttmc3 plan with SPTTN_ITEM_CLOCKS=1 (the kernel's
 diagnostics instantiation) and prints the spread of per-item and per-SM busy
@@ -19,7 +20,8 @@ from paper_2307_05740_b200.configs import make_workload  # noqa: E402
 
 def main():
     os.environ["SPTTN_ITEM_CLOCKS"] = "1"
-    w = make_workload("ttmc3", scale=float(os.environ.get("SWEEP_SCALE", "1")))
+    key = os.environ.get("BALANCE_KEY", "ttmc3")  # ttmc3 or ttmc4
+    w = make_workload(key, scale=float(os.environ.get("SWEEP_SCALE", "1")))
     c = w.cfg
     s = torch.cuda.Stream()
     dev = P.DeviceCsf(w.csf, stream=s)
@@ -43,7 +45,7 @@ def main():
         sm_busy = np.array([d[sm == i].sum() for i in np.unique(sm)])
         q = lambda a: " ".join(f"{x:7.1f}" for x in np.percentile(a, [0, 10, 50, 90, 100]))
         print(f"[{v}] items {len(d)} span {span:.1f} us; item us p0/10/50/90/100: {q(d)}")
-        print(f"   SM last end: {q(sm_end)}   SM busy sum/24: {q(sm_busy / 24)}")
+        print(f"   SM last end: {q(sm_end)}   SM busy sum: {q(sm_busy)}")
         print(f"   efficiency sum(d)/(span*items) = {d.sum() / (span * len(d)):.3f}")
         # work model fit over the runs (median item time per item)
         dm = np.median(np.stack([(r[:, 1] - r[:, 0]) / 1e3 for r in recs]), axis=0)
