@@ -925,13 +925,15 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
           spttn_dev::build_packed(D, D.order - 1, p->dec, s, 4);
           // order 3: one item per resident warp (k_mttkrp_pk: 4 CTAs of 8
           // warps per SM) — a single wave, and root slices stay within one
-          // fix-up chunk (one fix-up kernel); order 4 wants two waves of the
-          // 24-warp k_mttkrp_pq for balance
-          const int64_t w24 = static_cast<int64_t>(sms) * (D.order == 3 ? 32 : 48);
+          // fix-up chunk (one fix-up kernel)
+          // order 4: six items per resident warp (24 per SM) — fewer, longer
+          // items than the earlier 64-group cap (51620 items) halve the split
+          // slices the fix-up sums: step 641.5 -> 631.8 us at the BASELINE
+          // shape (4 items per warp 635.9, 8: 631.7, 1: 671.3)
+          const int64_t w24 = static_cast<int64_t>(sms) * (D.order == 3 ? 32 : 24 * 6);
           int64_t gchunk = env_int("SPTTN_GCHUNK", 0);
           if (gchunk <= 0)
-            gchunk = std::clamp<int64_t>((p->dec.n_groups + w24 - 1) / w24, 4,
-                                         p->mode == 3 ? 64 : 1024);
+            gchunk = std::clamp<int64_t>((p->dec.n_groups + w24 - 1) / w24, 4, 1024);
           // order 4: items cut at equal work, leaf steps + 4 per group (BASELINE
           // MTTKRP-4 kernel us: equal group counts 644, overhead 1: 637, 2: 631,
           // 4: 625, 8: 631)
