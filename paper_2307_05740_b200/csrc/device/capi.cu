@@ -940,6 +940,11 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
           const int ovhm = p->mode == 3 ? static_cast<int>(env_int("SPTTN_GROUP_OVERHEAD", 4)) : 0;
           spttn_dev::finish_unit_items(D, p->dec, p->dec.slice_grp, p->dec.n_groups, gchunk, tile, s,
                                        ovhm);
+          if (D.order == 4 && env_int("SPTTN_ITEM_CLOCKS", 0) == 1) {
+            const int64_t cb = std::max<int64_t>(1, 6 * p->dec.n_items) * sizeof(long long);
+            dev_malloc(reinterpret_cast<void**>(&p->item_clk), cb, s);
+            SPTTN_CUDA(cudaMemsetAsync(p->item_clk, 0, cb, s));
+          }
         }
       } else {
         const int G = spttn_dev::group_lanes_for(static_cast<int>(R));

@@ -150,12 +150,16 @@ struct StageM {
 
 // RC = compile-time rank (32 at the BASELINE shapes: full 256-byte rows over
 // 8 lanes, constant row strides, no column predicates) or 0 = a.R at run time
-template <int ORDER, bool VEC, int RC = 0>
+// CLK: diagnostics instantiation (SPTTN_ITEM_CLOCKS=1), per item {start ns,
+// end ns, SM, groups, leaf steps, tile flushes}
+template <int ORDER, bool VEC, int RC = 0, bool CLK = false>
 __global__ void __launch_bounds__(kBlock, 3) k_mttkrp_pq(RootOutArgs a) {
   grid_launch_dependents();
   __shared__ StageM stage[kBlock / 32];
   const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
   if (w >= a.n_items) return;  // warp-uniform
+  if (CLK && (threadIdx.x & 31) == 0) a.clk[6 * w] = globaltimer_ns();
+  int dbg_steps = 0, dbg_flush = 0;
   StageM& S = stage[threadIdx.x / 32];
   const int lane = threadIdx.x & 31;
   const int slot = lane >> 3;
@@ -256,6 +260,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_mttkrp_pq(RootOutArgs a) {
     for (int32_t g = g0; g < ge; ++g) {
       const int4 hh = S.hdr[mb][g - g0];
       const int n = hh.y;  // warp-uniform
+      if (CLK) dbg_steps += n;
       const int32_t u = S.node[mb][(g - g0) * kMSlots + slot];
       const int32_t j = ORDER == 4 ? S.node1[mb][(g - g0) * kMSlots + slot] : 0;
       const int32_t lbase = hh.x - L0 + slot;
@@ -306,6 +311,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_mttkrp_pq(RootOutArgs a) {
       }
       pending = true;
       if (g + 1 == sl_end) {
+        if (CLK) ++dbg_flush;
         flush(head ? 0 : -1);
         pending = false;
         head = false;
@@ -320,7 +326,15 @@ __global__ void __launch_bounds__(kBlock, 3) k_mttkrp_pq(RootOutArgs a) {
     }
     __syncwarp();  // stage buffers of this window are free after this point
   }
+  if (CLK && pending) ++dbg_flush;
   if (pending) flush(head ? 0 : 1);
+  if (CLK && lane == 0) {
+    a.clk[6 * w + 1] = globaltimer_ns();
+    a.clk[6 * w + 2] = smid();
+    a.clk[6 * w + 3] = cend - cbeg;
+    a.clk[6 * w + 4] = dbg_steps;
+    a.clk[6 * w + 5] = dbg_flush;
+  }
 }
 
 }  // namespace
@@ -333,7 +347,8 @@ void launch_mttkrp_pq(const RootOutArgs& a, int order, cudaStream_t s) {
     if (a.vec) k_mttkrp_pq<3, true><<<b, kBlock, 0, s>>>(a);
     else k_mttkrp_pq<3, false><<<b, kBlock, 0, s>>>(a);
   } else {
-    if (a.vec && a.R == 32) k_mttkrp_pq<4, true, 32><<<b, kBlock, 0, s>>>(a);
+    if (a.vec && a.R == 32 && a.clk) k_mttkrp_pq<4, true, 32, true><<<b, kBlock, 0, s>>>(a);
+    else if (a.vec && a.R == 32) k_mttkrp_pq<4, true, 32><<<b, kBlock, 0, s>>>(a);
     else if (a.vec) k_mttkrp_pq<4, true><<<b, kBlock, 0, s>>>(a);
     else k_mttkrp_pq<4, false><<<b, kBlock, 0, s>>>(a);
   }

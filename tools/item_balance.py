@@ -20,7 +20,7 @@ from paper_2307_05740_b200.configs import make_workload  # noqa: E402
 
 def main():
     os.environ["SPTTN_ITEM_CLOCKS"] = "1"
-    key = os.environ.get("BALANCE_KEY", "ttmc3")  # ttmc3 or ttmc4
+    key = os.environ.get("BALANCE_KEY", "ttmc3")  # ttmc3, ttmc4 or mttkrp4
     w = make_workload(key, scale=float(os.environ.get("SWEEP_SCALE", "1")))
     c = w.cfg
     s = torch.cuda.Stream()
