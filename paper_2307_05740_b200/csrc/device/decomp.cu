@@ -586,6 +586,127 @@ __global__ void __launch_bounds__(256) k_fix2(const int32_t* multi, const int32_
   }
 }
 
+// Epilogue in one launch: blocks [0, n_multi) each sum one heavy split slice
+// straight from its items' partial tiles (TAIL of the first item, HEAD of the
+// others; G thread groups stride the items in order, 8 loads in flight, then
+// the group sums are added in group order: a fixed order, deterministic);
+// the other blocks run k_fix1's warp-per-chunk pass for the single-chunk
+// split slices and zero the absent rows. One launch instead of k_fix1 then
+// k_fix2 — the second dependent launch cost ~4 us per step.
+// 1024 threads: a heavy slice's items are strided by up to 1024 / tile-quads
+// thread groups (MTTKRP-4: 128 groups over ~2500 items of its largest slice)
+constexpr int kFixBlock = 1024;
+template <bool V4>
+__global__ void __launch_bounds__(kFixBlock) k_fix_all(const int4* __restrict__ meta,
+                                                 const double* __restrict__ part, int64_t tile,
+                                                 int64_t n_chunk, const int32_t* absent_rows,
+                                                 int64_t n_absent, double* out,
+                                                 const int32_t* multi, int64_t n_multi,
+                                                 const int32_t* split_first,
+                                                 const int32_t* split_last,
+                                                 const int32_t* split_node, const int32_t* idx0) {
+  __shared__ double4 ws[kFixBlock];
+  const int64_t nv = V4 ? tile / 4 : tile;
+  if (blockIdx.x < n_multi) {
+    const int32_t sidx = multi[blockIdx.x];
+    const int32_t first = split_first[sidx], last = split_last[sidx];
+    const int64_t row = idx0[split_node[sidx]];
+    grid_dependency_wait();
+    const int64_t piece = nv < kFixBlock ? nv : kFixBlock;
+    const int G = static_cast<int>(kFixBlock / piece);
+    const int g = threadIdx.x / static_cast<int>(piece);
+    const int64_t el = threadIdx.x % piece;
+    for (int64_t p0 = 0; p0 < nv; p0 += piece) {
+      const int64_t e = p0 + el;
+      const bool act = g < G && e < nv;
+      double4 sum = make_double4(0, 0, 0, 0);
+      if (act) {
+        for (int32_t i0 = first + g; i0 <= last; i0 += 8 * G) {
+          double4 v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int32_t i = i0 + u * G;
+            const double* src = part + (static_cast<int64_t>(i) * 2 + (i == first ? 1 : 0)) * tile;
+            if (V4)
+              v[u] = i <= last ? reinterpret_cast<const double4*>(src)[e] : make_double4(0, 0, 0, 0);
+            else
+              v[u] = make_double4(i <= last ? src[e] : 0.0, 0, 0, 0);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (i0 + u * G <= last) {
+              sum.x += v[u].x;
+              sum.y += v[u].y;
+              sum.z += v[u].z;
+              sum.w += v[u].w;
+            }
+        }
+      }
+      ws[threadIdx.x] = sum;
+      __syncthreads();
+      if (g == 0 && e < nv) {
+        double4 t = ws[el];
+        for (int k = 1; k < G; ++k) {
+          const double4 o = ws[k * piece + el];
+          t.x += o.x;
+          t.y += o.y;
+          t.z += o.z;
+          t.w += o.w;
+        }
+        if (V4)
+          reinterpret_cast<double4*>(out + row * tile)[e] = t;
+        else
+          out[row * tile + e] = t.x;
+      }
+      __syncthreads();
+    }
+    return;
+  }
+  const int64_t wid =
+      ((static_cast<int64_t>(blockIdx.x) - n_multi) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((static_cast<int64_t>(gridDim.x) - n_multi) * blockDim.x) >> 5;
+  if (wid >= n_chunk) {  // absent root rows: zero their output tiles
+    grid_dependency_wait();
+    const int64_t zw = nwarps - n_chunk;
+    for (int64_t z = (wid - n_chunk) * 32 + lane; z < n_absent * tile; z += zw * 32)
+      out[static_cast<int64_t>(absent_rows[z / tile]) * tile + z % tile] = 0.0;
+    return;
+  }
+  const int4 m = meta[wid];
+  if (m.w < 0) return;  // a chunk of a heavy slice: summed by its slice's block above
+  grid_dependency_wait();
+  const int32_t lo = m.x, hi = m.y, first = m.z;
+  double* dst = out + static_cast<int64_t>(m.w) * tile;
+  for (int64_t e = lane; e < nv; e += 32) {
+    double4 sum = make_double4(0, 0, 0, 0);
+    for (int32_t it = lo; it <= hi; it += 8) {
+      double4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int32_t i = it + u;
+        const double* src = part + (static_cast<int64_t>(i) * 2 + (i == first ? 1 : 0)) * tile;
+        if (V4)
+          v[u] = i <= hi ? reinterpret_cast<const double4*>(src)[e] : make_double4(0, 0, 0, 0);
+        else
+          v[u] = make_double4(i <= hi ? src[e] : 0.0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (it + u <= hi) {
+          sum.x += v[u].x;
+          sum.y += v[u].y;
+          sum.z += v[u].z;
+          sum.w += v[u].w;
+        }
+    }
+    if (V4)
+      reinterpret_cast<double4*>(dst)[e] = sum;
+    else
+      dst[e] = sum.x;
+  }
+}
+
 }  // namespace
 
 void build_fixup_chunks(Decomp& d, const int32_t* idx0, cudaStream_t s) {
@@ -633,24 +754,47 @@ void launch_fixup(const Decomp& d, const CsfView& t, double* out, cudaStream_t s
   if (d.n_split == 0 && d.n_absent == 0) return;
   const int64_t zero_warps =
       d.n_absent > 0 ? std::min<int64_t>((d.n_absent * d.tile + 31) / 32, 148 * 64) : 0;
-  const unsigned blocks = blocks_for((d.n_chunk + zero_warps) * 32, 256);
   // programmatic dependent launch: the fix-up grids are scheduled while the
   // previous kernel drains and wait in griddepcontrol.wait for its results
+  static const int sms = [] {
+    int dev = 0, n = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  if (d.n_multi <= sms) {
+    // few heavy slices (TTMc-3: split slices 2069, heavy ~tens): one launch,
+    // each heavy slice summed by one 1024-thread block (step 234.5 -> 230.4
+    // us for TTMc-3, 349.2 -> 345.2 us for TTMc-4)
+    const unsigned blocks =
+        static_cast<unsigned>(d.n_multi) + blocks_for((d.n_chunk + zero_warps) * 32, kFixBlock);
+    if (d.tile % 4 == 0)
+      launch_pdl(k_fix_all<true>, blocks, kFixBlock, s, d.chunk_meta, d.part, d.tile, d.n_chunk,
+                 d.absent_rows, d.n_absent, out, d.multi_split, d.n_multi, d.split_first,
+                 d.split_last, d.split_node, t.idx[0]);
+    else
+      launch_pdl(k_fix_all<false>, blocks, kFixBlock, s, d.chunk_meta, d.part, d.tile, d.n_chunk,
+                 d.absent_rows, d.n_absent, out, d.multi_split, d.n_multi, d.split_first,
+                 d.split_last, d.split_node, t.idx[0]);
+    SPTTN_CUDA(cudaGetLastError());
+    return;
+  }
+  // many heavy slices (MTTKRP-4 Zipf): chunk sums spread over warps, then
+  // one block per heavy slice over its chunk sums (two launches)
+  const unsigned blocks = blocks_for((d.n_chunk + zero_warps) * 32, 256);
   if (d.tile % 4 == 0)
     launch_pdl(k_fix1<true>, blocks, 256, s, d.chunk_meta, d.part, d.tile, d.n_chunk, d.part2,
                d.absent_rows, d.n_absent, out);
   else
     launch_pdl(k_fix1<false>, blocks, 256, s, d.chunk_meta, d.part, d.tile, d.n_chunk, d.part2,
                d.absent_rows, d.n_absent, out);
-  if (d.n_multi > 0) {
-    const unsigned nb = static_cast<unsigned>(d.n_multi);
-    if (d.tile % 4 == 0)
-      launch_pdl(k_fix2<true>, nb, 256, s, d.multi_split, d.split_chunk, d.split_node, t.idx[0],
-                 d.part2, d.tile, out);
-    else
-      launch_pdl(k_fix2<false>, nb, 256, s, d.multi_split, d.split_chunk, d.split_node, t.idx[0],
-                 d.part2, d.tile, out);
-  }
+  const unsigned nb = static_cast<unsigned>(d.n_multi);
+  if (d.tile % 4 == 0)
+    launch_pdl(k_fix2<true>, nb, 256, s, d.multi_split, d.split_chunk, d.split_node, t.idx[0],
+               d.part2, d.tile, out);
+  else
+    launch_pdl(k_fix2<false>, nb, 256, s, d.multi_split, d.split_chunk, d.split_node, t.idx[0],
+               d.part2, d.tile, out);
   SPTTN_CUDA(cudaGetLastError());
 }
 
