@@ -163,6 +163,19 @@ void copy_factors(spttn_plan* p, const double* const* src, bool on_device, cudaS
 
 }  // namespace
 
+// side stream per device for plan-time work that overlaps an asynchronous
+// values upload (build_packed's leaf-stream fill)
+cudaStream_t spttn_dev::aux_stream() {
+  static std::mutex mu;
+  static cudaStream_t st[64] = {};
+  int dev = 0;
+  SPTTN_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev < 0 || dev >= 64) throw spttn_dev::Status(SPTTN_ECUDA, "device ordinal out of range");
+  if (!st[dev]) SPTTN_CUDA(cudaStreamCreateWithFlags(&st[dev], cudaStreamNonBlocking));
+  return st[dev];
+}
+
 extern "C" {
 
 const char* spttn_last_error(void) { return g_err.c_str(); }
@@ -474,6 +487,7 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
     cudaStream_t s = as_stream(stream);
     auto p = new spttn_plan;
     raw = p;
+    cudaEvent_t fill_done = nullptr;  // packed-stream fill on the side stream (build_packed)
     const auto& D = csf->d;
     p->kind = desc->kind;
     p->flags = desc->flags;
@@ -832,8 +846,8 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
           int32_t* leaf_k = nullptr;
           dev_malloc(reinterpret_cast<void**>(&leaf_k), std::max<int64_t>(1, nnz) * sizeof(int32_t), s);
           spttn_dev::expand_coords(D, 2, D.idx[2], leaf_k, s);
-          spttn_dev::build_packed(D, 3, p->dec, s, spttn_dev::kPackSlots, leaf_k);
-          spttn_dev::dfree(leaf_k, s);
+          spttn_dev::build_packed(D, 3, p->dec, s, spttn_dev::kPackSlots, leaf_k, &fill_done);
+          spttn_dev::dfree(leaf_k, spttn_dev::aux_stream());  // read by the fill
           // mode 4: one item per resident warp of k_ttmc4pa (a single wave of
           // 12-warp CTAs; BASELINE shape: 1773 items 338 us, 2 waves 346 us,
           // the earlier 2.66 waves 391 us — the last partial wave idled a
@@ -858,7 +872,7 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
         } else if (p->kind == SPTTN_NEST_TTMC3) {
           // packed length-sorted groups of 8 segments (pack.cu)
           spttn_dev::build_segments(D, 1, seg_len, chunk, p->dec, tile, s, false);
-          spttn_dev::build_packed(D, 2, p->dec, s);
+          spttn_dev::build_packed(D, 2, p->dec, s, spttn_dev::kPackSlots, nullptr, &fill_done);
           int64_t gchunk = env_int("SPTTN_GCHUNK", 0);
           if (gchunk <= 0) {
             // mode 10: one item per resident warp (a single wave; 2.6 waves of
@@ -972,6 +986,11 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
       p->launches = 1 + ((p->dec.n_split > 0 || p->dec.n_absent > 0) ? 1 : 0) +
                     (p->dec.n_multi > 0 ? 1 : 0);
       if (p->kind == SPTTN_NEST_MTTKRP3 && p->mode == 4) p->launches = 1;  // no fix-up pass
+    }
+    if (fill_done) {  // packed leaf streams filled on the side stream
+      SPTTN_CUDA(cudaStreamWaitEvent(s, fill_done, 0));
+      SPTTN_CUDA(cudaEventDestroy(fill_done));
+      fill_done = nullptr;
     }
     spttn_dev::plan_trace("plan: decomposition", s);
     SPTTN_CUDA(cudaStreamSynchronize(s));

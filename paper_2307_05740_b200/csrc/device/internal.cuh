@@ -238,8 +238,17 @@ void finish_unit_items(const DevCsf& csf, Decomp& d, const int32_t* slice_units,
 constexpr int kPackSlots = 8;  // TTMc-3 groups (128-byte rows)
 // leaf_coord2 (optional, per leaf) is packed alongside as pk2 (TTMc-4: the
 // leaf's level-2 coordinate).
+// fill_done != nullptr: the leaf streams (pk / pk2 / pv) and the group leaf
+// bases (grp_hdr .x) are filled on a side stream that waits for the CSF
+// values, so the plan's item / fix-up work on `s` overlaps an asynchronous
+// values upload; *fill_done is recorded when they are complete (the caller
+// makes its stream wait on it and destroys it). Group lengths / slices
+// (.y / .w), slot coordinates and slice_grp are ready on `s` either way.
 void build_packed(const DevCsf& csf, int leaf_level, Decomp& d, cudaStream_t s,
-                  int slots = kPackSlots, const int32_t* leaf_coord2 = nullptr);
+                  int slots = kPackSlots, const int32_t* leaf_coord2 = nullptr,
+                  cudaEvent_t* fill_done = nullptr);
+// side stream per device (plan-time work overlapping the values upload)
+cudaStream_t aux_stream();
 constexpr int kFixChunk = 8;  // items per pass-1 chunk (one batch of loads)
 void build_fixup_chunks(Decomp& d, const int32_t* idx0, cudaStream_t s);
 void launch_fixup(const Decomp& d, const CsfView& t, double* out, cudaStream_t s);

@@ -140,7 +140,7 @@ struct MaxOp {
 }  // namespace
 
 void build_packed(const DevCsf& csf, int leaf_level, Decomp& d, cudaStream_t s, int slots,
-                  const int32_t* leaf_coord2) {
+                  const int32_t* leaf_coord2, cudaEvent_t* fill_done) {
   plan_trace("pack: enter", s);
   const int32_t nseg = static_cast<int32_t>(d.n_seg);
   const int32_t n0 = static_cast<int32_t>(csf.level_size[0]);
@@ -219,22 +219,41 @@ void build_packed(const DevCsf& csf, int leaf_level, Decomp& d, cudaStream_t s, 
     SPTTN_CUDA(cudaMemsetAsync(d.pk2, 0, nl * sizeof(int32_t), s));
   }
   const CsfView t = csf.view();
-  csf.wait_values(s);  // the structure work above overlaps an async values upload
-  k_fill_groups<<<nblk(nseg, 256), 256, 0, s>>>(ids2, runstart, gid, leaf_off, d.seg_begin,
-                                                d.seg_node, d.seg_node1, t.idx[leaf_level],
-                                                leaf_coord2, t.vals, nseg, slots, d.grp_hdr,
-                                                d.grp_node, d.grp_node1, d.pk, d.pk2, d.pv);
+  // the fill needs the leaf values: on a side stream when the caller lets
+  // the rest of the plan run meanwhile (values may still be on the link)
+  cudaStream_t fs = s;
+  if (fill_done) {
+    fs = aux_stream();
+    cudaEvent_t ready = nullptr;
+    SPTTN_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    SPTTN_CUDA(cudaEventRecord(ready, s));
+    SPTTN_CUDA(cudaStreamWaitEvent(fs, ready, 0));
+    SPTTN_CUDA(cudaEventDestroy(ready));
+  }
+  csf.wait_values(fs);  // the structure work above overlaps an async values upload
+  k_fill_groups<<<nblk(nseg, 256), 256, 0, fs>>>(ids2, runstart, gid, leaf_off, d.seg_begin,
+                                                 d.seg_node, d.seg_node1, t.idx[leaf_level],
+                                                 leaf_coord2, t.vals, nseg, slots, d.grp_hdr,
+                                                 d.grp_node, d.grp_node1, d.pk, d.pk2, d.pv);
   dmalloc(&d.slice_grp, (static_cast<int64_t>(n0) + 1) * sizeof(int32_t), s);
   k_slice_groups<<<nblk(static_cast<int64_t>(ngroups) + 1, 256), 256, 0, s>>>(d.grp_hdr, ngroups,
                                                                             n0, d.slice_grp);
   SPTTN_CUDA(cudaGetLastError());
   for (void* p : {static_cast<void*>(keys), static_cast<void*>(keys2), static_cast<void*>(ids),
-                  static_cast<void*>(ids2), static_cast<void*>(head),
-                  static_cast<void*>(runstart), static_cast<void*>(end_at_start),
-                  static_cast<void*>(runend), static_cast<void*>(flag), static_cast<void*>(gid),
-                  static_cast<void*>(gleaves), static_cast<void*>(leaf_off)})
+                  static_cast<void*>(head), static_cast<void*>(end_at_start),
+                  static_cast<void*>(runend), static_cast<void*>(flag),
+                  static_cast<void*>(gleaves)})
     dfree(p, s);
-  SPTTN_CUDA(cudaStreamSynchronize(s));
+  // the fill's inputs are released in its own stream order
+  for (void* p : {static_cast<void*>(ids2), static_cast<void*>(runstart), static_cast<void*>(gid),
+                  static_cast<void*>(leaf_off)})
+    dfree(p, fs);
+  if (fill_done) {
+    SPTTN_CUDA(cudaEventCreateWithFlags(fill_done, cudaEventDisableTiming));
+    SPTTN_CUDA(cudaEventRecord(*fill_done, fs));
+  } else {
+    SPTTN_CUDA(cudaStreamSynchronize(s));
+  }
 }
 
 }  // namespace spttn_dev
