@@ -936,7 +936,7 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
         }
         if (p->mode == 2 || p->mode == 3) {
           spttn_dev::build_segments(D, unit_level, seg_len, chunk, p->dec, tile, s, false);
-          spttn_dev::build_packed(D, D.order - 1, p->dec, s, 4);
+          spttn_dev::build_packed(D, D.order - 1, p->dec, s, 4, nullptr, &fill_done);
           // order 3: one item per resident warp (k_mttkrp_pk: 4 CTAs of 8
           // warps per SM) — a single wave, and root slices stay within one
           // fix-up chunk (one fix-up kernel)
