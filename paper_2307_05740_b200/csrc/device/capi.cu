@@ -983,8 +983,10 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
         else
           spttn_dev::build_leaf_items(D, chunk, p->dec, tile, s);
       }
+      // fix-up: one launch, plus a second when the heavy split slices exceed
+      // one wave (decomp.cu launch_fixup)
       p->launches = 1 + ((p->dec.n_split > 0 || p->dec.n_absent > 0) ? 1 : 0) +
-                    (p->dec.n_multi > 0 ? 1 : 0);
+                    (p->dec.n_multi > sms ? 1 : 0);
       if (p->kind == SPTTN_NEST_MTTKRP3 && p->mode == 4) p->launches = 1;  // no fix-up pass
     }
     if (fill_done) {  // packed leaf streams filled on the side stream
