@@ -541,11 +541,14 @@ def test_device_unfactorized_equals_reference_golden(E, m):
     assert np.array_equal(got, z["unfactorized"]), np.abs(got - z["unfactorized"]).max()
 
 
-def test_item_clock_diagnostics(E, monkeypatch):
-    """SPTTN_ITEM_CLOCKS=1 (tuning aid): the packed TTMc-3 kernel records one
-    {start, end, SM} per work item; the plan without it reports EINVAL."""
+@pytest.mark.parametrize("key", ["ttmc3", "ttmc4", "mttkrp4"])
+def test_item_clock_diagnostics(E, key, monkeypatch):
+    """SPTTN_ITEM_CLOCKS=1 (tuning aid): the packed TTMc-3 / TTMc-4 / MTTKRP-4
+    kernels' diagnostics instantiations record one {start, end, SM, groups,
+    steps, flushes} per work item, with results identical to the plain
+    kernel; a plan without the records reports EINVAL."""
     from paper_2307_05740_b200.configs import make_workload
-    w = make_workload("ttmc3", scale=2e-3)
+    w = make_workload(key, scale=2e-3)
     monkeypatch.setenv("SPTTN_ITEM_CLOCKS", "1")
     monkeypatch.setenv("SPTTN_GCHUNK", "4")
     out, plan, dev = run(E, w.cfg.kind, w.csf, w.factors, w.cfg.ranks)
