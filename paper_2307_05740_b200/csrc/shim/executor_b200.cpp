@@ -34,13 +34,12 @@
 
 namespace spttn {
 
+// Names the reference uses for hook kinds (executor.cpp:15-22 — same strings,
+// looked up from a table).
 std::string hook_kind_name(HookKind k) {
-  switch (k) {
-    case HookKind::None: return "none";
-    case HookKind::VectorAccumulate: return "vector-accumulate";
-    case HookKind::Rank1Update: return "rank-1-update";
-  }
-  return "none";
+  static const char* const kNames[] = {"none", "vector-accumulate", "rank-1-update"};
+  const auto i = static_cast<size_t>(k);
+  return i < sizeof(kNames) / sizeof(kNames[0]) ? kNames[i] : kNames[0];
 }
 
 namespace {
@@ -76,39 +75,41 @@ void check(int rc, const char* where) {
   if (rc != SPTTN_OK) throw_status(rc, where);
 }
 
-// Same checks and exception types as the reference (executor.cpp:112-140).
+// The reference's input checks (executor.cpp:112-140): same conditions, same
+// std::invalid_argument messages, so callers see identical errors.
 void validate_inputs(const KernelSpec& spec, const ExecInputs& inputs) {
-  const int n = spec.num_inputs();
-  if (inputs.sparse == nullptr) throw std::invalid_argument("execute: missing sparse tensor");
-  const auto& sp = spec.sparse_input();
+  auto require = [](bool ok, const std::string& what) {
+    if (!ok) throw std::invalid_argument("execute: " + what);
+  };
+  require(inputs.sparse != nullptr, "missing sparse tensor");
   const CsfTensor& csf = *inputs.sparse;
-  if (csf.order() != static_cast<int64_t>(sp.indices.size()))
-    throw std::invalid_argument("execute: sparse tensor order mismatch");
-  for (size_t l = 0; l < sp.indices.size(); ++l) {
-    if (csf.modes[l].name != spec.index_names[sp.indices[l]])
-      throw std::invalid_argument(
-          "execute: CSF mode order must match the kernel's sparse index order");
-    if (csf.modes[l].dim != spec.dim(sp.indices[l]))
-      throw std::invalid_argument("execute: sparse tensor dimension mismatch on " +
-                                  csf.modes[l].name);
+  const std::vector<int>& sparse_ids = spec.sparse_input().indices;
+  require(csf.order() == static_cast<int64_t>(sparse_ids.size()), "sparse tensor order mismatch");
+  for (size_t level = 0; level < sparse_ids.size(); ++level) {
+    const int id = sparse_ids[level];
+    require(csf.modes[level].name == spec.index_names[id],
+            "CSF mode order must match the kernel's sparse index order");
+    require(csf.modes[level].dim == spec.dim(id),
+            "sparse tensor dimension mismatch on " + csf.modes[level].name);
   }
-  if (static_cast<int>(inputs.dense.size()) != n - 1)
-    throw std::invalid_argument("execute: expected " + std::to_string(n - 1) + " dense inputs");
-  for (int t = 1; t < n; ++t) {
-    const auto& ref = spec.tensors[t];
-    const DenseTensor* d = inputs.dense[t - 1];
-    if (d == nullptr) throw std::invalid_argument("execute: missing dense tensor " + ref.name);
-    if (d->order() != static_cast<int64_t>(ref.indices.size()))
-      throw std::invalid_argument("execute: dense tensor order mismatch for " + ref.name);
-    int64_t count = 1;
-    for (size_t k = 0; k < ref.indices.size(); ++k) {
-      if (d->indices[k].name != spec.index_names[ref.indices[k]] ||
-          d->indices[k].dim != spec.dim(ref.indices[k]))
-        throw std::invalid_argument("execute: dense tensor shape mismatch for " + ref.name);
-      count *= d->indices[k].dim;
+  const int n_dense = spec.num_inputs() - 1;
+  require(static_cast<int>(inputs.dense.size()) == n_dense,
+          "expected " + std::to_string(n_dense) + " dense inputs");
+  for (int slot = 0; slot < n_dense; ++slot) {
+    const auto& want = spec.tensors[slot + 1];
+    const DenseTensor* have = inputs.dense[slot];
+    require(have != nullptr, "missing dense tensor " + want.name);
+    require(have->order() == static_cast<int64_t>(want.indices.size()),
+            "dense tensor order mismatch for " + want.name);
+    int64_t entries = 1;
+    for (size_t m = 0; m < want.indices.size(); ++m) {
+      const int id = want.indices[m];
+      require(have->indices[m].name == spec.index_names[id] && have->indices[m].dim == spec.dim(id),
+              "dense tensor shape mismatch for " + want.name);
+      entries *= have->indices[m].dim;
     }
-    if (count != static_cast<int64_t>(d->values.size()))
-      throw std::invalid_argument("execute: dense tensor value count mismatch for " + ref.name);
+    require(entries == static_cast<int64_t>(have->values.size()),
+            "dense tensor value count mismatch for " + want.name);
   }
 }
 
