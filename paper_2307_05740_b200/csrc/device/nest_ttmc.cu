@@ -118,13 +118,18 @@ __global__ void __launch_bounds__(kBlock, 3) k_ttmc3pq(RootOutArgs a) {
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt)
+      for (int nt = 0; nt < 2; ++nt) {
+        const int r = 8 * mt + fh;
+        const int s = 8 * nt + 2 * fq;  // the lane's two columns s, s + 1
+        if (VECV && r < R && s < S_) {  // S % 4 == 0: the pair is in range, 16-byte aligned
+          *reinterpret_cast<double2*>(dst + r * S_ + s) =
+              make_double2(acc[(mt * 2 + nt) * 2], acc[(mt * 2 + nt) * 2 + 1]);
+        } else {
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int r = 8 * mt + fh;
-          const int s = 8 * nt + 2 * fq + e;
-          if (r < R && s < S_) dst[r * S_ + s] = acc[(mt * 2 + nt) * 2 + e];
+          for (int e = 0; e < 2; ++e)
+            if (r < R && s + e < S_) dst[r * S_ + s + e] = acc[(mt * 2 + nt) * 2 + e];
         }
+      }
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[e] = 0.0;
   };
@@ -533,14 +538,18 @@ __global__ void __launch_bounds__(NB, MB) k_ttmc4pa(RootOutArgs a) {
   auto flush = [&](int dslot) {
     double* dst = dslot < 0 ? a.out + static_cast<int64_t>(row) * tile
                             : a.part + (w * 2 + dslot) * tile;
+    // n-tiles 2m and 2m+1 hold the adjacent columns tt, tt + 1 of the same
+    // (h, ss) row: one 16-byte store per pair
 #pragma unroll
-    for (int nb = 0; nb < 8; ++nb)
+    for (int m = 0; m < 4; ++m)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int c = 2 * q + e;
-        const int ss = 4 * (c & 1) + (nb >> 1);
-        const int tt = 2 * (c >> 1) + (nb & 1);
-        if (h < R) dst[(h * 8 + ss) * 8 + tt] = acc[2 * nb + e];
+        const int ss = 4 * (c & 1) + m;
+        const int tt = 2 * (c >> 1);
+        if (h < R)
+          *reinterpret_cast<double2*>(dst + (h * 8 + ss) * 8 + tt) =
+              make_double2(acc[2 * (2 * m) + e], acc[2 * (2 * m + 1) + e]);
       }
 #pragma unroll
     for (int e = 0; e < 16; ++e) acc[e] = 0.0;
