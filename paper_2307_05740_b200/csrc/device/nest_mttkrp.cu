@@ -199,7 +199,10 @@ __global__ void __launch_bounds__(kBlock, 3) k_mttkrp_pq(RootOutArgs a) {
     if (slot == 0) {
       double* dst = dslot < 0 ? a.out + static_cast<int64_t>(row) * R
                               : a.part + (w * 2 + dslot) * static_cast<int64_t>(R);
-      store4(dst, c, R, make_double4(v[0], v[1], v[2], v[3]));
+      if (VEC && RC > 0)  // full 32-byte sectors (R = RC: every quad in range, aligned)
+        *reinterpret_cast<double4*>(dst + c) = make_double4(v[0], v[1], v[2], v[3]);
+      else
+        store4(dst, c, R, make_double4(v[0], v[1], v[2], v[3]));
     }
     acc = make_double4(0, 0, 0, 0);
   };
