@@ -22,8 +22,10 @@ HOSTFLAGS := -std=c++20 -O2 -fPIC -I$(REF)/include -Iinclude -I$(PKG)/csrc/devic
 
 DEV_OBJS  := $(patsubst $(PKG)/csrc/device/%.cu,build/device/%.o,$(DEV_SRC))
 
-all: device datagen probe oracle host
+all: device debug datagen probe oracle host
 device: $(LIB)/libspttn_b200.so
+# bounds-checked engine (device SPTTN_DCHECKs; SPTTN_DEBUG_BOUNDS=1 loads it)
+debug: $(LIB)/debug/libspttn_b200.so
 probe: $(LIB)/libspttn_probe.so
 datagen: $(LIB)/libspttn_datagen.so
 HAVE_HOST := $(and $(wildcard $(REF)/src/loop_nest.cpp),$(wildcard $(PKG)/csrc/shim/executor_b200.cpp))
@@ -46,6 +48,17 @@ build/device/generic.o: $(PKG)/csrc/device/generic.cu $(DEV_HDR)
 
 $(LIB)/libspttn_b200.so: $(DEV_OBJS)
 	@mkdir -p $(LIB)
+	$(NVCC) $(ARCH) -shared $^ -o $@ -lnvrtc -Xlinker -rpath,/usr/local/cuda/lib64
+
+DBG_OBJS  := $(patsubst $(PKG)/csrc/device/%.cu,build/device_dbg/%.o,$(DEV_SRC))
+build/device_dbg/%.o: $(PKG)/csrc/device/%.cu $(DEV_HDR)
+	@mkdir -p $(dir $@)
+	$(NVCC) $(NVFLAGS) -DSPTTN_DEBUG_BOUNDS -c $< -o $@
+build/device_dbg/generic.o: $(PKG)/csrc/device/generic.cu $(DEV_HDR)
+	@mkdir -p $(dir $@)
+	$(NVCC) $(NVFLAGS) -DSPTTN_DEBUG_BOUNDS -fmad=false -c $< -o $@
+$(LIB)/debug/libspttn_b200.so: $(DBG_OBJS)
+	@mkdir -p $(LIB)/debug
 	$(NVCC) $(ARCH) -shared $^ -o $@ -lnvrtc -Xlinker -rpath,/usr/local/cuda/lib64
 
 $(LIB)/libspttn_probe.so: $(PKG)/csrc/probe/fp64_peak.cu
@@ -89,7 +102,7 @@ clean:
 	rm -rf build $(LIB)
 	$(MAKE) -C oracle clean
 
-.PHONY: all device datagen probe host oracle clean
+.PHONY: all device debug datagen probe host oracle clean
 
 build/tests/plan_overhead: tests/cpp/plan_overhead.cpp $(LIB)/libspttn_b200_host.so
 	@mkdir -p $(dir $@)

@@ -89,7 +89,9 @@ def _load(name: str) -> C.CDLL:
 def engine() -> C.CDLL:
     global _engine
     if _engine is None:
-        lib = _load("libspttn_b200.so")
+        # SPTTN_DEBUG_BOUNDS=1: the bounds-checked build (device SPTTN_DCHECKs)
+        lib = _load("debug/libspttn_b200.so" if os.environ.get("SPTTN_DEBUG_BOUNDS") == "1"
+                    else "libspttn_b200.so")
         P = C.c_void_p
         lib.spttn_last_error.restype = C.c_char_p
         lib.spttn_build_info.restype = C.c_char_p

@@ -163,6 +163,13 @@ void copy_factors(spttn_plan* p, const double* const* src, bool on_device, cudaS
 
 }  // namespace
 
+namespace spttn_dev {
+// make `s` wait for a pending packed-stream fill (no-op when none)
+inline void csf_wait_fill(cudaEvent_t fill_done, cudaStream_t s) {
+  if (fill_done) SPTTN_CUDA(cudaStreamWaitEvent(s, fill_done, 0));
+}
+}  // namespace spttn_dev
+
 // side stream per device for plan-time work that overlaps an asynchronous
 // values upload (build_packed's leaf-stream fill)
 cudaStream_t spttn_dev::aux_stream() {
@@ -890,6 +897,16 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
           const int ovh = static_cast<int>(env_int("SPTTN_GROUP_OVERHEAD", 4));
           spttn_dev::finish_unit_items(D, p->dec, p->dec.slice_grp, p->dec.n_groups, gchunk, tile, s,
                                        ovh);
+#ifdef SPTTN_DEBUG_BOUNDS
+          // bounds-checked build only: SPTTN_DEBUG_POISON=1 plants an
+          // out-of-range leaf coordinate so tests can see the checks fire
+          if (env_int("SPTTN_DEBUG_POISON", 0) == 1 && p->dec.n_packed_leaves > 0) {
+            spttn_dev::csf_wait_fill(fill_done, s);
+            const int32_t bad = static_cast<int32_t>(D.dims[2] + 5);
+            SPTTN_CUDA(cudaMemcpyAsync(p->dec.pk, &bad, sizeof(bad), cudaMemcpyHostToDevice, s));
+            SPTTN_CUDA(cudaStreamSynchronize(s));
+          }
+#endif
           if (env_int("SPTTN_ITEM_CLOCKS", 0) == 1) {  // recorded by the 256-bit-gather kernel only
             const int64_t cb = std::max<int64_t>(1, 6 * p->dec.n_items) * sizeof(long long);
             dev_malloc(reinterpret_cast<void**>(&p->item_clk), cb, s);
@@ -1061,6 +1078,7 @@ int spttn_execute_stage(spttn_plan* p, int stage, void* stream) {
     a.part = p->dec.part;
     a.flags = ((p->flags & SPTTN_FLAG_RESIDUAL) ? 1 : 0) | (p->mode << 8);
     a.clk = p->item_clk;
+    for (int l = 0; l < 4; ++l) a.frows[l] = l < D.order ? D.dims[l] : 0;
     a.seg_begin = p->dec.seg_begin;
     a.seg_node = p->dec.seg_node;
     a.slice_seg = p->dec.slice_seg;

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 #include <stdexcept>
 #include <string>
@@ -24,6 +25,26 @@ struct Status : std::runtime_error {
   } while (0)
 
 constexpr int kWarp = 32;
+
+// Device bounds checks of the bounds-checked build (make debug ->
+// lib/debug/libspttn_b200.so, loaded with SPTTN_DEBUG_BOUNDS=1): every factor
+// row a kernel gathers, every staged-window index and every output row is
+// checked; a violation prints the site and traps the kernel. compute-sanitizer
+// is closed on this GPU pool, so this build is the memory-safety check the
+// tests run (tests/test_gpu_bounds.py). The product library compiles them out.
+#ifdef SPTTN_DEBUG_BOUNDS
+#define SPTTN_DCHECK(cond)                                                          \
+  do {                                                                              \
+    if (!(cond)) {                                                                  \
+      printf("SPTTN_DCHECK failed %s:%d: %s\n", __FILE__, __LINE__, #cond);          \
+      __trap();                                                                     \
+    }                                                                               \
+  } while (0)
+#else
+#define SPTTN_DCHECK(cond) \
+  do {                     \
+  } while (0)
+#endif
 
 __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
 

@@ -154,6 +154,7 @@ struct RootOutArgs {
   int64_t n_groups;
   const int32_t* item_unit;  // variable item boundaries (TTMc-3 default kernel) or nullptr
   long long* clk;            // per item {start ns, end ns, smid} (diagnostics) or nullptr
+  int64_t frows[4];          // rows of f[l] (= CSF mode sizes; bounds-checked build)
 };
 
 void launch_mttkrp3(const RootOutArgs& a, cudaStream_t s);

@@ -233,6 +233,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_mttkrp_pq(RootOutArgs a) {
     const int32_t L0 = uni(S.hdr[b][0].x);
     const int32_t L1 = uni(S.hdr[b][nw - 1].x + kMSlots * S.hdr[b][nw - 1].y);
     const unsigned n = static_cast<unsigned>(L1 - L0);
+    SPTTN_DCHECK(n <= static_cast<unsigned>(kMWLeaves));
     fence_proxy_async();
     expect_tx_elect(&S.mbar_leaf[lb], n * 12u);
     bulk_g2s_elect(&S.kk[lb][0], a.pk + L0, n * 4u, &S.mbar_leaf[lb]);
@@ -267,6 +268,9 @@ __global__ void __launch_bounds__(kBlock, 3) k_mttkrp_pq(RootOutArgs a) {
       const int32_t u = S.node[mb][(g - g0) * kMSlots + slot];
       const int32_t j = ORDER == 4 ? S.node1[mb][(g - g0) * kMSlots + slot] : 0;
       const int32_t lbase = hh.x - L0 + slot;
+      SPTTN_DCHECK(u >= 0 && u < a.frows[ORDER - 2]);
+      SPTTN_DCHECK(ORDER == 3 || (j >= 0 && j < a.frows[1]));
+      SPTTN_DCHECK(lbase + (n - 1) * kMSlots < kMWLeaves);
       const double4 ur = rowq(Funit, u, true);
       double4 tr = make_double4(0, 0, 0, 0);
       if (ORDER == 4) {
@@ -293,6 +297,8 @@ __global__ void __launch_bounds__(kBlock, 3) k_mttkrp_pq(RootOutArgs a) {
           tt[it] = S.tv[lbf][lbase + it * kMSlots];
         }
         double4 rr[kN];
+#pragma unroll
+        for (int it = 0; it < kN; ++it) SPTTN_DCHECK(kk[it] >= 0 && kk[it] < a.frows[ORDER - 1]);
 #pragma unroll
         for (int it = 0; it < kN; ++it) rr[it] = rowq(Fleaf, kk[it], true);
         // first step as a product (= fma with a zero addend, bit for bit)

@@ -115,6 +115,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_ttmc3pq(RootOutArgs a) {
   auto flush = [&](int dslot) {
     double* dst = dslot < 0 ? a.out + static_cast<int64_t>(row) * R * S_
                             : a.part + (w * 2 + dslot) * static_cast<int64_t>(R) * S_;
+    SPTTN_DCHECK(dslot >= 0 || (row >= 0 && row < a.frows[0]));
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -151,6 +152,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_ttmc3pq(RootOutArgs a) {
     const int32_t L0 = uni(S.hdr[b][0].x);
     const int32_t L1 = uni(S.hdr[b][nw - 1].x + kPackSlots * S.hdr[b][nw - 1].y);
     const unsigned n = static_cast<unsigned>(L1 - L0);
+    SPTTN_DCHECK(n <= static_cast<unsigned>(kGWLeaves));
     fence_proxy_async();
     expect_tx_elect(&S.mbar_leaf[lb], n * 12u);
     bulk_g2s_elect(&S.kk[lb][0], a.pk + L0, n * 4u, &S.mbar_leaf[lb]);
@@ -189,6 +191,8 @@ __global__ void __launch_bounds__(kBlock, 3) k_ttmc3pq(RootOutArgs a) {
       if (CLK) dbg_steps += n;
       const int32_t lbase = hh.x - L0 + gs;
       const int32_t j = S.node[mb][(g - g0) * kPackSlots + gs];
+      SPTTN_DCHECK(j >= 0 && j < a.frows[1]);
+      SPTTN_DCHECK(lbase + (n - 1) * kPackSlots < kGWLeaves);
       const double4 ur = row4<VECU>(U + static_cast<int64_t>(j) * R, 4 * gc, R);
       // X[s] += t * V[k,s] over the group's n (warp-uniform) leaf steps,
       // specialised per n: no predicated-off stream loads / gathers / FMAs
@@ -203,6 +207,8 @@ __global__ void __launch_bounds__(kBlock, 3) k_ttmc3pq(RootOutArgs a) {
           tt[it] = S.tv[lbf][lbase + it * kPackSlots];
         }
         double4 vr[kN];
+#pragma unroll
+        for (int it = 0; it < kN; ++it) SPTTN_DCHECK(kk[it] >= 0 && kk[it] < a.frows[2]);
 #pragma unroll
         for (int it = 0; it < kN; ++it) {
           if (VECV)
@@ -572,6 +578,7 @@ __global__ void __launch_bounds__(NB, MB) k_ttmc4pa(RootOutArgs a) {
     const int32_t L0 = uni(S.hdr[b][0].x);
     const int32_t L1 = uni(S.hdr[b][nw - 1].x + kPackSlots * S.hdr[b][nw - 1].y);
     const unsigned n = static_cast<unsigned>(L1 - L0);
+    SPTTN_DCHECK(n <= static_cast<unsigned>(kGWLeaves));
     fence_proxy_async();
     expect_tx_elect(&S.mbar_leaf[lb], n * 16u);
     bulk_g2s_elect(&S.ll[lb][0], a.pk + L0, n * 4u, &S.mbar_leaf[lb]);
@@ -583,6 +590,9 @@ __global__ void __launch_bounds__(NB, MB) k_ttmc4pa(RootOutArgs a) {
   // for the L1-allocating .ca at the BASELINE shape (fewer L1 wavefronts per
   // copy; the 128 KB V / W are L2-resident)
   auto issue_rows = [&](int buf, int lbuf, int32_t e) {
+    SPTTN_DCHECK(e >= 0 && e < kGWLeaves);
+    SPTTN_DCHECK(S.kk[lbuf][e] >= 0 && S.kk[lbuf][e] < a.frows[2]);
+    SPTTN_DCHECK(S.ll[lbuf][e] >= 0 && S.ll[lbuf][e] < a.frows[3]);
     cp_async16_cg(&S.vs[buf][st_off], V + static_cast<int64_t>(S.kk[lbuf][e]) * 8 + 2 * gc, 16);
     cp_async16_cg(&S.ws[buf][st_off], W + static_cast<int64_t>(S.ll[lbuf][e]) * 8 + 2 * gc, 16);
     cp_async_commit();
@@ -619,6 +629,7 @@ __global__ void __launch_bounds__(NB, MB) k_ttmc4pa(RootOutArgs a) {
       if (CLK) dbg_steps += n;
       const int32_t jA = S.node[mb][(g - g0) * kPackSlots + q];
       const int32_t jB = S.node[mb][(g - g0) * kPackSlots + 4 + q];
+      SPTTN_DCHECK(jA >= 0 && jA < a.frows[1] && jB >= 0 && jB < a.frows[1]);
       const double uA = h < R ? __ldg(U + static_cast<int64_t>(jA) * R + h) : 0.0;
       const double uB = h < R ? __ldg(U + static_cast<int64_t>(jB) * R + h) : 0.0;
       double YA[8], YB[8];

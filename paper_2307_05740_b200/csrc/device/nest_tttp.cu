@@ -56,6 +56,8 @@ __global__ void __launch_bounds__(kBlock) k_tttp3_piece(RootOutArgs a, const int
   for (int64_t pc = static_cast<int64_t>(blockIdx.x) * (kBlock / 32) + threadIdx.x / 32;
        pc < n_pieces; pc += warps) {
     const int4 piece = __ldg(pieces + pc);  // {i, leaf lo, leaf hi, -}, warp-uniform
+    SPTTN_DCHECK(piece.x >= 0 && piece.x < a.frows[0] && piece.y <= piece.z &&
+                 piece.z <= a.t.nlev[2]);
     const double4 ar = row4<VEC>(A + static_cast<int64_t>(piece.x) * R, c, R);
     for (int32_t b = piece.y; b < piece.z; b += kStep) {
       const int32_t base = b + grp * U;
@@ -67,6 +69,7 @@ __global__ void __launch_bounds__(kBlock) k_tttp3_piece(RootOutArgs a, const int
         const int2 jk = ok ? __ldg(leaf_jk + base + u) : make_int2(0, 0);  // one 8-byte load
         jj[u] = jk.x;
         kk[u] = jk.y;
+        SPTTN_DCHECK(jk.x >= 0 && jk.x < a.frows[1] && jk.y >= 0 && jk.y < a.frows[2]);
         tv[u] = ok ? __ldg(vals + base + u) : 0.0;
       }
       double part[U];
