@@ -129,6 +129,7 @@ __global__ void __launch_bounds__(kSmfWarps * 32, 1) k_mttkrp3_smf(RootOutArgs a
     const int32_t L1 =
         uni(S.hdr[b][o + nw - 1].x + kSSlots * (S.hdr[b][o + nw - 1].y & 7));
     const unsigned n = static_cast<unsigned>(L1 - L0);
+    SPTTN_DCHECK(n <= static_cast<unsigned>(kSWLeaves));
     fence_proxy_async();
     expect_tx_elect(&S.mbar_leaf[lb], n * 12u);
     bulk_g2s_elect(&S.kk[lb][0], a.pk + L0, n * 4u, &S.mbar_leaf[lb]);
@@ -184,6 +185,7 @@ __global__ void __launch_bounds__(kSmfWarps * 32, 1) k_mttkrp3_smf(RootOutArgs a
   double2 b0 = make_double2(0, 0), b1 = make_double2(0, 0);
   auto load_b = [&](int buf, int gi) {
     const int2 jj = *reinterpret_cast<const int2*>(&S.node[buf][gi * kSSlots + 2 * sp]);
+    SPTTN_DCHECK(jj.x >= 0 && jj.x < a.frows[1] * a.R && jj.y >= 0 && jj.y < a.frows[1] * a.R);
     b0 = ld128(Bh + jj.x);
     b1 = ld128(Bh + jj.y);
   };
@@ -221,7 +223,9 @@ __global__ void __launch_bounds__(kSmfWarps * 32, 1) k_mttkrp3_smf(RootOutArgs a
       const int lb = hh.x - L0 + 2 * sp;
       double2 X0 = make_double2(0, 0), X1 = make_double2(0, 0);
       auto leaf = [&](int it) {
+        SPTTN_DCHECK(lb + it * kSSlots + 1 < kSWLeaves);
         const int2 k2 = *reinterpret_cast<const int2*>(&S.kk[lbf][lb + it * kSSlots]);
+        SPTTN_DCHECK(k2.x >= 0 && k2.x < x.rows_c * 128 && k2.y >= 0 && k2.y < x.rows_c * 128);
         const double2 t2 = *reinterpret_cast<const double2*>(&S.tv[lbf][lb + it * kSSlots]);
         const double2 c0 = lds128(cs + k2.x);
         const double2 c1 = lds128(cs + k2.y);
