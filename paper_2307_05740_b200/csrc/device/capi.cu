@@ -828,8 +828,11 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
         if (p->kind == SPTTN_NEST_TTMC3) {
           // packed, TMA-staged, row-contiguous gathers (k_ttmc3pq); the
           // earlier variants (modes 0, 4, 6, 7, 11), the shuffle-transposed
-          // and the cp.async-fed kernels lost and were removed
+          // and the fully cp.async-fed kernels lost and were removed;
+          // 16 = mode 10 with U rows and single-leaf V rows fed by cp.async
           p->mode = 10;
+          if (env_int("SPTTN_TTMC3_PF", 1) == 1 && R == 16 && S == 16 && (p->vec & 4) && (p->vec & 8))
+            p->mode = 16;  // tiles fed by cp.async one group ahead (pair-permuted packing)
           seg_len = std::clamp(seg_len, 1, 4);
         }
         seg_len = std::max(seg_len, 1);
@@ -879,7 +882,8 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
         } else if (p->kind == SPTTN_NEST_TTMC3) {
           // packed length-sorted groups of 8 segments (pack.cu)
           spttn_dev::build_segments(D, 1, seg_len, chunk, p->dec, tile, s, false);
-          spttn_dev::build_packed(D, 2, p->dec, s, spttn_dev::kPackSlots, nullptr, &fill_done);
+          spttn_dev::build_packed(D, 2, p->dec, s, spttn_dev::kPackSlots, nullptr, &fill_done,
+                                  p->mode == 16);
           int64_t gchunk = env_int("SPTTN_GCHUNK", 0);
           if (gchunk <= 0) {
             // mode 10: one item per resident warp (a single wave; 2.6 waves of

@@ -245,9 +245,11 @@ constexpr int kPackSlots = 8;  // TTMc-3 groups (128-byte rows)
 // values upload; *fill_done is recorded when they are complete (the caller
 // makes its stream wait on it and destroys it). Group lengths / slices
 // (.y / .w), slot coordinates and slice_grp are ready on `s` either way.
+// pair_perm: slot s stored at position 2(s % (slots/2)) + s / (slots/2) of
+// its group's slot-coordinate and leaf rows (slots a and a + slots/2 adjacent).
 void build_packed(const DevCsf& csf, int leaf_level, Decomp& d, cudaStream_t s,
                   int slots = kPackSlots, const int32_t* leaf_coord2 = nullptr,
-                  cudaEvent_t* fill_done = nullptr);
+                  cudaEvent_t* fill_done = nullptr, bool pair_perm = false);
 // side stream per device (plan-time work overlapping the values upload)
 cudaStream_t aux_stream();
 constexpr int kFixChunk = 8;  // items per pass-1 chunk (one batch of loads)

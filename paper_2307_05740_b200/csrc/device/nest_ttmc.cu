@@ -74,7 +74,14 @@ constexpr size_t kPqSmem = (sizeof(StageT) + sizeof(StageQ)) * (kBlock / 32);
 
 // CLK (diagnostics build, SPTTN_ITEM_CLOCKS=1): per item {start ns, end ns,
 // SM, groups, leaf steps, tile flushes} for fitting the item work model
-template <bool VECU, bool VECV, bool CLK = false>
+// PF: U rows of every group and V rows of single-leaf groups are copied
+// into the fragment tiles by cp.async.cg (LDGSTS.BYPASS, already in the
+// swizzled tile layout) one group ahead within a staged window, so the
+// STS half of their register transposition disappears and the gathers
+// overlap the previous group's DMMAs. Needs the pair-permuted packing
+// (logical slots a, a+4 stored adjacently, so one 8-byte LDS yields the
+// two rows a lane copies) and R = S = 16 (one 128-byte row = 8 chunks).
+template <bool VECU, bool VECV, bool CLK = false, bool PF = false>
 __global__ void __launch_bounds__(kBlock, 3) k_ttmc3pq(RootOutArgs a) {
   grid_launch_dependents();
   extern __shared__ __align__(16) unsigned char pq_smem[];  // kPqSmem bytes
@@ -162,6 +169,28 @@ __global__ void __launch_bounds__(kBlock, 3) k_ttmc3pq(RootOutArgs a) {
   // swizzled tile: element (slot, col) at slot*16 + (col ^ 4*(slot&3) ^ 2*(slot&1))
   const int st_off = gs * 16 + ((4 * gc) ^ (4 * (gs & 3)));
   const int o_lo = st_off + 2 * (gs & 1), o_hi = st_off + 2 - 2 * (gs & 1);
+  // PF: storage position of logical slot gs in the pair-permuted packing,
+  // and the cp.async role (16-byte chunk cc of rows cr, cr + 4)
+  const int gpos = PF ? 2 * (gs & 3) + (gs >> 2) : gs;
+  const int cr = lane >> 3, cc = lane & 7;
+  const int cp_lo = cr * 16 + ((2 * cc) ^ (4 * (cr & 3)) ^ (2 * (cr & 1)));
+  const int cp_hi = (cr + 4) * 16 + ((2 * cc) ^ (4 * (cr & 3)) ^ (2 * (cr & 1)));
+  // cp.async of group gi's (window buffers b, lb) U rows and, if it is a
+  // single-leaf group, V rows into tile tp
+  auto prefetch = [&](int b, int lb, int32_t l0, int gl, int tp) {
+    const int4 h2 = S.hdr[b][gl];
+    const int2 nd = *reinterpret_cast<const int2*>(&S.node[b][gl * kPackSlots + 2 * cr]);
+    SPTTN_DCHECK(nd.x >= 0 && nd.y >= 0 && nd.x < a.frows[1] && nd.y < a.frows[1]);
+    cp_async16_cg(&Q.us[tp][cp_lo], U + static_cast<uint32_t>(nd.x) * 16u + 2 * cc, 16);
+    cp_async16_cg(&Q.us[tp][cp_hi], U + static_cast<uint32_t>(nd.y) * 16u + 2 * cc, 16);
+    if (h2.y == 1) {
+      const int2 k2 = *reinterpret_cast<const int2*>(&S.kk[lb][h2.x - l0 + 2 * cr]);
+      SPTTN_DCHECK(k2.x >= 0 && k2.y >= 0 && k2.x < a.frows[2] && k2.y < a.frows[2]);
+      cp_async16_cg(&Q.xs[tp][cp_lo], V + static_cast<uint32_t>(k2.x) * 16u + 2 * cc, 16);
+      cp_async16_cg(&Q.xs[tp][cp_hi], V + static_cast<uint32_t>(k2.y) * 16u + 2 * cc, 16);
+    }
+    cp_async_commit();
+  };
   int par = 0;
 
   const int32_t nwin = (cend - cbeg + kGW - 1) / kGW;
@@ -185,15 +214,24 @@ __global__ void __launch_bounds__(kBlock, 3) k_ttmc3pq(RootOutArgs a) {
     const int32_t g0 = cbeg + win * kGW;
     const int32_t ge = min(g0 + kGW, cend);
     const int32_t L0 = S.hdr[mb][0].x;
+    if (PF && g0 < ge) {
+      __syncwarp();
+      prefetch(mb, lbf, L0, 0, par);  // the window's first group: no earlier prefetch
+    }
     for (int32_t g = g0; g < ge; ++g) {
       const int4 hh = S.hdr[mb][g - g0];
       const int n = hh.y;  // warp-uniform
       if (CLK) dbg_steps += n;
-      const int32_t lbase = hh.x - L0 + gs;
-      const int32_t j = S.node[mb][(g - g0) * kPackSlots + gs];
+      if (PF) {
+        __syncwarp();  // tile par^1 (group g-1) is read by every lane
+        if (g + 1 < ge) prefetch(mb, lbf, L0, g + 1 - g0, par ^ 1);
+      }
+      const int32_t lbase = hh.x - L0 + gpos;
+      const int32_t j = S.node[mb][(g - g0) * kPackSlots + gpos];
       SPTTN_DCHECK(j >= 0 && j < a.frows[1]);
       SPTTN_DCHECK(lbase + (n - 1) * kPackSlots < kGWLeaves);
-      const double4 ur = row4<VECU>(U + static_cast<int64_t>(j) * R, 4 * gc, R);
+      const double4 ur = PF ? make_double4(0, 0, 0, 0)
+                            : row4<VECU>(U + static_cast<int64_t>(j) * R, 4 * gc, R);
       // X[s] += t * V[k,s] over the group's n (warp-uniform) leaf steps,
       // specialised per n: no predicated-off stream loads / gathers / FMAs
       double4 x = make_double4(0, 0, 0, 0);
@@ -219,19 +257,25 @@ __global__ void __launch_bounds__(kBlock, 3) k_ttmc3pq(RootOutArgs a) {
 #pragma unroll
         for (int it = 0; it < kN; ++it) fma4(x, tt[it], vr[it]);
       };
-      switch (n) {
-        case 1: steps(std::integral_constant<int, 1>{}); break;
-        case 2: steps(std::integral_constant<int, 2>{}); break;
-        case 3: steps(std::integral_constant<int, 3>{}); break;
-        default: steps(std::integral_constant<int, 4>{}); break;
-      }
-      // transpose X and U quads into fragment layout through the tile
       double* xs = Q.xs[par];
       double* us = Q.us[par];
-      *reinterpret_cast<double2*>(xs + o_lo) = make_double2(x.x, x.y);
-      *reinterpret_cast<double2*>(us + o_lo) = make_double2(ur.x, ur.y);
-      *reinterpret_cast<double2*>(xs + o_hi) = make_double2(x.z, x.w);
-      *reinterpret_cast<double2*>(us + o_hi) = make_double2(ur.z, ur.w);
+      if (!PF || n != 1) {
+        switch (n) {
+          case 1: steps(std::integral_constant<int, 1>{}); break;
+          case 2: steps(std::integral_constant<int, 2>{}); break;
+          case 3: steps(std::integral_constant<int, 3>{}); break;
+          default: steps(std::integral_constant<int, 4>{}); break;
+        }
+        // transpose X (and U) quads into fragment layout through the tile
+        *reinterpret_cast<double2*>(xs + o_lo) = make_double2(x.x, x.y);
+        *reinterpret_cast<double2*>(xs + o_hi) = make_double2(x.z, x.w);
+      }
+      if (!PF) {
+        *reinterpret_cast<double2*>(us + o_lo) = make_double2(ur.x, ur.y);
+        *reinterpret_cast<double2*>(us + o_hi) = make_double2(ur.z, ur.w);
+      } else {
+        if (g + 1 < ge) cp_async_wait<1>(); else cp_async_wait<0>();  // group g's copies
+      }
       __syncwarp();
       double af[2][2], bf[2][2];  // [K chunk][m / n tile]
 #pragma unroll
@@ -242,6 +286,15 @@ __global__ void __launch_bounds__(kBlock, 3) k_ttmc3pq(RootOutArgs a) {
         for (int mt = 0; mt < 2; ++mt) {
           af[kc][mt] = us[seg * 16 + ((8 * mt + fh) ^ sw)];
           bf[kc][mt] = xs[seg * 16 + ((8 * mt + fh) ^ sw)];
+        }
+      }
+      if (PF && n == 1) {  // X = t * V[k] for single-leaf segments (copied rows)
+#pragma unroll
+        for (int kc = 0; kc < 2; ++kc) {
+          const int seg = 4 * kc + fq;  // logical slot; stored at 2(seg&3) + (seg>>2)
+          const double tk = S.tv[lbf][hh.x - L0 + 2 * (seg & 3) + (seg >> 2)];
+          bf[kc][0] *= tk;
+          bf[kc][1] *= tk;
         }
       }
 #pragma unroll
@@ -752,8 +805,11 @@ void launch_ttmc3(const RootOutArgs& a, cudaStream_t s) {
                                     static_cast<int>(kPqSmem)));
     kern<<<static_cast<unsigned>(blocks), kBlock, kPqSmem, s>>>(a);
   };
+  const bool pf = (a.flags >> 8) == 16;
   if (wu && wv && a.clk)
-    go(k_ttmc3pq<true, true, true>);
+    go(pf ? k_ttmc3pq<true, true, true, true> : k_ttmc3pq<true, true, true>);
+  else if (wu && wv && pf)
+    go(k_ttmc3pq<true, true, false, true>);
   else if (wu && wv)
     go(k_ttmc3pq<true, true>);
   else if (wu)

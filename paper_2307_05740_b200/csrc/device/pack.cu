@@ -83,15 +83,17 @@ __global__ void k_fill_groups(const int32_t* ids, const int32_t* runstart, const
                               const int32_t* leaf_off, const int32_t* seg_begin,
                               const int32_t* seg_node, const int32_t* seg_node1,
                               const int32_t* kidx, const int32_t* kidx2, const double* vals,
-                              int32_t n, int slots, int4* hdr, int32_t* gnode, int32_t* gnode1,
-                              int32_t* pk, int32_t* pk2, double* pv) {
+                              int32_t n, int slots, bool pair_perm, int4* hdr, int32_t* gnode,
+                              int32_t* gnode1, int32_t* pk, int32_t* pk2, double* pv) {
   const int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   const int32_t g = gid[p] - 1;
-  const int32_t slot = (p - runstart[p]) % slots;
+  const int32_t slot0 = (p - runstart[p]) % slots;
+  // storage position of the slot (pair_perm: slots a and a + slots/2 adjacent)
+  const int32_t slot = pair_perm ? 2 * (slot0 % (slots / 2)) + slot0 / (slots / 2) : slot0;
   const int32_t s = ids[p];
   const int32_t base = leaf_off[g];
-  if (slot == 0) hdr[g].x = base;
+  if (slot0 == 0) hdr[g].x = base;
   gnode[static_cast<int64_t>(g) * slots + slot] = seg_node[s];
   if (gnode1) gnode1[static_cast<int64_t>(g) * slots + slot] = seg_node1[s];
   const int32_t b = seg_begin[s], len = seg_begin[s + 1] - b;
@@ -140,7 +142,7 @@ struct MaxOp {
 }  // namespace
 
 void build_packed(const DevCsf& csf, int leaf_level, Decomp& d, cudaStream_t s, int slots,
-                  const int32_t* leaf_coord2, cudaEvent_t* fill_done) {
+                  const int32_t* leaf_coord2, cudaEvent_t* fill_done, bool pair_perm) {
   plan_trace("pack: enter", s);
   const int32_t nseg = static_cast<int32_t>(d.n_seg);
   const int32_t n0 = static_cast<int32_t>(csf.level_size[0]);
@@ -233,7 +235,8 @@ void build_packed(const DevCsf& csf, int leaf_level, Decomp& d, cudaStream_t s, 
   csf.wait_values(fs);  // the structure work above overlaps an async values upload
   k_fill_groups<<<nblk(nseg, 256), 256, 0, fs>>>(ids2, runstart, gid, leaf_off, d.seg_begin,
                                                  d.seg_node, d.seg_node1, t.idx[leaf_level],
-                                                 leaf_coord2, t.vals, nseg, slots, d.grp_hdr,
+                                                 leaf_coord2, t.vals, nseg, slots, pair_perm,
+                                                 d.grp_hdr,
                                                  d.grp_node, d.grp_node1, d.pk, d.pk2, d.pv);
   dmalloc(&d.slice_grp, (static_cast<int64_t>(n0) + 1) * sizeof(int32_t), s);
   k_slice_groups<<<nblk(static_cast<int64_t>(ngroups) + 1, 256), 256, 0, s>>>(d.grp_hdr, ngroups,
