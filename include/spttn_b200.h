@@ -162,7 +162,10 @@ int spttn_read_output(spttn_plan* plan, double* host_out, int64_t count, void* s
  * [8] GENERIC decomposition: 0 sequential walk, 1 root slices written
  *     directly, 2 root ranges into per-worker outputs summed in worker
  *     order, 3 level-1 fibers (JIT only); -1 for the fused kernels,
- * [9] GENERIC: 1 when the forest runs as an NVRTC-compiled kernel.       */
+ * [9] GENERIC: 1 when the forest runs as an NVRTC-compiled kernel,
+ * [10] kernel variant of the fused nests (the SPTTN_*_MODE value chosen,
+ *     e.g. 5 = non-root MTTKRP-3 on the output-mode-major re-ordered
+ *     tensor); -1 for GENERIC.                                           */
 int spttn_plan_info(const spttn_plan* plan, int64_t* out, int n);
 
 /* Diagnostics (kernel tuning): with SPTTN_ITEM_CLOCKS=1 set at plan

@@ -42,6 +42,9 @@ struct spttn_plan {
   int64_t n_pieces = 0;
   int2* leaf_jk = nullptr;  // TTTP mode 3: per-leaf {j, k}
   spttn_dev::Decomp dec;
+  // non-root MTTKRP-3 mode 5: the tensor re-ordered so the output mode is
+  // the root (owned by the plan; the kernels run on it instead of csf)
+  spttn_dev::DevCsf* tcsf = nullptr;
   spttn_dev::GenericState gen;
   spg_program* prog = nullptr;  // host copy (GENERIC)
   const double** d_dense = nullptr;
@@ -52,6 +55,18 @@ struct spttn_plan {
   std::vector<int64_t> last_counters;   // GENERIC: madds, resets, log cursor, overflow
   long long* item_clk = nullptr;        // diagnostics: per item {start, end, smid}
 };
+
+static void free_tcsf(spttn_plan* p) {
+  if (!p->tcsf) return;
+  for (int l = 0; l < p->tcsf->order; ++l) {
+    spttn_dev::dfree(p->tcsf->idx[l]);
+    spttn_dev::dfree(p->tcsf->ptr[l]);
+  }
+  spttn_dev::dfree(p->tcsf->vals);
+  delete p->tcsf;
+  p->tcsf = nullptr;
+}
+
 
 namespace {
 
@@ -441,6 +456,7 @@ int spttn_plan_destroy(spttn_plan* p) {
     spttn_dev::dfree(p->pieces);
     spttn_dev::dfree(p->leaf_jk);
     spttn_dev::free_decomp(p->dec);
+    free_tcsf(p);
     spttn_dev::generic_free(p->gen);
     delete p->prog;
     delete p;
@@ -798,8 +814,39 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
       const bool nr_fits = R % 8 == 0 && facs_aligned16 && D.level_size[0] < (1 << 27) &&
                            spttn_dev::mttkrp3_nr_smem(rows_in, rows_out) <=
                                static_cast<size_t>(smem_optin_bytes());
-      p->mode = static_cast<int>(env_int("SPTTN_NONROOT_MODE", nr_fits ? 4 : 0));
+      // mode 5 (default when the root kernel's shared-memory form fits): the
+      // CSF re-ordered at plan time with the output mode as the root — (j,i,k)
+      // for mode j, (k,i,j) for mode k — and the root-output MTTKRP-3 kernel
+      // (k_mttkrp3_smf) on it: out[j] = sum_i A[i] * (sum_k t C[k]) and
+      // out[k] = sum_i A[i] * (sum_j t B[j]), the same sums regrouped. Owner-
+      // computes rows, no atomics, a fixed summation order (bit-reproducible).
+      const bool tr_fits = R % 16 == 0 && facs_aligned16 && D.level_size[0] < (1 << 27) &&
+                           (p->fac_size[0] / R) * R < (int64_t{1} << 31) &&
+                           spttn_dev::mttkrp3_smf_smem(rows_in) <=
+                               static_cast<size_t>(smem_optin_bytes());
+      p->mode = static_cast<int>(env_int("SPTTN_NONROOT_MODE", tr_fits ? 5 : nr_fits ? 4 : 0));
+      if (p->mode == 5 && !tr_fits) p->mode = nr_fits ? 4 : 0;
+      if (p->mode == 5) {
+        const int order_j[3] = {1, 0, 2}, order_k[3] = {2, 0, 1};
+        p->tcsf = new spttn_dev::DevCsf;
+        spttn_dev::csf_permute(D, nr_mode == 1 ? order_j : order_k, *p->tcsf, s);
+        const auto& TD = *p->tcsf;
+        const int64_t warps = static_cast<int64_t>(sm_count()) * 16 * 2;
+        const int64_t chunk = std::clamp<int64_t>((TD.level_size[1] + warps - 1) / warps, 8, 1024);
+        spttn_dev::build_segments(TD, 1, 4, chunk, p->dec, tile, s, false);
+        spttn_dev::build_packed(TD, 2, p->dec, s, 8);
+        if (smf_ranges(p, TD, sm_count(), tile, s)) {
+          spttn_dev::mttkrp3_smf_prepare(p->dec, static_cast<int>(R), s);
+          p->launches = 1;
+        } else {  // a root slice too heavy for one CTA: the atomic kernels
+          spttn_dev::free_decomp(p->dec);
+          p->dec = spttn_dev::Decomp{};
+          free_tcsf(p);
+          p->mode = nr_fits ? 4 : 0;
+        }
+      }
       if (p->mode == 4 && !nr_fits) p->mode = 0;
+      if (p->mode != 5) {
       spttn_dev::build_segments(D, 1, 4, 1, p->dec, 0, s, false);
       spttn_dev::build_packed(D, 2, p->dec, s, p->mode == 4 ? 8 : 4);
       if (p->mode == 4) {
@@ -807,6 +854,7 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
         p->dec.n_cta = std::max(1, sm_count() / static_cast<int>(R / 8));
       }
       p->launches = 2;  // memset + kernel
+      }
     } else {
       const bool sparse_out = p->kind == SPTTN_NEST_TTTP3;
       p->out_count = sparse_out ? nnz : D.dims[0] * tile;
@@ -1058,8 +1106,8 @@ int spttn_execute_stage(spttn_plan* p, int stage, void* stream) {
     if (!p) fail(SPTTN_EINVAL, "null plan");
     if (stage < -1 || stage > 1) fail(SPTTN_EINVAL, "stage must be -1, 0 or 1");
     cudaStream_t s = as_stream(stream);
-    const auto& D = p->csf->d;
-    D.wait_values(s);
+    p->csf->d.wait_values(s);
+    const auto& D = p->tcsf ? *p->tcsf : p->csf->d;
     if (p->kind == SPTTN_NEST_GENERIC) {
       if (stage != 1) {
         if (p->gen.jit_kernel)
@@ -1099,6 +1147,20 @@ int spttn_execute_stage(spttn_plan* p, int stage, void* stream) {
     if (stage != 1) switch (p->kind) {
       case SPTTN_NEST_MTTKRP3_J:
       case SPTTN_NEST_MTTKRP3_K:
+        if (p->mode == 5) {  // root kernel on the re-ordered tensor: A at level 1
+          a.f[1] = p->fac[0];
+          a.f[2] = p->fac[1];
+          spttn_dev::SmfArgs x{};
+          x.nq = static_cast<int>(p->R / 16);
+          x.n_cta = static_cast<int>(p->dec.n_cta);
+          x.rows_c = static_cast<int32_t>(p->fac_size[1] / p->R);
+          x.cta_grp = p->dec.cta_grp;
+          x.hdr2 = p->dec.hdr2;
+          x.absent_rows = p->dec.absent_rows;
+          x.n_absent = p->dec.n_absent;
+          spttn_dev::launch_mttkrp3_smf(a, x, s);
+          break;
+        }
         a.f[0] = p->fac[0];
         a.f[1] = p->fac[1];
         SPTTN_CUDA(cudaMemsetAsync(p->out, 0, std::max<int64_t>(1, p->out_count) * 8, s));
@@ -1205,12 +1267,13 @@ int spttn_plan_info(const spttn_plan* p, int64_t* out, int n) {
   return guarded([&] {
     if (!p) fail(SPTTN_EINVAL, "null plan");
     const bool gen = p->kind == SPTTN_NEST_GENERIC;
-    const int64_t v[10] = {p->launches,   p->dec.n_items, p->dec.n_split, p->dec.n_absent,
+    const int64_t v[11] = {p->launches,   p->dec.n_items, p->dec.n_split, p->dec.n_absent,
                            p->dec.n_items * 2 * p->dec.tile * 8,
                            p->kind,        p->dec.n_seg,   gen ? p->last_madds : -1,
                            gen ? p->gen.par_mode : -1,
-                           gen ? (p->gen.jit_kernel != nullptr ? 1 : 0) : -1};
-    for (int i = 0; i < n && i < 10; ++i) out[i] = v[i];
+                           gen ? (p->gen.jit_kernel != nullptr ? 1 : 0) : -1,
+                           gen ? -1 : p->mode};
+    for (int i = 0; i < n && i < 11; ++i) out[i] = v[i];
   });
 }
 

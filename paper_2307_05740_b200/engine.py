@@ -268,10 +268,10 @@ class Plan:
         return torch.as_tensor(_View(self.output_ptr, n), device="cuda")
 
     def info(self) -> dict:
-        out = (C.c_int64 * 10)()
-        _check(N.engine().spttn_plan_info(self.handle, out, 10))
+        out = (C.c_int64 * 11)()
+        _check(N.engine().spttn_plan_info(self.handle, out, 11))
         keys = ["launches", "items", "split_slices", "absent_rows", "scratch_bytes", "kind",
-                "segments", "device_madds", "generic_mode", "generic_jit"]
+                "segments", "device_madds", "generic_mode", "generic_jit", "variant"]
         return dict(zip(keys, list(out)))
 
     def item_clocks(self) -> np.ndarray:

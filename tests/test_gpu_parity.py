@@ -96,7 +96,7 @@ VARIANTS = [("SPTTN_MTTKRP_MODE", m, ["mttkrp3_small", "mttkrp3_r32", "mttkrp4_s
     [("SPTTN_TTTP_BATCH", m, ["tttp3_small", "tttp3_r64"]) for m in ("2", "4", "8")] + \
     [("SPTTN_TTMC4_MODE", m, ["ttmc4_small", "ttmc4_r8"]) for m in ("3", "4")] + \
     [("SPTTN_NONROOT_MODE", m, ["mttkrp3j_small", "mttkrp3j_r32", "mttkrp3k_small", "mttkrp3k_r32"])
-     for m in ("0", "4")]
+     for m in ("0", "4", "5")]
 
 
 @pytest.mark.parametrize("env,mode,names", VARIANTS, ids=[f"{v[0]}={v[1]}" for v in VARIANTS])
@@ -308,6 +308,37 @@ def test_nonroot_mttkrp(E, kind, shape):
     assert_parity(out, want, norm, f"nonroot kind={kind} {shape}")
     if shape == "empty":
         assert not np.any(out)
+    if shape == "baseline":  # the re-ordered root kernel: owner-computes, reproducible
+        assert plan.info()["variant"] == 5
+        plan.execute()
+        assert np.array_equal(plan.read_output(), out)
+
+
+@pytest.mark.parametrize("kind", [6, 7])
+@pytest.mark.parametrize("mode", ["0", "4", "5"])
+def test_nonroot_variants_with_absent_rows(E, kind, mode, monkeypatch):
+    """Every non-root variant on a tensor with absent output rows (mode-j /
+    mode-k indices that never occur): they must come out exactly zero — the
+    re-ordered variant (5) writes them from its absent-root-row list, the
+    atomic ones from the zeroed output."""
+    from paper_2307_05740_b200.tensor import Csf
+    monkeypatch.setenv("SPTTN_NONROOT_MODE", mode)
+    rng = np.random.default_rng(40 + kind)
+    dims = (300, 400, 500)
+    n = 60000
+    co = np.stack([rng.integers(0, dims[0], n), rng.integers(0, dims[1] - 50, n),
+                   rng.integers(0, dims[2] - 60, n)], 1).astype(np.int64)
+    co = np.unique(co, axis=0)
+    csf = Csf.from_coo(list(dims), co, rng.uniform(-1, 1, len(co)))
+    R = 32
+    fs = [rng.standard_normal((dims[0], R)), rng.standard_normal((dims[2 if kind == 6 else 1], R))]
+    out, plan, _ = run(E, kind, csf, fs, (R, 0, 0))
+    want, norm = oracle_with_norm(kind, csf, fs, (R, 0, 0))
+    assert_parity(out, want, norm, f"nonroot kind={kind} mode={mode}")
+    assert plan.info()["variant"] == int(mode)
+    rows = out.reshape(-1, R)
+    zrows = np.abs(np.asarray(norm).reshape(-1, R)).sum(1) == 0
+    assert zrows.sum() >= 50 and not np.any(rows[zrows])
 
 
 @pytest.mark.parametrize("order", [3, 4])
