@@ -210,7 +210,7 @@ int spttn_unfactorized(const spttn_unfact_desc* desc, spttn_csf* csf, double* ho
 /* [0] SM count, [1] compute capability major*10+minor, [2] L2 bytes,
  * [3] max shared memory per block (opt-in). */
 int spttn_device_info(int64_t* out, int n);
-/* Creates the CUDA context and the engine's memory pool up front (the C++
+/* Creates the CUDA context up front (the C++
  * drop-in calls it when it is loaded, so the first prepare() does not pay for
  * context creation; SPTTN_LAZY_INIT=1 skips that). SPTTN_ECUDA without a
  * device. */
@@ -220,9 +220,10 @@ int spttn_init(void);
 int spttn_synchronize(void* stream);
 /* Build identification string (arch, nvcc version). */
 const char* spttn_build_info(void);
-/* Device memory of CSF layouts and plans comes from a per-device
- * stream-ordered pool that keeps freed pages mapped, so rebuilding plans is
- * cheap. Returns the pools' cached (unused) pages to the driver. */
+/* Device memory of CSF layouts and plans comes from a per-device caching
+ * allocator (whole cudaMalloc blocks kept on a free list and reused in stream
+ * order), so rebuilding plans is cheap. Synchronises the device and returns
+ * the cached (unused) blocks to the driver. */
 int spttn_release_cached(void);
 
 #ifdef __cplusplus

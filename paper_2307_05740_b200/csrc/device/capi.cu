@@ -223,7 +223,7 @@ int spttn_init(void) {
       fail(SPTTN_ECUDA, "no CUDA device");
     }
     SPTTN_CUDA(cudaFree(nullptr));  // creates the primary context
-    void* p = nullptr;              // and the engine's memory pool
+    void* p = nullptr;              // and touches the allocator (first cudaMalloc)
     spttn_dev::dmalloc_raw(&p, 256, nullptr);
     spttn_dev::dfree(p, nullptr);
     SPTTN_CUDA(cudaStreamSynchronize(nullptr));

@@ -352,14 +352,18 @@ void launch_mttkrp_pq(const RootOutArgs& a, int order, cudaStream_t s) {
   const int64_t blocks = (a.n_items * 32 + kBlock - 1) / kBlock;
   if (blocks == 0) return;
   const unsigned b = static_cast<unsigned>(blocks);
+  auto go = [&](auto kern) {  // items are sized for 3 resident CTAs per SM
+    pin_carveout(kern, 3, 0);
+    kern<<<b, kBlock, 0, s>>>(a);
+  };
   if (order == 3) {
-    if (a.vec) k_mttkrp_pq<3, true><<<b, kBlock, 0, s>>>(a);
-    else k_mttkrp_pq<3, false><<<b, kBlock, 0, s>>>(a);
+    if (a.vec) go(k_mttkrp_pq<3, true>);
+    else go(k_mttkrp_pq<3, false>);
   } else {
-    if (a.vec && a.R == 32 && a.clk) k_mttkrp_pq<4, true, 32, true><<<b, kBlock, 0, s>>>(a);
-    else if (a.vec && a.R == 32) k_mttkrp_pq<4, true, 32><<<b, kBlock, 0, s>>>(a);
-    else if (a.vec) k_mttkrp_pq<4, true><<<b, kBlock, 0, s>>>(a);
-    else k_mttkrp_pq<4, false><<<b, kBlock, 0, s>>>(a);
+    if (a.vec && a.R == 32 && a.clk) go(k_mttkrp_pq<4, true, 32, true>);
+    else if (a.vec && a.R == 32) go(k_mttkrp_pq<4, true, 32>);
+    else if (a.vec) go(k_mttkrp_pq<4, true>);
+    else go(k_mttkrp_pq<4, false>);
   }
   SPTTN_CUDA(cudaGetLastError());
 }
@@ -368,8 +372,12 @@ void launch_mttkrp_pk(const RootOutArgs& a, cudaStream_t s) {  // order 3
   const int64_t blocks = (a.n_items * 32 + kBlock - 1) / kBlock;
   if (blocks == 0) return;
   const unsigned b = static_cast<unsigned>(blocks);
-  if (a.vec) k_mttkrp_pk<3, true><<<b, kBlock, 0, s>>>(a);
-  else k_mttkrp_pk<3, false><<<b, kBlock, 0, s>>>(a);
+  auto go = [&](auto kern) {
+    pin_carveout(kern, 4, 0);
+    kern<<<b, kBlock, 0, s>>>(a);
+  };
+  if (a.vec) go(k_mttkrp_pk<3, true>);
+  else go(k_mttkrp_pk<3, false>);
   SPTTN_CUDA(cudaGetLastError());
 }
 

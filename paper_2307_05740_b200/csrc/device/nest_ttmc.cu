@@ -803,6 +803,7 @@ void launch_ttmc3(const RootOutArgs& a, cudaStream_t s) {
   auto go = [&](auto kern) {
     SPTTN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(kPqSmem)));
+    pin_carveout(kern, 3, kPqSmem);  // the items are one per resident warp at 3 CTAs per SM
     kern<<<static_cast<unsigned>(blocks), kBlock, kPqSmem, s>>>(a);
   };
   const bool pf = (a.flags >> 8) == 16;
@@ -833,6 +834,7 @@ void launch_ttmc4(const RootOutArgs& a, cudaStream_t s) {
       const size_t sm = t4a_smem_bytes(nb);
       SPTTN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(sm)));
+      pin_carveout(kern, 1, sm);
       kern<<<static_cast<unsigned>((a.n_items * 32 + nb - 1) / nb), nb, sm, s>>>(a);
     };
     if (a.clk)  // diagnostics instantiation (SPTTN_ITEM_CLOCKS=1)
@@ -842,10 +844,14 @@ void launch_ttmc4(const RootOutArgs& a, cudaStream_t s) {
   } else {  // packed, 4 x 2 (s, t) blocks per lane (any R, S, T <= 8)
     const bool vv = a.vec & 2, vw = a.vec & 4;
     const unsigned b = static_cast<unsigned>(blocks);
-    if (vv && vw) k_ttmc4pq<true, true><<<b, kBlock, 0, s>>>(a);
-    else if (vv) k_ttmc4pq<true, false><<<b, kBlock, 0, s>>>(a);
-    else if (vw) k_ttmc4pq<false, true><<<b, kBlock, 0, s>>>(a);
-    else k_ttmc4pq<false, false><<<b, kBlock, 0, s>>>(a);
+    auto goq = [&](auto kern) {
+      pin_carveout(kern, 2, 0);
+      kern<<<b, kBlock, 0, s>>>(a);
+    };
+    if (vv && vw) goq(k_ttmc4pq<true, true>);
+    else if (vv) goq(k_ttmc4pq<true, false>);
+    else if (vw) goq(k_ttmc4pq<false, true>);
+    else goq(k_ttmc4pq<false, false>);
   }
   SPTTN_CUDA(cudaGetLastError());
 }

@@ -71,7 +71,7 @@ def device_info() -> dict:
 
 
 def release_cached() -> None:
-    """spttn_release_cached: return the engine pool's unused device pages."""
+    """spttn_release_cached: return the engine's cached (unused) device blocks to the driver."""
     _check(N.engine().spttn_release_cached())
 
 
