@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <unordered_set>
 #include <vector>
@@ -350,22 +351,33 @@ void unfactorized_run(const void* desc, const DevCsf& csf, const double* const* 
 // that the residency the plan's single-wave items are sized for does not rest
 // on the driver's default choice: measured on TTMc-3 (3 CTAs of 61 KB per SM),
 // a preferred carveout of 50-60 % fits only 2 (320 vs 212 us), 40 % one
-// (413 us), 75-100 % all three. Applied once per kernel.
+// (413 us), 75-100 % all three. Applied once per kernel. `fixed_pct` pins a
+// measured optimum instead: MTTKRP-4 runs 8 % faster with the largest
+// shared-memory split although 47 % fits its 3 CTAs (620 us at 47-85 %, 569 us
+// at 90-100 %), TTTP (no shared memory) 1 % faster at 0 % than at the
+// driver's default (2.72 vs 2.75 ms; 3.39 ms at 100 %).
 template <class K>
-inline void pin_carveout(K kern, int blocks_per_sm, size_t dyn_smem) {
+inline void pin_carveout(K kern, int blocks_per_sm, size_t dyn_smem, int fixed_pct = -1) {
+  if (const char* cv = std::getenv("SPTTN_CARVEOUT")) {  // tuning override, every pinned kernel
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(cv));
+    return;
+  }
   static std::mutex mu;
   static std::unordered_set<const void*> done;
   {
     std::lock_guard<std::mutex> lk(mu);
     if (!done.insert(reinterpret_cast<const void*>(kern)).second) return;
   }
-  cudaFuncAttributes fa;
-  if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess) return;
-  int dev = 0, max_sm = 233472;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&max_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-  const size_t need = static_cast<size_t>(blocks_per_sm) * (fa.sharedSizeBytes + dyn_smem + 1024);
-  const int pct = static_cast<int>(std::min<size_t>(100, (need * 100 + max_sm - 1) / max_sm));
+  int pct = fixed_pct;
+  if (pct < 0) {
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess) return;
+    int dev = 0, max_sm = 233472;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&max_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    const size_t need = static_cast<size_t>(blocks_per_sm) * (fa.sharedSizeBytes + dyn_smem + 1024);
+    pct = static_cast<int>(std::min<size_t>(100, (need * 100 + max_sm - 1) / max_sm));
+  }
   cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
 }
 

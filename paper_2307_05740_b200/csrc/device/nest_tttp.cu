@@ -162,9 +162,13 @@ void launch_tttp3_pieces(const RootOutArgs& a, const int4* pieces, int64_t n_pie
   const int G = group_lanes_for(a.R);
   const int64_t blocks = std::min<int64_t>((n_pieces + 7) / 8, static_cast<int64_t>(sms) * 8);
   const unsigned nb = static_cast<unsigned>(blocks);
+  auto go = [&](auto kern) {
+    pin_carveout(kern, 0, 0, 0);  // no shared memory: all of it to L1
+    kern<<<nb, kBlock, 0, s>>>(a, pieces, n_pieces, leaf_jk);
+  };
 #define SPTTN_TTTP_P(GG, UU)                                                                     \
-  if (a.vec) k_tttp3_piece<GG, UU, true><<<nb, kBlock, 0, s>>>(a, pieces, n_pieces, leaf_jk);    \
-  else k_tttp3_piece<GG, UU, false><<<nb, kBlock, 0, s>>>(a, pieces, n_pieces, leaf_jk);
+  if (a.vec) go(k_tttp3_piece<GG, UU, true>);                                                    \
+  else go(k_tttp3_piece<GG, UU, false>);
   const bool b8 = batch >= 8;
   switch (G) {
     case 1: SPTTN_TTTP_P(1, 1) break;
