@@ -223,7 +223,15 @@ const char* spttn_build_info(void);
 /* Device memory of CSF layouts and plans comes from a per-device caching
  * allocator (whole cudaMalloc blocks kept on a free list and reused in stream
  * order), so rebuilding plans is cheap. Synchronises the device and returns
- * the cached (unused) blocks to the driver. */
+ * the cached (unused) blocks to the driver.
+ * Stream lifetime: the temporaries of spttn_csf_create* / spttn_plan_create
+ * are freed in the order of the stream passed to them; such a block later
+ * reused on another stream makes that stream wait on an event recorded on
+ * the first one at reuse time. A stream given to those calls must therefore
+ * outlive the engine's use, or be followed by spttn_release_cached() before
+ * it is destroyed (an event record that fails on a dead stream falls back
+ * to a device synchronisation). Destroy calls synchronise and free on the
+ * default stream. */
 int spttn_release_cached(void);
 
 #ifdef __cplusplus
