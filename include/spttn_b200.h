@@ -230,8 +230,8 @@ const char* spttn_build_info(void);
  * the first one at reuse time. A stream given to those calls must therefore
  * outlive the engine's use, or be followed by spttn_release_cached() before
  * it is destroyed (an event record that fails on a dead stream falls back
- * to a device synchronisation). Destroy calls synchronise and free on the
- * default stream. */
+ * to a device synchronisation). Destroy calls synchronise the device first,
+ * so the blocks they release carry no stream ordering. */
 int spttn_release_cached(void);
 
 #ifdef __cplusplus

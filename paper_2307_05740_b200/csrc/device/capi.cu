@@ -225,8 +225,8 @@ int spttn_init(void) {
     SPTTN_CUDA(cudaFree(nullptr));  // creates the primary context
     void* p = nullptr;              // and touches the allocator (first cudaMalloc)
     spttn_dev::dmalloc_raw(&p, 256, nullptr);
-    spttn_dev::dfree(p, nullptr);
     SPTTN_CUDA(cudaStreamSynchronize(nullptr));
+    spttn_dev::dfree(p);
   });
 }
 
@@ -839,6 +839,7 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
           spttn_dev::mttkrp3_smf_prepare(p->dec, static_cast<int>(R), s);
           p->launches = 1;
         } else {  // a root slice too heavy for one CTA: the atomic kernels
+          SPTTN_CUDA(cudaStreamSynchronize(s));  // default-stream frees are for idle blocks
           spttn_dev::free_decomp(p->dec);
           p->dec = spttn_dev::Decomp{};
           free_tcsf(p);
@@ -999,6 +1000,7 @@ int spttn_plan_create(const spttn_plan_desc* desc, spttn_csf* csf, void* stream,
           if (smf_ranges(p, D, sms, tile, s)) {
             spttn_dev::mttkrp3_smf_prepare(p->dec, static_cast<int>(R), s);
           } else {
+            SPTTN_CUDA(cudaStreamSynchronize(s));  // default-stream frees are for idle blocks
             spttn_dev::free_decomp(p->dec);
             p->mode = 2;
           }

@@ -115,14 +115,17 @@ struct Decomp {
   int2* hdr2 = nullptr;            // [n_groups+2] k_mttkrp3_smf headers
 };
 
-// ---- device memory (mem.cu): one stream-ordered pool per device ---------
+// ---- device memory (mem.cu): caching allocator over cudaMalloc blocks ---
 void dmalloc_raw(void** p, size_t bytes, cudaStream_t s);
 template <class T>
 inline void dmalloc(T** p, size_t bytes, cudaStream_t s) {
   dmalloc_raw(reinterpret_cast<void**>(p), bytes, s);
 }
-// Frees in stream order on `s`; owners free with s = 0 after synchronising.
-void dfree(void* p, cudaStream_t s = 0);
+// Frees in stream order on `s`. Owners (plan / CSF destroy) synchronise first
+// and free with the default kStreamIdle: the block has no pending work and may
+// be reused on any stream without an ordering event.
+inline const cudaStream_t kStreamIdle = reinterpret_cast<cudaStream_t>(static_cast<intptr_t>(-16));
+void dfree(void* p, cudaStream_t s = kStreamIdle);
 void release_cached();
 // Page-locked host staging blocks (size classes over cudaHostAlloc slabs), so
 // a small plan's uploads / downloads are single DMA copies without a

@@ -19,7 +19,8 @@
 //
 // Stream order: dfree(p, s) makes the block reusable by work enqueued on `s`
 // after the call; a request on another stream first makes that stream wait
-// on an event recorded on `s` (lazily, at reuse). Requests are rounded to
+// on an event recorded on `s` (lazily, at reuse). Blocks freed by their owner
+// after a synchronisation (kStreamIdle, the default) need no ordering. Requests are rounded to
 // 512 B (small) or 2 MB (large) and served by the smallest cached block that
 // wastes at most a quarter. On an out-of-memory cudaMalloc the cache is
 // returned to the driver and the request retried. spttn_release_cached()
@@ -90,7 +91,7 @@ void dmalloc_raw(void** p, size_t bytes, cudaStream_t s) {
       auto pick = c.free_by_size.end();
       for (auto j = it; j != c.free_by_size.end() && j->first <= cap; ++j) {
         if (pick == c.free_by_size.end()) pick = j;
-        if (j->second.stream == s) { pick = j; break; }
+        if (j->second.stream == s || j->second.stream == kStreamIdle) { pick = j; break; }
         if (j->first != it->first) break;  // only scan the smallest size for a same-stream block
       }
       if (pick != c.free_by_size.end()) {
@@ -101,7 +102,7 @@ void dmalloc_raw(void** p, size_t bytes, cudaStream_t s) {
       }
     }
     if (hit.ptr) {
-      if (hit.stream != s) {  // order the new owner's work after the old stream's
+      if (hit.stream != s && hit.stream != kStreamIdle) {  // order after the old stream's work
         cudaEvent_t ev = nullptr;
         bool ok = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess &&
                   cudaEventRecord(ev, hit.stream) == cudaSuccess &&
