@@ -134,16 +134,16 @@ __global__ void __launch_bounds__(kBlock, 4) k_mttkrp_pk(RootOutArgs a) {
 // per-stage mbarriers. k_mttkrp_pk loaded them with __ldg right before the
 // gathers they feed: two dependent L2 round trips per group (ncu: long
 // scoreboard 67 %, data pipe 57 %).
-constexpr int kMW = 8;                     // groups per window
 constexpr int kMSlots = 4;
-constexpr int kMWLeaves = kMW * kMSlots * 4;  // leaves per window (len <= 4)
 
+// MW = groups per window (leaves per window: MW * kMSlots * 4, len <= 4)
+template <int MW>
 struct StageM {
-  alignas(16) int4 hdr[3][kMW];
-  alignas(16) int32_t node[3][kMW * kMSlots];
-  alignas(16) int32_t node1[3][kMW * kMSlots];
-  alignas(16) int32_t kk[2][kMWLeaves];
-  alignas(16) double tv[2][kMWLeaves];
+  alignas(16) int4 hdr[3][MW];
+  alignas(16) int32_t node[3][MW * kMSlots];
+  alignas(16) int32_t node1[3][MW * kMSlots];
+  alignas(16) int32_t kk[2][MW * kMSlots * 4];
+  alignas(16) double tv[2][MW * kMSlots * 4];
   uint64_t mbar_meta[3];
   uint64_t mbar_leaf[2];
 };
@@ -152,15 +152,18 @@ struct StageM {
 // 8 lanes, constant row strides, no column predicates) or 0 = a.R at run time
 // CLK: diagnostics instantiation (SPTTN_ITEM_CLOCKS=1), per item {start ns,
 // end ns, SM, groups, leaf steps, tile flushes}
-template <int ORDER, bool VEC, int RC = 0, bool CLK = false>
+template <int ORDER, bool VEC, int RC = 0, bool CLK = false, int MW = 8>
 __global__ void __launch_bounds__(kBlock, 3) k_mttkrp_pq(RootOutArgs a) {
+  constexpr int kMW = MW;
+  constexpr int kMWLeaves = MW * kMSlots * 4;
   grid_launch_dependents();
-  __shared__ StageM stage[kBlock / 32];
+  extern __shared__ __align__(16) unsigned char pq_smem_raw[];
+  StageM<MW>* stage = reinterpret_cast<StageM<MW>*>(pq_smem_raw);
   const int64_t w = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / 32;
   if (w >= a.n_items) return;  // warp-uniform
   if (CLK && (threadIdx.x & 31) == 0) a.clk[6 * w] = globaltimer_ns();
   int dbg_steps = 0, dbg_flush = 0;
-  StageM& S = stage[threadIdx.x / 32];
+  StageM<MW>& S = stage[threadIdx.x / 32];
   const int lane = threadIdx.x & 31;
   const int slot = lane >> 3;
   const int c = (lane & 7) * 4;
@@ -352,11 +355,24 @@ void launch_mttkrp_pq(const RootOutArgs& a, int order, cudaStream_t s) {
   const int64_t blocks = (a.n_items * 32 + kBlock - 1) / kBlock;
   if (blocks == 0) return;
   const unsigned b = static_cast<unsigned>(blocks);
-  auto go = [&](auto kern) {  // items are sized for 3 resident CTAs per SM
+  auto gow = [&](auto kern, size_t sm) {  // items are sized for 3 resident CTAs per SM
+    SPTTN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(sm)));
     // order 4: the largest shared-memory split (smallest L1) measured fastest
-    pin_carveout(kern, 3, 0, order == 4 ? 100 : -1);
-    kern<<<b, kBlock, 0, s>>>(a);
+    pin_carveout(kern, 3, sm, order == 4 ? 100 : -1);
+    kern<<<b, kBlock, sm, s>>>(a);
   };
+  auto go = [&](auto kern) { gow(kern, sizeof(StageM<8>) * (kBlock / 32)); };
+  // order 4, R = 32: windows of 16 groups (the 100 % carveout leaves room for
+  // 3 x 68 KB of staging): 565 -> 553 us; SPTTN_M4_WIN=8 selects the 8-group windows
+  static const int mw = std::getenv("SPTTN_M4_WIN") ? std::atoi(std::getenv("SPTTN_M4_WIN")) : 16;
+  if (order == 4 && a.vec && a.R == 32 && mw == 16) {
+    const size_t sm = sizeof(StageM<16>) * (kBlock / 32);
+    if (a.clk) gow(k_mttkrp_pq<4, true, 32, true, 16>, sm);
+    else gow(k_mttkrp_pq<4, true, 32, false, 16>, sm);
+    SPTTN_CUDA(cudaGetLastError());
+    return;
+  }
   if (order == 3) {
     if (a.vec) go(k_mttkrp_pq<3, true>);
     else go(k_mttkrp_pq<3, false>);
