@@ -542,14 +542,21 @@ __global__ void __launch_bounds__(kBlock, 2) k_ttmc4pq(RootOutArgs a) {
 // were the tile stores waiting on their gathers (long-scoreboard 30 % at
 // 12.8 warps per SM); here the gather of step s+1 is in flight while step s
 // is computed, with no extra registers.
+// TTMc-4 staging windows (1 CTA of 12 warps per SM: room for larger windows
+// than TTMc-3's 3 CTAs)
+#ifndef SPTTN_GW4
+#define SPTTN_GW4 12
+#endif
+constexpr int kGW4 = SPTTN_GW4;                      // groups per window
+constexpr int kGW4Leaves = kGW4 * kPackSlots * 4;    // leaves per window (len <= 4)
 struct StageT4a {
   alignas(16) double vs[2][kPackSlots * 8];  // V rows (64 bytes, swizzled), double-buffered
   alignas(16) double ws[2][kPackSlots * 8];  // W rows
-  alignas(16) int4 hdr[3][kGW];
-  alignas(16) int32_t node[3][kGW * kPackSlots];
-  alignas(16) int32_t ll[2][kGWLeaves];
-  alignas(16) int32_t kk[2][kGWLeaves];
-  alignas(16) double tv[2][kGWLeaves];
+  alignas(16) int4 hdr[3][kGW4];
+  alignas(16) int32_t node[3][kGW4 * kPackSlots];
+  alignas(16) int32_t ll[2][kGW4Leaves];
+  alignas(16) int32_t kk[2][kGW4Leaves];
+  alignas(16) double tv[2][kGW4Leaves];
   uint64_t mbar_meta[3];
   uint64_t mbar_leaf[2];
 };
@@ -614,8 +621,8 @@ __global__ void __launch_bounds__(NB, MB) k_ttmc4pa(RootOutArgs a) {
     for (int e = 0; e < 16; ++e) acc[e] = 0.0;
   };
   auto issue_meta = [&](int32_t wi) {
-    const int32_t g0 = cbeg + wi * kGW;
-    const int32_t nw = min(g0 + kGW, cend) - g0;
+    const int32_t g0 = cbeg + wi * kGW4;
+    const int32_t nw = min(g0 + kGW4, cend) - g0;
     const int b = wi % 3;
     const unsigned hb = nw * sizeof(int4), nb = nw * kPackSlots * sizeof(int32_t);
     fence_proxy_async();
@@ -624,14 +631,14 @@ __global__ void __launch_bounds__(NB, MB) k_ttmc4pa(RootOutArgs a) {
     bulk_g2s_elect(&S.node[b][0], a.grp_node + static_cast<int64_t>(g0) * kPackSlots, nb, &S.mbar_meta[b]);
   };
   auto issue_leaves = [&](int32_t wi) {
-    const int32_t g0 = cbeg + wi * kGW;
-    const int32_t nw = min(g0 + kGW, cend) - g0;
+    const int32_t g0 = cbeg + wi * kGW4;
+    const int32_t nw = min(g0 + kGW4, cend) - g0;
     const int b = wi % 3, lb = wi & 1;
     mbar_wait(&S.mbar_meta[b], (wi / 3) & 1);
     const int32_t L0 = uni(S.hdr[b][0].x);
     const int32_t L1 = uni(S.hdr[b][nw - 1].x + kPackSlots * S.hdr[b][nw - 1].y);
     const unsigned n = static_cast<unsigned>(L1 - L0);
-    SPTTN_DCHECK(n <= static_cast<unsigned>(kGWLeaves));
+    SPTTN_DCHECK(n <= static_cast<unsigned>(kGW4Leaves));
     fence_proxy_async();
     expect_tx_elect(&S.mbar_leaf[lb], n * 16u);
     bulk_g2s_elect(&S.ll[lb][0], a.pk + L0, n * 4u, &S.mbar_leaf[lb]);
@@ -643,7 +650,7 @@ __global__ void __launch_bounds__(NB, MB) k_ttmc4pa(RootOutArgs a) {
   // for the L1-allocating .ca at the BASELINE shape (fewer L1 wavefronts per
   // copy; the 128 KB V / W are L2-resident)
   auto issue_rows = [&](int buf, int lbuf, int32_t e) {
-    SPTTN_DCHECK(e >= 0 && e < kGWLeaves);
+    SPTTN_DCHECK(e >= 0 && e < kGW4Leaves);
     SPTTN_DCHECK(S.kk[lbuf][e] >= 0 && S.kk[lbuf][e] < a.frows[2]);
     SPTTN_DCHECK(S.ll[lbuf][e] >= 0 && S.ll[lbuf][e] < a.frows[3]);
     cp_async16_cg(&S.vs[buf][st_off], V + static_cast<int64_t>(S.kk[lbuf][e]) * 8 + 2 * gc, 16);
@@ -651,7 +658,7 @@ __global__ void __launch_bounds__(NB, MB) k_ttmc4pa(RootOutArgs a) {
     cp_async_commit();
   };
 
-  const int32_t nwin = (cend - cbeg + kGW - 1) / kGW;
+  const int32_t nwin = (cend - cbeg + kGW4 - 1) / kGW4;
   if (lane == 0) {
     for (int b = 0; b < 3; ++b) mbar_init(&S.mbar_meta[b], 1);
     for (int b = 0; b < 2; ++b) mbar_init(&S.mbar_leaf[b], 1);
@@ -673,8 +680,8 @@ __global__ void __launch_bounds__(NB, MB) k_ttmc4pa(RootOutArgs a) {
     if (win + 2 < nwin) issue_meta(win + 2);
     mbar_wait(&S.mbar_meta[mb], (win / 3) & 1);
     mbar_wait(&S.mbar_leaf[lbf], (win / 2) & 1);
-    const int32_t g0 = cbeg + win * kGW;
-    const int32_t ge = min(g0 + kGW, cend);
+    const int32_t g0 = cbeg + win * kGW4;
+    const int32_t ge = min(g0 + kGW4, cend);
     const int32_t L0 = S.hdr[mb][0].x;
     for (int32_t g = g0; g < ge; ++g) {
       const int4 hh = S.hdr[mb][g - g0];
